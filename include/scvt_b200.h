@@ -1,0 +1,153 @@
+/*
+ * scvt_b200.h — C ABI of the B200-native SCVT energy/gradient + Lloyd-P-LBFGS hot path.
+ *
+ * The reference (`scvtmesh` 0.1.0, pure Python) has no FFI: its drop-in boundary is the
+ * duck-typed evaluator protocol consumed by `optimizer.minimize`
+ * (/root/reference/pkg/src/scvtmesh/optimizer.py:278-391) and implemented by
+ * `MeshEvaluator.evaluate` (pipeline.py:261-279).  Each entry point below replaces one piece
+ * of that protocol or of the optimizer's vector algebra; the citation names the reference
+ * code it stands in for.  The Python package `paper_1709_06924_b200` binds these with ctypes
+ * (see INTEGRATION.md), exactly as a maintainer would bind them from the reference.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers to caller-owned, contiguous float64 / int64
+ *     buffers (row-major (n,3) for points/vectors).  The library never frees caller memory.
+ *   - Scalars documented as "host out" are written to host memory; those calls synchronise
+ *     the context's stream.  All other calls are stream-ordered on the context stream.
+ *   - Return value: SCVT_OK (0) or one of the status codes below (1:1 with scvtmesh.errors).
+ *     `scvt_last_error` gives the message.  One context per (process, device).
+ */
+#ifndef SCVT_B200_H
+#define SCVT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum scvt_status {
+    SCVT_OK = 0,
+    SCVT_ERR_INSUFFICIENT_POINTS = 1, /* InsufficientPointsError  delaunay.py:189-199        */
+    SCVT_ERR_DEGENERATE_TRIANGLE = 2, /* DegenerateTriangleError  delaunay.py:157-160        */
+    SCVT_ERR_COVERAGE = 3,            /* CoverageError            delaunay.py:295-302        */
+    SCVT_ERR_CENTROID_AT_ORIGIN = 4,  /* CentroidAtOriginError    optimizer.py:240-246       */
+    SCVT_ERR_NONPOSITIVE_DIAGONAL = 5,/* NonpositiveDiagonalError cvt_core.py:176-189        */
+    SCVT_ERR_NON_DESCENT = 6,         /* NonDescentError          optimizer.py:165-166       */
+    SCVT_ERR_LINE_SEARCH = 7,         /* LineSearchFailure        optimizer.py:190-192       */
+    SCVT_ERR_POLE_AMBIGUITY = 8,      /* PoleAmbiguityError       density.py:82-90           */
+    SCVT_ERR_CONFIG = 9,              /* ConfigError / ValueError                             */
+    SCVT_ERR_CAPACITY = 10,           /* n > n_max, valence/polygon capacity exceeded          */
+    SCVT_ERR_CUDA = 11,               /* CUDA runtime failure                                  */
+    SCVT_ERR_NCCL = 12                /* collective failure (multi-GPU plumbing)               */
+};
+
+/* density kinds (density.py:116-129 + BASELINE tanh^4 variants, DECISIONS.md D3/D4) */
+enum scvt_density_kind {
+    SCVT_DENSITY_CONST = 0,   /* rho = 1                                                      */
+    SCVT_DENSITY_X3 = 1,      /* (1-g) z^4 + g                                                */
+    SCVT_DENSITY_X16 = 2,     /* reference tanh plateau, elliptical distance (density.py:100) */
+    SCVT_DENSITY_TANH = 3,    /* reference tanh plateau, geodesic distance (x64 / 'tanh')     */
+    SCVT_DENSITY_TANH4 = 4,   /* (((1-g)/2)(tanh((b-d)/a)+1)+g)^4, one centre                 */
+    SCVT_DENSITY_TANH4X2 = 5  /* same, d = min over two centres                               */
+};
+
+typedef struct scvt_config {
+    int32_t density_kind;     /* enum scvt_density_kind                                        */
+    int32_t measure;          /* 0 = "flat", 1 = "sphere"  (cvt_core.py:67-92)                 */
+    double gamma, beta, alpha;
+    double center[6];         /* one or two unit centres (x,y,z)                               */
+    double w_lon, w_lat;      /* x16 only                                                      */
+    int32_t n_nodes;          /* composite rule size = 4^depth * Q  (<= SCVT_MAX_NODES)        */
+    int32_t lbfgs_m;          /* correction pairs kept (optimizer.py:79-90)                    */
+    const double* node_l1;    /* HOST arrays [n_nodes]: barycentric (l1, l2) of each composite */
+    const double* node_l2;    /*   node relative to the fan sub-triangle (v0, v1, v2) and its  */
+    const double* node_w;     /*   weight  w_q / 4^depth  (geometry.py:142-185 + 383-407)      */
+} scvt_config;
+
+#define SCVT_MAX_NODES 2304
+#define SCVT_MAX_DEGREE 32
+
+typedef struct scvt_ctx scvt_ctx;
+
+/* lifecycle ---------------------------------------------------------------------------- */
+int scvt_create(scvt_ctx** ctx, int device, int64_t n_max, const scvt_config* cfg);
+int scvt_destroy(scvt_ctx* ctx);
+const char* scvt_last_error(const scvt_ctx* ctx);
+/* cudaStream_t as void*; NULL = legacy default stream */
+int scvt_set_stream(scvt_ctx* ctx, void* stream);
+/* library version string */
+const char* scvt_version(void);
+
+/* triangulation ------------------------------------------------------------------------
+ * Replaces convex_hull_delaunay (delaunay.py:181-202) incl. _ccw_outward/_canonical_sort
+ * (133-147, 172-178): writes the canonical (2n-4, 3) int64 triangle list (CCW seen from
+ * outside, min-ID first, lexicographically sorted) and one flag byte per triangle
+ * (1 = an edge of it failed the FP64 in-circle filter: cocircular candidate).
+ * stats_host[0..5] = {triangle count, flagged triangles, max valence, filter-undecided
+ * directed edges, symbolic-perturbation tie-breaks, max candidate passes of one cell}. */
+int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out,
+                     uint8_t* flags_out, int64_t* stats_host);
+
+/* evaluation ---------------------------------------------------------------------------
+ * Replaces MeshEvaluator.evaluate (pipeline.py:261-279) = triangulation + Voronoi fans
+ * (delaunay.py:337-380) + depth-d subdivision (383-407) + cell_quadrature
+ * (cvt_core.py:55-117) + gradient assembly.  Outputs (device): grad (n,3) =
+ * 2(c.z)z - 2c, first (n,3) = c, mass (n,) = m (may be NULL), lloyd_diag (n,) = 2 c.z.
+ * scalars_host[0..2] = {energy, grad_norm, obtuse triangle count}. */
+int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                  double* mass, double* lloyd_diag, double* scalars_host);
+
+/* Moments only over an externally supplied canonical triangulation (T,3) int64 — used by
+ * parity tests to isolate the quadrature from the triangulation. Same outputs as above. */
+int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n,
+                               const int64_t* triangles, int64_t t, double* grad,
+                               double* first, double* mass, double* lloyd_diag,
+                               double* scalars_host);
+
+/* optimizer vector algebra -------------------------------------------------------------
+ * CorrectionHistory (optimizer.py:79-114): ring of at most lbfgs_m (s, y) pairs held on
+ * the device inside ctx. */
+int scvt_history_clear(scvt_ctx* ctx);
+int scvt_history_size(scvt_ctx* ctx, int32_t* size_host);
+/* gamma = y.s / y.y of the newest pair, 1 when empty (optimizer.py:109-114); host out */
+int scvt_history_gamma(scvt_ctx* ctx, double* gamma_host);
+/* s = z_new - z_old, y = g_new - g_old; push unless y.s <= 1e-14 |s||y| (optimizer.py:98-104,
+ * 351-353).  pushed_host = 1/0; movement_host = max |z_new - z_old| (optimizer.py:355). */
+int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new,
+                      const double* g_old, const double* g_new, int64_t n,
+                      int32_t* pushed_host, double* movement_host);
+/* two_loop_direction (optimizer.py:147-167): q = -H g with h0 = diag(1/lloyd_diag) blockwise
+ * when inv_diag_src != NULL (LloydDiagonal, optimizer.py:127-134; the ARRAY passed is
+ * lloyd_diag itself, inverted on the fly), else gamma*I (GammaIdentity, 117-124).
+ * qg_host = q.g (caller raises NonDescentError when >= 0). */
+int scvt_lbfgs_direction(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
+                         double gamma, int64_t n, double* q_out, double* qg_host);
+/* q3 = q - (q.z) z rowwise (optimizer.py:322-323); dphi0_host = sum g.q3 (333) */
+int scvt_tangent_project(scvt_ctx* ctx, const double* q, const double* z, const double* g,
+                         int64_t n, double* q3_out, double* dphi0_host);
+/* v = z + alpha q3; norms = |v|; zt = v / norms (optimizer.py:325-328) */
+int scvt_trial_point(scvt_ctx* ctx, const double* z, const double* q3, double alpha, int64_t n,
+                     double* zt_out, double* norms_out);
+/* d = sum g . (q3 / norms) (optimizer.py:330); host out */
+int scvt_directional_derivative(scvt_ctx* ctx, const double* g, const double* q3,
+                                const double* norms, int64_t n, double* d_host);
+/* lloyd_step (optimizer.py:240-246): z = c / |c|, SCVT_ERR_CENTROID_AT_ORIGIN if |c| <= 1e-12 */
+int scvt_lloyd_step(scvt_ctx* ctx, const double* first, int64_t n, double* z_out);
+/* min over v[0..len) (host out) — nonpositive-diagonal test (cvt_core.py:184) */
+int scvt_min(scvt_ctx* ctx, const double* v, int64_t len, double* min_host);
+/* max |a - b| over len doubles (host out) — movement of the Lloyd method (optimizer.py:355) */
+int scvt_max_abs_diff(scvt_ctx* ctx, const double* a, const double* b, int64_t len,
+                      double* max_host);
+/* y = a * x over len doubles (the -gamma g fallback, optimizer.py:321) */
+int scvt_scale(scvt_ctx* ctx, double a, const double* x, int64_t len, double* y);
+/* normalise rows of (n,3) in place (optimizer.py:290) */
+int scvt_normalize_rows(scvt_ctx* ctx, double* z, int64_t n);
+
+/* launches of library kernels since the context was created (bench accounting) */
+int64_t scvt_launch_count(const scvt_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCVT_B200_H */

@@ -1,0 +1,144 @@
+"""ctypes binding of the C ABI in include/scvt_b200.h (libscvtb200.so, built in-tree).
+
+There is no CPU fallback: if the shared library is missing or a CUDA device is absent, the
+first call raises `DeviceError` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import STATUS_ERRORS, DeviceError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libscvtb200.so"
+LIB_PATH = os.path.join(HERE, LIB_NAME)
+
+_c_int_p = ctypes.POINTER(ctypes.c_int)
+_c_i32_p = ctypes.POINTER(ctypes.c_int32)
+_c_i64_p = ctypes.POINTER(ctypes.c_int64)
+_c_dbl_p = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+class ScvtConfig(ctypes.Structure):
+    """Mirror of `scvt_config` (include/scvt_b200.h)."""
+
+    _fields_ = [
+        ("density_kind", ctypes.c_int32),
+        ("measure", ctypes.c_int32),
+        ("gamma", ctypes.c_double),
+        ("beta", ctypes.c_double),
+        ("alpha", ctypes.c_double),
+        ("center", ctypes.c_double * 6),
+        ("w_lon", ctypes.c_double),
+        ("w_lat", ctypes.c_double),
+        ("n_nodes", ctypes.c_int32),
+        ("lbfgs_m", ctypes.c_int32),
+        ("node_l1", _c_dbl_p),
+        ("node_l2", _c_dbl_p),
+        ("node_w", _c_dbl_p),
+    ]
+
+
+# every exported symbol with (restype, argtypes); tests check the .so exports exactly these
+SIGNATURES = {
+    "scvt_create": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, ctypes.c_int64,
+                                   ctypes.POINTER(ScvtConfig)]),
+    "scvt_destroy": (ctypes.c_int, [_vp]),
+    "scvt_last_error": (ctypes.c_char_p, [_vp]),
+    "scvt_set_stream": (ctypes.c_int, [_vp, _vp]),
+    "scvt_version": (ctypes.c_char_p, []),
+    "scvt_triangulate": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _c_i64_p]),
+    "scvt_evaluate": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _c_dbl_p]),
+    "scvt_evaluate_on_triangles": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                                                  _vp, _vp, _vp, _vp, _c_dbl_p]),
+    "scvt_history_clear": (ctypes.c_int, [_vp]),
+    "scvt_history_size": (ctypes.c_int, [_vp, _c_i32_p]),
+    "scvt_history_gamma": (ctypes.c_int, [_vp, _c_dbl_p]),
+    "scvt_history_push": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _c_i32_p,
+                                         _c_dbl_p]),
+    "scvt_lbfgs_direction": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int64, _vp,
+                                            _c_dbl_p]),
+    "scvt_tangent_project": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp, _c_dbl_p]),
+    "scvt_trial_point": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int64, _vp,
+                                        _vp]),
+    "scvt_directional_derivative": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64,
+                                                   _c_dbl_p]),
+    "scvt_lloyd_step": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
+    "scvt_min": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _c_dbl_p]),
+    "scvt_max_abs_diff": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _c_dbl_p]),
+    "scvt_scale": (ctypes.c_int, [_vp, ctypes.c_double, _vp, ctypes.c_int64, _vp]),
+    "scvt_normalize_rows": (ctypes.c_int, [_vp, _vp, ctypes.c_int64]),
+    "scvt_launch_count": (ctypes.c_int64, [_vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str | None = None):
+    """Load (once) and return the CDLL with typed signatures.  Raises DeviceError if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or os.environ.get("SCVT_B200_LIB", LIB_PATH)
+        if not os.path.exists(p):
+            raise DeviceError(
+                f"{p} not found: build the CUDA library first "
+                "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+        lib = ctypes.CDLL(p)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, ctx=None, what: str = ""):
+    """Map a C status code onto the scvtmesh exception hierarchy."""
+    if rc == 0:
+        return
+    msg = ""
+    if ctx is not None:
+        try:
+            msg = load().scvt_last_error(ctx).decode(errors="replace")
+        except Exception:  # pragma: no cover - message retrieval must not mask the error
+            msg = ""
+    exc = STATUS_ERRORS.get(rc, DeviceError)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+def dptr(t) -> int:
+    """Device pointer of a torch tensor (or None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def make_config(density_params: dict, measure: str, l1: np.ndarray, l2: np.ndarray,
+                w: np.ndarray, lbfgs_m: int):
+    cfg = ScvtConfig()
+    cfg.density_kind = int(density_params["density_kind"])
+    if measure not in ("flat", "sphere"):
+        raise ValueError(f"unknown integration measure {measure!r}")
+    cfg.measure = 0 if measure == "flat" else 1
+    cfg.gamma = density_params["gamma"]
+    cfg.beta = density_params["beta"]
+    cfg.alpha = density_params["alpha"]
+    for k in range(6):
+        cfg.center[k] = float(density_params["center"][k])
+    cfg.w_lon = density_params["w_lon"]
+    cfg.w_lat = density_params["w_lat"]
+    cfg.n_nodes = len(w)
+    cfg.lbfgs_m = int(lbfgs_m)
+    keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (l1, l2, w)]
+    cfg.node_l1 = keep[0].ctypes.data_as(_c_dbl_p)
+    cfg.node_l2 = keep[1].ctypes.data_as(_c_dbl_p)
+    cfg.node_w = keep[2].ctypes.data_as(_c_dbl_p)
+    return cfg, keep

@@ -1,0 +1,661 @@
+// scvt_device.cuh — __host__ __device__ building blocks of the SCVT hot path.
+//
+// Everything here is pure per-element arithmetic, written once and used by the sm_100a
+// kernels (scvt_kernels.cu).  The test-only host harness (tests/native/) compiles the same
+// functions for the CPU so the combinatorics can be exercised without a GPU; the shipped
+// library has no CPU path.
+//
+// Reference citations are /root/reference/pkg/src/scvtmesh/<file>.py:<line>.
+#pragma once
+
+#include <stdint.h>
+#include <math.h>
+
+#ifdef __CUDACC__
+#define SCVT_HD __host__ __device__ __forceinline__
+#else
+#define SCVT_HD inline
+#endif
+
+namespace scvt {
+
+// ------------------------------------------------------------------ status bits (device)
+enum : int {
+    ST_OK = 0,
+    ST_DUPLICATE = 1 << 0,        // two identical generators -> InsufficientPointsError
+    ST_UNBOUNDED = 1 << 1,        // cell reaches the gnomonic hemisphere limit
+    ST_POLY_OVERFLOW = 1 << 2,    // clip polygon exceeded MAXV edges
+    ST_DEG_OVERFLOW = 1 << 3,     // valence exceeded SCVT_MAX_DEGREE
+    ST_INCONSISTENT = 1 << 4,     // cycles of adjacent cells disagree (not a manifold)
+    ST_NOT_DELAUNAY = 1 << 5,     // certified non-locally-Delaunay edge
+    ST_EULER = 1 << 6,            // sum of valences != 6n - 12
+    ST_POLE = 1 << 7,             // x16 density evaluated within 1e-9 of a pole
+    ST_DEGENERATE_TRI = 1 << 8,   // zero-normal triangle in the fan construction
+    ST_CENTROID = 1 << 9,         // |c| <= 1e-12 in a Lloyd step
+};
+
+constexpr int MAXV = 64;          // polygon edges while clipping
+constexpr int MAXDEG = 32;        // stored valence (== SCVT_MAX_DEGREE)
+constexpr double BOX_L = 1.0e4;   // initial gnomonic box half-width (cell < ~89.99 deg)
+
+// ------------------------------------------------------------------ small vector helpers
+struct V3 { double x, y, z; };
+
+SCVT_HD V3 v3(double x, double y, double z) { V3 r; r.x = x; r.y = y; r.z = z; return r; }
+SCVT_HD V3 add(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
+SCVT_HD V3 sub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+SCVT_HD V3 mul(V3 a, double s) { return v3(a.x * s, a.y * s, a.z * s); }
+SCVT_HD double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+SCVT_HD V3 cross(V3 a, V3 b) {
+    return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+SCVT_HD V3 load3(const double* p, int64_t i) { return v3(p[3 * i], p[3 * i + 1], p[3 * i + 2]); }
+
+SCVT_HD double rsqrt_d(double x) {
+#ifdef __CUDA_ARCH__
+    return rsqrt(x);
+#else
+    return 1.0 / sqrt(x);
+#endif
+}
+
+// numpy's np.linalg.norm of a 3-vector is sqrt(x*x + y*y + z*z) evaluated as a dot product;
+// we use the same expression.
+SCVT_HD double norm3(V3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+
+// ------------------------------------------------------------------ cube-map buckets
+// Face = dominant axis and sign; (u, v) = the other two coordinates over |dominant|;
+// equi-angular cell index so buckets have near-uniform solid angle.  Bucketing is FP32:
+// range queries are conservative (angular margin + one-bucket widening) so the FP32
+// rounding of keys vs ranges can never drop a candidate.
+SCVT_HD int face_axes_b(int a) { return a == 0 ? 1 : 0; }
+SCVT_HD int face_axes_c(int a) { return a == 2 ? 1 : 2; }
+
+SCVT_HD int bucket_index_1d(float u, int G) {
+    float t = (atanf(u) * (float)(4.0 / M_PI) + 1.0f) * 0.5f * (float)G;
+    int k = (int)floorf(t);
+    return k < 0 ? 0 : (k >= G ? G - 1 : k);
+}
+
+SCVT_HD uint32_t bucket_key(V3 p, int G) {
+    double c[3] = {p.x, p.y, p.z};
+    double ax = fabs(p.x), ay = fabs(p.y), az = fabs(p.z);
+    int a = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
+    int sgn = c[a] >= 0.0 ? 0 : 1;
+    double den = fabs(c[a]);
+    float u = (float)(c[face_axes_b(a)] / den), v = (float)(c[face_axes_c(a)] / den);
+    int face = 2 * a + sgn;
+    return (uint32_t)((face * G + bucket_index_1d(u, G)) * G + bucket_index_1d(v, G));
+}
+
+// Per-axis coordinate bounds of the spherical cap {y : |y - p| <= r} (FP32, conservative).
+struct CapBox { float lo[3], hi[3]; };
+
+SCVT_HD CapBox cap_box(V3 p, double r) {
+    CapBox b;
+    float th = 2.0f * asinf(fminf(1.0f, 0.5f * (float)r)) + 2e-4f;
+    float c[3] = {(float)p.x, (float)p.y, (float)p.z};
+    const float PI = 3.14159265358979f;
+    for (int k = 0; k < 3; ++k) {
+        float ck = fmaxf(-1.0f, fminf(1.0f, c[k]));
+        float ang = acosf(ck);
+        float a_lo = ang - th, a_hi = ang + th;
+        b.hi[k] = a_lo <= 0.0f ? 1.0f : cosf(a_lo) + 1e-5f;
+        b.lo[k] = a_hi >= PI ? -1.0f : cosf(a_hi) - 1e-5f;
+    }
+    return b;
+}
+
+// Conservative bucket rectangle of the cap on face `face`; false if the cap misses it.
+SCVT_HD bool cap_face_range(const CapBox& cb, int face, int G, int* iu0, int* iu1, int* iv0,
+                            int* iv1) {
+    int a = face >> 1;
+    bool neg = face & 1;
+    float s_lo = neg ? -cb.hi[a] : cb.lo[a];
+    float s_hi = neg ? -cb.lo[a] : cb.hi[a];
+    const float inv_sqrt3 = 0.57735026f - 1e-4f;
+    if (s_hi < inv_sqrt3) return false;
+    float t_lo = fmaxf(s_lo, inv_sqrt3), t_hi = s_hi;
+    int b = face_axes_b(a), cc = face_axes_c(a);
+    float umin = fminf(cb.lo[b] / t_lo, cb.lo[b] / t_hi), umax = fmaxf(cb.hi[b] / t_lo, cb.hi[b] / t_hi);
+    float vmin = fminf(cb.lo[cc] / t_lo, cb.lo[cc] / t_hi), vmax = fmaxf(cb.hi[cc] / t_lo, cb.hi[cc] / t_hi);
+    umin = fmaxf(umin, -1.0f); umax = fminf(umax, 1.0f);
+    vmin = fmaxf(vmin, -1.0f); vmax = fminf(vmax, 1.0f);
+    int a0 = bucket_index_1d(umin, G) - 1, a1 = bucket_index_1d(umax, G) + 1;
+    int b0 = bucket_index_1d(vmin, G) - 1, b1 = bucket_index_1d(vmax, G) + 1;
+    *iu0 = a0 < 0 ? 0 : a0; *iu1 = a1 >= G ? G - 1 : a1;
+    *iv0 = b0 < 0 ? 0 : b0; *iv1 = b1 >= G ? G - 1 : b1;
+    return true;
+}
+
+// ------------------------------------------------------------------ predicates
+// insphere on the unit sphere == orient3d: for CCW-outward (o, a, b), point c lies inside
+// the circumcircle of (o, a, b) iff det[a-o, b-o, c-o] > 0.  Three tiers:
+//   1. FP64 static filter (decides almost always);
+//   2. double-double evaluation (error ~1e-30 of the permanent);
+//   3. exact ties -> Simulation of Simplicity: the lowest-index point of the four is
+//      pushed radially outward by an infinitesimal, i.e. treated as inside the circle of the
+//      other three.  Every cell that meets the same four points therefore takes the same
+//      decision, which keeps the cycles of a cocircular quad mutually consistent.
+struct DD { double hi, lo; };
+
+SCVT_HD DD dd_two_sum(double a, double b) {
+    double s = a + b;
+    double bb = s - a;
+    DD r; r.hi = s; r.lo = (a - (s - bb)) + (b - bb);
+    return r;
+}
+SCVT_HD DD dd_two_prod(double a, double b) {
+    double p = a * b;
+    DD r; r.hi = p; r.lo = fma(a, b, -p);
+    return r;
+}
+SCVT_HD DD dd_norm(double hi, double lo) {
+    double s = hi + lo;
+    DD r; r.hi = s; r.lo = lo - (s - hi);
+    return r;
+}
+SCVT_HD DD dd_add(DD a, DD b) {
+    DD s = dd_two_sum(a.hi, b.hi);
+    DD t = dd_two_sum(a.lo, b.lo);
+    double lo = s.lo + t.hi;
+    DD u = dd_norm(s.hi, lo);
+    return dd_norm(u.hi, u.lo + t.lo);
+}
+SCVT_HD DD dd_neg(DD a) { a.hi = -a.hi; a.lo = -a.lo; return a; }
+SCVT_HD DD dd_mul(DD a, DD b) {
+    DD p = dd_two_prod(a.hi, b.hi);
+    double lo = p.lo + (a.hi * b.lo + a.lo * b.hi);
+    return dd_norm(p.hi, lo);
+}
+SCVT_HD DD dd_diff(double a, double b) { return dd_two_sum(a, -b); }
+
+// det[a-o, b-o, c-o] in double-double; *perm gets the permanent (magnitude scale)
+SCVT_HD DD orient_dd(V3 o, V3 a, V3 b, V3 c, double* perm) {
+    DD ax = dd_diff(a.x, o.x), ay = dd_diff(a.y, o.y), az = dd_diff(a.z, o.z);
+    DD bx = dd_diff(b.x, o.x), by = dd_diff(b.y, o.y), bz = dd_diff(b.z, o.z);
+    DD cx = dd_diff(c.x, o.x), cy = dd_diff(c.y, o.y), cz = dd_diff(c.z, o.z);
+    DD m1 = dd_add(dd_mul(by, cz), dd_neg(dd_mul(bz, cy)));
+    DD m2 = dd_add(dd_mul(bz, cx), dd_neg(dd_mul(bx, cz)));
+    DD m3 = dd_add(dd_mul(bx, cy), dd_neg(dd_mul(by, cx)));
+    *perm = fabs(ax.hi) * (fabs(by.hi * cz.hi) + fabs(bz.hi * cy.hi)) +
+            fabs(ay.hi) * (fabs(bz.hi * cx.hi) + fabs(bx.hi * cz.hi)) +
+            fabs(az.hi) * (fabs(bx.hi * cy.hi) + fabs(by.hi * cx.hi));
+    return dd_add(dd_add(dd_mul(ax, m1), dd_mul(ay, m2)), dd_mul(az, m3));
+}
+
+// FP64 value + static filter; returns sign or 0 when undecided
+SCVT_HD int orient_filter(V3 o, V3 a, V3 b, V3 c) {
+    V3 ao = sub(a, o), bo = sub(b, o), co = sub(c, o);
+    double m1 = bo.y * co.z, m2 = bo.z * co.y;
+    double m3 = bo.z * co.x, m4 = bo.x * co.z;
+    double m5 = bo.x * co.y, m6 = bo.y * co.x;
+    double det = ao.x * (m1 - m2) + ao.y * (m3 - m4) + ao.z * (m5 - m6);
+    double perm = fabs(ao.x) * (fabs(m1) + fabs(m2)) + fabs(ao.y) * (fabs(m3) + fabs(m4)) +
+                  fabs(ao.z) * (fabs(m5) + fabs(m6));
+    const double eps = 1.1102230246251565e-16;   // 2^-53
+    double bound = (16.0 * eps) * perm;          // differences carry rounding too
+    if (det > bound) return 1;
+    if (det < -bound) return -1;
+    return 0;
+}
+
+// Robust sign of det[a-o, b-o, c-o] with SoS tie-breaking; *tier = 0/1/2 (filter/dd/sos)
+SCVT_HD int orient_robust(V3 o, V3 a, V3 b, V3 c, int io, int ia, int ib, int ic, int* tier) {
+    int s = orient_filter(o, a, b, c);
+    if (s) { *tier = 0; return s; }
+    double perm;
+    DD d = orient_dd(o, a, b, c, &perm);
+    double v = d.hi + d.lo;
+    if (fabs(v) > 1e-28 * perm) { *tier = 1; return v > 0 ? 1 : -1; }
+    *tier = 2;
+    // push the lowest-index point radially outward (D is affine in each point)
+    const double f = 1.0 + 9.5367431640625e-07;   // 1 + 2^-20
+    int lo = io, which = 0;
+    if (ia < lo) { lo = ia; which = 1; }
+    if (ib < lo) { lo = ib; which = 2; }
+    if (ic < lo) { lo = ic; which = 3; }
+    if (which == 0) o = mul(o, f);
+    else if (which == 1) a = mul(a, f);
+    else if (which == 2) b = mul(b, f);
+    else c = mul(c, f);
+    d = orient_dd(o, a, b, c, &perm);
+    v = d.hi + d.lo;
+    return v > 0 ? 1 : (v < 0 ? -1 : 1);
+}
+
+// Legacy interface for the verification pass: sign with an "ambiguous" flag when the FP64
+// filter cannot decide (such edges are reported as flagged cocircular candidates).
+SCVT_HD int insphere_sign(V3 o, V3 a, V3 b, V3 c, bool* ambiguous) {
+    int s = orient_filter(o, a, b, c);
+    *ambiguous = s == 0;
+    if (s) return s;
+    double perm;
+    DD d = orient_dd(o, a, b, c, &perm);
+    double v = d.hi + d.lo;
+    return v > 0 ? 1 : (v < 0 ? -1 : 0);
+}
+
+// ------------------------------------------------------------------ Voronoi cell clipping
+// The spherical Voronoi cell of z_i is the cone {x : x.(z_j - z_i) <= 0 for all j}.  In the
+// gnomonic plane x = z_i + u1 e1 + u2 e2 each neighbour contributes the half-plane
+// u.d <= |d|^2 / 2 with d = z_j - z_i (well conditioned for close pairs).  The polygon's
+// edge labels in CCW order are the Delaunay neighbours of i in CCW order seen from outside,
+// so (i, n_t, n_{t+1}) are exactly the CCW-outward hull facets at i (the triangles Qhull
+// returns through convex_hull_delaunay, delaunay.py:181-202).  A polygon vertex between
+// edges labelled l and r is the circumcentre of (i, l, r); whether a new neighbour j cuts it
+// is the in-circle test of j against (i, l, r), decided by `orient_robust` whenever the
+// FP64 value of the half-plane test falls inside its rounding band.
+struct Poly {
+    int n;
+    double ax[MAXV], ay[MAXV], b[MAXV];   // edge k line: ax*u + ay*v <= b
+    double vx[MAXV], vy[MAXV];            // vertex k = start of edge k
+    int lab[MAXV];                        // neighbour id, -1 for the initial box
+};
+
+SCVT_HD void poly_init(Poly& P) {
+    const double L = BOX_L;
+    // CCW: bottom (v >= -L), right (u <= L), top (v <= L), left (u >= -L)
+    P.n = 4;
+    P.ax[0] = 0;  P.ay[0] = -1; P.b[0] = L; P.vx[0] = -L; P.vy[0] = -L; P.lab[0] = -1;
+    P.ax[1] = 1;  P.ay[1] = 0;  P.b[1] = L; P.vx[1] = L;  P.vy[1] = -L; P.lab[1] = -1;
+    P.ax[2] = 0;  P.ay[2] = 1;  P.b[2] = L; P.vx[2] = L;  P.vy[2] = L;  P.lab[2] = -1;
+    P.ax[3] = -1; P.ay[3] = 0;  P.b[3] = L; P.vx[3] = -L; P.vy[3] = L;  P.lab[3] = -1;
+}
+
+SCVT_HD void line_meet(double a1x, double a1y, double b1, double a2x, double a2y, double b2,
+                       double* x, double* y) {
+    double det = a1x * a2y - a1y * a2x;
+    double inv = 1.0 / det;
+    *x = (b1 * a2y - b2 * a1y) * inv;
+    *y = (a1x * b2 - a2x * b1) * inv;
+}
+
+// squared chord between z_i and the sphere point above gnomonic vertex (x, y)
+SCVT_HD double vertex_chord2(double x, double y) {
+    double q = x * x + y * y;
+    double s = sqrt(1.0 + q);
+    return 2.0 * q / (s * (s + 1.0));
+}
+
+struct ClipCtx {
+    const double* z;   // (n,3) generator coordinates by id
+    V3 zi;
+    int i;
+    int tie_breaks;    // count of SoS decisions
+};
+
+// Clip by a.u <= b (label j, position zj).  Returns 0 = unchanged, 1 = clipped, <0 = error.
+SCVT_HD int poly_clip(Poly& P, Poly& T, double ax, double ay, double b, int j, V3 zj,
+                      ClipCtx& cc) {
+    int n = P.n;
+    bool out[MAXV];
+    int nout = 0;
+    for (int k = 0; k < n; ++k) {
+        double t1 = ax * P.vx[k], t2 = ay * P.vy[k];
+        double s = t1 + t2 - b;
+        double tol = 1e-9 * (fabs(t1) + fabs(t2) + b);
+        bool o;
+        if (s > tol) o = true;
+        else if (s < -tol) o = false;
+        else {
+            int km = k == 0 ? n - 1 : k - 1;
+            int l = P.lab[km], r = P.lab[k];
+            if (l >= 0 && r >= 0) {
+                int tier;
+                o = orient_robust(cc.zi, load3(cc.z, l), load3(cc.z, r), zj, cc.i, l, r, j,
+                                  &tier) > 0;
+                cc.tie_breaks += tier == 2;
+            } else {
+                o = s > 0.0;
+            }
+        }
+        out[k] = o;
+        nout += o;
+    }
+    if (nout == 0) return 0;
+    if (nout == n) return -1;                 // empty: cannot happen for a true cell
+    int first = -1, last = -1, runs = 0;
+    for (int k = 0; k < n; ++k) {
+        int km = k == 0 ? n - 1 : k - 1;
+        int kp = k == n - 1 ? 0 : k + 1;
+        if (out[k] && !out[km]) { first = k; ++runs; }
+        if (out[k] && !out[kp]) last = k;
+    }
+    if (runs != 1 || first < 0 || last < 0) return -2;   // non-convex decision pattern
+    int ein = first == 0 ? n - 1 : first - 1;    // edge entering the outside run
+    double Ax, Ay, Bx, By;
+    line_meet(P.ax[ein], P.ay[ein], P.b[ein], ax, ay, b, &Ax, &Ay);
+    line_meet(ax, ay, b, P.ax[last], P.ay[last], P.b[last], &Bx, &By);
+    // surviving edges: last, last+1, ..., ein (cyclic), then the new edge
+    int m = 0;
+    int k = last;
+    while (true) {
+        if (m >= MAXV - 1) return -3;
+        T.ax[m] = P.ax[k]; T.ay[m] = P.ay[k]; T.b[m] = P.b[k]; T.lab[m] = P.lab[k];
+        if (k == last) { T.vx[m] = Bx; T.vy[m] = By; }
+        else { T.vx[m] = P.vx[k]; T.vy[m] = P.vy[k]; }
+        ++m;
+        if (k == ein) break;
+        k = k == n - 1 ? 0 : k + 1;
+    }
+    T.ax[m] = ax; T.ay[m] = ay; T.b[m] = b; T.lab[m] = j; T.vx[m] = Ax; T.vy[m] = Ay;
+    ++m;
+    T.n = m;
+    return 1;
+}
+
+SCVT_HD double poly_max_chord2(const Poly& P, bool* has_box) {
+    double r2 = 0.0;
+    bool box = false;
+    for (int k = 0; k < P.n; ++k) {
+        r2 = fmax(r2, vertex_chord2(P.vx[k], P.vy[k]));
+        box |= P.lab[k] < 0;
+    }
+    *has_box = box;
+    return r2;
+}
+
+// Tangent frame at z (seed = least aligned axis; e1 x e2 = z, right-handed).
+SCVT_HD void tangent_frame(V3 z, V3* e1, V3* e2) {
+    double ax = fabs(z.x), ay = fabs(z.y), az = fabs(z.z);
+    V3 seed = (ax <= ay && ax <= az) ? v3(1, 0, 0) : (ay <= az ? v3(0, 1, 0) : v3(0, 0, 1));
+    V3 t = cross(z, seed);
+    t = mul(t, 1.0 / norm3(t));
+    *e1 = t;
+    *e2 = cross(z, t);
+}
+
+struct GridView {
+    const double* zs;       // (n,4) positions sorted by bucket (x,y,z,pad)
+    const int* ids;         // (n,) original id of sorted slot
+    const int* start;       // (6G^2+1) bucket start offsets into the sorted arrays
+    const double* z;        // (n,3) positions by id
+    int G;
+    int64_t n;
+};
+
+constexpr int CAND = 48;    // nearest-first candidate list per pass
+
+struct CellStats { int rounds; int passes; int tie_breaks; };
+
+// Build the Voronoi cell of generator i by nearest-first half-plane clipping with a
+// security-radius certificate: a point j can cut the cell only if |z_j - z_i| < 2R with R
+// the largest vertex chord, so once every point within r >= 2R is processed the cell is
+// final.  Writes the CCW neighbour cycle rotated so its smallest id leads; returns the
+// valence (>0) or -status.
+SCVT_HD int build_cell(const GridView& g, int i, V3 zi, int* nbr_out, CellStats* st,
+                       Poly& P, Poly& T) {
+    V3 e1, e2;
+    tangent_frame(zi, &e1, &e2);
+    poly_init(P);
+    Poly* cur = &P;
+    Poly* tmp = &T;
+    ClipCtx cc;
+    cc.z = g.z; cc.zi = zi; cc.i = i; cc.tie_breaks = 0;
+    uint32_t key = bucket_key(zi, g.G);
+    int cnt = g.start[key + 1] - g.start[key];
+    double area_b = 4.0 * M_PI / (6.0 * (double)g.G * (double)g.G);
+    double h = sqrt(area_b / (double)(cnt > 0 ? cnt : 1));
+    double r2 = 9.0 * h * h;                  // first pass radius 3h
+    if (r2 > 4.0) r2 = 4.0000001;
+    double lo_c2 = -1.0;                      // exclusive lower bound (c2, id)
+    int lo_id = 0x7fffffff;
+    double R2 = 8.0;                          // current max vertex chord^2 (box => all)
+    bool box = true;
+    int status = 0;
+    int rounds = 0, passes = 0;
+    double cd[CAND];
+    int cid[CAND], cp[CAND];
+    while (true) {
+        ++passes;
+        if (passes > 4096) { status |= ST_POLY_OVERFLOW; break; }
+        int m = 0;
+        bool overflow = false;
+        double lim = 4.0 * R2 * (1.0 + 1e-12);
+        CapBox cb = cap_box(zi, sqrt(r2));
+        for (int face = 0; face < 6; ++face) {
+            int iu0, iu1, iv0, iv1;
+            if (!cap_face_range(cb, face, g.G, &iu0, &iu1, &iv0, &iv1)) continue;
+            for (int iu = iu0; iu <= iu1; ++iu) {
+                int rowbase = (face * g.G + iu) * g.G;
+                int p0 = g.start[rowbase + iv0], p1 = g.start[rowbase + iv1 + 1];
+                for (int p = p0; p < p1; ++p) {
+                    int j = g.ids[p];
+                    if (j == i) continue;
+                    const double* q = g.zs + 4 * (int64_t)p;
+                    double dx = q[0] - zi.x, dy = q[1] - zi.y, dz = q[2] - zi.z;
+                    double c2 = dx * dx + dy * dy + dz * dz;
+                    if (c2 > r2 || c2 >= lim) continue;
+                    if (c2 < lo_c2 || (c2 == lo_c2 && j <= lo_id)) continue;
+                    if (c2 == 0.0) { status |= ST_DUPLICATE; continue; }
+                    // insert into the sorted list (key = (c2, j))
+                    if (m == CAND) {
+                        if (c2 > cd[m - 1] || (c2 == cd[m - 1] && j > cid[m - 1])) {
+                            overflow = true;
+                            continue;
+                        }
+                        overflow = true;
+                        --m;
+                    }
+                    int t = m++;
+                    while (t > 0 && (cd[t - 1] > c2 || (cd[t - 1] == c2 && cid[t - 1] > j))) {
+                        cd[t] = cd[t - 1]; cid[t] = cid[t - 1]; cp[t] = cp[t - 1];
+                        --t;
+                    }
+                    cd[t] = c2; cid[t] = j; cp[t] = p;
+                }
+            }
+        }
+        bool early = false;
+        for (int t = 0; t < m; ++t) {
+            if (cd[t] >= 4.0 * R2 * (1.0 + 1e-12)) { early = true; break; }
+            const double* q = g.zs + 4 * (int64_t)cp[t];
+            V3 zj = v3(q[0], q[1], q[2]);
+            V3 d = sub(zj, zi);
+            int rc = poly_clip(*cur, *tmp, dot(d, e1), dot(d, e2), 0.5 * cd[t], cid[t], zj, cc);
+            if (rc < 0) { status |= ST_POLY_OVERFLOW; break; }
+            if (rc == 1) {
+                Poly* sw = cur; cur = tmp; tmp = sw;
+                R2 = poly_max_chord2(*cur, &box);
+                if (box) R2 = 8.0;
+            }
+        }
+        if (status) break;
+        if (overflow && !early) {
+            // dense neighbourhood of a large cell: sweep the rest of the range unsorted
+            ++passes;
+            double klo = cd[m - 1];
+            int kid = cid[m - 1];
+            for (int face = 0; face < 6 && !status; ++face) {
+                int iu0, iu1, iv0, iv1;
+                if (!cap_face_range(cb, face, g.G, &iu0, &iu1, &iv0, &iv1)) continue;
+                for (int iu = iu0; iu <= iu1 && !status; ++iu) {
+                    int rowbase = (face * g.G + iu) * g.G;
+                    int p0 = g.start[rowbase + iv0], p1 = g.start[rowbase + iv1 + 1];
+                    for (int p = p0; p < p1; ++p) {
+                        int j = g.ids[p];
+                        if (j == i) continue;
+                        const double* q = g.zs + 4 * (int64_t)p;
+                        V3 zj = v3(q[0], q[1], q[2]);
+                        V3 d = sub(zj, zi);
+                        double c2 = dot(d, d);
+                        if (c2 > r2 || c2 >= 4.0 * R2 * (1.0 + 1e-12)) continue;
+                        if (c2 < klo || (c2 == klo && j <= kid)) continue;
+                        if (c2 == 0.0) { status |= ST_DUPLICATE; continue; }
+                        int rc = poly_clip(*cur, *tmp, dot(d, e1), dot(d, e2), 0.5 * c2, j, zj, cc);
+                        if (rc < 0) { status |= ST_POLY_OVERFLOW; break; }
+                        if (rc == 1) {
+                            Poly* sw = cur; cur = tmp; tmp = sw;
+                            R2 = poly_max_chord2(*cur, &box);
+                            if (box) R2 = 8.0;
+                        }
+                    }
+                }
+            }
+            if (status) break;
+        }
+        ++rounds;
+        if (r2 >= 4.0) {
+            if (box) status |= ST_UNBOUNDED;
+            break;
+        }
+        if (!box && 4.0 * R2 * (1.0 + 1e-9) <= r2) break;   // security radius certified
+        lo_c2 = r2;
+        lo_id = 0x7fffffff;
+        double want = box ? 4.0 * r2 : 4.0 * R2 * (1.0 + 1e-9);
+        r2 = want >= 4.0 ? 4.0000001 : want;
+    }
+    st->rounds = rounds;
+    st->passes = passes;
+    st->tie_breaks = cc.tie_breaks;
+    if (status) return -status;
+    int n = cur->n;
+    if (n > MAXDEG) return -ST_DEG_OVERFLOW;
+    int lead = 0;
+    for (int k = 1; k < n; ++k)
+        if (cur->lab[k] < cur->lab[lead]) lead = k;
+    for (int k = 0; k < n; ++k) {
+        int kk = lead + k;
+        if (kk >= n) kk -= n;
+        nbr_out[k] = cur->lab[kk];
+    }
+    return n;
+}
+
+// ------------------------------------------------------------------ density
+enum DensityKind { DEN_CONST = 0, DEN_X3 = 1, DEN_X16 = 2, DEN_TANH = 3, DEN_TANH4 = 4,
+                   DEN_TANH4X2 = 5 };
+
+struct DensityParams {
+    int kind;
+    double gamma, beta, alpha;
+    double c0x, c0y, c0z, c1x, c1y, c1z;
+    double w_lon, w_lat;
+    double lat_c, lon_c, cos_lat_c, sin_lat_c;   // x16 centre (precomputed on host)
+};
+
+SCVT_HD double geodesic(V3 a, V3 b) { return atan2(norm3(cross(a, b)), dot(a, b)); }
+
+// density.py:116-129 with the BASELINE variants; y is unit.  *pole set for x16 near poles.
+template <int KIND>
+SCVT_HD double density_eval(const DensityParams& p, V3 y, int* pole) {
+    if (KIND == DEN_CONST) return 1.0;
+    if (KIND == DEN_X3) {
+        double z2 = y.z * y.z;
+        return (1.0 - p.gamma) * (z2 * z2) + p.gamma;
+    }
+    if (KIND == DEN_TANH4 || KIND == DEN_TANH4X2) {
+        double d = geodesic(y, v3(p.c0x, p.c0y, p.c0z));
+        if (KIND == DEN_TANH4X2) d = fmin(d, geodesic(y, v3(p.c1x, p.c1y, p.c1z)));
+        double t = 0.5 * (1.0 - p.gamma) * (tanh((p.beta - d) / p.alpha) + 1.0) + p.gamma;
+        double t2 = t * t;
+        return t2 * t2;
+    }
+    double d;
+    if (KIND == DEN_X16) {
+        // density.py:100-113 (elliptical distance)
+        double horiz = hypot(y.x, y.y);
+        if (horiz < 1e-9) *pole = 1;
+        double lat_x = atan2(y.z, horiz), lon_x = atan2(y.y, y.x);
+        double clx = cos(lat_x);
+        V3 x_ic = v3(clx * cos(p.lon_c), clx * sin(p.lon_c), sin(lat_x));
+        V3 x_ci = v3(p.cos_lat_c * cos(lon_x), p.cos_lat_c * sin(lon_x), p.sin_lat_c);
+        double dl = geodesic(y, x_ic) / p.w_lon, dt = geodesic(y, x_ci) / p.w_lat;
+        d = sqrt(dl * dl + dt * dt);
+    } else {
+        d = geodesic(y, v3(p.c0x, p.c0y, p.c0z));
+    }
+    return (tanh((p.beta - d) / p.alpha) + 1.0) / (2.0 * (1.0 - p.gamma)) + p.gamma;
+}
+
+// ------------------------------------------------------------------ fan geometry
+// One incidence = (generator i, Delaunay triangle (i, j, k) CCW).  The two fan
+// sub-triangles owned by i (delaunay.py:357-361) are (v_i, m_ij, oc) and (m_ki, v_i, oc);
+// this holds for every rotation of the canonical (a, b, c).
+struct SubTri { V3 v0, e1, e2; double area; };
+
+struct FanPair {
+    SubTri s[2];
+    int obtuse;       // 1 if any of the triangle's 6 signed areas is negative (counted at min id)
+    int degenerate;
+};
+
+SCVT_HD V3 planar_circumcenter(V3 a, V3 b, V3 c) {
+    // geometry.py:105-119
+    V3 ab = sub(b, a), ac = sub(c, a);
+    V3 n = cross(ab, ac);
+    double n2 = dot(n, n), ab2 = dot(ab, ab), ac2 = dot(ac, ac);
+    V3 num = add(mul(cross(n, ab), ac2), mul(cross(ac, n), ab2));
+    double den = 2.0 * n2;
+    return add(a, v3(num.x / den, num.y / den, num.z / den));
+}
+
+SCVT_HD double signed_area(V3 v0, V3 v1, V3 v2, V3 nhat) {
+    return 0.5 * dot(cross(sub(v1, v0), sub(v2, v0)), nhat);
+}
+
+SCVT_HD FanPair fan_pair(V3 vi, V3 vj, V3 vk, int i, int j, int k) {
+    // canonical rotation: min id first (delaunay.py:133-141); oc and n use that order
+    V3 va, vb, vc;
+    if (i < j && i < k) { va = vi; vb = vj; vc = vk; }
+    else if (j < k) { va = vj; vb = vk; vc = vi; }
+    else { va = vk; vb = vi; vc = vj; }
+    FanPair f;
+    V3 oc = planar_circumcenter(va, vb, vc);
+    V3 n = cross(sub(vb, va), sub(vc, va));
+    double nn = norm3(n);
+    f.degenerate = !(nn > 0.0);
+    n = v3(n.x / nn, n.y / nn, n.z / nn);
+    if (dot(n, add(add(va, vb), vc)) < 0.0) n = mul(n, -1.0);
+    V3 mij = mul(add(vi, vj), 0.5);
+    V3 mki = mul(add(vk, vi), 0.5);
+    f.s[0].v0 = vi;  f.s[0].e1 = sub(mij, vi); f.s[0].e2 = sub(oc, vi);
+    f.s[0].area = signed_area(vi, mij, oc, n);
+    f.s[1].v0 = mki; f.s[1].e1 = sub(vi, mki); f.s[1].e2 = sub(oc, mki);
+    f.s[1].area = signed_area(mki, vi, oc, n);
+    // obtuse flag for the whole triangle (delaunay.py:366-369): recompute all six areas
+    V3 mjk = mul(add(vj, vk), 0.5);
+    double a2 = signed_area(mij, vj, oc, n), a3 = signed_area(vj, mjk, oc, n);
+    double a4 = signed_area(mjk, vk, oc, n), a5 = signed_area(vk, mki, oc, n);
+    f.obtuse = (f.s[0].area < 0) | (f.s[1].area < 0) | (a2 < 0) | (a3 < 0) | (a4 < 0) | (a5 < 0);
+    return f;
+}
+
+// Accumulate sum_q w_q rho(y_q) {1, y_q, |y_q - z|^2} over the composite nodes of one
+// sub-triangle (cvt_core.py:80-100 with the subdivision of delaunay.py:383-407 folded into
+// the node table).  acc = {m, cx, cy, cz, E}.
+template <int KIND, bool SPHERE>
+SCVT_HD void subtri_moments(const SubTri& s, V3 z, const double* l1, const double* l2,
+                            const double* w, int nq, const DensityParams& dp, double* acc,
+                            int* pole) {
+    double m = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, e = 0.0;
+    double plane_d = 0.0;
+    if (SPHERE) {
+        V3 nv = cross(s.e1, s.e2);
+        double nn = norm3(nv);
+        if (nn == 0.0) nn = 1.0;
+        plane_d = fabs(dot(nv, s.v0) / nn);
+    }
+    for (int q = 0; q < nq; ++q) {
+        double a = l1[q], b = l2[q];
+        double x = s.v0.x + a * s.e1.x + b * s.e2.x;
+        double y = s.v0.y + a * s.e1.y + b * s.e2.y;
+        double zz = s.v0.z + a * s.e1.z + b * s.e2.z;
+        double r2 = x * x + y * y + zz * zz;
+        double inv = rsqrt_d(r2);
+        V3 yv = v3(x * inv, y * inv, zz * inv);
+        double rho = density_eval<KIND>(dp, yv, pole);
+        if (SPHERE) rho *= plane_d * inv * inv * inv;
+        double wr = w[q] * rho;
+        m += wr;
+        cx += wr * yv.x; cy += wr * yv.y; cz += wr * yv.z;
+        V3 d = sub(yv, z);
+        e += wr * dot(d, d);
+    }
+    acc[0] += s.area * m;
+    acc[1] += s.area * cx; acc[2] += s.area * cy; acc[3] += s.area * cz;
+    acc[4] += s.area * e;
+}
+
+}  // namespace scvt

@@ -1,0 +1,1198 @@
+// scvt_kernels.cu — sm_100a kernels + C ABI (include/scvt_b200.h) of the SCVT hot path.
+//
+// Pipeline of one evaluation (MeshEvaluator.evaluate, pipeline.py:261-279):
+//   k_bucket_keys -> CUB radix sort -> k_bucket_start -> k_gather_sorted   (cube-map grid)
+//   k_cells        per-generator Voronoi cell by half-plane clipping with a security-radius
+//                  certificate  (replaces Qhull, delaunay.py:181-202)
+//   k_verify       cycle consistency + local-Delaunay filter on every edge
+//   CUB scan -> k_fill_incidences   (one incidence per (generator, incident triangle))
+//   k_quad         fan sub-triangles + subdivided quadrature + density, FP64
+//                  (delaunay.py:337-407, cvt_core.py:55-117, density.py:116-129)
+//   k_gather       per-generator moments -> gradient epilogue (pipeline.py:265-279)
+//   k_reduce_*     deterministic fixed-shape reductions (energy, |g|^2, obtuse count)
+// plus the LBFGS vector kernels (optimizer.py:79-167, 322-355).
+//
+// All reductions use a fixed grid shape so results are bitwise reproducible run to run.
+
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "scvt_device.cuh"
+#include "scvt_cells_warp.cuh"
+#include "../../include/scvt_b200.h"
+
+using namespace scvt;
+
+namespace {
+
+constexpr int RED_BLOCKS = 296;      // 2 x 148 SMs: fixed reduction shape
+constexpr int RED_THREADS = 256;
+constexpr int VEC_THREADS = 256;
+constexpr int QUAD_THREADS = 128;
+constexpr int CELL_THREADS = 64;
+constexpr int MAX_SLOTS = 64;        // partial-sum slots
+
+// ------------------------------------------------------------------ grid kernels
+__global__ void k_bucket_keys(const double* __restrict__ z, int n, int G,
+                              uint32_t* __restrict__ keys, int* __restrict__ vals) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = bucket_key(load3(z, i), G);
+    vals[i] = i;
+}
+
+__global__ void k_bucket_start(const uint32_t* __restrict__ skeys, int n, int nb,
+                               int* __restrict__ start) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    // lower_bound of b in sorted keys
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (skeys[mid] < (uint32_t)b) lo = mid + 1; else hi = mid;
+    }
+    start[b] = lo;
+}
+
+__global__ void k_gather_sorted(const double* __restrict__ z, const int* __restrict__ ids, int n,
+                                double* __restrict__ zs) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int i = ids[p];
+    double4 v = make_double4(z[3 * (int64_t)i], z[3 * (int64_t)i + 1], z[3 * (int64_t)i + 2], 0.0);
+    reinterpret_cast<double4*>(zs)[p] = v;
+}
+
+// Fast path: one warp per generator (bucket order), polygon in registers.
+__global__ void __launch_bounds__(CELL_WARPS * 32)
+k_cells_warp(GridView g, int* __restrict__ nbr, int* __restrict__ deg, int* __restrict__ status,
+             int* __restrict__ stats) {
+    __shared__ double s_c2[CELL_WARPS][WCAND];
+    __shared__ int s_j[CELL_WARPS][WCAND];
+    __shared__ int s_p[CELL_WARPS][WCAND];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (int64_t)blockIdx.x * CELL_WARPS + w;
+    if (p >= g.n) return;   // warp-uniform
+    const int i = g.ids[p];
+    const double* q = g.zs + 4 * p;
+    V3 zi = v3(q[0], q[1], q[2]);
+    CellStats cs;
+    int d = build_cell_warp(g, i, zi, lane, s_c2[w], s_j[w], s_p[w], nbr + (int64_t)i * MAXDEG, &cs);
+    if (lane == 0) {
+        if (d == -ST_POLY_OVERFLOW) {
+            deg[i] = -1;                         // single-thread fallback below
+            atomicAdd(&stats[5], 1);
+        } else if (d < 0) {
+            atomicOr(status, -d);
+            deg[i] = 0;
+        } else {
+            deg[i] = d;
+            atomicMax(&stats[0], d);
+        }
+        if (cs.rounds > 1) atomicAdd(&stats[1], 1);
+        atomicMax(&stats[2], cs.passes);
+        if (cs.tie_breaks) atomicAdd(&stats[4], cs.tie_breaks);
+    }
+}
+
+// Fallback: one thread per generator the warp builder handed back (deg == -1).
+__global__ void __launch_bounds__(CELL_THREADS)
+k_cells(GridView g, int* __restrict__ nbr, int* __restrict__ deg, int* __restrict__ status,
+        int* __restrict__ stats) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= g.n) return;
+    int i = g.ids[p];
+    if (deg[i] != -1) return;
+    V3 zi = v3(g.zs[4 * (int64_t)p], g.zs[4 * (int64_t)p + 1], g.zs[4 * (int64_t)p + 2]);
+    Poly P, T;
+    CellStats cs;
+    int d = build_cell(g, i, zi, nbr + (int64_t)i * MAXDEG, &cs, P, T);
+    if (d < 0) {
+        atomicOr(status, -d);
+        deg[i] = 0;
+    } else {
+        deg[i] = d;
+        atomicMax(&stats[0], d);
+    }
+    if (cs.tie_breaks) atomicAdd(&stats[4], cs.tie_breaks);
+}
+
+__device__ __forceinline__ int find_in_cycle(const int* __restrict__ row, int d, int x) {
+    for (int k = 0; k < d; ++k)
+        if (row[k] == x) return k;
+    return -1;
+}
+
+// consistency of adjacent cycles + local Delaunay filter (edge (i, n_t) with triangles
+// (i, n_t, n_{t+1}) and (i, n_{t-1}, n_t))
+__global__ void k_verify(const double* __restrict__ z, int n, const int* __restrict__ nbr,
+                         const int* __restrict__ deg, uint8_t* __restrict__ amb,
+                         int* __restrict__ status, int* __restrict__ stats) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = deg[i];
+    const int* row = nbr + (int64_t)i * MAXDEG;
+    if (d < 3) { atomicOr(status, ST_INCONSISTENT); return; }
+    V3 zi = load3(z, i);
+    int namb = 0;
+    for (int t = 0; t < d; ++t) {
+        int a = row[t], b = row[t + 1 == d ? 0 : t + 1], c = row[t == 0 ? d - 1 : t - 1];
+        int da = deg[a];
+        const int* ra = nbr + (int64_t)a * MAXDEG;
+        int p = find_in_cycle(ra, da, i);
+        bool ok = p >= 0 && ra[p == 0 ? da - 1 : p - 1] == b;
+        if (!ok) atomicOr(status, ST_INCONSISTENT);
+        bool am;
+        int s = insphere_sign(zi, load3(z, a), load3(z, b), load3(z, c), &am);
+        amb[(int64_t)i * MAXDEG + t] = am ? 1 : 0;
+        if (am) ++namb;
+        else if (s >= 0) atomicOr(status, ST_NOT_DELAUNAY);
+    }
+    if (namb) atomicAdd(&stats[3], namb);
+}
+
+__global__ void k_fill_incidences(int n, const int* __restrict__ deg,
+                                  const int* __restrict__ inc_start, int* __restrict__ inc_gen,
+                                  int cap) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int s = inc_start[i], d = deg[i];
+    for (int t = 0; t < d; ++t)
+        if (s + t < cap) inc_gen[s + t] = i;
+}
+
+// ------------------------------------------------------------------ quadrature
+struct QuadArgs {
+    const double* z;
+    const int* nbr;
+    const int* deg;
+    const int* inc_start;
+    const int* inc_gen;
+    int n;
+    int n_inc;            // expected incidences 6n - 12
+    const double* nodes;  // device [3][nq]: l1, l2, w
+    int nq;
+    DensityParams dp;
+    double* part;         // [5][n_inc] SoA
+    uint8_t* obtuse;      // [n_inc]
+    int* status;
+};
+
+template <int KIND, bool SPHERE>
+__global__ void __launch_bounds__(QUAD_THREADS)
+k_quad(QuadArgs a) {
+    extern __shared__ double s_nodes[];
+    for (int q = threadIdx.x; q < 3 * a.nq; q += blockDim.x) s_nodes[q] = a.nodes[q];
+    __syncthreads();
+    int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= a.n_inc) return;
+    if (a.inc_start[a.n] != a.n_inc) {   // not a closed triangulation: nothing to integrate
+        if (u == 0) atomicOr(a.status, ST_EULER);
+        return;
+    }
+    int i = a.inc_gen[u];
+    int t = u - a.inc_start[i];
+    int d = a.deg[i];
+    const int* row = a.nbr + (int64_t)i * MAXDEG;
+    int j = row[t], k = row[t + 1 == d ? 0 : t + 1];
+    V3 vi = load3(a.z, i), vj = load3(a.z, j), vk = load3(a.z, k);
+    FanPair f = fan_pair(vi, vj, vk, i, j, k);
+    if (f.degenerate) atomicOr(a.status, ST_DEGENERATE_TRI);
+    double acc[5] = {0, 0, 0, 0, 0};
+    int pole = 0;
+    const double* l1 = s_nodes;
+    const double* l2 = s_nodes + a.nq;
+    const double* w = s_nodes + 2 * a.nq;
+    subtri_moments<KIND, SPHERE>(f.s[0], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
+    subtri_moments<KIND, SPHERE>(f.s[1], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
+    if (pole) atomicOr(a.status, ST_POLE);
+    int64_t N = a.n_inc;
+    a.part[u] = acc[0];
+    a.part[N + u] = acc[1];
+    a.part[2 * N + u] = acc[2];
+    a.part[3 * N + u] = acc[3];
+    a.part[4 * N + u] = acc[4];
+    a.obtuse[u] = (f.obtuse && i < j && i < k) ? 1 : 0;
+}
+
+// per generator: fixed-order sum over its incidences, then the gradient epilogue
+__global__ void k_gather(const double* __restrict__ z, int n, const int* __restrict__ inc_start,
+                         const double* __restrict__ part, const uint8_t* __restrict__ obtuse,
+                         int64_t n_inc, const int* __restrict__ status, double* __restrict__ grad,
+                         double* __restrict__ first, double* __restrict__ mass,
+                         double* __restrict__ diag, double* __restrict__ e_gen,
+                         double* __restrict__ g2_gen, double* __restrict__ ob_gen) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double m = 0, cx = 0, cy = 0, cz = 0, e = 0, ob = 0;
+    if (inc_start[n] == n_inc) {
+        for (int u = inc_start[i]; u < inc_start[i + 1]; ++u) {
+            m += part[u];
+            cx += part[n_inc + u];
+            cy += part[2 * n_inc + u];
+            cz += part[3 * n_inc + u];
+            e += part[4 * n_inc + u];
+            ob += obtuse[u];
+        }
+    }
+    V3 zi = load3(z, i);
+    double czd = cx * zi.x + cy * zi.y + cz * zi.z;
+    double gx = 2.0 * czd * zi.x - 2.0 * cx;
+    double gy = 2.0 * czd * zi.y - 2.0 * cy;
+    double gz = 2.0 * czd * zi.z - 2.0 * cz;
+    grad[3 * (int64_t)i] = gx; grad[3 * (int64_t)i + 1] = gy; grad[3 * (int64_t)i + 2] = gz;
+    first[3 * (int64_t)i] = cx; first[3 * (int64_t)i + 1] = cy; first[3 * (int64_t)i + 2] = cz;
+    if (mass) mass[i] = m;
+    diag[i] = 2.0 * czd;
+    e_gen[i] = e;
+    g2_gen[i] = gx * gx + gy * gy + gz * gz;
+    ob_gen[i] = ob;
+}
+
+// ------------------------------------------------------------------ deterministic reductions
+// op 0 = sum, 1 = max, 2 = min.  Stage 1 writes RED_BLOCKS partials per array.
+template <int OP>
+__device__ __forceinline__ double red_op(double a, double b) {
+    return OP == 0 ? a + b : (OP == 1 ? fmax(a, b) : fmin(a, b));
+}
+template <int OP>
+__device__ __forceinline__ double red_identity() {
+    return OP == 0 ? 0.0 : (OP == 1 ? -INFINITY : INFINITY);
+}
+
+template <int OP>
+__device__ double block_reduce(double v) {
+    __shared__ double sh[RED_THREADS];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = RED_THREADS / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = red_op<OP>(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// partials[slot * RED_BLOCKS + block] = op over x[k] (k = block*T + tid + j*RED_BLOCKS*T)
+template <int OP>
+__global__ void __launch_bounds__(RED_THREADS)
+k_reduce_stage1(const double* __restrict__ x, int64_t len, double* __restrict__ partials) {
+    double v = red_identity<OP>();
+    for (int64_t k = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < len;
+         k += (int64_t)RED_BLOCKS * RED_THREADS)
+        v = red_op<OP>(v, x[k]);
+    v = block_reduce<OP>(v);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+}
+
+// dot products: partials of sum a[k]*b[k]
+__global__ void __launch_bounds__(RED_THREADS)
+k_dot_stage1(const double* __restrict__ a, const double* __restrict__ b, int64_t len,
+             double* __restrict__ partials) {
+    double v = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < len;
+         k += (int64_t)RED_BLOCKS * RED_THREADS)
+        v += a[k] * b[k];
+    v = block_reduce<0>(v);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+}
+
+// partials of max |a[k] - b[k]| (movement, optimizer.py:355)
+__global__ void __launch_bounds__(RED_THREADS)
+k_absdiff_stage1(const double* __restrict__ a, const double* __restrict__ b, int64_t len,
+                 double* __restrict__ partials);
+
+// sum over the RED_BLOCKS partials in a fixed order (called by every block that needs it)
+template <int OP>
+__device__ double finish_partials(const double* __restrict__ partials) {
+    double v = red_identity<OP>();
+    for (int k = threadIdx.x; k < RED_BLOCKS; k += RED_THREADS) v = red_op<OP>(v, partials[k]);
+    return block_reduce<OP>(v);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(RED_THREADS)
+k_reduce_stage2(const double* __restrict__ partials, int nslots, double* __restrict__ out) {
+    for (int s = 0; s < nslots; ++s) {
+        double v = finish_partials<OP>(partials + s * RED_BLOCKS);
+        if (threadIdx.x == 0) out[s] = v;
+    }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_absdiff_stage1(const double* __restrict__ a, const double* __restrict__ b, int64_t len,
+                 double* __restrict__ partials) {
+    double v = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < len;
+         k += (int64_t)RED_BLOCKS * RED_THREADS)
+        v = fmax(v, fabs(a[k] - b[k]));
+    v = block_reduce<1>(v);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+}
+
+// ------------------------------------------------------------------ LBFGS vector kernels
+__global__ void k_copy(const double* __restrict__ x, int64_t len, double* __restrict__ y) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len;
+         k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = x[k];
+}
+
+__global__ void k_scale(double a, const double* __restrict__ x, int64_t len,
+                        double* __restrict__ y) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len;
+         k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = a * x[k];
+}
+
+// backward step of the two-loop: a = rho * (s.q) from partials; q -= a*y; store a
+__global__ void __launch_bounds__(RED_THREADS)
+k_twoloop_back(double* __restrict__ q, const double* __restrict__ y, int64_t len,
+               const double* __restrict__ partials, double rho, double* __restrict__ a_store) {
+    double a = rho * finish_partials<0>(partials);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a_store = a;
+    for (int64_t k = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < len;
+         k += (int64_t)gridDim.x * RED_THREADS)
+        q[k] -= a * y[k];
+}
+
+// forward step: b = rho * (y.q); q += s*(a - b); optional negation at the end
+__global__ void __launch_bounds__(RED_THREADS)
+k_twoloop_fwd(double* __restrict__ q, const double* __restrict__ s, int64_t len,
+              const double* __restrict__ partials, double rho, const double* __restrict__ a_store,
+              int negate) {
+    double b = rho * finish_partials<0>(partials);
+    double c = *a_store - b;
+    for (int64_t k = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < len;
+         k += (int64_t)gridDim.x * RED_THREADS) {
+        double v = q[k] + s[k] * c;
+        q[k] = negate ? -v : v;
+    }
+}
+
+// h0 application (LloydDiagonal: q * (1/d) blockwise; GammaIdentity: gamma*q), with the
+// final negation folded in when there is no forward loop
+__global__ void k_apply_h0(double* __restrict__ q, const double* __restrict__ diag, double gamma,
+                           int64_t n, int negate) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < 3 * n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        double v = diag ? q[k] * (1.0 / diag[k / 3]) : gamma * q[k];
+        q[k] = negate ? -v : v;
+    }
+}
+
+// s = z_new - z_old, y = g_new - g_old; stage-1 partials of y.s, s.s, y.y and max|s|
+__global__ void __launch_bounds__(RED_THREADS)
+k_history_pair(const double* __restrict__ zo, const double* __restrict__ zn,
+               const double* __restrict__ go, const double* __restrict__ gn, int64_t len,
+               double* __restrict__ s, double* __restrict__ y, double* __restrict__ partials) {
+    double ys = 0, ss = 0, yy = 0, mv = 0;
+    for (int64_t k = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < len;
+         k += (int64_t)RED_BLOCKS * RED_THREADS) {
+        double sk = zn[k] - zo[k], yk = gn[k] - go[k];
+        s[k] = sk; y[k] = yk;
+        ys += yk * sk; ss += sk * sk; yy += yk * yk; mv = fmax(mv, fabs(sk));
+    }
+    ys = block_reduce<0>(ys); ss = block_reduce<0>(ss); yy = block_reduce<0>(yy);
+    mv = block_reduce<1>(mv);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = ys;
+        partials[RED_BLOCKS + blockIdx.x] = ss;
+        partials[2 * RED_BLOCKS + blockIdx.x] = yy;
+        partials[3 * RED_BLOCKS + blockIdx.x] = mv;
+    }
+}
+
+__global__ void k_history_finish(const double* __restrict__ partials, double* __restrict__ out) {
+    double ys = finish_partials<0>(partials);
+    double ss = finish_partials<0>(partials + RED_BLOCKS);
+    double yy = finish_partials<0>(partials + 2 * RED_BLOCKS);
+    double mv = finish_partials<1>(partials + 3 * RED_BLOCKS);
+    if (threadIdx.x == 0) { out[0] = ys; out[1] = ss; out[2] = yy; out[3] = mv; }
+}
+
+// q3 = q - (q.z) z per row; partials of g.q3
+__global__ void __launch_bounds__(RED_THREADS)
+k_tangent(const double* __restrict__ q, const double* __restrict__ z,
+          const double* __restrict__ g, int64_t n, double* __restrict__ q3,
+          double* __restrict__ partials) {
+    double v = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        double qx = q[3 * i], qy = q[3 * i + 1], qz = q[3 * i + 2];
+        double zx = z[3 * i], zy = z[3 * i + 1], zz = z[3 * i + 2];
+        double qd = qx * zx + qy * zy + qz * zz;
+        double ax = qx - qd * zx, ay = qy - qd * zy, az = qz - qd * zz;
+        q3[3 * i] = ax; q3[3 * i + 1] = ay; q3[3 * i + 2] = az;
+        v += g[3 * i] * ax + g[3 * i + 1] * ay + g[3 * i + 2] * az;
+    }
+    v = block_reduce<0>(v);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+}
+
+__global__ void k_trial(const double* __restrict__ z, const double* __restrict__ q3, double alpha,
+                        int64_t n, double* __restrict__ zt, double* __restrict__ norms) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double vx = z[3 * i] + alpha * q3[3 * i];
+        double vy = z[3 * i + 1] + alpha * q3[3 * i + 1];
+        double vz = z[3 * i + 2] + alpha * q3[3 * i + 2];
+        double nr = sqrt(vx * vx + vy * vy + vz * vz);
+        norms[i] = nr;
+        zt[3 * i] = vx / nr; zt[3 * i + 1] = vy / nr; zt[3 * i + 2] = vz / nr;
+    }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_dirderiv(const double* __restrict__ g, const double* __restrict__ q3,
+           const double* __restrict__ norms, int64_t n, double* __restrict__ partials) {
+    double v = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        double nr = norms[i];
+        v += g[3 * i] * (q3[3 * i] / nr) + g[3 * i + 1] * (q3[3 * i + 1] / nr) +
+             g[3 * i + 2] * (q3[3 * i + 2] / nr);
+    }
+    v = block_reduce<0>(v);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+}
+
+__global__ void k_lloyd(const double* __restrict__ c, int64_t n, double* __restrict__ z,
+                        int* __restrict__ status) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double x = c[3 * i], y = c[3 * i + 1], w = c[3 * i + 2];
+        double nr = sqrt(x * x + y * y + w * w);
+        if (!(nr > 1e-12)) atomicOr(status, ST_CENTROID);
+        z[3 * i] = x / nr; z[3 * i + 1] = y / nr; z[3 * i + 2] = w / nr;
+    }
+}
+
+__global__ void k_normalize(double* __restrict__ z, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double x = z[3 * i], y = z[3 * i + 1], w = z[3 * i + 2];
+        double nr = sqrt(x * x + y * y + w * w);
+        z[3 * i] = x / nr; z[3 * i + 1] = y / nr; z[3 * i + 2] = w / nr;
+    }
+}
+
+// ------------------------------------------------------------------ canonical triangles
+__global__ void k_tri_count(int n, const int* __restrict__ nbr, const int* __restrict__ deg,
+                            int* __restrict__ cnt) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i == n) { cnt[n] = 0; return; }
+    int d = deg[i], c = 0;
+    const int* row = nbr + (int64_t)i * MAXDEG;
+    for (int t = 0; t < d; ++t) {
+        int a = row[t], b = row[t + 1 == d ? 0 : t + 1];
+        c += (i < a && i < b);
+    }
+    cnt[i] = c;
+}
+
+__global__ void k_tri_emit(int n, const int* __restrict__ nbr, const int* __restrict__ deg,
+                           const uint8_t* __restrict__ amb, const int* __restrict__ off,
+                           int64_t tmax, int64_t* __restrict__ tri, uint8_t* __restrict__ flags) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = deg[i];
+    const int* row = nbr + (int64_t)i * MAXDEG;
+    int la[MAXDEG], lb[MAXDEG], lf[MAXDEG];
+    int m = 0;
+    for (int t = 0; t < d; ++t) {
+        int tp = t + 1 == d ? 0 : t + 1;
+        int a = row[t], b = row[tp];
+        if (!(i < a && i < b)) continue;
+        int f = amb[(int64_t)i * MAXDEG + t] | amb[(int64_t)i * MAXDEG + tp];
+        // third edge (a, b) seen from a: b's slot in a's cycle
+        int da = deg[a];
+        const int* ra = nbr + (int64_t)a * MAXDEG;
+        int pb = find_in_cycle(ra, da, b);
+        if (pb >= 0) f |= amb[(int64_t)a * MAXDEG + pb];
+        int pi = find_in_cycle(ra, da, i);
+        if (pi >= 0) f |= amb[(int64_t)a * MAXDEG + pi];
+        // insertion sort by second id
+        int k = m++;
+        while (k > 0 && la[k - 1] > a) { la[k] = la[k - 1]; lb[k] = lb[k - 1]; lf[k] = lf[k - 1]; --k; }
+        la[k] = a; lb[k] = b; lf[k] = f;
+    }
+    int64_t o = off[i];
+    for (int k = 0; k < m; ++k) {
+        if (o + k >= tmax) break;
+        tri[3 * (o + k)] = i; tri[3 * (o + k) + 1] = la[k]; tri[3 * (o + k) + 2] = lb[k];
+        if (flags) flags[o + k] = (uint8_t)lf[k];
+    }
+}
+
+// ------------------------------------------------------------------ cycles from a triangle list
+__global__ void k_tl_fill(const int64_t* __restrict__ tri, int64_t t, int* __restrict__ cursor,
+                          int* __restrict__ pairs, int* __restrict__ status) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= t) return;
+    int v[3] = {(int)tri[3 * r], (int)tri[3 * r + 1], (int)tri[3 * r + 2]};
+    for (int c = 0; c < 3; ++c) {
+        int i = v[c], j = v[(c + 1) % 3], k = v[(c + 2) % 3];
+        int slot = atomicAdd(&cursor[i], 1);
+        if (slot >= MAXDEG) { atomicOr(status, ST_DEG_OVERFLOW); continue; }
+        pairs[((int64_t)i * MAXDEG + slot) * 2] = j;
+        pairs[((int64_t)i * MAXDEG + slot) * 2 + 1] = k;
+    }
+}
+
+// chain the (next, prev) pairs of each vertex into the CCW cycle starting at its min id
+__global__ void k_tl_chain(int n, const int* __restrict__ pairs, const int* __restrict__ cursor,
+                           int* __restrict__ nbr, int* __restrict__ deg, int* __restrict__ status) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = cursor[i];
+    if (d > MAXDEG || d < 3) { deg[i] = 0; atomicOr(status, ST_INCONSISTENT); return; }
+    const int* pr = pairs + (int64_t)i * MAXDEG * 2;
+    int start = pr[0];
+    for (int s = 1; s < d; ++s) start = min(start, pr[2 * s]);
+    int* row = nbr + (int64_t)i * MAXDEG;
+    int cur = start;
+    for (int t = 0; t < d; ++t) {
+        row[t] = cur;
+        int nx = -1;
+        for (int s = 0; s < d; ++s)
+            if (pr[2 * s] == cur) { nx = pr[2 * s + 1]; break; }
+        if (nx < 0) { atomicOr(status, ST_INCONSISTENT); deg[i] = 0; return; }
+        cur = nx;
+    }
+    if (cur != start) atomicOr(status, ST_INCONSISTENT);
+    deg[i] = d;
+}
+
+}  // namespace
+
+// ====================================================================== context
+struct scvt_ctx {
+    int device = 0;
+    int64_t n_max = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    // config
+    DensityParams dp{};
+    int measure = 0;
+    int nq = 0;
+    int m = 7;
+    double* d_nodes = nullptr;   // [3][nq]
+    // grid
+    int g_max = 1;
+    uint32_t* d_keys = nullptr; uint32_t* d_skeys = nullptr;
+    int* d_vals = nullptr; int* d_ids = nullptr;
+    int* d_start = nullptr;
+    double* d_zs = nullptr;
+    void* d_cub = nullptr; size_t cub_bytes = 0;
+    // cells
+    int* d_nbr = nullptr; int* d_deg = nullptr; uint8_t* d_amb = nullptr;
+    int* d_inc_start = nullptr; int* d_inc_gen = nullptr;
+    int* d_pairs = nullptr; int* d_cursor = nullptr;
+    // quadrature
+    double* d_part = nullptr; uint8_t* d_obt = nullptr;
+    double* d_egen = nullptr; double* d_g2gen = nullptr; double* d_obgen = nullptr;
+    // reductions and status
+    double* d_partials = nullptr;      // [MAX_SLOTS][RED_BLOCKS]
+    double* d_scal = nullptr;          // [MAX_SLOTS]
+    int* d_status = nullptr;           // [1 + 4 stats]
+    double* h_scal = nullptr;          // pinned [MAX_SLOTS]
+    int* h_status = nullptr;           // pinned [8]
+    // LBFGS history
+    double* d_S = nullptr; double* d_Y = nullptr;   // [m][3 n_max]
+    double* d_alpha = nullptr;                      // [m]
+    std::vector<double> rho, ys, yy;
+    int hist_head = 0, hist_count = 0;
+    double* d_tmp_s = nullptr; double* d_tmp_y = nullptr;   // staging for push
+};
+
+namespace {
+
+int fail(scvt_ctx* c, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(ctx, SCVT_ERR_CUDA, "%s: %s (%s:%d)", #call,                  \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                  \
+    } while (0)
+
+#define LAUNCHED()                                                                    \
+    do {                                                                              \
+        ++ctx->launches;                                                              \
+        cudaError_t e_ = cudaGetLastError();                                          \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(ctx, SCVT_ERR_CUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                          \
+    } while (0)
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+int grid_for(int64_t n) {
+    double g = sqrt((double)n / 12.0);
+    int G = (int)g;
+    return G < 1 ? 1 : G;
+}
+
+int status_to_code(scvt_ctx* ctx, int st) {
+    if (!st) return SCVT_OK;
+    if (st & ST_DUPLICATE)
+        return fail(ctx, SCVT_ERR_INSUFFICIENT_POINTS,
+                    "duplicate generators: points fell inside the convex hull");
+    if (st & ST_UNBOUNDED)
+        return fail(ctx, SCVT_ERR_INSUFFICIENT_POINTS,
+                    "a Voronoi cell spans a hemisphere (degenerate global point set)");
+    if (st & (ST_POLY_OVERFLOW | ST_DEG_OVERFLOW))
+        return fail(ctx, SCVT_ERR_CAPACITY, "valence exceeds %d (status 0x%x)", MAXDEG, st);
+    if (st & ST_POLE)
+        return fail(ctx, SCVT_ERR_POLE_AMBIGUITY, "longitude undefined within 1e-9 of a pole");
+    if (st & ST_CENTROID)
+        return fail(ctx, SCVT_ERR_CENTROID_AT_ORIGIN, "first moment ~0");
+    if (st & ST_DEGENERATE_TRI)
+        return fail(ctx, SCVT_ERR_DEGENERATE_TRIANGLE, "degenerate triangle in the fan");
+    return fail(ctx, SCVT_ERR_COVERAGE,
+                "triangulation certificate failed (status 0x%x: %s%s%s)", st,
+                (st & ST_INCONSISTENT) ? "inconsistent cycles " : "",
+                (st & ST_NOT_DELAUNAY) ? "non-Delaunay edge " : "",
+                (st & ST_EULER) ? "Euler count" : "");
+}
+
+template <typename T>
+int dalloc(scvt_ctx* ctx, T** p, size_t count) {
+    CK(cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
+    return SCVT_OK;
+}
+
+#define TRY(x)                 \
+    do {                       \
+        int r_ = (x);          \
+        if (r_) return r_;     \
+    } while (0)
+
+// read back `nd` scalars from d_scal and the status block; synchronises the stream
+int readback(scvt_ctx* ctx, int nd) {
+    if (nd) CK(cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, nd * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SCVT_OK;
+}
+
+int reset_status(scvt_ctx* ctx) {
+    CK(cudaMemsetAsync(ctx->d_status, 0, 16 * sizeof(int), ctx->stream));
+    return SCVT_OK;
+}
+
+// dot(a, b) -> partial slot
+int dot_to_slot(scvt_ctx* ctx, const double* a, const double* b, int64_t len, int slot) {
+    k_dot_stage1<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(a, b, len,
+                                                             ctx->d_partials + slot * RED_BLOCKS);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+// sum(slots) -> d_scal[0..nslots) -> host
+int finish_slots(scvt_ctx* ctx, int nslots) {
+    k_reduce_stage2<0><<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials, nslots, ctx->d_scal);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+// ---------------------------------------------------------------------- triangulation core
+int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
+    if (n < 4) return fail(ctx, SCVT_ERR_INSUFFICIENT_POINTS,
+                           "need >= 4 points on the sphere, got %lld", (long long)n);
+    if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n=%lld > n_max=%lld",
+                                    (long long)n, (long long)ctx->n_max);
+    int G = std::min(grid_for(n), ctx->g_max);
+    int nb = 6 * G * G;
+    cudaStream_t s = ctx->stream;
+    k_bucket_keys<<<blocks_for(n, 256), 256, 0, s>>>(z, (int)n, G, ctx->d_keys, ctx->d_vals);
+    LAUNCHED();
+    int bits = 1;
+    while ((1 << bits) < nb) ++bits;
+    size_t tb = ctx->cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_keys, ctx->d_skeys, ctx->d_vals,
+                                       ctx->d_ids, (int)n, 0, bits, s));
+    k_bucket_start<<<blocks_for(nb + 1, 256), 256, 0, s>>>(ctx->d_skeys, (int)n, nb, ctx->d_start);
+    LAUNCHED();
+    k_gather_sorted<<<blocks_for(n, 256), 256, 0, s>>>(z, ctx->d_ids, (int)n, ctx->d_zs);
+    LAUNCHED();
+    GridView g;
+    g.zs = ctx->d_zs; g.ids = ctx->d_ids; g.start = ctx->d_start; g.z = z; g.G = G; g.n = n;
+    k_cells_warp<<<blocks_for(n, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
+        g, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
+    LAUNCHED();
+    k_cells<<<blocks_for(n, CELL_THREADS), CELL_THREADS, 0, s>>>(g, ctx->d_nbr, ctx->d_deg,
+                                                                ctx->d_status, ctx->d_status + 8);
+    LAUNCHED();
+    k_verify<<<blocks_for(n, 128), 128, 0, s>>>(z, (int)n, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
+                                               ctx->d_status, ctx->d_status + 8);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int cells_from_triangles(scvt_ctx* ctx, const int64_t* tri, int64_t t, int64_t n) {
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemsetAsync(ctx->d_cursor, 0, n * sizeof(int), s));
+    k_tl_fill<<<blocks_for(t, 256), 256, 0, s>>>(tri, t, ctx->d_cursor, ctx->d_pairs,
+                                                 ctx->d_status);
+    LAUNCHED();
+    k_tl_chain<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_pairs, ctx->d_cursor,
+                                                  ctx->d_nbr, ctx->d_deg, ctx->d_status);
+    LAUNCHED();
+    CK(cudaMemsetAsync(ctx->d_amb, 0, (size_t)n * MAXDEG, s));
+    return SCVT_OK;
+}
+
+template <int KIND>
+int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t smem) {
+    if (ctx->measure)
+        k_quad<KIND, true><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
+    else
+        k_quad<KIND, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+            double* mass, double* diag, double* scalars_host) {
+    cudaStream_t s = ctx->stream;
+    // incidence CSR over the cycles (deg[n] = 0 terminates the exclusive scan)
+    CK(cudaMemsetAsync(ctx->d_deg + n, 0, sizeof(int), s));
+    size_t tb = ctx->cub_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, ctx->d_deg, ctx->d_inc_start, (int)n + 1, s));
+    int64_t n_inc = 6 * n - 12;
+    k_fill_incidences<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_deg, ctx->d_inc_start,
+                                                         ctx->d_inc_gen, (int)n_inc);
+    LAUNCHED();
+    QuadArgs a;
+    a.z = z; a.nbr = ctx->d_nbr; a.deg = ctx->d_deg; a.inc_start = ctx->d_inc_start;
+    a.inc_gen = ctx->d_inc_gen; a.n = (int)n; a.n_inc = (int)n_inc; a.nodes = ctx->d_nodes;
+    a.nq = ctx->nq; a.dp = ctx->dp; a.part = ctx->d_part; a.obtuse = ctx->d_obt;
+    a.status = ctx->d_status;
+    unsigned grid = blocks_for(n_inc, QUAD_THREADS);
+    size_t smem = 3 * (size_t)ctx->nq * sizeof(double);
+    switch (ctx->dp.kind) {
+        case DEN_CONST: TRY(launch_quad_kind<DEN_CONST>(ctx, a, grid, smem)); break;
+        case DEN_X3: TRY(launch_quad_kind<DEN_X3>(ctx, a, grid, smem)); break;
+        case DEN_X16: TRY(launch_quad_kind<DEN_X16>(ctx, a, grid, smem)); break;
+        case DEN_TANH: TRY(launch_quad_kind<DEN_TANH>(ctx, a, grid, smem)); break;
+        case DEN_TANH4: TRY(launch_quad_kind<DEN_TANH4>(ctx, a, grid, smem)); break;
+        case DEN_TANH4X2: TRY(launch_quad_kind<DEN_TANH4X2>(ctx, a, grid, smem)); break;
+        default: return fail(ctx, SCVT_ERR_CONFIG, "bad density kind %d", ctx->dp.kind);
+    }
+    k_gather<<<blocks_for(n, 256), 256, 0, s>>>(z, (int)n, ctx->d_inc_start, ctx->d_part,
+                                                ctx->d_obt, n_inc, ctx->d_status, grad, first,
+                                                mass, diag, ctx->d_egen, ctx->d_g2gen,
+                                                ctx->d_obgen);
+    LAUNCHED();
+    k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_egen, n, ctx->d_partials);
+    LAUNCHED();
+    k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_g2gen, n,
+                                                          ctx->d_partials + RED_BLOCKS);
+    LAUNCHED();
+    k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_obgen, n,
+                                                          ctx->d_partials + 2 * RED_BLOCKS);
+    LAUNCHED();
+    TRY(finish_slots(ctx, 3));
+    TRY(readback(ctx, 3));
+    int st = ctx->h_status[0];
+    if (st) return status_to_code(ctx, st);
+    scalars_host[0] = ctx->h_scal[0];
+    scalars_host[1] = sqrt(ctx->h_scal[1]);
+    scalars_host[2] = ctx->h_scal[2];
+    return SCVT_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* scvt_version(void) { return "scvt_b200 0.1.0 (sm_100a)"; }
+
+const char* scvt_last_error(const scvt_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int64_t scvt_launch_count(const scvt_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int scvt_set_stream(scvt_ctx* ctx, void* stream) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    ctx->stream = (cudaStream_t)stream;
+    return SCVT_OK;
+}
+
+int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cfg) {
+    if (!out || !cfg) return SCVT_ERR_CONFIG;
+    *out = nullptr;
+    scvt_ctx* ctx = new scvt_ctx();
+    ctx->device = device;
+    ctx->n_max = n_max;
+    auto bail = [&](int code) { *out = ctx; return code; };
+    if (n_max < 4 || n_max > (int64_t)1 << 28)
+        return bail(fail(ctx, SCVT_ERR_CONFIG, "n_max=%lld out of range", (long long)n_max));
+    if (cfg->n_nodes < 1 || cfg->n_nodes > SCVT_MAX_NODES || !cfg->node_l1 || !cfg->node_l2 ||
+        !cfg->node_w)
+        return bail(fail(ctx, SCVT_ERR_CONFIG, "bad node table (n_nodes=%d)", cfg->n_nodes));
+    if (cfg->density_kind < 0 || cfg->density_kind > 5)
+        return bail(fail(ctx, SCVT_ERR_CONFIG, "bad density kind %d", cfg->density_kind));
+    if (cfg->lbfgs_m < 1 || cfg->lbfgs_m > 32)
+        return bail(fail(ctx, SCVT_ERR_CONFIG, "lbfgs_m=%d out of range", cfg->lbfgs_m));
+    {
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess)
+            return bail(fail(ctx, SCVT_ERR_CUDA, "cudaSetDevice(%d): %s", device,
+                             cudaGetErrorString(e)));
+    }
+    DensityParams& dp = ctx->dp;
+    dp.kind = cfg->density_kind;
+    dp.gamma = cfg->gamma; dp.beta = cfg->beta; dp.alpha = cfg->alpha;
+    dp.c0x = cfg->center[0]; dp.c0y = cfg->center[1]; dp.c0z = cfg->center[2];
+    dp.c1x = cfg->center[3]; dp.c1y = cfg->center[4]; dp.c1z = cfg->center[5];
+    dp.w_lon = cfg->w_lon; dp.w_lat = cfg->w_lat;
+    if (dp.kind == DEN_X16) {
+        double horiz = hypot(dp.c0x, dp.c0y);
+        if (horiz < 1e-9)
+            return bail(fail(ctx, SCVT_ERR_POLE_AMBIGUITY, "x16 centre at a pole"));
+        dp.lat_c = atan2(dp.c0z, horiz);
+        dp.lon_c = atan2(dp.c0y, dp.c0x);
+        dp.cos_lat_c = cos(dp.lat_c);
+        dp.sin_lat_c = sin(dp.lat_c);
+    }
+    ctx->measure = cfg->measure;
+    ctx->nq = cfg->n_nodes;
+    ctx->m = cfg->lbfgs_m;
+    int64_t n = n_max;
+    int G = grid_for(n);
+    ctx->g_max = G;
+    int64_t nb = 6LL * G * G;
+    int64_t n_inc = 6 * n;
+    int r = SCVT_OK;
+#define AL(p, cnt) \
+    if ((r = dalloc(ctx, &ctx->p, (size_t)(cnt)))) return bail(r)
+    AL(d_nodes, 3 * ctx->nq);
+    AL(d_keys, n); AL(d_skeys, n); AL(d_vals, n); AL(d_ids, n);
+    AL(d_start, nb + 1);
+    AL(d_zs, 4 * n);
+    AL(d_nbr, n * MAXDEG); AL(d_deg, n + 1); AL(d_amb, n * MAXDEG);
+    AL(d_inc_start, n + 1); AL(d_inc_gen, n_inc);
+    AL(d_pairs, n * MAXDEG * 2); AL(d_cursor, n + 1);
+    AL(d_part, 5 * n_inc); AL(d_obt, n_inc);
+    AL(d_egen, n); AL(d_g2gen, n); AL(d_obgen, n);
+    AL(d_partials, (int64_t)MAX_SLOTS * RED_BLOCKS);
+    AL(d_scal, MAX_SLOTS);
+    AL(d_status, 16);
+    AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
+    AL(d_alpha, ctx->m);
+    AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
+#undef AL
+    {
+        cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_SLOTS * sizeof(double));
+        cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
+        if (e1 != cudaSuccess || e2 != cudaSuccess)
+            return bail(fail(ctx, SCVT_ERR_CUDA, "cudaMallocHost failed"));
+    }
+    // CUB temp storage: max of radix sort (n) and scan (n+1)
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b1, ctx->d_keys, ctx->d_skeys, ctx->d_vals,
+                                    ctx->d_ids, (int)n, 0, 32);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, ctx->d_deg, ctx->d_inc_start, (int)n + 1);
+    ctx->cub_bytes = std::max(b1, b2);
+    if ((r = dalloc(ctx, (char**)&ctx->d_cub, ctx->cub_bytes))) return bail(r);
+    // node table
+    std::vector<double> tbl(3 * (size_t)ctx->nq);
+    for (int q = 0; q < ctx->nq; ++q) {
+        tbl[q] = cfg->node_l1[q];
+        tbl[ctx->nq + q] = cfg->node_l2[q];
+        tbl[2 * ctx->nq + q] = cfg->node_w[q];
+    }
+    {
+        cudaError_t e = cudaMemcpy(ctx->d_nodes, tbl.data(), tbl.size() * sizeof(double),
+                                   cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return bail(fail(ctx, SCVT_ERR_CUDA, "node upload failed"));
+    }
+    size_t smem = 3 * (size_t)ctx->nq * sizeof(double);
+    if (smem > 48 * 1024) {
+        // opt in to large dynamic shared memory for every instantiation
+#define OPT(K)                                                                             \
+    cudaFuncSetAttribute(k_quad<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(k_quad<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+        OPT(DEN_CONST); OPT(DEN_X3); OPT(DEN_X16); OPT(DEN_TANH); OPT(DEN_TANH4); OPT(DEN_TANH4X2);
+#undef OPT
+    }
+    ctx->rho.assign(ctx->m, 0.0);
+    ctx->ys.assign(ctx->m, 0.0);
+    ctx->yy.assign(ctx->m, 0.0);
+    *out = ctx;
+    return SCVT_OK;
+}
+
+int scvt_destroy(scvt_ctx* ctx) {
+    if (!ctx) return SCVT_OK;
+    void* dev[] = {ctx->d_nodes, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
+                   ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
+                   ctx->d_inc_start, ctx->d_inc_gen, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
+                   ctx->d_obt, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, ctx->d_partials,
+                   ctx->d_scal, ctx->d_status, ctx->d_S, ctx->d_Y, ctx->d_alpha,
+                   ctx->d_tmp_s, ctx->d_tmp_y};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+    if (ctx->h_status) cudaFreeHost(ctx->h_status);
+    delete ctx;
+    return SCVT_OK;
+}
+
+int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out,
+                     uint8_t* flags_out, int64_t* stats_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    TRY(reset_status(ctx));
+    TRY(build_cells(ctx, z, n));
+    cudaStream_t s = ctx->stream;
+    // canonical triangles: count per min-id generator, scan, emit sorted
+    k_tri_count<<<blocks_for(n + 1, 256), 256, 0, s>>>((int)n, ctx->d_nbr, ctx->d_deg,
+                                                       ctx->d_cursor);
+    LAUNCHED();
+    // counts live in d_cursor[0..n] (n+1 entries incl. trailing 0); scan into inc_start
+    size_t tb = ctx->cub_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, ctx->d_cursor, ctx->d_inc_start,
+                                     (int)n + 1, s));
+    k_tri_emit<<<blocks_for(n, 128), 128, 0, s>>>((int)n, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
+                                                  ctx->d_inc_start, 2 * n - 4, tri_out, flags_out);
+    LAUNCHED();
+    int total = 0;
+    CK(cudaMemcpyAsync(&total, ctx->d_inc_start + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TRY(readback(ctx, 0));
+    int st = ctx->h_status[0];
+    if (stats_host) {
+        stats_host[0] = total;
+        stats_host[1] = 0;                  // flagged triangles, filled below
+        stats_host[2] = ctx->h_status[8];   // max valence
+        stats_host[3] = ctx->h_status[11];  // ambiguous (filter-undecided) directed edges
+        stats_host[4] = ctx->h_status[12];  // SoS tie-breaks taken while clipping
+        stats_host[5] = ctx->h_status[10];  // max candidate passes of one cell
+    }
+    if (st) return status_to_code(ctx, st);
+    if (total != 2 * n - 4)
+        return fail(ctx, SCVT_ERR_COVERAGE, "triangulation not closed: K=%lld, T=%d (want %lld)",
+                    (long long)n, total, (long long)(2 * n - 4));
+    if (stats_host && flags_out) {
+        // flagged triangle count
+        std::vector<uint8_t> f((size_t)total);
+        CK(cudaMemcpy(f.data(), flags_out, f.size(), cudaMemcpyDeviceToHost));
+        int64_t c = 0;
+        for (uint8_t v : f) c += v != 0;
+        stats_host[1] = c;
+    }
+    return SCVT_OK;
+}
+
+int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                  double* mass, double* lloyd_diag, double* scalars_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    TRY(reset_status(ctx));
+    TRY(build_cells(ctx, z, n));
+    return moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
+}
+
+int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const int64_t* tri,
+                               int64_t t, double* grad, double* first, double* mass,
+                               double* lloyd_diag, double* scalars_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n > n_max");
+    if (t != 2 * n - 4) return fail(ctx, SCVT_ERR_COVERAGE, "T=%lld != 2n-4", (long long)t);
+    TRY(reset_status(ctx));
+    TRY(cells_from_triangles(ctx, tri, t, n));
+    return moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
+}
+
+// ---------------------------------------------------------------------- optimizer algebra
+int scvt_history_clear(scvt_ctx* ctx) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    ctx->hist_head = 0;
+    ctx->hist_count = 0;
+    return SCVT_OK;
+}
+
+int scvt_history_size(scvt_ctx* ctx, int32_t* size_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    *size_host = ctx->hist_count;
+    return SCVT_OK;
+}
+
+int scvt_history_gamma(scvt_ctx* ctx, double* gamma_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (ctx->hist_count == 0) { *gamma_host = 1.0; return SCVT_OK; }
+    int newest = (ctx->hist_head + ctx->hist_count - 1) % ctx->m;
+    *gamma_host = ctx->ys[newest] / ctx->yy[newest];
+    return SCVT_OK;
+}
+
+int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new, const double* g_old,
+                      const double* g_new, int64_t n, int32_t* pushed_host, double* movement_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    int64_t len = 3 * n;
+    // candidate slot: the next one in the ring (overwrites the oldest when full)
+    int slot = (ctx->hist_head + ctx->hist_count) % ctx->m;
+    // stage into tmp buffers so a rejected pair never clobbers the oldest stored one
+    k_history_pair<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(
+        z_old, z_new, g_old, g_new, len, ctx->d_tmp_s, ctx->d_tmp_y, ctx->d_partials);
+    LAUNCHED();
+    k_history_finish<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials, ctx->d_scal);
+    LAUNCHED();
+    TRY(readback(ctx, 4));
+    double ys = ctx->h_scal[0], ss = ctx->h_scal[1], yy = ctx->h_scal[2];
+    *movement_host = ctx->h_scal[3];
+    if (ys <= 1e-14 * sqrt(ss) * sqrt(yy)) {   // optimizer.py:98-104
+        *pushed_host = 0;
+        return SCVT_OK;
+    }
+    // swap the staged vectors into the ring slot (pointer-free copy on the device)
+    CK(cudaMemcpyAsync(ctx->d_S + (int64_t)slot * 3 * ctx->n_max, ctx->d_tmp_s,
+                       len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_Y + (int64_t)slot * 3 * ctx->n_max, ctx->d_tmp_y,
+                       len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->launches += 2;
+    ctx->rho[slot] = 1.0 / ys;
+    ctx->ys[slot] = ys;
+    ctx->yy[slot] = yy;
+    if (ctx->hist_count < ctx->m) ++ctx->hist_count;
+    else ctx->hist_head = (ctx->hist_head + 1) % ctx->m;
+    *pushed_host = 1;
+    return SCVT_OK;
+}
+
+int scvt_lbfgs_direction(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
+                         int64_t n, double* q, double* qg_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    int64_t len = 3 * n;
+    cudaStream_t s = ctx->stream;
+    unsigned vb = RED_BLOCKS;
+    k_copy<<<vb, VEC_THREADS, 0, s>>>(g, len, q);
+    LAUNCHED();
+    int cnt = ctx->hist_count;
+    int64_t stride = 3 * ctx->n_max;
+    // backward: newest -> oldest
+    for (int r = cnt - 1; r >= 0; --r) {
+        int slot = (ctx->hist_head + r) % ctx->m;
+        TRY(dot_to_slot(ctx, ctx->d_S + slot * stride, q, len, 0));
+        k_twoloop_back<<<vb, RED_THREADS, 0, s>>>(q, ctx->d_Y + slot * stride, len,
+                                                   ctx->d_partials, ctx->rho[slot],
+                                                   ctx->d_alpha + slot);
+        LAUNCHED();
+    }
+    k_apply_h0<<<vb, VEC_THREADS, 0, s>>>(q, lloyd_diag, gamma, n, cnt == 0 ? 1 : 0);
+    LAUNCHED();
+    // forward: oldest -> newest, negate on the last
+    for (int r = 0; r < cnt; ++r) {
+        int slot = (ctx->hist_head + r) % ctx->m;
+        TRY(dot_to_slot(ctx, ctx->d_Y + slot * stride, q, len, 0));
+        k_twoloop_fwd<<<vb, RED_THREADS, 0, s>>>(q, ctx->d_S + slot * stride, len,
+                                                  ctx->d_partials, ctx->rho[slot],
+                                                  ctx->d_alpha + slot, r == cnt - 1 ? 1 : 0);
+        LAUNCHED();
+    }
+    TRY(dot_to_slot(ctx, q, g, len, 0));
+    TRY(finish_slots(ctx, 1));
+    TRY(readback(ctx, 1));
+    *qg_host = ctx->h_scal[0];
+    return SCVT_OK;
+}
+
+int scvt_tangent_project(scvt_ctx* ctx, const double* q, const double* z, const double* g,
+                         int64_t n, double* q3, double* dphi0_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    k_tangent<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(q, z, g, n, q3, ctx->d_partials);
+    LAUNCHED();
+    TRY(finish_slots(ctx, 1));
+    TRY(readback(ctx, 1));
+    *dphi0_host = ctx->h_scal[0];
+    return SCVT_OK;
+}
+
+int scvt_trial_point(scvt_ctx* ctx, const double* z, const double* q3, double alpha, int64_t n,
+                     double* zt, double* norms) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    k_trial<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(z, q3, alpha, n, zt, norms);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int scvt_directional_derivative(scvt_ctx* ctx, const double* g, const double* q3,
+                                const double* norms, int64_t n, double* d_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    k_dirderiv<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(g, q3, norms, n, ctx->d_partials);
+    LAUNCHED();
+    TRY(finish_slots(ctx, 1));
+    TRY(readback(ctx, 1));
+    *d_host = ctx->h_scal[0];
+    return SCVT_OK;
+}
+
+int scvt_lloyd_step(scvt_ctx* ctx, const double* first, int64_t n, double* z_out) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    TRY(reset_status(ctx));
+    k_lloyd<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(first, n, z_out, ctx->d_status);
+    LAUNCHED();
+    TRY(readback(ctx, 0));
+    if (ctx->h_status[0]) return status_to_code(ctx, ctx->h_status[0]);
+    return SCVT_OK;
+}
+
+int scvt_min(scvt_ctx* ctx, const double* v, int64_t len, double* min_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    k_reduce_stage1<2><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(v, len, ctx->d_partials);
+    LAUNCHED();
+    k_reduce_stage2<2><<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials, 1, ctx->d_scal);
+    LAUNCHED();
+    TRY(readback(ctx, 1));
+    *min_host = ctx->h_scal[0];
+    return SCVT_OK;
+}
+
+int scvt_max_abs_diff(scvt_ctx* ctx, const double* a, const double* b, int64_t len,
+                      double* max_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    k_absdiff_stage1<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(a, b, len, ctx->d_partials);
+    LAUNCHED();
+    k_reduce_stage2<1><<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials, 1, ctx->d_scal);
+    LAUNCHED();
+    TRY(readback(ctx, 1));
+    *max_host = ctx->h_scal[0];
+    return SCVT_OK;
+}
+
+int scvt_scale(scvt_ctx* ctx, double a, const double* x, int64_t len, double* y) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    k_scale<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(a, x, len, y);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int scvt_normalize_rows(scvt_ctx* ctx, double* z, int64_t n) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    k_normalize<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(z, n);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+}  // extern "C"

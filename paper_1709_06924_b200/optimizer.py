@@ -1,0 +1,329 @@
+"""Lloyd / LBFGS / Lloyd-preconditioned LBFGS driver (drop-in for `scvtmesh.optimizer`).
+
+The control flow — two-loop with fallbacks, tangent projection, strong-Wolfe bracketing and
+zoom, Lloyd fallback, curvature-guarded history, stopping rules — is the reference's
+(optimizer.py:147-391) line for line, because its branch decisions define parity.  Every
+vector lives on the GPU: the evaluator's kernels produce energy/gradient, and the LBFGS
+vector algebra (two-loop dots/axpys, projection, trial points, directional derivatives,
+history pushes) runs as FP64 kernels of the same library (include/scvt_b200.h).  The host
+only sees the scalars the branch decisions need.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import (
+    CentroidAtOriginError,
+    LineSearchFailure,
+    NonDescentError,
+)
+from .pipeline import EvalResult, MeshEvaluator
+
+logger = logging.getLogger(__name__)
+
+EPS_CURVATURE = 1e-14        # optimizer.py:32 (enforced inside scvt_history_push)
+WOLFE_C1 = 1e-4              # optimizer.py:33
+WOLFE_C2 = 0.9               # optimizer.py:34
+MAX_LINE_SEARCH_EVALS = 10   # optimizer.py:35
+
+METHODS = ("lloyd", "lbfgs", "lloyd-plbfgs")
+
+
+@dataclass
+class StoppingCriteria:
+    """optimizer.py:40-53."""
+
+    max_iterations: int = 2000
+    movement_tol: float = 5e-4
+    grad_tol: float = 5e-4
+    stall_tol: float = 1e-7
+
+    def __post_init__(self):
+        if min(self.movement_tol, self.grad_tol, self.stall_tol) <= 0:
+            raise ValueError("stopping tolerances must be positive")
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be >= 1")
+
+
+@dataclass
+class IterationRecord:
+    """optimizer.py:56-63."""
+
+    n: int
+    energy: float
+    grad_norm: float
+    step: float
+    fevals: int | None
+    time_ms: float
+
+
+@dataclass
+class MinimizeResult:
+    """optimizer.py:249-257 (``points`` and ``final`` arrays are NumPy)."""
+
+    points: np.ndarray
+    records: list
+    reason: str
+    fevals: int
+    resets: int
+    wall_time: float
+    final: EvalResult = field(repr=False, default=None)
+
+
+def wolfe_line_search(phi, f0: float, dphi0: float, c1: float = WOLFE_C1, c2: float = WOLFE_C2,
+                      max_evals: int = MAX_LINE_SEARCH_EVALS, initial_step: float = 1.0):
+    """Strong-Wolfe bracketing + quadratic zoom (optimizer.py:170-237), scalar logic only."""
+    if dphi0 >= 0.0:
+        raise NonDescentError(f"line search needs a descent direction, dphi0={dphi0:.3e}")
+    evals = 0
+    best = None
+
+    def record(alpha, f, payload):
+        nonlocal best
+        if f < f0 and (best is None or f < best[0]):
+            best = (f, alpha, payload)
+
+    def exhausted_result():
+        if best is None:
+            raise LineSearchFailure(f"no decrease within {max_evals} evaluations")
+        f, alpha, payload = best
+        return alpha, f, payload, evals, True
+
+    def zoom(lo, f_lo, d_lo, hi, f_hi):
+        nonlocal evals
+        while evals < max_evals:
+            span = hi - lo
+            denom = 2.0 * (f_hi - f_lo - d_lo * span)
+            alpha = lo - d_lo * span * span / denom if denom != 0.0 else lo + 0.5 * span
+            low, high = (lo, hi) if lo < hi else (hi, lo)
+            margin = 0.1 * abs(span)
+            if not (low + margin <= alpha <= high - margin):
+                alpha = lo + 0.5 * span
+            f, d, payload = phi(alpha)
+            evals += 1
+            record(alpha, f, payload)
+            if f > f0 + c1 * alpha * dphi0 or f >= f_lo:
+                hi, f_hi = alpha, f
+            else:
+                if abs(d) <= -c2 * dphi0:
+                    return alpha, f, payload, evals, False
+                if d * span >= 0.0:
+                    hi, f_hi = lo, f_lo
+                lo, f_lo, d_lo = alpha, f, d
+        return exhausted_result()
+
+    alpha_prev, f_prev, d_prev = 0.0, f0, dphi0
+    alpha = initial_step
+    first = True
+    while evals < max_evals:
+        f, d, payload = phi(alpha)
+        evals += 1
+        record(alpha, f, payload)
+        if f > f0 + c1 * alpha * dphi0 or (not first and f >= f_prev):
+            return zoom(alpha_prev, f_prev, d_prev, alpha, f)
+        if abs(d) <= -c2 * dphi0:
+            return alpha, f, payload, evals, False
+        if d >= 0.0:
+            return zoom(alpha, f, d, alpha_prev, f_prev)
+        alpha_prev, f_prev, d_prev = alpha, f, d
+        alpha *= 2.0
+        first = False
+    return exhausted_result()
+
+
+class _DeviceOps:
+    """Thin wrappers over the optimizer entry points of the C ABI."""
+
+    def __init__(self, ctx, n: int):
+        self.ctx = ctx
+        self.n = n
+
+    def history_clear(self):
+        self.ctx.call("scvt_history_clear")
+
+    def gamma(self) -> float:
+        g = ctypes.c_double()
+        self.ctx.call("scvt_history_gamma", ctypes.byref(g))
+        return g.value
+
+    def direction(self, g, diag, gamma, q) -> float:
+        qg = ctypes.c_double()
+        self.ctx.call("scvt_lbfgs_direction", _lib.dptr(g), _lib.dptr(diag), float(gamma), self.n,
+                      _lib.dptr(q), ctypes.byref(qg))
+        return qg.value
+
+    def tangent(self, q, z, g, q3) -> float:
+        d = ctypes.c_double()
+        self.ctx.call("scvt_tangent_project", _lib.dptr(q), _lib.dptr(z), _lib.dptr(g), self.n,
+                      _lib.dptr(q3), ctypes.byref(d))
+        return d.value
+
+    def trial(self, z, q3, alpha, zt, norms):
+        self.ctx.call("scvt_trial_point", _lib.dptr(z), _lib.dptr(q3), float(alpha), self.n,
+                      _lib.dptr(zt), _lib.dptr(norms))
+
+    def dirderiv(self, g, q3, norms) -> float:
+        d = ctypes.c_double()
+        self.ctx.call("scvt_directional_derivative", _lib.dptr(g), _lib.dptr(q3),
+                      _lib.dptr(norms), self.n, ctypes.byref(d))
+        return d.value
+
+    def lloyd(self, first, z_out):
+        self.ctx.call("scvt_lloyd_step", _lib.dptr(first), self.n, _lib.dptr(z_out),
+                      what="lloyd_step")
+
+    def minimum(self, v) -> float:
+        m = ctypes.c_double()
+        self.ctx.call("scvt_min", _lib.dptr(v), v.numel(), ctypes.byref(m))
+        return m.value
+
+    def scale(self, a, x, y):
+        self.ctx.call("scvt_scale", float(a), _lib.dptr(x), x.numel(), _lib.dptr(y))
+
+    def push(self, z_old, z_new, g_old, g_new):
+        pushed = ctypes.c_int32()
+        mv = ctypes.c_double()
+        self.ctx.call("scvt_history_push", _lib.dptr(z_old), _lib.dptr(z_new), _lib.dptr(g_old),
+                      _lib.dptr(g_new), self.n, ctypes.byref(pushed), ctypes.byref(mv))
+        return bool(pushed.value), mv.value
+
+    def max_abs_diff(self, a, b) -> float:
+        m = ctypes.c_double()
+        self.ctx.call("scvt_max_abs_diff", _lib.dptr(a), _lib.dptr(b), a.numel(), ctypes.byref(m))
+        return m.value
+
+    def normalize(self, z):
+        self.ctx.call("scvt_normalize_rows", _lib.dptr(z), self.n)
+
+
+def _to_host(res: EvalResult) -> EvalResult:
+    return EvalResult(energy=res.energy, grad=res.grad.cpu().numpy(), grad_norm=res.grad_norm,
+                      lloyd_diag=res.lloyd_diag.cpu().numpy(), first=res.first.cpu().numpy(),
+                      migration=res.migration, mass=res.mass.cpu().numpy(),
+                      obtuse_count=res.obtuse_count)
+
+
+def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCriteria | None = None,
+             corrections: int = 7, callback=None) -> MinimizeResult:
+    """Drive one of the iteration methods to a stopping criterion (optimizer.py:278-391).
+
+    ``points``: (K, 3) NumPy array or CUDA tensor.  ``callback(n, z_new, res_new)`` receives
+    CUDA tensors (zero-copy).  Returns NumPy ``points`` and ``final``."""
+    import torch
+
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}; expected one of {METHODS}")
+    if not isinstance(evaluator, MeshEvaluator):
+        raise TypeError("minimize drives the GPU MeshEvaluator of this package")
+    criteria = criteria or StoppingCriteria()
+    z, _ = evaluator._as_device(points)
+    z = z.clone()
+    k = z.shape[0]
+    ctx = evaluator._ensure_ctx(k, corrections)
+    ops = _DeviceOps(ctx, k)
+    ops.normalize(z)                                           # optimizer.py:290
+    t0 = time.perf_counter()
+    res = evaluator.evaluate_device(z)                         # optimizer.py:293
+    fevals_total = 1
+    ops.history_clear()                                        # CorrectionHistory(m)
+    records: list[IterationRecord] = []
+    resets = 0
+    reason = "max-iterations"
+    q = torch.empty_like(z)
+    q3 = torch.empty_like(z)
+
+    for n in range(1, criteria.max_iterations + 1):
+        t_iter = time.perf_counter()
+        f_prev = res.energy
+        if method == "lloyd":
+            z_new = torch.empty_like(z)
+            ops.lloyd(res.first, z_new)                        # optimizer.py:304
+            res_new = evaluator.evaluate_device(z_new)
+            fevals_total += 1
+            fevals_iter = None
+            alpha = 1.0
+            movement = ops.max_abs_diff(z_new, z)
+        else:
+            # _initial_inverse (optimizer.py:260-275)
+            diag = None
+            gamma = ops.gamma()
+            if method == "lloyd-plbfgs":
+                if ops.minimum(res.lloyd_diag) <= 0.0:
+                    logger.warning("nonpositive Lloyd diagonal; falling back to gamma identity")
+                else:
+                    diag = res.lloyd_diag
+            qg = ops.direction(res.grad, diag, gamma, q)       # two_loop_direction
+            if qg >= 0.0:
+                logger.warning("non-descent direction at iteration %d; history reset", n)
+                ops.history_clear()
+                resets += 1
+                qg = ops.direction(res.grad, diag, gamma, q)
+                if qg >= 0.0:
+                    ops.scale(-ops.gamma(), res.grad, q)        # q = -hist.gamma() * g
+            dphi0 = ops.tangent(q, z, res.grad, q3)            # optimizer.py:322-333
+            q3_now = q3.clone()
+
+            def phi(alpha, z=z, q3=q3_now):
+                zt = torch.empty_like(z)
+                norms = torch.empty(k, dtype=torch.float64, device=z.device)
+                ops.trial(z, q3, alpha, zt, norms)
+                r = evaluator.evaluate_device(zt)
+                d = ops.dirderiv(r.grad, q3, norms)
+                return r.energy, d, (zt, r)
+
+            try:
+                alpha, _, payload, evals, exhausted = wolfe_line_search(phi, res.energy, dphi0)
+                z_new, res_new = payload
+                fevals_iter = evals
+                if exhausted:
+                    logger.debug("line search exhausted at iteration %d", n)
+            except (NonDescentError, LineSearchFailure) as exc:
+                logger.warning("line search failed at iteration %d (%s); Lloyd fallback", n, exc)
+                ops.history_clear()
+                resets += 1
+                z_new = torch.empty_like(z)
+                try:
+                    ops.lloyd(res.first, z_new)
+                except CentroidAtOriginError:
+                    raise
+                res_new = evaluator.evaluate_device(z_new)
+                fevals_iter = 1
+                alpha = 0.0
+            fevals_total += fevals_iter
+            _, movement = ops.push(z, z_new, res.grad, res_new.grad)   # optimizer.py:351-355
+        records.append(IterationRecord(
+            n=n, energy=res_new.energy, grad_norm=res_new.grad_norm, step=alpha,
+            fevals=fevals_iter, time_ms=(time.perf_counter() - t_iter) * 1e3))
+        if callback is not None:
+            callback(n, z_new, res_new)
+        z, res = z_new, res_new
+        if movement <= criteria.movement_tol:
+            reason = "movement"
+            break
+        if abs(res.energy - f_prev) / abs(f_prev) < criteria.stall_tol:
+            reason = "energy-stall"
+            break
+        if res.grad_norm / res.energy <= criteria.grad_tol:
+            reason = "gradient"
+            break
+    torch.cuda.current_stream().synchronize()
+    wall = time.perf_counter() - t0
+    return MinimizeResult(points=z.cpu().numpy(), records=records, reason=reason,
+                          fevals=fevals_total, resets=resets, wall_time=wall, final=_to_host(res))
+
+
+def lloyd_step(points, first_moments) -> np.ndarray:
+    """optimizer.py:240-246 (host convenience for NumPy callers)."""
+    first_moments = np.asarray(first_moments, dtype=float)
+    norms = np.linalg.norm(first_moments, axis=1)
+    if np.any(norms <= 1e-12):
+        bad = np.flatnonzero(norms <= 1e-12)
+        raise CentroidAtOriginError(f"first moment ~0 for cells {bad[:8].tolist()}")
+    return first_moments / norms[:, None]
