@@ -144,6 +144,16 @@ int scvt_scale(scvt_ctx* ctx, double a, const double* x, int64_t len, double* y)
 /* normalise rows of (n,3) in place (optimizer.py:290) */
 int scvt_normalize_rows(scvt_ctx* ctx, double* z, int64_t n);
 
+/* live CUDA-event timing of the evaluation kernels (bench roofline).  When enabled, every
+ * scvt_evaluate records events around the cell-construction kernels, the quadrature kernel
+ * and the whole evaluation on the context stream; read accumulates them:
+ * ms_out[0..2] / counts_out[0..2] = {cells, quadrature, evaluate}. */
+int scvt_profile_enable(scvt_ctx* ctx, int on);
+int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int reset);
+/* measured FP64 DFMA throughput of `device` in TFLOP/s (2 FLOPs per FMA): the FP64
+ * roofline denominator, which MEASURED_PEAKS.json does not carry */
+int scvt_fp64_peak(int device, double* tflops_out);
+
 /* launches of library kernels since the context was created (bench accounting) */
 int64_t scvt_launch_count(const scvt_ctx* ctx);
 

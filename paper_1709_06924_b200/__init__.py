@@ -11,7 +11,7 @@ from .density import DensityField, density_preset, sample_by_density
 from .errors import *  # noqa: F401,F403
 from .geometry import (QUADRATURE_RULES, QuadratureRule, composite_nodes, icosahedron_vertices,
                        normalize, random_sphere_points)
-from .optimizer import IterationRecord, MinimizeResult, StoppingCriteria, minimize
+from .optimizer import IterationRecord, MinimizeResult, Minimizer, StoppingCriteria, minimize
 from .pipeline import (EvalResult, MeshEvaluator, SphericalTriangulation, bisect,
                        bisection_ladder, parallel_iteration)
 
@@ -31,6 +31,7 @@ __all__ = [
     "IterationRecord",
     "MinimizeResult",
     "minimize",
+    "Minimizer",
     "MeshEvaluator",
     "EvalResult",
     "SphericalTriangulation",

@@ -202,13 +202,30 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
                         double c2 = 0.0;
                         int j = -1;
                         V3 zj = v3(0, 0, 0);
+                        double cax = 0.0, cay = 0.0;
                         if (p < p1) {
                             j = g.ids[p];
                             const double* q = g.zs + 4 * (int64_t)p;
                             zj = v3(q[0], q[1], q[2]);
                             V3 d = sub(zj, zi);
                             c2 = dot(d, d);
-                            acc = j != i && c2 <= r2 && c2 > lo_c2 && c2 > 0.0;
+                            acc = j != i && c2 <= r2 && c2 > lo_c2 && c2 > 0.0 &&
+                                  c2 < 4.0 * R2 * (1.0 + 1e-12);
+                            cax = dot(d, e1);
+                            cay = dot(d, e2);
+                        }
+                        // vertex-disk test, one candidate per lane: j can cut the cell only if
+                        // some current vertex is (about) as close to z_j as to z_i
+                        if (__any_sync(FULL, acc)) {
+                            bool may = false;
+                            const double cb2 = 0.5 * c2;
+                            for (int k = 0; k < P.n; ++k) {
+                                double vx = __shfl_sync(FULL, P.vx, k);
+                                double vy = __shfl_sync(FULL, P.vy, k);
+                                double t1 = cax * vx, t2 = cay * vy;
+                                may |= t1 + t2 - cb2 > -1e-9 * (fabs(t1) + fabs(t2) + cb2);
+                            }
+                            acc = acc && may;
                         }
                         unsigned ma = __ballot_sync(FULL, acc);
                         while (ma) {

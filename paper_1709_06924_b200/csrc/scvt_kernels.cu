@@ -613,6 +613,11 @@ struct scvt_ctx {
     std::vector<double> rho, ys, yy;
     int hist_head = 0, hist_count = 0;
     double* d_tmp_s = nullptr; double* d_tmp_y = nullptr;   // staging for push
+    // live per-kernel timing (bench roofline): pairs {cells, quad, evaluate}
+    bool prof = false;
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    double prof_ms[4] = {0, 0, 0, 0};
+    int64_t prof_n[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -739,12 +744,14 @@ int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
     LAUNCHED();
     GridView g;
     g.zs = ctx->d_zs; g.ids = ctx->d_ids; g.start = ctx->d_start; g.z = z; g.G = G; g.n = n;
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], s));
     k_cells_warp<<<blocks_for(n, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
         g, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
     LAUNCHED();
     k_cells<<<blocks_for(n, CELL_THREADS), CELL_THREADS, 0, s>>>(g, ctx->d_nbr, ctx->d_deg,
                                                                 ctx->d_status, ctx->d_status + 8);
     LAUNCHED();
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
     k_verify<<<blocks_for(n, 128), 128, 0, s>>>(z, (int)n, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                                                ctx->d_status, ctx->d_status + 8);
     LAUNCHED();
@@ -792,6 +799,7 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
     a.status = ctx->d_status;
     unsigned grid = blocks_for(n_inc, QUAD_THREADS);
     size_t smem = 3 * (size_t)ctx->nq * sizeof(double);
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[2], s));
     switch (ctx->dp.kind) {
         case DEN_CONST: TRY(launch_quad_kind<DEN_CONST>(ctx, a, grid, smem)); break;
         case DEN_X3: TRY(launch_quad_kind<DEN_X3>(ctx, a, grid, smem)); break;
@@ -801,6 +809,7 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
         case DEN_TANH4X2: TRY(launch_quad_kind<DEN_TANH4X2>(ctx, a, grid, smem)); break;
         default: return fail(ctx, SCVT_ERR_CONFIG, "bad density kind %d", ctx->dp.kind);
     }
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[3], s));
     k_gather<<<blocks_for(n, 256), 256, 0, s>>>(z, (int)n, ctx->d_inc_start, ctx->d_part,
                                                 ctx->d_obt, n_inc, ctx->d_status, grad, first,
                                                 mass, diag, ctx->d_egen, ctx->d_g2gen,
@@ -815,7 +824,19 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
                                                           ctx->d_partials + 2 * RED_BLOCKS);
     LAUNCHED();
     TRY(finish_slots(ctx, 3));
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[5], s));
     TRY(readback(ctx, 3));
+    if (ctx->prof) {
+        float a = 0.f, b = 0.f, c = 0.f;
+        CK(cudaEventElapsedTime(&b, ctx->ev[2], ctx->ev[3]));
+        CK(cudaEventElapsedTime(&c, ctx->ev[4], ctx->ev[5]));
+        if (ctx->prof_n[3] == 0) {   // cells pair recorded only on the scvt_evaluate path
+            CK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+            ctx->prof_ms[0] += a; ++ctx->prof_n[0];
+        }
+        ctx->prof_ms[1] += b; ++ctx->prof_n[1];
+        ctx->prof_ms[2] += c; ++ctx->prof_n[2];
+    }
     int st = ctx->h_status[0];
     if (st) return status_to_code(ctx, st);
     scalars_host[0] = ctx->h_scal[0];
@@ -834,6 +855,24 @@ const char* scvt_version(void) { return "scvt_b200 0.1.0 (sm_100a)"; }
 const char* scvt_last_error(const scvt_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
 int64_t scvt_launch_count(const scvt_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int scvt_profile_enable(scvt_ctx* ctx, int on) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (on && !ctx->ev[0])
+        for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+    ctx->prof = on != 0;
+    return SCVT_OK;
+}
+
+int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int reset) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    for (int k = 0; k < 3; ++k) {
+        ms_out[k] = ctx->prof_ms[k];
+        counts_out[k] = ctx->prof_n[k];
+        if (reset) { ctx->prof_ms[k] = 0.0; ctx->prof_n[k] = 0; }
+    }
+    return SCVT_OK;
+}
 
 int scvt_set_stream(scvt_ctx* ctx, void* stream) {
     if (!ctx) return SCVT_ERR_CONFIG;
@@ -956,6 +995,8 @@ int scvt_destroy(scvt_ctx* ctx) {
                    ctx->d_tmp_s, ctx->d_tmp_y};
     for (void* p : dev)
         if (p) cudaFree(p);
+    for (cudaEvent_t e : ctx->ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
     if (ctx->h_status) cudaFreeHost(ctx->h_status);
     delete ctx;
@@ -1009,6 +1050,8 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
 int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
                   double* mass, double* lloyd_diag, double* scalars_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+    ctx->prof_n[3] = 0;
     TRY(reset_status(ctx));
     TRY(build_cells(ctx, z, n));
     return moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
@@ -1020,6 +1063,8 @@ int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const 
     if (!ctx) return SCVT_ERR_CONFIG;
     if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n > n_max");
     if (t != 2 * n - 4) return fail(ctx, SCVT_ERR_COVERAGE, "T=%lld != 2n-4", (long long)t);
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+    ctx->prof_n[3] = 1;   // no cell-construction pair on this path
     TRY(reset_status(ctx));
     TRY(cells_from_triangles(ctx, tri, t, n));
     return moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);

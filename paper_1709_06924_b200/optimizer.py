@@ -210,43 +210,49 @@ def _to_host(res: EvalResult) -> EvalResult:
                       obtuse_count=res.obtuse_count)
 
 
-def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCriteria | None = None,
-             corrections: int = 7, callback=None) -> MinimizeResult:
-    """Drive one of the iteration methods to a stopping criterion (optimizer.py:278-391).
+class Minimizer:
+    """The state of one `minimize` run, advanced one iteration at a time.
 
-    ``points``: (K, 3) NumPy array or CUDA tensor.  ``callback(n, z_new, res_new)`` receives
-    CUDA tensors (zero-copy).  Returns NumPy ``points`` and ``final``."""
-    import torch
+    `minimize` is `Minimizer(...)` + `step()` until a stopping rule fires; the benchmark
+    drives `step()` directly so warm-up and timed iterations continue one trajectory."""
 
-    if method not in METHODS:
-        raise ValueError(f"unknown method {method!r}; expected one of {METHODS}")
-    if not isinstance(evaluator, MeshEvaluator):
-        raise TypeError("minimize drives the GPU MeshEvaluator of this package")
-    criteria = criteria or StoppingCriteria()
-    z, _ = evaluator._as_device(points)
-    z = z.clone()
-    k = z.shape[0]
-    ctx = evaluator._ensure_ctx(k, corrections)
-    ops = _DeviceOps(ctx, k)
-    ops.normalize(z)                                           # optimizer.py:290
-    t0 = time.perf_counter()
-    res = evaluator.evaluate_device(z)                         # optimizer.py:293
-    fevals_total = 1
-    ops.history_clear()                                        # CorrectionHistory(m)
-    records: list[IterationRecord] = []
-    resets = 0
-    reason = "max-iterations"
-    q = torch.empty_like(z)
-    q3 = torch.empty_like(z)
+    def __init__(self, points, method: str, evaluator: MeshEvaluator, corrections: int = 7):
+        import torch
 
-    for n in range(1, criteria.max_iterations + 1):
+        if method not in METHODS:
+            raise ValueError(f"unknown method {method!r}; expected one of {METHODS}")
+        if not isinstance(evaluator, MeshEvaluator):
+            raise TypeError("minimize drives the GPU MeshEvaluator of this package")
+        self.torch = torch
+        self.method = method
+        self.evaluator = evaluator
+        z, _ = evaluator._as_device(points)
+        self.z = z.clone()
+        self.k = self.z.shape[0]
+        self.ctx = evaluator._ensure_ctx(self.k, corrections)
+        self.ops = _DeviceOps(self.ctx, self.k)
+        self.ops.normalize(self.z)                               # optimizer.py:290
+        self.res = evaluator.evaluate_device(self.z)             # optimizer.py:293
+        self.fevals = 1
+        self.ops.history_clear()                                 # CorrectionHistory(m)
+        self.resets = 0
+        self.n = 0
+        self.q = torch.empty_like(self.z)
+        self.q3 = torch.empty_like(self.z)
+
+    def step(self):
+        """One iteration (optimizer.py:300-366).  Returns (record, movement, z_new, res_new)
+        and advances the state; the caller applies the stopping rules."""
+        torch = self.torch
+        ops, ev, z, res, k = self.ops, self.evaluator, self.z, self.res, self.k
+        self.n += 1
+        n = self.n
         t_iter = time.perf_counter()
-        f_prev = res.energy
-        if method == "lloyd":
+        if self.method == "lloyd":
             z_new = torch.empty_like(z)
-            ops.lloyd(res.first, z_new)                        # optimizer.py:304
-            res_new = evaluator.evaluate_device(z_new)
-            fevals_total += 1
+            ops.lloyd(res.first, z_new)                          # optimizer.py:304
+            res_new = ev.evaluate_device(z_new)
+            self.fevals += 1
             fevals_iter = None
             alpha = 1.0
             movement = ops.max_abs_diff(z_new, z)
@@ -254,27 +260,27 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
             # _initial_inverse (optimizer.py:260-275)
             diag = None
             gamma = ops.gamma()
-            if method == "lloyd-plbfgs":
+            if self.method == "lloyd-plbfgs":
                 if ops.minimum(res.lloyd_diag) <= 0.0:
                     logger.warning("nonpositive Lloyd diagonal; falling back to gamma identity")
                 else:
                     diag = res.lloyd_diag
-            qg = ops.direction(res.grad, diag, gamma, q)       # two_loop_direction
+            q, q3 = self.q, self.q3
+            qg = ops.direction(res.grad, diag, gamma, q)         # two_loop_direction
             if qg >= 0.0:
                 logger.warning("non-descent direction at iteration %d; history reset", n)
                 ops.history_clear()
-                resets += 1
+                self.resets += 1
                 qg = ops.direction(res.grad, diag, gamma, q)
                 if qg >= 0.0:
-                    ops.scale(-ops.gamma(), res.grad, q)        # q = -hist.gamma() * g
-            dphi0 = ops.tangent(q, z, res.grad, q3)            # optimizer.py:322-333
-            q3_now = q3.clone()
+                    ops.scale(-ops.gamma(), res.grad, q)          # q = -hist.gamma() * g
+            dphi0 = ops.tangent(q, z, res.grad, q3)              # optimizer.py:322-333
 
-            def phi(alpha, z=z, q3=q3_now):
+            def phi(alpha, z=z, q3=q3):
                 zt = torch.empty_like(z)
                 norms = torch.empty(k, dtype=torch.float64, device=z.device)
                 ops.trial(z, q3, alpha, zt, norms)
-                r = evaluator.evaluate_device(zt)
+                r = ev.evaluate_device(zt)
                 d = ops.dirderiv(r.grad, q3, norms)
                 return r.energy, d, (zt, r)
 
@@ -287,24 +293,39 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
             except (NonDescentError, LineSearchFailure) as exc:
                 logger.warning("line search failed at iteration %d (%s); Lloyd fallback", n, exc)
                 ops.history_clear()
-                resets += 1
+                self.resets += 1
                 z_new = torch.empty_like(z)
-                try:
-                    ops.lloyd(res.first, z_new)
-                except CentroidAtOriginError:
-                    raise
-                res_new = evaluator.evaluate_device(z_new)
+                ops.lloyd(res.first, z_new)
+                res_new = ev.evaluate_device(z_new)
                 fevals_iter = 1
                 alpha = 0.0
-            fevals_total += fevals_iter
+            self.fevals += fevals_iter
             _, movement = ops.push(z, z_new, res.grad, res_new.grad)   # optimizer.py:351-355
-        records.append(IterationRecord(
-            n=n, energy=res_new.energy, grad_norm=res_new.grad_norm, step=alpha,
-            fevals=fevals_iter, time_ms=(time.perf_counter() - t_iter) * 1e3))
+        rec = IterationRecord(n=n, energy=res_new.energy, grad_norm=res_new.grad_norm, step=alpha,
+                              fevals=fevals_iter, time_ms=(time.perf_counter() - t_iter) * 1e3)
+        self.z, self.res = z_new, res_new
+        return rec, movement, z_new, res_new
+
+
+def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCriteria | None = None,
+             corrections: int = 7, callback=None) -> MinimizeResult:
+    """Drive one of the iteration methods to a stopping criterion (optimizer.py:278-391).
+
+    ``points``: (K, 3) NumPy array or CUDA tensor.  ``callback(n, z_new, res_new)`` receives
+    CUDA tensors (zero-copy).  Returns NumPy ``points`` and ``final``."""
+    criteria = criteria or StoppingCriteria()
+    t0 = time.perf_counter()
+    st = Minimizer(points, method, evaluator, corrections)
+    records: list[IterationRecord] = []
+    reason = "max-iterations"
+    for _ in range(criteria.max_iterations):
+        f_prev = st.res.energy
+        rec, movement, z_new, res_new = st.step()
+        records.append(rec)
         if callback is not None:
-            callback(n, z_new, res_new)
-        z, res = z_new, res_new
-        if movement <= criteria.movement_tol:
+            callback(rec.n, z_new, res_new)
+        res = st.res
+        if movement <= criteria.movement_tol:                   # optimizer.py:368-376
             reason = "movement"
             break
         if abs(res.energy - f_prev) / abs(f_prev) < criteria.stall_tol:
@@ -313,10 +334,11 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
         if res.grad_norm / res.energy <= criteria.grad_tol:
             reason = "gradient"
             break
-    torch.cuda.current_stream().synchronize()
+    st.torch.cuda.current_stream().synchronize()
     wall = time.perf_counter() - t0
-    return MinimizeResult(points=z.cpu().numpy(), records=records, reason=reason,
-                          fevals=fevals_total, resets=resets, wall_time=wall, final=_to_host(res))
+    return MinimizeResult(points=st.z.cpu().numpy(), records=records, reason=reason,
+                          fevals=st.fevals, resets=st.resets, wall_time=wall,
+                          final=_to_host(st.res))
 
 
 def lloyd_step(points, first_moments) -> np.ndarray:
