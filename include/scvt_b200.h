@@ -63,7 +63,17 @@ typedef struct scvt_config {
     const double* node_l1;    /* HOST arrays [n_nodes]: barycentric (l1, l2) of each composite */
     const double* node_l2;    /*   node relative to the fan sub-triangle (v0, v1, v2) and its  */
     const double* node_w;     /*   weight  w_q / 4^depth  (geometry.py:142-185 + 383-407)      */
+    /* optional piecewise-polynomial form of rho^(1/4) for the tanh4 kinds (NULL = evaluate
+     * the closed form with atan2/tanh per node).  HOST array [2][table_intervals]
+     * [table_degree+1]: branch 0 in x = |y - c|, branch 1 in x = |y + c|, x in [0, sqrt 2],
+     * interval width table_width, local variable tau = 2 (x/w - k) - 1, monomial coeffs. */
+    int32_t table_intervals;
+    int32_t table_degree;     /* must equal SCVT_TABLE_DEGREE                               */
+    double table_width;
+    const double* table_coef;
 } scvt_config;
+
+#define SCVT_TABLE_DEGREE 8
 
 #define SCVT_MAX_NODES 2304
 #define SCVT_MAX_DEGREE 32

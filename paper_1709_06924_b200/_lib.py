@@ -42,6 +42,10 @@ class ScvtConfig(ctypes.Structure):
         ("node_l1", _c_dbl_p),
         ("node_l2", _c_dbl_p),
         ("node_w", _c_dbl_p),
+        ("table_intervals", ctypes.c_int32),
+        ("table_degree", ctypes.c_int32),
+        ("table_width", ctypes.c_double),
+        ("table_coef", _c_dbl_p),
     ]
 
 
@@ -125,7 +129,7 @@ def dptr(t) -> int:
 
 
 def make_config(density_params: dict, measure: str, l1: np.ndarray, l2: np.ndarray,
-                w: np.ndarray, lbfgs_m: int):
+                w: np.ndarray, lbfgs_m: int, use_table: bool = True):
     cfg = ScvtConfig()
     cfg.density_kind = int(density_params["density_kind"])
     if measure not in ("flat", "sphere"):
@@ -144,4 +148,13 @@ def make_config(density_params: dict, measure: str, l1: np.ndarray, l2: np.ndarr
     cfg.node_l1 = keep[0].ctypes.data_as(_c_dbl_p)
     cfg.node_l2 = keep[1].ctypes.data_as(_c_dbl_p)
     cfg.node_w = keep[2].ctypes.data_as(_c_dbl_p)
+    table = density_params.get("table") if use_table else None
+    if table is not None:
+        coef, width = table
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        keep.append(coef)
+        cfg.table_intervals = coef.shape[1]
+        cfg.table_degree = coef.shape[2] - 1
+        cfg.table_width = float(width)
+        cfg.table_coef = coef.ctypes.data_as(_c_dbl_p)
     return cfg, keep

@@ -525,7 +525,11 @@ SCVT_HD int build_cell(const GridView& g, int i, V3 zi, int* nbr_out, CellStats*
 
 // ------------------------------------------------------------------ density
 enum DensityKind { DEN_CONST = 0, DEN_X3 = 1, DEN_X16 = 2, DEN_TANH = 3, DEN_TANH4 = 4,
-                   DEN_TANH4X2 = 5 };
+                   DEN_TANH4X2 = 5,
+                   // internal: tanh4 kinds evaluated through the rho^(1/4) table
+                   DEN_TANH4_TAB = 6, DEN_TANH4X2_TAB = 7 };
+
+constexpr int TAB_P = 8;   // polynomial degree of the rho^(1/4) table (SCVT_TABLE_DEGREE)
 
 struct DensityParams {
     int kind;
@@ -533,7 +537,32 @@ struct DensityParams {
     double c0x, c0y, c0z, c1x, c1y, c1z;
     double w_lon, w_lat;
     double lat_c, lon_c, cos_lat_c, sin_lat_c;   // x16 centre (precomputed on host)
+    const double* tab;   // [2][tab_k][TAB_P+1] (shared memory inside the kernel)
+    int tab_k;
+    double tab_invw;
 };
+
+// u = rho^(1/4) of the tanh^4 profile from the table (density.tanh4_table): chord to the
+// centre when d <= 90 deg, chord to its antipode otherwise; Horner in tau.
+SCVT_HD double tab_u(const DensityParams& p, V3 y, V3 c) {
+    V3 dm = sub(y, c);
+    double r2 = dot(dm, dm);
+    int br = 0;
+    if (r2 > 2.0) {
+        V3 dp = add(y, c);
+        r2 = dot(dp, dp);
+        br = 1;
+    }
+    double t = sqrt(r2) * p.tab_invw;
+    int k = (int)t;
+    if (k > p.tab_k - 1) k = p.tab_k - 1;
+    double tau = 2.0 * (t - (double)k) - 1.0;
+    const double* co = p.tab + (br * p.tab_k + k) * (TAB_P + 1);
+    double acc = co[TAB_P];
+#pragma unroll
+    for (int j = TAB_P - 1; j >= 0; --j) acc = fma(acc, tau, co[j]);
+    return acc;
+}
 
 SCVT_HD double geodesic(V3 a, V3 b) { return atan2(norm3(cross(a, b)), dot(a, b)); }
 
@@ -544,6 +573,12 @@ SCVT_HD double density_eval(const DensityParams& p, V3 y, int* pole) {
     if (KIND == DEN_X3) {
         double z2 = y.z * y.z;
         return (1.0 - p.gamma) * (z2 * z2) + p.gamma;
+    }
+    if (KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB) {
+        double u = tab_u(p, y, v3(p.c0x, p.c0y, p.c0z));
+        if (KIND == DEN_TANH4X2_TAB) u = fmax(u, tab_u(p, y, v3(p.c1x, p.c1y, p.c1z)));
+        double u2 = u * u;
+        return u2 * u2;
     }
     if (KIND == DEN_TANH4 || KIND == DEN_TANH4X2) {
         double d = geodesic(y, v3(p.c0x, p.c0y, p.c0z));

@@ -158,14 +158,29 @@ __global__ void k_verify(const double* __restrict__ z, int n, const int* __restr
     if (namb) atomicAdd(&stats[3], namb);
 }
 
-__global__ void k_fill_incidences(int n, const int* __restrict__ deg,
-                                  const int* __restrict__ inc_start, int* __restrict__ inc_gen,
-                                  int cap) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int s = inc_start[i], d = deg[i];
+// incidence CSR in bucket (spatial) order: sorted slot p -> generator ids[p]
+__global__ void k_deg_sorted(int n, const int* __restrict__ ids, const int* __restrict__ deg,
+                             int* __restrict__ degs) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > n) return;
+    degs[p] = p == n ? 0 : deg[ids[p]];
+}
+
+__global__ void k_fill_incidences(int n, const int* __restrict__ ids, const int* __restrict__ deg,
+                                  const int* __restrict__ inc_start, int* __restrict__ inc_base,
+                                  int* __restrict__ inc_gen, int cap) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int i = ids[p];
+    int s = inc_start[p], d = deg[i];
+    inc_base[i] = s;
     for (int t = 0; t < d; ++t)
         if (s + t < cap) inc_gen[s + t] = i;
+}
+
+__global__ void k_iota(int n, int* __restrict__ ids) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) ids[p] = p;
 }
 
 // ------------------------------------------------------------------ quadrature
@@ -173,11 +188,13 @@ struct QuadArgs {
     const double* z;
     const int* nbr;
     const int* deg;
-    const int* inc_start;
+    const int* inc_start;   // [n+1] in sorted order (total at [n])
+    const int* inc_base;    // [n] by generator id
     const int* inc_gen;
     int n;
     int n_inc;            // expected incidences 6n - 12
     const double* nodes;  // device [3][nq]: l1, l2, w
+    const double* table;  // device rho^(1/4) table (tanh4 kinds) or null
     int nq;
     DensityParams dp;
     double* part;         // [5][n_inc] SoA
@@ -190,6 +207,12 @@ __global__ void __launch_bounds__(QUAD_THREADS)
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
     for (int q = threadIdx.x; q < 3 * a.nq; q += blockDim.x) s_nodes[q] = a.nodes[q];
+    if (KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB) {
+        double* s_tab = s_nodes + 3 * a.nq;
+        const int nt = 2 * a.dp.tab_k * (TAB_P + 1);
+        for (int q = threadIdx.x; q < nt; q += blockDim.x) s_tab[q] = a.table[q];
+        a.dp.tab = s_tab;
+    }
     __syncthreads();
     int u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= a.n_inc) return;
@@ -198,7 +221,7 @@ k_quad(QuadArgs a) {
         return;
     }
     int i = a.inc_gen[u];
-    int t = u - a.inc_start[i];
+    int t = u - a.inc_base[i];
     int d = a.deg[i];
     const int* row = a.nbr + (int64_t)i * MAXDEG;
     int j = row[t], k = row[t + 1 == d ? 0 : t + 1];
@@ -224,6 +247,7 @@ k_quad(QuadArgs a) {
 
 // per generator: fixed-order sum over its incidences, then the gradient epilogue
 __global__ void k_gather(const double* __restrict__ z, int n, const int* __restrict__ inc_start,
+                         const int* __restrict__ inc_base, const int* __restrict__ deg,
                          const double* __restrict__ part, const uint8_t* __restrict__ obtuse,
                          int64_t n_inc, const int* __restrict__ status, double* __restrict__ grad,
                          double* __restrict__ first, double* __restrict__ mass,
@@ -233,7 +257,8 @@ __global__ void k_gather(const double* __restrict__ z, int n, const int* __restr
     if (i >= n) return;
     double m = 0, cx = 0, cy = 0, cz = 0, e = 0, ob = 0;
     if (inc_start[n] == n_inc) {
-        for (int u = inc_start[i]; u < inc_start[i + 1]; ++u) {
+        const int u0 = inc_base[i], u1 = u0 + deg[i];
+        for (int u = u0; u < u1; ++u) {
             m += part[u];
             cx += part[n_inc + u];
             cy += part[2 * n_inc + u];
@@ -587,6 +612,7 @@ struct scvt_ctx {
     int nq = 0;
     int m = 7;
     double* d_nodes = nullptr;   // [3][nq]
+    double* d_table = nullptr;   // [2][tab_k][TAB_P+1] rho^(1/4) table (tanh4 kinds)
     // grid
     int g_max = 1;
     uint32_t* d_keys = nullptr; uint32_t* d_skeys = nullptr;
@@ -596,7 +622,7 @@ struct scvt_ctx {
     void* d_cub = nullptr; size_t cub_bytes = 0;
     // cells
     int* d_nbr = nullptr; int* d_deg = nullptr; uint8_t* d_amb = nullptr;
-    int* d_inc_start = nullptr; int* d_inc_gen = nullptr;
+    int* d_inc_start = nullptr; int* d_inc_gen = nullptr; int* d_inc_base = nullptr;
     int* d_pairs = nullptr; int* d_cursor = nullptr;
     // quadrature
     double* d_part = nullptr; uint8_t* d_obt = nullptr;
@@ -761,6 +787,8 @@ int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
 int cells_from_triangles(scvt_ctx* ctx, const int64_t* tri, int64_t t, int64_t n) {
     cudaStream_t s = ctx->stream;
     CK(cudaMemsetAsync(ctx->d_cursor, 0, n * sizeof(int), s));
+    k_iota<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids);
+    LAUNCHED();
     k_tl_fill<<<blocks_for(t, 256), 256, 0, s>>>(tri, t, ctx->d_cursor, ctx->d_pairs,
                                                  ctx->d_status);
     LAUNCHED();
@@ -784,21 +812,26 @@ int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t sme
 int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
             double* mass, double* diag, double* scalars_host) {
     cudaStream_t s = ctx->stream;
-    // incidence CSR over the cycles (deg[n] = 0 terminates the exclusive scan)
-    CK(cudaMemsetAsync(ctx->d_deg + n, 0, sizeof(int), s));
+    // incidence CSR over the cycles, generators in bucket order (spatially coherent warps)
+    k_deg_sorted<<<blocks_for(n + 1, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_deg,
+                                                        ctx->d_cursor);
+    LAUNCHED();
     size_t tb = ctx->cub_bytes;
-    CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, ctx->d_deg, ctx->d_inc_start, (int)n + 1, s));
+    CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, ctx->d_cursor, ctx->d_inc_start, (int)n + 1, s));
     int64_t n_inc = 6 * n - 12;
-    k_fill_incidences<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_deg, ctx->d_inc_start,
+    k_fill_incidences<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_deg,
+                                                         ctx->d_inc_start, ctx->d_inc_base,
                                                          ctx->d_inc_gen, (int)n_inc);
     LAUNCHED();
     QuadArgs a;
     a.z = z; a.nbr = ctx->d_nbr; a.deg = ctx->d_deg; a.inc_start = ctx->d_inc_start;
+    a.inc_base = ctx->d_inc_base;
     a.inc_gen = ctx->d_inc_gen; a.n = (int)n; a.n_inc = (int)n_inc; a.nodes = ctx->d_nodes;
     a.nq = ctx->nq; a.dp = ctx->dp; a.part = ctx->d_part; a.obtuse = ctx->d_obt;
+    a.table = ctx->d_table;
     a.status = ctx->d_status;
     unsigned grid = blocks_for(n_inc, QUAD_THREADS);
-    size_t smem = 3 * (size_t)ctx->nq * sizeof(double);
+    size_t smem = (3 * (size_t)ctx->nq + 2 * (size_t)ctx->dp.tab_k * (TAB_P + 1)) * sizeof(double);
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[2], s));
     switch (ctx->dp.kind) {
         case DEN_CONST: TRY(launch_quad_kind<DEN_CONST>(ctx, a, grid, smem)); break;
@@ -807,10 +840,13 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
         case DEN_TANH: TRY(launch_quad_kind<DEN_TANH>(ctx, a, grid, smem)); break;
         case DEN_TANH4: TRY(launch_quad_kind<DEN_TANH4>(ctx, a, grid, smem)); break;
         case DEN_TANH4X2: TRY(launch_quad_kind<DEN_TANH4X2>(ctx, a, grid, smem)); break;
+        case DEN_TANH4_TAB: TRY(launch_quad_kind<DEN_TANH4_TAB>(ctx, a, grid, smem)); break;
+        case DEN_TANH4X2_TAB: TRY(launch_quad_kind<DEN_TANH4X2_TAB>(ctx, a, grid, smem)); break;
         default: return fail(ctx, SCVT_ERR_CONFIG, "bad density kind %d", ctx->dp.kind);
     }
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[3], s));
-    k_gather<<<blocks_for(n, 256), 256, 0, s>>>(z, (int)n, ctx->d_inc_start, ctx->d_part,
+    k_gather<<<blocks_for(n, 256), 256, 0, s>>>(z, (int)n, ctx->d_inc_start, ctx->d_inc_base,
+                                                ctx->d_deg, ctx->d_part,
                                                 ctx->d_obt, n_inc, ctx->d_status, grad, first,
                                                 mass, diag, ctx->d_egen, ctx->d_g2gen,
                                                 ctx->d_obgen);
@@ -917,6 +953,18 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         dp.cos_lat_c = cos(dp.lat_c);
         dp.sin_lat_c = sin(dp.lat_c);
     }
+    dp.tab = nullptr;
+    dp.tab_k = 0;
+    dp.tab_invw = 0.0;
+    if (cfg->table_coef && (dp.kind == DEN_TANH4 || dp.kind == DEN_TANH4X2)) {
+        if (cfg->table_degree != TAB_P || cfg->table_intervals < 1 || cfg->table_intervals > 1024 ||
+            !(cfg->table_width > 0.0))
+            return bail(fail(ctx, SCVT_ERR_CONFIG, "bad density table (degree %d, intervals %d)",
+                             cfg->table_degree, cfg->table_intervals));
+        dp.tab_k = cfg->table_intervals;
+        dp.tab_invw = 1.0 / cfg->table_width;
+        dp.kind = dp.kind == DEN_TANH4 ? DEN_TANH4_TAB : DEN_TANH4X2_TAB;
+    }
     ctx->measure = cfg->measure;
     ctx->nq = cfg->n_nodes;
     ctx->m = cfg->lbfgs_m;
@@ -929,11 +977,12 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 #define AL(p, cnt) \
     if ((r = dalloc(ctx, &ctx->p, (size_t)(cnt)))) return bail(r)
     AL(d_nodes, 3 * ctx->nq);
+    AL(d_table, 2 * (int64_t)dp.tab_k * (TAB_P + 1));
     AL(d_keys, n); AL(d_skeys, n); AL(d_vals, n); AL(d_ids, n);
     AL(d_start, nb + 1);
     AL(d_zs, 4 * n);
     AL(d_nbr, n * MAXDEG); AL(d_deg, n + 1); AL(d_amb, n * MAXDEG);
-    AL(d_inc_start, n + 1); AL(d_inc_gen, n_inc);
+    AL(d_inc_start, n + 1); AL(d_inc_gen, n_inc); AL(d_inc_base, n);
     AL(d_pairs, n * MAXDEG * 2); AL(d_cursor, n + 1);
     AL(d_part, 5 * n_inc); AL(d_obt, n_inc);
     AL(d_egen, n); AL(d_g2gen, n); AL(d_obgen, n);
@@ -969,13 +1018,20 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
                                    cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return bail(fail(ctx, SCVT_ERR_CUDA, "node upload failed"));
     }
-    size_t smem = 3 * (size_t)ctx->nq * sizeof(double);
+    if (dp.tab_k) {
+        cudaError_t e = cudaMemcpy(ctx->d_table, cfg->table_coef,
+                                   2 * (size_t)dp.tab_k * (TAB_P + 1) * sizeof(double),
+                                   cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return bail(fail(ctx, SCVT_ERR_CUDA, "table upload failed"));
+    }
+    size_t smem = (3 * (size_t)ctx->nq + 2 * (size_t)dp.tab_k * (TAB_P + 1)) * sizeof(double);
     if (smem > 48 * 1024) {
         // opt in to large dynamic shared memory for every instantiation
 #define OPT(K)                                                                             \
     cudaFuncSetAttribute(k_quad<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     cudaFuncSetAttribute(k_quad<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
         OPT(DEN_CONST); OPT(DEN_X3); OPT(DEN_X16); OPT(DEN_TANH); OPT(DEN_TANH4); OPT(DEN_TANH4X2);
+        OPT(DEN_TANH4_TAB); OPT(DEN_TANH4X2_TAB);
 #undef OPT
     }
     ctx->rho.assign(ctx->m, 0.0);
@@ -987,9 +1043,9 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
-    void* dev[] = {ctx->d_nodes, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
+    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
-                   ctx->d_inc_start, ctx->d_inc_gen, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
+                   ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
                    ctx->d_obt, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, ctx->d_partials,
                    ctx->d_scal, ctx->d_status, ctx->d_S, ctx->d_Y, ctx->d_alpha,
                    ctx->d_tmp_s, ctx->d_tmp_y};

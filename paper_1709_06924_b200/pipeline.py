@@ -107,8 +107,10 @@ class _Context:
 class MeshEvaluator:
     """Energy / gradient evaluator on one B200 (pipeline.py:101-286 protocol).
 
-    Extra keyword ``subdivision`` (depth d of `subdivide_fans`, delaunay.py:383-407, applied
-    to every fan sub-triangle; DECISIONS.md D2) and ``device``.  ``covering``/``workers``/
+    Extra keywords ``subdivision`` (depth d of `subdivide_fans`, delaunay.py:383-407, applied
+    to every fan sub-triangle; DECISIONS.md D2), ``device`` and ``density_table`` (tanh^4
+    densities: evaluate rho through the piecewise polynomial of `density.tanh4_table`
+    instead of atan2/tanh per node; both agree to ~1e-15).  ``covering``/``workers``/
     ``backend`` are accepted for signature compatibility; the GPU path is always the
     covering-free global path, which the reference's region path reproduces bitwise
     (SURVEY.md §6.3).  ``laplacian`` (SuperLU graph Laplacian, cvt_core.py:192-240) is out of
@@ -117,7 +119,7 @@ class MeshEvaluator:
     def __init__(self, density: DensityField, rule: QuadratureRule | str, covering=None,
                  workers: int = 1, backend: str = "process", laplacian: str | None = None,
                  measure: str = "flat", eps_proj: float = EPS_PROJ, *, subdivision: int = 0,
-                 device: int | None = None):
+                 device: int | None = None, density_table: bool = True):
         if laplacian is not None:
             raise ConfigError("the Laplacian preconditioner is outside this hot path")
         if measure not in ("flat", "sphere"):
@@ -132,6 +134,7 @@ class MeshEvaluator:
         self.eps_proj = eps_proj
         self.subdivision = int(subdivision)
         self.device = device
+        self.density_table = bool(density_table)
         self.fallbacks = 0
         self.evaluations = 0
         self._l1, self._l2, self._w = composite_nodes(self.rule, self.subdivision)
@@ -156,7 +159,7 @@ class MeshEvaluator:
         if self._ctx is not None:
             self._ctx.close()
         cfg, keep = _lib.make_config(device_params(self.density), self.measure, self._l1,
-                                     self._l2, self._w, m)
+                                     self._l2, self._w, m, self.density_table)
         self._ctx = _Context(self._device_index(), max(n, 4), cfg)
         del keep
         self._m = m

@@ -258,3 +258,15 @@ def test_c4_full_size_properties():
     v = z[ref]
     area = 0.5 * np.linalg.norm(np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0]), axis=1).sum()
     assert abs(r1.mass.sum() - area) <= 1e-11 * area
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
+def test_density_table_vs_closed_form(cfg):
+    """rho^(1/4) table (density.tanh4_table) against per-node atan2/tanh on the GPU."""
+    z = P.sample_by_density(P.density_preset(cfg), 40962, 0)
+    with P.MeshEvaluator(P.density_preset(cfg), "7pt", subdivision=3) as a, \
+            P.MeshEvaluator(P.density_preset(cfg), "7pt", subdivision=3, density_table=False) as b:
+        ra, rb = a.evaluate(z), b.evaluate(z)
+    assert rel(ra.mass, rb.mass) <= 1e-13
+    assert rel(ra.first, rb.first) <= 1e-13
+    assert abs(ra.energy - rb.energy) <= 1e-13 * rb.energy
