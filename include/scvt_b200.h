@@ -94,8 +94,9 @@ const char* scvt_version(void);
  * (133-147, 172-178): writes the canonical (2n-4, 3) int64 triangle list (CCW seen from
  * outside, min-ID first, lexicographically sorted) and one flag byte per triangle
  * (1 = an edge of it failed the FP64 in-circle filter: cocircular candidate).
- * stats_host[0..5] = {triangle count, flagged triangles, max valence, filter-undecided
- * directed edges, symbolic-perturbation tie-breaks, max candidate passes of one cell}. */
+ * stats_host[0..7] = {triangle count, flagged triangles, max valence, filter-undecided
+ * directed edges, symbolic-perturbation tie-breaks, max candidate passes of one cell,
+ * cells that needed the unsorted sweep, 32-point batches those sweeps visited}. */
 int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out,
                      uint8_t* flags_out, int64_t* stats_host);
 

@@ -88,12 +88,62 @@ __device__ __forceinline__ int wpoly_clip(WPoly& P, int lane, double ax, double 
     return 1;
 }
 
+// max vertex chord^2: chord^2 is monotone in |u|^2, so reduce |u|^2 and convert once
 __device__ __forceinline__ double wpoly_R2(const WPoly& P, int lane, bool* box) {
-    double c = lane < P.n ? vertex_chord2(P.vx, P.vy) : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) c = fmax(c, __shfl_xor_sync(FULL, c, off));
     *box = __any_sync(FULL, lane < P.n && P.lab < 0);
-    return *box ? 8.0 : c;
+    if (*box) return 8.0;
+    double q = lane < P.n ? P.vx * P.vx + P.vy * P.vy : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) q = fmax(q, __shfl_xor_sync(FULL, q, off));
+    double s = sqrt(1.0 + q);
+    return 2.0 * q / (s * (s + 1.0));
+}
+
+// local point density from the 3x3 bucket neighbourhood of `key` (same face only)
+__device__ __forceinline__ double local_spacing2(const GridView& g, uint32_t key) {
+    const int G = g.G;
+    const int face = key / (G * G), rem = key % (G * G), iu = rem / G, iv = rem % G;
+    const int u0 = max(iu - 1, 0), u1 = min(iu + 1, G - 1);
+    const int v0 = max(iv - 1, 0), v1 = min(iv + 1, G - 1);
+    int cnt = 0;
+    for (int u = u0; u <= u1; ++u) {
+        const int row = (face * G + u) * G;
+        cnt += g.start[row + v1 + 1] - g.start[row + v0];
+    }
+    const double nb = (double)((u1 - u0 + 1) * (v1 - v0 + 1));
+    const double area_b = 4.0 * M_PI / (6.0 * (double)G * (double)G);
+    return nb * area_b / (double)(cnt > 1 ? cnt : 1);
+}
+
+// Bounding cap (centre, chord radius) of the bucket block [ua..ub] x [va..vb] on `face`.
+// Lines of constant u (or v) are great circles, so the block is a convex spherical
+// quadrilateral and its farthest point from the centre is a corner.
+__device__ __forceinline__ void face_point(int face, float u, float v, float* x, float* y, float* z) {
+    const int a = face >> 1;
+    const float sg = (face & 1) ? -1.0f : 1.0f;
+    float c[3];
+    c[a] = sg;
+    c[face_axes_b(a)] = u;
+    c[face_axes_c(a)] = v;
+    const float inv = rsqrtf(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    *x = c[0] * inv; *y = c[1] * inv; *z = c[2] * inv;
+}
+
+__device__ __forceinline__ void block_cap(int face, int G, int ua, int ub, int va, int vb,
+                                          float* cx, float* cy, float* cz, float* rad) {
+    const float k = 1.5707963267948966f / (float)G;     // equi-angular step
+    const float a0 = ua * k - 0.78539816f, a1 = (ub + 1) * k - 0.78539816f;
+    const float b0 = va * k - 0.78539816f, b1 = (vb + 1) * k - 0.78539816f;
+    face_point(face, tanf(0.5f * (a0 + a1)), tanf(0.5f * (b0 + b1)), cx, cy, cz);
+    const float tu[2] = {tanf(a0), tanf(a1)}, tv[2] = {tanf(b0), tanf(b1)};
+    float r2 = 0.f;
+    for (int q = 0; q < 4; ++q) {
+        float x, y, z;
+        face_point(face, tu[q & 1], tv[q >> 1], &x, &y, &z);
+        const float dx = x - *cx, dy = y - *cy, dz = z - *cz;
+        r2 = fmaxf(r2, dx * dx + dy * dy + dz * dz);
+    }
+    *rad = sqrtf(r2) * 1.0001f + 1e-5f;
 }
 
 // Returns valence > 0, -ST_* for genuine failures, or -ST_POLY_OVERFLOW to request the
@@ -106,16 +156,13 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
     wpoly_init(P, lane);
     ClipCtx cc;
     cc.z = g.z; cc.zi = zi; cc.i = i; cc.tie_breaks = 0;
-    uint32_t key = bucket_key(zi, g.G);
-    int cnt = g.start[key + 1] - g.start[key];
-    double area_b = 4.0 * M_PI / (6.0 * (double)g.G * (double)g.G);
-    double h2 = area_b / (double)(cnt > 0 ? cnt : 1);
-    double r2 = 12.25 * h2;                    // first radius 3.5 h
+    double h2 = local_spacing2(g, bucket_key(zi, g.G));
+    double r2 = 9.0 * h2;                      // first radius 3 h
     if (r2 > 4.0) r2 = 4.0000001;
     double lo_c2 = -1.0;                       // exclusive lower bound on c2
     double R2 = 8.0;
     bool box = true;
-    int status = 0, rounds = 0, passes = 0;
+    int status = 0, rounds = 0, passes = 0, sweep_visits = 0;
     const unsigned lt_mask = (1u << lane) - 1u;
     while (true) {
         ++passes;
@@ -124,21 +171,23 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
         double lim = 4.0 * R2 * (1.0 + 1e-12);
         int count = 0;
         // ---- gather candidates in (lo_c2, r2] that can still cut the cell
-        for (int face = 0; face < 6; ++face) {
+        for (int face = 0; face < 6 && count <= WCAND; ++face) {
             int iu0, iu1, iv0, iv1;
             if (!cap_face_range(cb, face, g.G, &iu0, &iu1, &iv0, &iv1)) continue;
-            for (int iu = iu0; iu <= iu1; ++iu) {
+            for (int iu = iu0; iu <= iu1 && count <= WCAND; ++iu) {
                 int rowbase = (face * g.G + iu) * g.G;
                 int p0 = g.start[rowbase + iv0], p1 = g.start[rowbase + iv1 + 1];
-                for (int base = p0; base < p1; base += 32) {
+                for (int base = p0; base < p1 && count <= WCAND; base += 32) {
                     int p = base + lane;
                     bool acc = false;
                     double c2 = 0.0;
                     int j = -1;
                     if (p < p1) {
-                        j = g.ids[p];
-                        const double* q = g.zs + 4 * (int64_t)p;
-                        double dx = q[0] - zi.x, dy = q[1] - zi.y, dz = q[2] - zi.z;
+                        j = __ldg(g.ids + p);
+                        const double2* q2 = reinterpret_cast<const double2*>(g.zs + 4 * (int64_t)p);
+                        double2 xy = __ldg(q2);
+                        double zz = __ldg(g.zs + 4 * (int64_t)p + 2);
+                        double dx = xy.x - zi.x, dy = xy.y - zi.y, dz = zz - zi.z;
                         c2 = dx * dx + dy * dy + dz * dz;
                         acc = j != i && c2 <= r2 && c2 < lim && c2 > lo_c2;
                         if (acc && c2 == 0.0) { status |= ST_DUPLICATE; acc = false; }
@@ -188,58 +237,106 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
             }
             __syncwarp();
         } else {
-            // ---- dense neighbourhood of a large cell: clip in scan order
+            // ---- dense neighbourhood of a large cell: hierarchical sweep.  Lanes first test
+            // 8x8-bucket blocks against the vertex circumdisks (a point can cut the cell only
+            // inside some disk |y - y_k| < R_k); only intersecting blocks are scanned, their
+            // points tested per lane, and survivors clipped one at a time.
             ++passes;
+            float vyx = 0.f, vyy = 0.f, vyz = 0.f, vR = 0.f;
+            bool dirty = true;
             for (int face = 0; face < 6 && !status; ++face) {
                 int iu0, iu1, iv0, iv1;
                 if (!cap_face_range(cb, face, g.G, &iu0, &iu1, &iv0, &iv1)) continue;
-                for (int iu = iu0; iu <= iu1 && !status; ++iu) {
-                    int rowbase = (face * g.G + iu) * g.G;
-                    int p0 = g.start[rowbase + iv0], p1 = g.start[rowbase + iv1 + 1];
-                    for (int base = p0; base < p1 && !status; base += 32) {
-                        int p = base + lane;
-                        bool acc = false;
-                        double c2 = 0.0;
-                        int j = -1;
-                        V3 zj = v3(0, 0, 0);
-                        double cax = 0.0, cay = 0.0;
-                        if (p < p1) {
-                            j = g.ids[p];
-                            const double* q = g.zs + 4 * (int64_t)p;
-                            zj = v3(q[0], q[1], q[2]);
-                            V3 d = sub(zj, zi);
-                            c2 = dot(d, d);
-                            acc = j != i && c2 <= r2 && c2 > lo_c2 && c2 > 0.0 &&
-                                  c2 < 4.0 * R2 * (1.0 + 1e-12);
-                            cax = dot(d, e1);
-                            cay = dot(d, e2);
+                const int bu0 = iu0 >> 3, bu1 = iu1 >> 3, bv0 = iv0 >> 3, bv1 = iv1 >> 3;
+                const int nbv = bv1 - bv0 + 1, nblk = (bu1 - bu0 + 1) * nbv;
+                for (int b0 = 0; b0 < nblk && !status; b0 += 32) {
+                    if (dirty) {   // per-lane vertex circumdisk on the sphere (float, conservative)
+                        if (lane < P.n && P.lab >= 0) {
+                            double x = zi.x + P.vx * e1.x + P.vy * e2.x;
+                            double y = zi.y + P.vx * e1.y + P.vy * e2.y;
+                            double w = zi.z + P.vx * e1.z + P.vy * e2.z;
+                            double inv = rsqrt(x * x + y * y + w * w);
+                            x *= inv; y *= inv; w *= inv;
+                            double rx = x - zi.x, ry = y - zi.y, rz = w - zi.z;
+                            vyx = (float)x; vyy = (float)y; vyz = (float)w;
+                            vR = (float)sqrt(rx * rx + ry * ry + rz * rz);
+                        } else {
+                            vyx = vyy = vyz = 0.f;
+                            vR = 3.0f;       // box vertex: covers everything
                         }
-                        // vertex-disk test, one candidate per lane: j can cut the cell only if
-                        // some current vertex is (about) as close to z_j as to z_i
-                        if (__any_sync(FULL, acc)) {
-                            bool may = false;
-                            const double cb2 = 0.5 * c2;
-                            for (int k = 0; k < P.n; ++k) {
-                                double vx = __shfl_sync(FULL, P.vx, k);
-                                double vy = __shfl_sync(FULL, P.vy, k);
-                                double t1 = cax * vx, t2 = cay * vy;
-                                may |= t1 + t2 - cb2 > -1e-9 * (fabs(t1) + fabs(t2) + cb2);
+                        dirty = false;
+                    }
+                    const int bk = b0 + lane;
+                    bool hit = false;
+                    int ua = 0, ub = -1, va = 0, vb = -1;
+                    float cx = 0.f, cy = 0.f, cz = 0.f, crad = 0.f;
+                    if (bk < nblk) {
+                        const int bu = bu0 + bk / nbv, bv = bv0 + bk % nbv;
+                        ua = max(bu << 3, iu0); ub = min((bu << 3) + 7, iu1);
+                        va = max(bv << 3, iv0); vb = min((bv << 3) + 7, iv1);
+                        block_cap(face, g.G, ua, ub, va, vb, &cx, &cy, &cz, &crad);
+                    }
+                    for (int k = 0; k < P.n; ++k) {
+                        float kx = __shfl_sync(FULL, vyx, k), ky = __shfl_sync(FULL, vyy, k);
+                        float kz = __shfl_sync(FULL, vyz, k), kr = __shfl_sync(FULL, vR, k);
+                        float dx = kx - cx, dy = ky - cy, dz = kz - cz;
+                        float lim2 = kr + crad + 1e-4f;
+                        hit |= dx * dx + dy * dy + dz * dz < lim2 * lim2;
+                    }
+                    unsigned mb = __ballot_sync(FULL, hit && bk < nblk);
+                    while (mb && !status) {
+                        const int src = __ffs(mb) - 1;
+                        mb &= mb - 1u;
+                        const int bua = __shfl_sync(FULL, ua, src), bub = __shfl_sync(FULL, ub, src);
+                        const int bva = __shfl_sync(FULL, va, src), bvb = __shfl_sync(FULL, vb, src);
+                        for (int iu = bua; iu <= bub && !status; ++iu) {
+                            int rowbase = (face * g.G + iu) * g.G;
+                            int p0 = g.start[rowbase + bva], p1 = g.start[rowbase + bvb + 1];
+                            for (int base = p0; base < p1 && !status; base += 32) {
+                                sweep_visits += 32;
+                                int p = base + lane;
+                                bool acc = false;
+                                double c2 = 0.0;
+                                int j = -1;
+                                V3 zj = v3(0, 0, 0);
+                                double cax = 0.0, cay = 0.0;
+                                if (p < p1) {
+                                    j = g.ids[p];
+                                    const double* q = g.zs + 4 * (int64_t)p;
+                                    zj = v3(q[0], q[1], q[2]);
+                                    V3 d = sub(zj, zi);
+                                    c2 = dot(d, d);
+                                    acc = j != i && c2 <= r2 && c2 > lo_c2 && c2 > 0.0 &&
+                                          c2 < 4.0 * R2 * (1.0 + 1e-12);
+                                    cax = dot(d, e1);
+                                    cay = dot(d, e2);
+                                }
+                                if (__any_sync(FULL, acc)) {
+                                    bool may = false;
+                                    const double cb2 = 0.5 * c2;
+                                    for (int k = 0; k < P.n; ++k) {
+                                        double vx = __shfl_sync(FULL, P.vx, k);
+                                        double vy = __shfl_sync(FULL, P.vy, k);
+                                        double t1 = cax * vx, t2 = cay * vy;
+                                        may |= t1 + t2 - cb2 > -1e-9 * (fabs(t1) + fabs(t2) + cb2);
+                                    }
+                                    acc = acc && may;
+                                }
+                                unsigned ma = __ballot_sync(FULL, acc);
+                                while (ma) {
+                                    int sl = __ffs(ma) - 1;
+                                    ma &= ma - 1u;
+                                    double cs = __shfl_sync(FULL, c2, sl);
+                                    int js = __shfl_sync(FULL, j, sl);
+                                    V3 zs = v3(__shfl_sync(FULL, zj.x, sl), __shfl_sync(FULL, zj.y, sl),
+                                               __shfl_sync(FULL, zj.z, sl));
+                                    if (cs >= 4.0 * R2 * (1.0 + 1e-12)) continue;
+                                    V3 d = sub(zs, zi);
+                                    int rc = wpoly_clip(P, lane, dot(d, e1), dot(d, e2), 0.5 * cs, js, zs, cc);
+                                    if (rc < 0) { status = ST_POLY_OVERFLOW; break; }
+                                    if (rc == 1) { R2 = wpoly_R2(P, lane, &box); dirty = true; }
+                                }
                             }
-                            acc = acc && may;
-                        }
-                        unsigned ma = __ballot_sync(FULL, acc);
-                        while (ma) {
-                            int src = __ffs(ma) - 1;
-                            ma &= ma - 1u;
-                            double cs = __shfl_sync(FULL, c2, src);
-                            int js = __shfl_sync(FULL, j, src);
-                            V3 zs = v3(__shfl_sync(FULL, zj.x, src), __shfl_sync(FULL, zj.y, src),
-                                       __shfl_sync(FULL, zj.z, src));
-                            if (cs >= 4.0 * R2 * (1.0 + 1e-12)) continue;
-                            V3 d = sub(zs, zi);
-                            int rc = wpoly_clip(P, lane, dot(d, e1), dot(d, e2), 0.5 * cs, js, zs, cc);
-                            if (rc < 0) { status = ST_POLY_OVERFLOW; break; }
-                            if (rc == 1) R2 = wpoly_R2(P, lane, &box);
                         }
                     }
                 }
@@ -258,6 +355,7 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
     }
     st->rounds = rounds;
     st->passes = passes;
+    st->sweep_visits = sweep_visits;
     st->tie_breaks = __reduce_add_sync(FULL, cc.tie_breaks);
     if (status) return -status;
     const int n = P.n;

@@ -377,7 +377,7 @@ struct GridView {
 
 constexpr int CAND = 48;    // nearest-first candidate list per pass
 
-struct CellStats { int rounds; int passes; int tie_breaks; };
+struct CellStats { int rounds; int passes; int tie_breaks; int sweep_visits; };
 
 // Build the Voronoi cell of generator i by nearest-first half-plane clipping with a
 // security-radius certificate: a point j can cut the cell only if |z_j - z_i| < 2R with R
@@ -509,6 +509,7 @@ SCVT_HD int build_cell(const GridView& g, int i, V3 zi, int* nbr_out, CellStats*
     st->rounds = rounds;
     st->passes = passes;
     st->tie_breaks = cc.tie_breaks;
+    st->sweep_visits = 0;
     if (status) return -status;
     int n = cur->n;
     if (n > MAXDEG) return -ST_DEG_OVERFLOW;

@@ -71,7 +71,7 @@ __global__ void k_gather_sorted(const double* __restrict__ z, const int* __restr
 }
 
 // Fast path: one warp per generator (bucket order), polygon in registers.
-__global__ void __launch_bounds__(CELL_WARPS * 32)
+__global__ void __launch_bounds__(CELL_WARPS * 32, 4)
 k_cells_warp(GridView g, int* __restrict__ nbr, int* __restrict__ deg, int* __restrict__ status,
              int* __restrict__ stats) {
     __shared__ double s_c2[CELL_WARPS][WCAND];
@@ -99,6 +99,10 @@ k_cells_warp(GridView g, int* __restrict__ nbr, int* __restrict__ deg, int* __re
         if (cs.rounds > 1) atomicAdd(&stats[1], 1);
         atomicMax(&stats[2], cs.passes);
         if (cs.tie_breaks) atomicAdd(&stats[4], cs.tie_breaks);
+        if (cs.sweep_visits) {
+            atomicAdd(&stats[6], 1);
+            atomicAdd(&stats[7], cs.sweep_visits >> 5);
+        }
     }
 }
 
@@ -1087,6 +1091,8 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
         stats_host[3] = ctx->h_status[11];  // ambiguous (filter-undecided) directed edges
         stats_host[4] = ctx->h_status[12];  // SoS tie-breaks taken while clipping
         stats_host[5] = ctx->h_status[10];  // max candidate passes of one cell
+        stats_host[6] = ctx->h_status[14];  // cells that needed the unsorted sweep
+        stats_host[7] = ctx->h_status[15];  // 32-point batches visited by those sweeps
     }
     if (st) return status_to_code(ctx, st);
     if (total != 2 * n - 4)

@@ -254,12 +254,13 @@ class MeshEvaluator:
         t = max(2 * n - 4, 1)
         tri = torch.empty((t, 3), dtype=torch.int64, device=z.device)
         flags = torch.empty(t, dtype=torch.uint8, device=z.device)
-        st = (ctypes.c_int64 * 6)()
+        st = (ctypes.c_int64 * 8)()
         ctx.call("scvt_triangulate", _lib.dptr(z), n, _lib.dptr(tri), _lib.dptr(flags), st,
                  what="triangulate")
         stats = {"triangles": int(st[0]), "flagged": int(st[1]), "max_valence": int(st[2]),
                  "ambiguous_edges": int(st[3]), "tie_breaks": int(st[4]),
-                 "max_passes": int(st[5])}
+                 "max_passes": int(st[5]), "sweep_cells": int(st[6]),
+                 "sweep_batches": int(st[7])}
         return tri, flags, stats
 
     def triangulation(self, points) -> SphericalTriangulation:
