@@ -1,0 +1,175 @@
+"""The cell builder and fan quadrature of csrc/scvt_device.cuh, compiled for the CPU by the
+TEST-ONLY harness (tests/native/host_harness.cpp), against Qhull and the golden moments.
+
+This exercises the exact device arithmetic (predicates, clipping, certificate, quadrature)
+without a GPU; the GPU kernels (warp-cooperative builder, k_quad) are checked by
+tests/test_gpu_parity.py on the B200."""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import ROOT, rel
+
+SRC = os.path.join(ROOT, "tests", "native", "host_harness.cpp")
+SO = os.path.join(ROOT, "tests", "native", "libscvt_host_harness.so")
+P = ctypes.POINTER
+dp = lambda a: a.ctypes.data_as(P(ctypes.c_double))  # noqa: E731
+ip = lambda a: a.ctypes.data_as(P(ctypes.c_int))  # noqa: E731
+
+
+@pytest.fixture(scope="module")
+def h():
+    deps = [SRC, os.path.join(ROOT, "paper_1709_06924_b200", "csrc", "scvt_device.cuh")]
+    if not os.path.exists(SO) or any(os.path.getmtime(d) > os.path.getmtime(SO) for d in deps):
+        subprocess.run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", SO, SRC], check=True)
+    return ctypes.CDLL(SO)
+
+
+def cells(h, z):
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    n = len(z)
+    nbr = np.zeros((n, 32), np.int32)
+    deg = np.zeros(n, np.int32)
+    st = np.zeros(4, np.int32)
+    s = h.harness_cells(dp(z), n, ip(nbr), ip(deg), ip(st))
+    return s, nbr, deg, st
+
+
+def triangles(nbr, deg):
+    out = []
+    for i in range(len(deg)):
+        r = nbr[i, :deg[i]]
+        for t in range(len(r)):
+            a, b = r[t], r[(t + 1) % len(r)]
+            if i < a and i < b:
+                out.append((i, a, b))
+    t = np.array(out, np.int64)
+    return t[np.lexsort((t[:, 2], t[:, 1], t[:, 0]))]
+
+
+def consistent(nbr, deg):
+    n = len(deg)
+    for i in range(n):
+        r = list(nbr[i, :deg[i]])
+        for t in range(len(r)):
+            a, b = r[t], r[(t + 1) % len(r)]
+            ra = list(nbr[a, :deg[a]])
+            if i not in ra or ra[ra.index(i) - 1] != b:
+                return False
+    return int(deg.sum()) == 6 * n - 12
+
+
+@pytest.mark.parametrize("kind,n", [("uniform", 2562), ("uniform", 40962), ("c4", 2562),
+                                    ("c4", 40962), ("c5", 40962), ("c3", 40962), ("c5", 10242)])
+def test_cells_match_qhull(h, kind, n):
+    z = O.random_sphere_points(n, 0) if kind == "uniform" else \
+        O.sample_by_density(O.density_for(kind), n, 0)
+    s, nbr, deg, st = cells(h, z)
+    assert s == 0
+    np.testing.assert_array_equal(triangles(nbr, deg), O.convex_hull_delaunay(z))
+
+
+@pytest.mark.parametrize("name", ["tet", "ico", "rnd50", "rnd162"])
+def test_small_sets(h, gold, name):
+    g = gold("small_sets")
+    s, nbr, deg, _ = cells(h, g[name + "_z"])
+    assert s == 0
+    np.testing.assert_array_equal(triangles(nbr, deg), g[name + "_triangles"])
+
+
+def test_cocircular_cube_is_consistent(h):
+    """Cube vertices: six exactly cocircular quads.  Symbolic perturbation must give one
+    consistent triangulation (Qhull's choice may differ: flagged degeneracy)."""
+    cube = O.normalize(np.array([[x, y, z] for x in (-1, 1) for y in (-1, 1) for z in (-1, 1)],
+                                float))
+    s, nbr, deg, st = cells(h, cube)
+    assert s == 0 and consistent(nbr, deg)
+    assert st[3] > 0   # tie-breaks were needed
+
+
+def test_bisected_icosahedra(h):
+    ico = O.icosahedron_vertices()
+    z = ico
+    for _ in range(3):
+        e = O.triangle_edges(O.convex_hull_delaunay(z))
+        z = np.vstack([z, O.normalize(z[e[:, 0]] + z[e[:, 1]])])
+        s, nbr, deg, _ = cells(h, z)
+        assert s == 0 and consistent(nbr, deg)
+        np.testing.assert_array_equal(triangles(nbr, deg), O.convex_hull_delaunay(z))
+
+
+@pytest.mark.parametrize("name", ["rnd5", "rnd6"])
+def test_hemisphere_sets_detected(h, gold, name):
+    """Hull misses the origin -> a Voronoi cell would span a hemisphere -> ST_UNBOUNDED."""
+    s, _, _, _ = cells(h, gold("small_sets")[name + "_z"])
+    assert s & 2
+
+
+def test_duplicates_detected(h):
+    z = O.random_sphere_points(300, 3)
+    z[10] = z[20]
+    s, _, _, _ = cells(h, z)
+    assert s & 1
+
+
+def test_insphere_predicate(h):
+    o = np.array([1.0, 0, 0]); a = np.array([0, 1.0, 0]); b = np.array([0, 0, 1.0])
+    am = ctypes.c_int(0)
+    far = O.normalize(np.array([-1.0, -1.0, -1.0]))
+    near = O.normalize(np.array([1.0, 1.0, 1.0]))
+    assert h.harness_insphere(dp(o), dp(a), dp(b), dp(far), ctypes.byref(am)) == -1
+    assert h.harness_insphere(dp(o), dp(a), dp(b), dp(near), ctypes.byref(am)) == 1
+    assert am.value == 0
+
+
+def _quad(h, z, nbr, deg, rule, depth, field, sphere=0):
+    from paper_1709_06924_b200 import density as D, geometry as G
+
+    l1, l2, w = G.composite_nodes(G.QUADRATURE_RULES[rule], depth)
+    p = D.device_params(field)
+    prm = np.zeros(15)
+    prm[0:3] = [p["gamma"], p["beta"], p["alpha"]]
+    prm[3:9] = p["center"]
+    prm[9:11] = [p["w_lon"], p["w_lat"]]
+    if field.variant == "x16":
+        c = field.center
+        lat, lon = np.arctan2(c[2], np.hypot(c[0], c[1])), np.arctan2(c[1], c[0])
+        prm[11:15] = [lat, lon, np.cos(lat), np.sin(lat)]
+    out = np.zeros((len(z), 5))
+    ob = ctypes.c_int(0)
+    h.harness_quad(dp(np.ascontiguousarray(z)), len(z), ip(nbr), ip(deg), dp(l1), dp(l2), dp(w),
+                   len(w), p["density_kind"], dp(prm), sphere, dp(out), ctypes.byref(ob))
+    return out, ob.value
+
+
+@pytest.mark.parametrize("rule,depth", [("4pt", 0), ("9pt", 0), ("7pt", 1), ("7pt", 3)])
+def test_quadrature_vs_golden(h, gold, rule, depth):
+    from paper_1709_06924_b200 import density as D
+
+    g = gold("c1_eval")
+    z = g["z"]
+    _, nbr, deg, _ = cells(h, z)
+    out, ob = _quad(h, z, nbr, deg, rule, depth, D.density_preset("const"))
+    p = f"{rule}_d{depth}_"
+    assert rel(out[:, 0], g[p + "mass"]) <= 1e-13
+    assert rel(out[:, 1:4], g[p + "first"]) <= 1e-13
+    assert abs(out[:, 4].sum() - g[p + "energy"]) <= 1e-13 * g[p + "energy"]
+    assert ob == int(g["obtuse_count"])
+
+
+@pytest.mark.parametrize("cfg", ["x3", "x16", "x64", "c3", "c4", "c5"])
+def test_density_kinds_vs_golden(h, gold, cfg):
+    from paper_1709_06924_b200 import density as D
+
+    g = gold("density_eval")
+    z = g["uniform_z"]
+    _, nbr, deg, _ = cells(h, z)
+    out, _ = _quad(h, z, nbr, deg, "4pt", 0, D.density_preset(cfg))
+    p = f"uniform_{cfg}_4pt_d0_"
+    assert rel(out[:, 1:4], g[p + "first"]) <= 1e-13
+    assert rel(out[:, 0], g[p + "mass"]) <= 1e-13

@@ -1,0 +1,154 @@
+"""Host-side logic of the package (no GPU): rules and composite node tables, density table,
+sampling, scalar line search, stopping rules, ladders, config plumbing."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1709_06924_b200 as P
+from paper_1709_06924_b200 import density as D
+from paper_1709_06924_b200 import geometry as G
+from paper_1709_06924_b200.optimizer import wolfe_line_search
+
+
+def test_rules_equal_oracle():
+    for k in ("4pt", "9pt", "7pt"):
+        np.testing.assert_array_equal(G.QUADRATURE_RULES[k].bary, O.RULES[k].bary)
+        np.testing.assert_array_equal(G.QUADRATURE_RULES[k].weights, O.RULES[k].weights)
+
+
+@pytest.mark.parametrize("rule", ["4pt", "9pt", "7pt"])
+@pytest.mark.parametrize("depth", [0, 1, 2, 3])
+def test_composite_weights(rule, depth):
+    l1, l2, w = G.composite_nodes(G.QUADRATURE_RULES[rule], depth)
+    assert len(w) == 4 ** depth * len(G.QUADRATURE_RULES[rule].weights)
+    assert abs(w.sum() - 1.0) < 1e-14
+    assert np.all((l1 >= 0) & (l2 >= 0) & (l1 + l2 <= 1))
+
+
+def test_composite_depth0_is_rule():
+    r = G.QUADRATURE_RULES["9pt"]
+    l1, l2, w = G.composite_nodes(r, 0)
+    np.testing.assert_array_equal(l1, r.bary[:, 1])
+    np.testing.assert_array_equal(l2, r.bary[:, 2])
+    np.testing.assert_array_equal(w, r.weights)
+
+
+@pytest.mark.parametrize("rule,deg", [("4pt", 3), ("9pt", 5), ("7pt", 5)])
+def test_composite_exactness(rule, deg):
+    """Subdivided rules stay exact for total degree <= rule degree on the reference triangle
+    (integral of x^a y^b = a! b! / (a+b+2)!, area-normalised by 2)."""
+    from math import factorial
+
+    l1, l2, w = G.composite_nodes(G.QUADRATURE_RULES[rule], 2)
+    for a in range(deg + 1):
+        for b in range(deg + 1 - a):
+            exact = 2.0 * factorial(a) * factorial(b) / factorial(a + b + 2)
+            assert abs(np.sum(w * l1 ** a * l2 ** b) - exact) < 1e-14
+
+
+def test_composite_nodes_match_reference_subdivision():
+    """Node positions of the composite table == rule applied to the leaves of
+    subdivide_fans (delaunay.py:383-407) incl. leaf vertex order (asymmetric 4pt rule)."""
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal((1, 3, 3))
+    fans = O.Fans(v, np.zeros(1, np.int64), np.zeros(1, np.int64), np.ones(1), 0)
+    sub = O.subdivide(fans, 3)
+    rule = O.RULES["4pt"]
+    ref = np.einsum("qv,svj->sqj", rule.bary, sub.verts).reshape(-1, 3)
+    l1, l2, _ = G.composite_nodes(G.QUADRATURE_RULES["4pt"], 3)
+    v0, v1, v2 = v[0]
+    mine = v0 + l1[:, None] * (v1 - v0) + l2[:, None] * (v2 - v0)
+    d = np.abs(np.sort(ref, axis=0) - np.sort(mine, axis=0)).max()
+    assert d < 1e-14
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_tanh4_table_accuracy(name):
+    """rho^(1/4) table vs the closed form (both branches, random points): <= 3e-15 relative."""
+    f = D.density_preset(name)
+    coef, w = D.tanh4_table(f)
+    rng = np.random.default_rng(1)
+    y = D.normalize(rng.standard_normal((200000, 3)))
+    u = np.zeros(len(y))
+    for c in np.atleast_2d(f.center):
+        x0 = np.linalg.norm(y - c, axis=1)
+        x1 = np.linalg.norm(y + c, axis=1)
+        uc = np.where(x0 ** 2 <= 2, D.eval_tanh4_table(coef[0], w, x0),
+                      D.eval_tanh4_table(coef[1], w, x1))
+        u = np.maximum(u, uc)
+    ref = D.eval_density(f, y) ** 0.25
+    assert np.max(np.abs(u - ref) / ref) <= 3e-15
+
+
+@pytest.mark.parametrize("name", ["const", "x3", "x16", "x64", "c3", "c4", "c5"])
+def test_density_host_eval_equals_oracle(name):
+    z = P.random_sphere_points(5000, 2)
+    np.testing.assert_array_equal(np.broadcast_to(D.eval_density(D.density_preset(name), z), 5000),
+                                  np.broadcast_to(O.eval_density(O.density_for(name), z), 5000))
+    assert D.density_preset(name).max_value == O.density_for(name).max_value
+
+
+def test_sampler_matches_oracle():
+    for name in ("c4", "c5"):
+        np.testing.assert_array_equal(P.sample_by_density(D.density_preset(name), 3000, 0),
+                                      O.sample_by_density(O.density_for(name), 3000, 0))
+
+
+def test_density_kinds():
+    assert D.density_preset("const").kind == 0
+    assert D.density_preset("x16").kind == 2
+    assert D.density_preset("x64").kind == 3
+    assert D.density_preset("c4").kind == 4
+    assert D.density_preset("c5").kind == 5
+    p = D.device_params(D.density_preset("c5"))
+    assert p["table"] is not None and p["center"][3:].any()
+
+
+def _quadratic_phi(a, b, c):
+    return lambda alpha: (a * alpha ** 2 + b * alpha + c, 2 * a * alpha + b, alpha)
+
+
+@pytest.mark.parametrize("a,b", [(1.0, -1.0), (0.05, -1.0), (10.0, -1.0), (1e-4, -1e-3)])
+def test_line_search_equals_oracle(a, b):
+    phi = _quadratic_phi(a, b, 3.0)
+    mine = wolfe_line_search(phi, 3.0, b)
+    ref = O.wolfe_line_search(phi, 3.0, b)
+    assert mine == ref
+
+
+def test_line_search_failure_and_nondescent():
+    with pytest.raises(P.LineSearchFailure):
+        wolfe_line_search(lambda al: (10.0 + al, 1.0, al), 1.0, -1.0)
+    with pytest.raises(P.NonDescentError):
+        wolfe_line_search(lambda al: (al, 1.0, al), 0.0, 0.5)
+
+
+def test_stopping_criteria_validation():
+    with pytest.raises(ValueError):
+        P.StoppingCriteria(movement_tol=0.0)
+    with pytest.raises(ValueError):
+        P.StoppingCriteria(max_iterations=0)
+
+
+def test_bisection_ladder_and_bisect():
+    assert P.bisection_ladder(655362, floor=2562) == [2562, 10242, 40962, 163842, 655362]
+    ico = P.icosahedron_vertices()
+    t = O.convex_hull_delaunay(ico)
+    tri = P.SphericalTriangulation(t, np.zeros((len(t), 3)), np.zeros(len(t)))
+    z = P.bisect(ico, tri)
+    assert len(z) == 42 and np.allclose(np.linalg.norm(z, axis=1), 1.0)
+
+
+def test_same_public_names_as_reference():
+    ref = ["DensityField", "density_preset", "QuadratureRule", "QUADRATURE_RULES",
+           "StoppingCriteria", "minimize", "MeshEvaluator", "bisect", "bisection_ladder"]
+    for name in ref:
+        assert hasattr(P, name), name
+
+
+def test_unknown_method_and_laplacian_rejected():
+    with pytest.raises(P.ConfigError):
+        P.MeshEvaluator(P.density_preset("const"), "4pt", laplacian="a6")
+    with pytest.raises(ValueError):
+        P.MeshEvaluator(P.density_preset("const"), "4pt", measure="bogus")
