@@ -116,6 +116,32 @@ int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n,
                                double* first, double* mass, double* lloyd_diag,
                                double* scalars_host);
 
+/* sharded evaluation (one process per GPU) -------------------------------------------------
+ * The generators are split into `nshards` equal ranges of the cube-map bucket order; shard s
+ * owns rows [s*R, (s+1)*R) with R = scvt_shard_rows(n, nshards).  Per evaluation:
+ *   scvt_shard_cells    grid (replicated) + cells of the owned generators -> cyc_send
+ *                       int32 [R][34] = {id, valence, 32 neighbour ids}   (id -1 = padding)
+ *   <caller all-gathers cyc_send -> cyc_all [nshards*R][34]>
+ *   scvt_shard_moments  certificate of the owned cells against all cycles, owned fan
+ *                       quadrature -> res_send f64 [R][8] = {id, m, c(3), E, obtuse, 0};
+ *                       status_host = device status bits (0 = ok)
+ *   <caller all-reduces status (max); nonzero -> scvt_shard_status maps it to a code>
+ *   <caller all-gathers res_send -> res_all [nshards*R][8]>
+ *   scvt_shard_finish   scatter to id order, gradient epilogue and the fixed-shape
+ *                       reductions -> identical outputs to scvt_evaluate, bitwise, for any
+ *                       shard count.
+ * Stands in for the reference's region path (pipeline.py:171-242: partition, per-region
+ * triangulation on a worker pool, gather in fixed region order). */
+int64_t scvt_shard_rows(int64_t n, int nshards);
+int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                     int32_t* cyc_send);
+int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                       const int32_t* cyc_all, double* res_send, int32_t* status_host);
+int scvt_shard_status(scvt_ctx* ctx, int32_t status);
+int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                      const double* res_all, double* grad, double* first, double* mass,
+                      double* lloyd_diag, double* scalars_host);
+
 /* optimizer vector algebra -------------------------------------------------------------
  * CorrectionHistory (optimizer.py:79-114): ring of at most lbfgs_m (s, y) pairs held on
  * the device inside ctx. */

@@ -12,6 +12,7 @@ from .errors import *  # noqa: F401,F403
 from .geometry import (QUADRATURE_RULES, QuadratureRule, composite_nodes, icosahedron_vertices,
                        normalize, random_sphere_points)
 from .optimizer import IterationRecord, MinimizeResult, Minimizer, StoppingCriteria, minimize
+from .parallel import ShardedMeshEvaluator
 from .pipeline import (EvalResult, MeshEvaluator, SphericalTriangulation, bisect,
                        bisection_ladder, parallel_iteration)
 
@@ -33,6 +34,7 @@ __all__ = [
     "minimize",
     "Minimizer",
     "MeshEvaluator",
+    "ShardedMeshEvaluator",
     "EvalResult",
     "SphericalTriangulation",
     "parallel_iteration",

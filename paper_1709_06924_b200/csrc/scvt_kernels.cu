@@ -72,14 +72,14 @@ __global__ void k_gather_sorted(const double* __restrict__ z, const int* __restr
 
 // Fast path: one warp per generator (bucket order), polygon in registers.
 __global__ void __launch_bounds__(CELL_WARPS * 32, 4)
-k_cells_warp(GridView g, int* __restrict__ nbr, int* __restrict__ deg, int* __restrict__ status,
-             int* __restrict__ stats) {
+k_cells_warp(GridView g, int p_lo, int p_hi, int* __restrict__ nbr, int* __restrict__ deg,
+             int* __restrict__ status, int* __restrict__ stats) {
     __shared__ double s_c2[CELL_WARPS][WCAND];
     __shared__ int s_j[CELL_WARPS][WCAND];
     __shared__ int s_p[CELL_WARPS][WCAND];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t p = (int64_t)blockIdx.x * CELL_WARPS + w;
-    if (p >= g.n) return;   // warp-uniform
+    const int64_t p = p_lo + (int64_t)blockIdx.x * CELL_WARPS + w;
+    if (p >= p_hi) return;   // warp-uniform
     const int i = g.ids[p];
     const double* q = g.zs + 4 * p;
     V3 zi = v3(q[0], q[1], q[2]);
@@ -108,10 +108,10 @@ k_cells_warp(GridView g, int* __restrict__ nbr, int* __restrict__ deg, int* __re
 
 // Fallback: one thread per generator the warp builder handed back (deg == -1).
 __global__ void __launch_bounds__(CELL_THREADS)
-k_cells(GridView g, int* __restrict__ nbr, int* __restrict__ deg, int* __restrict__ status,
-        int* __restrict__ stats) {
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= g.n) return;
+k_cells(GridView g, int p_lo, int p_hi, int* __restrict__ nbr, int* __restrict__ deg,
+        int* __restrict__ status, int* __restrict__ stats) {
+    int p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= p_hi) return;
     int i = g.ids[p];
     if (deg[i] != -1) return;
     V3 zi = v3(g.zs[4 * (int64_t)p], g.zs[4 * (int64_t)p + 1], g.zs[4 * (int64_t)p + 2]);
@@ -136,11 +136,13 @@ __device__ __forceinline__ int find_in_cycle(const int* __restrict__ row, int d,
 
 // consistency of adjacent cycles + local Delaunay filter (edge (i, n_t) with triangles
 // (i, n_t, n_{t+1}) and (i, n_{t-1}, n_t))
-__global__ void k_verify(const double* __restrict__ z, int n, const int* __restrict__ nbr,
-                         const int* __restrict__ deg, uint8_t* __restrict__ amb,
-                         int* __restrict__ status, int* __restrict__ stats) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+__global__ void k_verify(const double* __restrict__ z, const int* __restrict__ ids, int p_lo,
+                         int p_hi, const int* __restrict__ nbr, const int* __restrict__ deg,
+                         uint8_t* __restrict__ amb, int* __restrict__ status,
+                         int* __restrict__ stats) {
+    int p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= p_hi) return;
+    int i = ids[p];
     int d = deg[i];
     const int* row = nbr + (int64_t)i * MAXDEG;
     if (d < 3) { atomicOr(status, ST_INCONSISTENT); return; }
@@ -163,20 +165,20 @@ __global__ void k_verify(const double* __restrict__ z, int n, const int* __restr
 }
 
 // incidence CSR in bucket (spatial) order: sorted slot p -> generator ids[p]
-__global__ void k_deg_sorted(int n, const int* __restrict__ ids, const int* __restrict__ deg,
-                             int* __restrict__ degs) {
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p > n) return;
-    degs[p] = p == n ? 0 : deg[ids[p]];
+__global__ void k_deg_sorted(int p_lo, int cnt, const int* __restrict__ ids,
+                             const int* __restrict__ deg, int* __restrict__ degs) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q > cnt) return;
+    degs[q] = q == cnt ? 0 : deg[ids[p_lo + q]];
 }
 
-__global__ void k_fill_incidences(int n, const int* __restrict__ ids, const int* __restrict__ deg,
-                                  const int* __restrict__ inc_start, int* __restrict__ inc_base,
-                                  int* __restrict__ inc_gen, int cap) {
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    int i = ids[p];
-    int s = inc_start[p], d = deg[i];
+__global__ void k_fill_incidences(int p_lo, int cnt, const int* __restrict__ ids,
+                                  const int* __restrict__ deg, const int* __restrict__ inc_start,
+                                  int* __restrict__ inc_base, int* __restrict__ inc_gen, int cap) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= cnt) return;
+    int i = ids[p_lo + q];
+    int s = inc_start[q], d = deg[i];
     inc_base[i] = s;
     for (int t = 0; t < d; ++t)
         if (s + t < cap) inc_gen[s + t] = i;
@@ -192,10 +194,11 @@ struct QuadArgs {
     const double* z;
     const int* nbr;
     const int* deg;
-    const int* inc_start;   // [n+1] in sorted order (total at [n])
+    const int* inc_start;   // [cnt+1] over the owned sorted slots (total at [cnt])
     const int* inc_base;    // [n] by generator id
     const int* inc_gen;
     int n;
+    int cnt;                // owned sorted slots
     int n_inc;            // expected incidences 6n - 12
     const double* nodes;  // device [3][nq]: l1, l2, w
     const double* table;  // device rho^(1/4) table (tanh4 kinds) or null
@@ -220,7 +223,7 @@ k_quad(QuadArgs a) {
     __syncthreads();
     int u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= a.n_inc) return;
-    if (a.inc_start[a.n] != a.n_inc) {   // not a closed triangulation: nothing to integrate
+    if (a.inc_start[a.cnt] != a.n_inc) {   // not a closed triangulation: nothing to integrate
         if (u == 0) atomicOr(a.status, ST_EULER);
         return;
     }
@@ -249,8 +252,23 @@ k_quad(QuadArgs a) {
     a.obtuse[u] = (f.obtuse && i < j && i < k) ? 1 : 0;
 }
 
+// gradient epilogue (pipeline.py:265-279): g = 2(c.z)z - 2c, diag = 2 c.z
+__device__ __forceinline__ void epilogue(const double* __restrict__ z, int i, double cx, double cy,
+                                         double cz, double* __restrict__ grad,
+                                         double* __restrict__ diag, double* __restrict__ g2) {
+    V3 zi = load3(z, i);
+    double czd = cx * zi.x + cy * zi.y + cz * zi.z;
+    double gx = 2.0 * czd * zi.x - 2.0 * cx;
+    double gy = 2.0 * czd * zi.y - 2.0 * cy;
+    double gz = 2.0 * czd * zi.z - 2.0 * cz;
+    grad[3 * (int64_t)i] = gx; grad[3 * (int64_t)i + 1] = gy; grad[3 * (int64_t)i + 2] = gz;
+    diag[i] = 2.0 * czd;
+    g2[i] = gx * gx + gy * gy + gz * gz;
+}
+
 // per generator: fixed-order sum over its incidences, then the gradient epilogue
-__global__ void k_gather(const double* __restrict__ z, int n, const int* __restrict__ inc_start,
+__global__ void k_gather(const double* __restrict__ z, int n, int cnt,
+                         const int* __restrict__ inc_start,
                          const int* __restrict__ inc_base, const int* __restrict__ deg,
                          const double* __restrict__ part, const uint8_t* __restrict__ obtuse,
                          int64_t n_inc, const int* __restrict__ status, double* __restrict__ grad,
@@ -260,7 +278,7 @@ __global__ void k_gather(const double* __restrict__ z, int n, const int* __restr
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double m = 0, cx = 0, cy = 0, cz = 0, e = 0, ob = 0;
-    if (inc_start[n] == n_inc) {
+    if (inc_start[cnt] == n_inc) {
         const int u0 = inc_base[i], u1 = u0 + deg[i];
         for (int u = u0; u < u1; ++u) {
             m += part[u];
@@ -271,18 +289,93 @@ __global__ void k_gather(const double* __restrict__ z, int n, const int* __restr
             ob += obtuse[u];
         }
     }
-    V3 zi = load3(z, i);
-    double czd = cx * zi.x + cy * zi.y + cz * zi.z;
-    double gx = 2.0 * czd * zi.x - 2.0 * cx;
-    double gy = 2.0 * czd * zi.y - 2.0 * cy;
-    double gz = 2.0 * czd * zi.z - 2.0 * cz;
-    grad[3 * (int64_t)i] = gx; grad[3 * (int64_t)i + 1] = gy; grad[3 * (int64_t)i + 2] = gz;
+    epilogue(z, i, cx, cy, cz, grad, diag, g2_gen);
     first[3 * (int64_t)i] = cx; first[3 * (int64_t)i + 1] = cy; first[3 * (int64_t)i + 2] = cz;
     if (mass) mass[i] = m;
-    diag[i] = 2.0 * czd;
     e_gen[i] = e;
-    g2_gen[i] = gx * gx + gy * gy + gz * gz;
     ob_gen[i] = ob;
+}
+
+// ------------------------------------------------------------------ shard exchange rows
+constexpr int CYC_ROW = 2 + MAXDEG;   // [id, deg, nbr...] int32
+constexpr int RES_ROW = 8;            // [id, m, cx, cy, cz, E, obtuse, 0] f64
+
+__global__ void k_pack_cycles(const int* __restrict__ ids, int p_lo, int cnt, int cap,
+                              const int* __restrict__ nbr, const int* __restrict__ deg,
+                              int* __restrict__ out) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= cap) return;
+    int* row = out + (int64_t)q * CYC_ROW;
+    if (q >= cnt) { row[0] = -1; row[1] = 0; return; }
+    int i = ids[p_lo + q];
+    int d = deg[i];
+    row[0] = i;
+    row[1] = d;
+    for (int t = 0; t < MAXDEG; ++t) row[2 + t] = t < d ? nbr[(int64_t)i * MAXDEG + t] : -1;
+}
+
+__global__ void k_unpack_cycles(const int* __restrict__ rows, int nrows, int n,
+                                int* __restrict__ nbr, int* __restrict__ deg,
+                                int* __restrict__ degsum, int* __restrict__ status) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const int* row = rows + (int64_t)r * CYC_ROW;
+    int i = row[0];
+    if (i < 0) return;
+    if (i >= n) { atomicOr(status, ST_INCONSISTENT); return; }
+    int d = row[1];
+    deg[i] = d;
+    for (int t = 0; t < d && t < MAXDEG; ++t) nbr[(int64_t)i * MAXDEG + t] = row[2 + t];
+    atomicAdd(degsum, d);
+}
+
+// owned slots: fixed-order incidence sums packed as exchange rows
+__global__ void k_gather_pack(int p_lo, int cnt, int cap, const int* __restrict__ ids,
+                              const int* __restrict__ inc_base, const int* __restrict__ deg,
+                              const double* __restrict__ part, const uint8_t* __restrict__ obtuse,
+                              int64_t n_inc, double* __restrict__ out) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= cap) return;
+    double* row = out + (int64_t)q * RES_ROW;
+    if (q >= cnt) {
+        row[0] = -1.0;
+        for (int c = 1; c < RES_ROW; ++c) row[c] = 0.0;
+        return;
+    }
+    int i = ids[p_lo + q];
+    double m = 0, cx = 0, cy = 0, cz = 0, e = 0, ob = 0;
+    const int u0 = inc_base[i], u1 = u0 + deg[i];
+    for (int u = u0; u < u1; ++u) {
+        m += part[u];
+        cx += part[n_inc + u];
+        cy += part[2 * n_inc + u];
+        cz += part[3 * n_inc + u];
+        e += part[4 * n_inc + u];
+        ob += obtuse[u];
+    }
+    row[0] = (double)i; row[1] = m; row[2] = cx; row[3] = cy; row[4] = cz; row[5] = e;
+    row[6] = ob; row[7] = 0.0;
+}
+
+__global__ void k_unpack_results(const double* __restrict__ rows, int nrows, int n,
+                                 const double* __restrict__ z, double* __restrict__ grad,
+                                 double* __restrict__ first, double* __restrict__ mass,
+                                 double* __restrict__ diag, double* __restrict__ e_gen,
+                                 double* __restrict__ g2_gen, double* __restrict__ ob_gen,
+                                 int* __restrict__ seen) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const double* row = rows + (int64_t)r * RES_ROW;
+    if (row[0] < 0.0) return;
+    int i = (int)row[0];
+    if (i >= n) return;
+    double cx = row[2], cy = row[3], cz = row[4];
+    epilogue(z, i, cx, cy, cz, grad, diag, g2_gen);
+    first[3 * (int64_t)i] = cx; first[3 * (int64_t)i + 1] = cy; first[3 * (int64_t)i + 2] = cz;
+    if (mass) mass[i] = row[1];
+    e_gen[i] = row[5];
+    ob_gen[i] = row[6];
+    atomicAdd(seen, 1);
 }
 
 // ------------------------------------------------------------------ deterministic reductions
@@ -753,7 +846,8 @@ int finish_slots(scvt_ctx* ctx, int nslots) {
 }
 
 // ---------------------------------------------------------------------- triangulation core
-int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
+// cube-map grid over all n points (replicated on every shard; deterministic)
+int build_grid(scvt_ctx* ctx, const double* z, int64_t n, GridView* gv) {
     if (n < 4) return fail(ctx, SCVT_ERR_INSUFFICIENT_POINTS,
                            "need >= 4 points on the sphere, got %lld", (long long)n);
     if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n=%lld > n_max=%lld",
@@ -772,20 +866,42 @@ int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
     LAUNCHED();
     k_gather_sorted<<<blocks_for(n, 256), 256, 0, s>>>(z, ctx->d_ids, (int)n, ctx->d_zs);
     LAUNCHED();
-    GridView g;
-    g.zs = ctx->d_zs; g.ids = ctx->d_ids; g.start = ctx->d_start; g.z = z; g.G = G; g.n = n;
+    gv->zs = ctx->d_zs; gv->ids = ctx->d_ids; gv->start = ctx->d_start; gv->z = z; gv->G = G;
+    gv->n = n;
+    return SCVT_OK;
+}
+
+// Voronoi cells of the generators in sorted slots [lo, hi)
+int build_cells_range(scvt_ctx* ctx, const GridView& g, int64_t lo, int64_t hi) {
+    cudaStream_t s = ctx->stream;
+    int64_t cnt = hi - lo;
+    if (cnt <= 0) return SCVT_OK;
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], s));
-    k_cells_warp<<<blocks_for(n, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
-        g, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
+    k_cells_warp<<<blocks_for(cnt, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
+        g, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
     LAUNCHED();
-    k_cells<<<blocks_for(n, CELL_THREADS), CELL_THREADS, 0, s>>>(g, ctx->d_nbr, ctx->d_deg,
-                                                                ctx->d_status, ctx->d_status + 8);
+    k_cells<<<blocks_for(cnt, CELL_THREADS), CELL_THREADS, 0, s>>>(
+        g, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
     LAUNCHED();
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
-    k_verify<<<blocks_for(n, 128), 128, 0, s>>>(z, (int)n, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
-                                               ctx->d_status, ctx->d_status + 8);
+    return SCVT_OK;
+}
+
+int verify_range(scvt_ctx* ctx, const double* z, int64_t lo, int64_t hi) {
+    int64_t cnt = hi - lo;
+    if (cnt <= 0) return SCVT_OK;
+    k_verify<<<blocks_for(cnt, 128), 128, 0, ctx->stream>>>(
+        z, ctx->d_ids, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_amb, ctx->d_status,
+        ctx->d_status + 8);
     LAUNCHED();
     return SCVT_OK;
+}
+
+int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
+    GridView g;
+    TRY(build_grid(ctx, z, n, &g));
+    TRY(build_cells_range(ctx, g, 0, n));
+    return verify_range(ctx, z, 0, n);
 }
 
 int cells_from_triangles(scvt_ctx* ctx, const int64_t* tri, int64_t t, int64_t n) {
@@ -813,30 +929,39 @@ int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t sme
     return SCVT_OK;
 }
 
-int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
-            double* mass, double* diag, double* scalars_host) {
+// incidence CSR over the sorted slots [lo, hi) (spatially coherent warps)
+int incidences_range(scvt_ctx* ctx, int64_t lo, int64_t hi, int64_t cap) {
     cudaStream_t s = ctx->stream;
-    // incidence CSR over the cycles, generators in bucket order (spatially coherent warps)
-    k_deg_sorted<<<blocks_for(n + 1, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_deg,
-                                                        ctx->d_cursor);
+    int64_t cnt = hi - lo;
+    k_deg_sorted<<<blocks_for(cnt + 1, 256), 256, 0, s>>>((int)lo, (int)cnt, ctx->d_ids,
+                                                          ctx->d_deg, ctx->d_cursor);
     LAUNCHED();
     size_t tb = ctx->cub_bytes;
-    CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, ctx->d_cursor, ctx->d_inc_start, (int)n + 1, s));
-    int64_t n_inc = 6 * n - 12;
-    k_fill_incidences<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_deg,
-                                                         ctx->d_inc_start, ctx->d_inc_base,
-                                                         ctx->d_inc_gen, (int)n_inc);
+    CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, ctx->d_cursor, ctx->d_inc_start,
+                                     (int)cnt + 1, s));
+    k_fill_incidences<<<blocks_for(cnt, 256), 256, 0, s>>>((int)lo, (int)cnt, ctx->d_ids,
+                                                           ctx->d_deg, ctx->d_inc_start,
+                                                           ctx->d_inc_base, ctx->d_inc_gen,
+                                                           (int)cap);
     LAUNCHED();
+    return SCVT_OK;
+}
+
+// fan quadrature over n_inc incidences of the slots [lo, hi)
+int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi,
+               int64_t n_inc) {
     QuadArgs a;
     a.z = z; a.nbr = ctx->d_nbr; a.deg = ctx->d_deg; a.inc_start = ctx->d_inc_start;
     a.inc_base = ctx->d_inc_base;
-    a.inc_gen = ctx->d_inc_gen; a.n = (int)n; a.n_inc = (int)n_inc; a.nodes = ctx->d_nodes;
+    a.inc_gen = ctx->d_inc_gen; a.n = (int)n; a.cnt = (int)(hi - lo); a.n_inc = (int)n_inc;
+    a.nodes = ctx->d_nodes;
     a.nq = ctx->nq; a.dp = ctx->dp; a.part = ctx->d_part; a.obtuse = ctx->d_obt;
     a.table = ctx->d_table;
     a.status = ctx->d_status;
+    if (n_inc <= 0) return SCVT_OK;
     unsigned grid = blocks_for(n_inc, QUAD_THREADS);
     size_t smem = (3 * (size_t)ctx->nq + 2 * (size_t)ctx->dp.tab_k * (TAB_P + 1)) * sizeof(double);
-    if (ctx->prof) CK(cudaEventRecord(ctx->ev[2], s));
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     switch (ctx->dp.kind) {
         case DEN_CONST: TRY(launch_quad_kind<DEN_CONST>(ctx, a, grid, smem)); break;
         case DEN_X3: TRY(launch_quad_kind<DEN_X3>(ctx, a, grid, smem)); break;
@@ -848,13 +973,14 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
         case DEN_TANH4X2_TAB: TRY(launch_quad_kind<DEN_TANH4X2_TAB>(ctx, a, grid, smem)); break;
         default: return fail(ctx, SCVT_ERR_CONFIG, "bad density kind %d", ctx->dp.kind);
     }
-    if (ctx->prof) CK(cudaEventRecord(ctx->ev[3], s));
-    k_gather<<<blocks_for(n, 256), 256, 0, s>>>(z, (int)n, ctx->d_inc_start, ctx->d_inc_base,
-                                                ctx->d_deg, ctx->d_part,
-                                                ctx->d_obt, n_inc, ctx->d_status, grad, first,
-                                                mass, diag, ctx->d_egen, ctx->d_g2gen,
-                                                ctx->d_obgen);
-    LAUNCHED();
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    return SCVT_OK;
+}
+
+// fixed-shape reductions of E_i, |g_i|^2, obtuse_i over ALL n generators (id order), so the
+// scalars are bitwise identical whatever the shard count; reads back and checks status
+int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host) {
+    cudaStream_t s = ctx->stream;
     k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_egen, n, ctx->d_partials);
     LAUNCHED();
     k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_g2gen, n,
@@ -883,6 +1009,24 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
     scalars_host[1] = sqrt(ctx->h_scal[1]);
     scalars_host[2] = ctx->h_scal[2];
     return SCVT_OK;
+}
+
+int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+            double* mass, double* diag, double* scalars_host) {
+    int64_t n_inc = 6 * n - 12;   // Euler: a closed triangulation has exactly 6n-12 incidences
+    TRY(incidences_range(ctx, 0, n, n_inc));
+    TRY(quad_range(ctx, z, n, 0, n, n_inc));
+    k_gather<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
+        z, (int)n, (int)n, ctx->d_inc_start, ctx->d_inc_base, ctx->d_deg, ctx->d_part, ctx->d_obt,
+        n_inc, ctx->d_status, grad, first, mass, diag, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen);
+    LAUNCHED();
+    return reduce_finish(ctx, n, scalars_host);
+}
+
+inline void shard_range(int64_t n, int shard, int nshards, int64_t* lo, int64_t* hi) {
+    int64_t cap = (n + nshards - 1) / nshards;
+    *lo = std::min<int64_t>(n, (int64_t)shard * cap);
+    *hi = std::min<int64_t>(n, *lo + cap);
 }
 
 }  // namespace
@@ -1130,6 +1274,90 @@ int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const 
     TRY(reset_status(ctx));
     TRY(cells_from_triangles(ctx, tri, t, n));
     return moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
+}
+
+// ---------------------------------------------------------------------- sharded evaluation
+int64_t scvt_shard_rows(int64_t n, int nshards) {
+    return nshards > 0 ? (n + nshards - 1) / nshards : 0;
+}
+
+int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                     int32_t* cyc_send) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (nshards < 1 || shard < 0 || shard >= nshards)
+        return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+    ctx->prof_n[3] = 0;
+    TRY(reset_status(ctx));
+    GridView g;
+    TRY(build_grid(ctx, z, n, &g));
+    int64_t lo, hi, cap = scvt_shard_rows(n, nshards);
+    shard_range(n, shard, nshards, &lo, &hi);
+    TRY(build_cells_range(ctx, g, lo, hi));
+    k_pack_cycles<<<blocks_for(cap, 128), 128, 0, ctx->stream>>>(
+        ctx->d_ids, (int)lo, (int)(hi - lo), (int)cap, ctx->d_nbr, ctx->d_deg, cyc_send);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                       const int32_t* cyc_all, double* res_send, int32_t* status_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    cudaStream_t s = ctx->stream;
+    int64_t lo, hi, cap = scvt_shard_rows(n, nshards);
+    shard_range(n, shard, nshards, &lo, &hi);
+    // every rank gets every cycle: needed to certify its own cells against their neighbours
+    CK(cudaMemsetAsync(ctx->d_status + 13, 0, sizeof(int), s));
+    k_unpack_cycles<<<blocks_for(cap * nshards, 128), 128, 0, s>>>(
+        cyc_all, (int)(cap * nshards), (int)n, ctx->d_nbr, ctx->d_deg, ctx->d_status + 13,
+        ctx->d_status);
+    LAUNCHED();
+    TRY(verify_range(ctx, z, lo, hi));
+    TRY(incidences_range(ctx, lo, hi, 6 * n));
+    int tot[2] = {0, 0};
+    CK(cudaMemcpyAsync(&tot[0], ctx->d_inc_start + (hi - lo), sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tot[1], ctx->d_status + 13, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (tot[1] != 6 * n - 12) {
+        CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *status_host = ctx->h_status[0] | ST_EULER;
+        return SCVT_OK;
+    }
+    TRY(quad_range(ctx, z, n, lo, hi, tot[0]));
+    k_gather_pack<<<blocks_for(cap, 128), 128, 0, s>>>(
+        (int)lo, (int)(hi - lo), (int)cap, ctx->d_ids, ctx->d_inc_base, ctx->d_deg, ctx->d_part,
+        ctx->d_obt, tot[0], res_send);
+    LAUNCHED();
+    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *status_host = ctx->h_status[0];
+    return SCVT_OK;
+}
+
+int scvt_shard_status(scvt_ctx* ctx, int32_t status) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    return status_to_code(ctx, status);
+}
+
+int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                      const double* res_all, double* grad, double* first, double* mass,
+                      double* lloyd_diag, double* scalars_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    cudaStream_t s = ctx->stream;
+    int64_t cap = scvt_shard_rows(n, nshards);
+    CK(cudaMemsetAsync(ctx->d_status + 13, 0, sizeof(int), s));
+    k_unpack_results<<<blocks_for(cap * nshards, 128), 128, 0, s>>>(
+        res_all, (int)(cap * nshards), (int)n, z, grad, first, mass, lloyd_diag, ctx->d_egen,
+        ctx->d_g2gen, ctx->d_obgen, ctx->d_status + 13);
+    LAUNCHED();
+    TRY(reduce_finish(ctx, n, scalars_host));
+    int seen = 0;
+    CK(cudaMemcpy(&seen, ctx->d_status + 13, sizeof(int), cudaMemcpyDeviceToHost));
+    if (seen != n)
+        return fail(ctx, SCVT_ERR_COVERAGE, "shard results cover %d of %lld generators", seen,
+                    (long long)n);
+    return SCVT_OK;
 }
 
 // ---------------------------------------------------------------------- optimizer algebra

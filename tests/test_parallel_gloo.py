@@ -1,0 +1,151 @@
+"""The multi-GPU orchestration (paper_1709_06924_b200/parallel.py) under gloo with world
+size 2 on CPU.  The CUDA backend cannot run here, so a NumPy stand-in backend (oracle
+arithmetic, same exchange-row formats) is plugged into the SAME `sharded_evaluate`: shard
+ranges, packing, both all-gathers, the status agreement and the final scatter/reduction are
+what is under test.  The CUDA backend's bitwise equivalence across shard counts is checked on
+the B200 (tests/test_gpu_parity.py::test_sharded_evaluation_is_bitwise_identical)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_1709_06924_b200.parallel import CYC_ROW, RES_ROW, shard_range, shard_rows, sharded_evaluate
+
+
+class NumpyShardBackend:
+    def __init__(self, density="const", rule="4pt", fail_on=None):
+        self.density = O.density_for(density)
+        self.rule = O.RULES[rule]
+        self.fail_on = fail_on
+
+    def buffers(self, n, nshards, device):
+        r = shard_rows(n, nshards)
+        return (torch.zeros((r, CYC_ROW), dtype=torch.int32),
+                torch.zeros((nshards * r, CYC_ROW), dtype=torch.int32),
+                torch.zeros((r, RES_ROW), dtype=torch.float64),
+                torch.zeros((nshards * r, RES_ROW), dtype=torch.float64))
+
+    def cells(self, z, shard, nshards, cyc_send):
+        z = z.numpy()
+        n = len(z)
+        tri = O.convex_hull_delaunay(z)
+        nxt = [dict() for _ in range(n)]
+        for a, b, c in tri:
+            nxt[a][b] = c
+            nxt[b][c] = a
+            nxt[c][a] = b
+        lo, hi = shard_range(n, shard, nshards)
+        cyc_send.fill_(-1)
+        for q, i in enumerate(range(lo, hi)):
+            start = min(nxt[i])
+            cyc, cur = [], start
+            while True:
+                cyc.append(cur)
+                cur = nxt[i][cur]
+                if cur == start:
+                    break
+            cyc_send[q, 0] = i
+            cyc_send[q, 1] = len(cyc)
+            cyc_send[q, 2:2 + len(cyc)] = torch.tensor(cyc, dtype=torch.int32)
+
+    def moments(self, z, shard, nshards, cyc_all, res_send):
+        zz = z.numpy()
+        n = len(zz)
+        rows = cyc_all.numpy()
+        rows = rows[rows[:, 0] >= 0]
+        ids = np.sort(rows[:, 0])
+        if not np.array_equal(ids, np.arange(n)):
+            return 1 << 4                                   # ST_INCONSISTENT
+        tris = []
+        for r in rows:
+            i, d = r[0], r[1]
+            for t in range(d):
+                a, b = r[2 + t], r[2 + (t + 1) % d]
+                if i < a and i < b:
+                    tris.append((i, a, b))
+        tri = O.canonical_sort(np.array(tris))
+        f = O.build_fans(zz, tri)
+        nodes = np.einsum("qv,svj->sqj", self.rule.bary, f.verts)
+        nodes = nodes / np.linalg.norm(nodes, axis=-1, keepdims=True)
+        rho = O.eval_density(self.density, nodes)
+        w = self.rule.weights
+        sub_m = (rho @ w) * f.signed_area
+        sub_c = np.einsum("sq,q,sqj->sj", rho, w, nodes) * f.signed_area[:, None]
+        diff = nodes - zz[f.cells][:, None, :]
+        sub_e = ((rho * np.einsum("sqj,sqj->sq", diff, diff)) @ w) * f.signed_area
+        m = np.zeros(n); c = np.zeros((n, 3)); e = np.zeros(n)
+        np.add.at(m, f.cells, sub_m); np.add.at(c, f.cells, sub_c); np.add.at(e, f.cells, sub_e)
+        lo, hi = shard_range(n, shard, nshards)
+        res_send.fill_(0.0)
+        res_send[:, 0] = -1.0
+        for q, i in enumerate(range(lo, hi)):
+            res_send[q, :6] = torch.tensor([i, m[i], c[i, 0], c[i, 1], c[i, 2], e[i]])
+        if self.fail_on is not None and shard == self.fail_on:
+            return 1 << 0                                   # ST_DUPLICATE on one rank only
+        return 0
+
+    def raise_status(self, status):
+        raise RuntimeError(f"status {status}")
+
+    def finish(self, z, nshards, res_all):
+        zz = z.numpy()
+        n = len(zz)
+        rows = res_all.numpy()
+        rows = rows[rows[:, 0] >= 0]
+        order = rows[:, 0].astype(np.int64)
+        first = np.zeros((n, 3)); e = np.zeros(n); m = np.zeros(n)
+        first[order] = rows[:, 2:5]; e[order] = rows[:, 5]; m[order] = rows[:, 1]
+        cz = np.einsum("ij,ij->i", first, zz)
+        grad = 2.0 * cz[:, None] * zz - 2.0 * first
+        return {"energy": float(e.sum()), "first": first, "grad": grad, "mass": m,
+                "covered": len(order)}
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fail_on, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        z = torch.from_numpy(O.random_sphere_points(1202, 5))
+        try:
+            r = sharded_evaluate(NumpyShardBackend(fail_on=fail_on), z, rank, world)
+            out[rank] = {"energy": r["energy"], "first": r["first"], "covered": r["covered"]}
+        except RuntimeError as exc:
+            out[rank] = {"error": str(exc)}
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, fail_on=None):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), fail_on, out), nprocs=world, join=True)
+    return dict(out)
+
+
+def test_gloo_two_ranks_match_single_process():
+    out = _run(2)
+    z = O.random_sphere_points(1202, 5)
+    ref = O.Evaluator(O.density_for("const"), "4pt", 0).evaluate(z)
+    for rank in (0, 1):
+        assert out[rank]["covered"] == 1202
+        np.testing.assert_allclose(out[rank]["first"], ref.first, rtol=0, atol=1e-15)
+        assert abs(out[rank]["energy"] - ref.energy) <= 1e-14 * ref.energy
+    np.testing.assert_array_equal(out[0]["first"], out[1]["first"])
+    assert out[0]["energy"] == out[1]["energy"]
+
+
+def test_gloo_error_on_one_rank_raises_on_all():
+    out = _run(2, fail_on=1)
+    assert "error" in out[0] and "error" in out[1]
