@@ -73,7 +73,7 @@ typedef struct scvt_config {
     const double* table_coef;
 } scvt_config;
 
-#define SCVT_TABLE_DEGREE 8
+#define SCVT_TABLE_DEGREE 6
 
 #define SCVT_MAX_NODES 2304
 #define SCVT_MAX_DEGREE 32

@@ -530,7 +530,7 @@ enum DensityKind { DEN_CONST = 0, DEN_X3 = 1, DEN_X16 = 2, DEN_TANH = 3, DEN_TAN
                    // internal: tanh4 kinds evaluated through the rho^(1/4) table
                    DEN_TANH4_TAB = 6, DEN_TANH4X2_TAB = 7 };
 
-constexpr int TAB_P = 8;   // polynomial degree of the rho^(1/4) table (SCVT_TABLE_DEGREE)
+constexpr int TAB_P = 6;   // polynomial degree of the rho^(1/4) table (SCVT_TABLE_DEGREE)
 
 struct DensityParams {
     int kind;
@@ -546,14 +546,12 @@ struct DensityParams {
 // u = rho^(1/4) of the tanh^4 profile from the table (density.tanh4_table): chord to the
 // centre when d <= 90 deg, chord to its antipode otherwise; Horner in tau.
 SCVT_HD double tab_u(const DensityParams& p, V3 y, V3 c) {
-    V3 dm = sub(y, c);
+    // chord to the nearer of c and -c (|y - c|^2 = 2 - 2 y.c for unit vectors): a select,
+    // not a predicated second chord
+    const int br = dot(y, c) < 0.0;
+    const double s = br ? -1.0 : 1.0;
+    V3 dm = v3(y.x - s * c.x, y.y - s * c.y, y.z - s * c.z);
     double r2 = dot(dm, dm);
-    int br = 0;
-    if (r2 > 2.0) {
-        V3 dp = add(y, c);
-        r2 = dot(dp, dp);
-        br = 1;
-    }
     double t = sqrt(r2) * p.tab_invw;
     int k = (int)t;
     if (k > p.tab_k - 1) k = p.tab_k - 1;
@@ -667,12 +665,14 @@ SCVT_HD void subtri_moments(const SubTri& s, V3 z, const double* l1, const doubl
                             int* pole) {
     double m = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, e = 0.0;
     double plane_d = 0.0;
+    // (two independent nodes per iteration give the FP64 pipe ILP to hide its latency)
     if (SPHERE) {
         V3 nv = cross(s.e1, s.e2);
         double nn = norm3(nv);
         if (nn == 0.0) nn = 1.0;
         plane_d = fabs(dot(nv, s.v0) / nn);
     }
+#pragma unroll 2
     for (int q = 0; q < nq; ++q) {
         double a = l1[q], b = l2[q];
         double x = s.v0.x + a * s.e1.x + b * s.e2.x;
