@@ -48,17 +48,14 @@ __global__ void k_bucket_keys(const double* __restrict__ z, int n, int G,
     vals[i] = i;
 }
 
+// start[b] = first sorted slot with key >= b: slot p fills the buckets (key[p-1], key[p]]
 __global__ void k_bucket_start(const uint32_t* __restrict__ skeys, int n, int nb,
                                int* __restrict__ start) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b > nb) return;
-    // lower_bound of b in sorted keys
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (skeys[mid] < (uint32_t)b) lo = mid + 1; else hi = mid;
-    }
-    start[b] = lo;
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > n) return;
+    int lo = p == 0 ? 0 : (int)skeys[p - 1] + 1;
+    int hi = p == n ? nb : (int)skeys[p];
+    for (int b = lo; b <= hi; ++b) start[b] = p;
 }
 
 __global__ void k_gather_sorted(const double* __restrict__ z, const int* __restrict__ ids, int n,
@@ -774,9 +771,18 @@ int fail(scvt_ctx* c, int code, const char* fmt, ...) {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// buckets per face side: ~2 points per bucket at the mean density times a refinement factor
+// (SCVT_GRID_REFINE, default 1) so dense regions of very non-uniform sets stay shallow
+double grid_refine() {
+    const char* e = getenv("SCVT_GRID_REFINE");
+    double f = e ? atof(e) : 1.0;
+    return f > 0.1 && f < 16.0 ? f : 1.0;
+}
+
 int grid_for(int64_t n) {
-    double g = sqrt((double)n / 12.0);
+    double g = sqrt((double)n / 12.0) * grid_refine();
     int G = (int)g;
+    if (G > 4096) G = 4096;
     return G < 1 ? 1 : G;
 }
 
@@ -862,7 +868,7 @@ int build_grid(scvt_ctx* ctx, const double* z, int64_t n, GridView* gv) {
     size_t tb = ctx->cub_bytes;
     CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_keys, ctx->d_skeys, ctx->d_vals,
                                        ctx->d_ids, (int)n, 0, bits, s));
-    k_bucket_start<<<blocks_for(nb + 1, 256), 256, 0, s>>>(ctx->d_skeys, (int)n, nb, ctx->d_start);
+    k_bucket_start<<<blocks_for(n + 1, 256), 256, 0, s>>>(ctx->d_skeys, (int)n, nb, ctx->d_start);
     LAUNCHED();
     k_gather_sorted<<<blocks_for(n, 256), 256, 0, s>>>(z, ctx->d_ids, (int)n, ctx->d_zs);
     LAUNCHED();
