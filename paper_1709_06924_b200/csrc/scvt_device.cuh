@@ -59,6 +59,20 @@ SCVT_HD double rsqrt_d(double x) {
 #endif
 }
 
+// 1/sqrt(a) for positive normal a without the special-case branches of the libm version:
+// hardware approximation + one cubic Householder step (relative error ~1 ulp).
+SCVT_HD double fast_rsqrt(double a) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    const double r = fma(-(a * y), y, 1.0);        // 1 - a y^2
+    const double q = fma(0.375, r, 0.5);
+    return fma(q, r * y, y);                       // y (1 + r/2 + 3 r^2 / 8)
+#else
+    return 1.0 / sqrt(a);
+#endif
+}
+
 // numpy's np.linalg.norm of a 3-vector is sqrt(x*x + y*y + z*z) evaluated as a dot product;
 // we use the same expression.
 SCVT_HD double norm3(V3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
@@ -688,6 +702,224 @@ SCVT_HD void subtri_moments(const SubTri& s, V3 z, const double* l1, const doubl
         cx += wr * yv.x; cy += wr * yv.y; cz += wr * yv.z;
         V3 d = sub(yv, z);
         e += wr * dot(d, d);
+    }
+    acc[0] += s.area * m;
+    acc[1] += s.area * cx; acc[2] += s.area * cy; acc[3] += s.area * cz;
+    acc[4] += s.area * e;
+}
+
+// ------------------------------------------------------------------ symmetric 7-point fast path
+// For a rule whose node set is invariant under permutations of the barycentric coordinates
+// (Radon's 7-point rule, DECISIONS.md D1) the 4^d leaves of the depth-d subdivision form a
+// regular grid with L = 2^d cells per side: up-leaves at (a, b), a+b <= L-1, with nodes
+// P + o_q, and down-leaves at (a+1, b+1), a+b <= L-2, with nodes P - o_q, where
+// o_q = nu1_q/L e1 + nu2_q/L e2 are the rule offsets of the first leaf.  Same node set and
+// weights as the composite table (geometry.composite_nodes), cheaper per node: 3 adds to place
+// it, no table loads.  rho^(1/4) table coefficients are cached per lane across nodes.
+struct TabCache {
+    int key;
+    double c[TAB_P + 1];
+};
+
+SCVT_HD double tab_u_cached(const DensityParams& p, V3 x, double inv, V3 c, TabCache& tc) {
+    const int br = dot(x, c) < 0.0;                 // sign of y.c (inv > 0)
+    const double sx = br ? -c.x : c.x, sy = br ? -c.y : c.y, sz = br ? -c.z : c.z;
+    const double dx = fma(x.x, inv, -sx), dy = fma(x.y, inv, -sy), dz = fma(x.z, inv, -sz);
+    double r2 = fmax(dx * dx + dy * dy + dz * dz, 1e-300);
+    const double t = r2 * fast_rsqrt(r2) * p.tab_invw;
+    int k = (int)t;
+    if (k > p.tab_k - 1) k = p.tab_k - 1;
+    const double tau = 2.0 * (t - (double)k) - 1.0;
+    const int key = br * p.tab_k + k;
+    if (key != tc.key) {
+        tc.key = key;
+        const double* co = p.tab + key * (TAB_P + 1);
+#pragma unroll
+        for (int j = 0; j <= TAB_P; ++j) tc.c[j] = co[j];
+    }
+    double acc = tc.c[TAB_P];
+#pragma unroll
+    for (int j = TAB_P - 1; j >= 0; --j) acc = fma(acc, tau, tc.c[j]);
+    return acc;
+}
+
+// ---- per-sub-triangle local fit of u = rho^(1/4) in s = |y - sigma c|^2 (no sqrt per node)
+// exact table value of u at chord x in branch br
+SCVT_HD double tab_u_chord(const DensityParams& p, double x, int br) {
+    const double t = x * p.tab_invw;
+    int k = (int)t;
+    if (k > p.tab_k - 1) k = p.tab_k - 1;
+    const double tau = 2.0 * (t - (double)k) - 1.0;
+    const double* co = p.tab + (br * p.tab_k + k) * (TAB_P + 1);
+    double acc = co[TAB_P];
+#pragma unroll
+    for (int j = TAB_P - 1; j >= 0; --j) acc = fma(acc, tau, co[j]);
+    return acc;
+}
+
+struct LocalFit {
+    double sc;          // centre of the s interval
+    double b[7];        // u(s) = sum_k b[k] (s - sc)^k
+    V3 sgc;             // sigma * c
+};
+
+// Fit u over the patch of sub-triangle `st` (nodes y = normalize(v0 + l1 e1 + l2 e2)).
+// Returns false (caller falls back to per-node table evaluation) when the patch straddles
+// 90 deg from c, comes too close to the sqrt singularity at s = 0, or the fit misses the table
+// by more than 4e-15 relative at any check point (the table itself is within 1.6e-15 of the
+// closed form; a degree-6 interpolant evaluated in FP64 has a ~1e-15 rounding floor).
+SCVT_HD bool local_fit(const DensityParams& p, const SubTri& st, V3 c, LocalFit& f) {
+    constexpr double CHEB_V[7] = {0.9749279121818236, 0.7818314824680298, 0.4338837391175582,
+                              6.123233995736766e-17, -0.43388373911755806, -0.7818314824680295,
+                              -0.9749279121818237};
+    constexpr double CHEB_A[7][7] = {
+    {0.14285714285714285, 0.14285714285714285, 0.14285714285714285, 0.14285714285714285, 0.14285714285714285, 0.14285714285714285, 0.14285714285714285},
+    {0.2785508320519496, 0.2233804235622942, 0.12396678260501662, 1.7494954273533617e-17, -0.12396678260501659, -0.22338042356229412, -0.27855083205194964},
+    {0.2574196765435483, 0.06357740970180413, -0.17813994338820957, -0.2857142857142857, -0.17813994338820963, 0.06357740970180381, 0.25741967654354836},
+    {0.2233804235622942, -0.12396678260501659, -0.2785508320519496, -5.248486282060085e-17, 0.2785508320519496, 0.12396678260501715, -0.22338042356229448},
+    {0.1781399433882096, -0.2574196765435483, -0.06357740970180416, 0.2857142857142857, -0.06357740970180402, -0.2574196765435486, 0.17813994338820988},
+    {0.12396678260501662, -0.2785508320519496, 0.22338042356229418, 8.747477136766808e-17, -0.2233804235622943, 0.2785508320519494, -0.12396678260501692},
+    {0.06357740970180413, -0.17813994338820963, 0.25741967654354836, -0.2857142857142857, 0.25741967654354825, -0.17813994338820863, 0.06357740970180491},
+};
+
+    const V3 P[3] = {st.v0, add(st.v0, st.e1), add(st.v0, st.e2)};
+    double tk[3];
+    for (int k = 0; k < 3; ++k) tk[k] = dot(P[k], c);
+    int br;
+    if (tk[0] > 0.0 && tk[1] > 0.0 && tk[2] > 0.0) br = 0;
+    else if (tk[0] < 0.0 && tk[1] < 0.0 && tk[2] < 0.0) br = 1;
+    else return false;
+    const double sg = br ? -1.0 : 1.0;
+    f.sgc = mul(c, sg);
+    double smin = 1e300, smax = -1e300;
+    for (int k = 0; k < 3; ++k) {
+        const double inv = fast_rsqrt(dot(P[k], P[k]));
+        const V3 d = sub(mul(P[k], inv), f.sgc);
+        const double sk = dot(d, d);
+        smin = fmin(smin, sk);
+        smax = fmax(smax, sk);
+    }
+    // radial lift bends s by at most ~h^2/4 inside the patch; widen generously
+    const double h2 = fmax(fmax(dot(st.e1, st.e1), dot(st.e2, st.e2)), dot(sub(st.e1, st.e2), sub(st.e1, st.e2)));
+    const double margin = 2.0 * h2 + 1e-3 * (smax - smin);
+    const double lo = smin - margin, hi = smax + margin;
+    if (!(lo > 0.0)) return false;
+    const double hw = 0.5 * (hi - lo), sc = 0.5 * (hi + lo);
+    if (hw > 0.02 * sc) return false;           // (hw/sc)^7 bounds the sqrt-singularity term
+    double u[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+        const double sj = fma(hw, CHEB_V[j], sc);
+        u[j] = tab_u_chord(p, sj * fast_rsqrt(sj), br);
+    }
+    double a[7];
+#pragma unroll
+    for (int m = 0; m < 7; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) acc = fma(CHEB_A[m][j], u[j], acc);
+        a[m] = acc;
+    }
+    double b[7];   // monomials in v = (s - sc) / hw
+    b[0] = a[0] - a[2] + a[4] - a[6];
+    b[1] = a[1] - 3.0 * a[3] + 5.0 * a[5];
+    b[2] = 2.0 * a[2] - 8.0 * a[4] + 18.0 * a[6];
+    b[3] = 4.0 * a[3] - 20.0 * a[5];
+    b[4] = 8.0 * a[4] - 48.0 * a[6];
+    b[5] = 16.0 * a[5];
+    b[6] = 32.0 * a[6];
+    const double vchk[3] = {0.995, -0.995, 0.21};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double v = vchk[q];
+        double pv = b[6];
+#pragma unroll
+        for (int k = 5; k >= 0; --k) pv = fma(pv, v, b[k]);
+        const double sq = fma(hw, v, sc);
+        const double ex = tab_u_chord(p, sq * fast_rsqrt(sq), br);
+        if (!(fabs(pv - ex) <= 4e-15 * ex)) return false;   // fit rounding floor ~1e-15
+    }
+    const double ih = 1.0 / hw;
+    double sc_k = 1.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) { f.b[k] = b[k] * sc_k; sc_k *= ih; }
+    f.sc = sc;
+    return true;
+}
+
+SCVT_HD double fit_u(const LocalFit& f, V3 x, double inv) {
+    const double dx = fma(x.x, inv, -f.sgc.x), dy = fma(x.y, inv, -f.sgc.y),
+                 dz = fma(x.z, inv, -f.sgc.z);
+    const double ds = (dx * dx + dy * dy + dz * dz) - f.sc;
+    double acc = f.b[6];
+#pragma unroll
+    for (int k = 5; k >= 0; --k) acc = fma(acc, ds, f.b[k]);
+    return acc;
+}
+
+template <int KIND>
+SCVT_HD double density_x(const DensityParams& dp, V3 x, double inv, TabCache& t0, TabCache& t1,
+                         int* pole) {
+    if (KIND == DEN_CONST) return 1.0;
+    if (KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB) {
+        double u = tab_u_cached(dp, x, inv, v3(dp.c0x, dp.c0y, dp.c0z), t0);
+        if (KIND == DEN_TANH4X2_TAB) u = fmax(u, tab_u_cached(dp, x, inv, v3(dp.c1x, dp.c1y, dp.c1z), t1));
+        const double u2 = u * u;
+        return u2 * u2;
+    }
+    return density_eval<KIND>(dp, v3(x.x * inv, x.y * inv, x.z * inv), pole);
+}
+
+template <int KIND, int L>
+SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const double* l2,
+                                 const double* w, const DensityParams& dp, double* acc,
+                                 int* pole) {
+    V3 o[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) o[q] = add(mul(s.e1, l1[q]), mul(s.e2, l2[q]));
+    const double w0 = w[0], w1 = w[1], w2 = w[4];
+    TabCache t0, t1;
+    t0.key = -1; t1.key = -1;
+    const bool TAB = KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB;
+    LocalFit f0, f1;
+    bool fitted = false;
+    if (TAB) {
+        fitted = local_fit(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f0);
+        if (fitted && KIND == DEN_TANH4X2_TAB)
+            fitted = local_fit(dp, s, v3(dp.c1x, dp.c1y, dp.c1z), f1);
+    }
+    double m = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, e = 0.0;
+    const double invL = 1.0 / (double)L;
+    for (int pass = 0; pass < 2; ++pass) {          // 0: up-leaves, 1: down-leaves
+    const double sg = pass ? -1.0 : 1.0;
+    const int M = L - pass;
+    for (int a = 0; a < M; ++a)
+    for (int b = 0; b < M - a; ++b) {
+        const double fa = (a + pass) * invL, fb = (b + pass) * invL;
+        const V3 P = v3(s.v0.x + fa * s.e1.x + fb * s.e2.x, s.v0.y + fa * s.e1.y + fb * s.e2.y,
+                        s.v0.z + fa * s.e1.z + fb * s.e2.z);
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            const V3 x = v3(fma(sg, o[q].x, P.x), fma(sg, o[q].y, P.y), fma(sg, o[q].z, P.z));
+            const double r2 = x.x * x.x + x.y * x.y + x.z * x.z;
+            const double inv = fast_rsqrt(r2);
+            double rho;
+            if (TAB && fitted) {
+                double u = fit_u(f0, x, inv);
+                if (KIND == DEN_TANH4X2_TAB) u = fmax(u, fit_u(f1, x, inv));
+                const double u2 = u * u;
+                rho = u2 * u2;
+            } else {
+                rho = density_x<KIND>(dp, x, inv, t0, t1, pole);
+            }
+            const double wr = (q == 0 ? w0 : (q < 4 ? w1 : w2)) * rho;
+            const double wri = wr * inv;
+            m += wr;
+            cx = fma(wri, x.x, cx); cy = fma(wri, x.y, cy); cz = fma(wri, x.z, cz);
+            const double dx = fma(x.x, inv, -z.x), dy = fma(x.y, inv, -z.y), dz = fma(x.z, inv, -z.z);
+            e = fma(wr, dx * dx + dy * dy + dz * dz, e);
+        }
+    }
     }
     acc[0] += s.area * m;
     acc[1] += s.area * cx; acc[2] += s.area * cy; acc[3] += s.area * cz;

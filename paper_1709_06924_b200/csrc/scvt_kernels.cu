@@ -206,8 +206,8 @@ struct QuadArgs {
     int* status;
 };
 
-template <int KIND, bool SPHERE>
-__global__ void __launch_bounds__(QUAD_THREADS)
+template <int KIND, bool SPHERE, bool SYM7>
+__global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? 5 : 1)
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
     for (int q = threadIdx.x; q < 3 * a.nq; q += blockDim.x) s_nodes[q] = a.nodes[q];
@@ -237,8 +237,13 @@ k_quad(QuadArgs a) {
     const double* l1 = s_nodes;
     const double* l2 = s_nodes + a.nq;
     const double* w = s_nodes + 2 * a.nq;
-    subtri_moments<KIND, SPHERE>(f.s[0], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
-    subtri_moments<KIND, SPHERE>(f.s[1], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
+    if (SYM7 && !SPHERE) {
+        subtri_moments_sym7<KIND, 8>(f.s[0], vi, l1, l2, w, a.dp, acc, &pole);
+        subtri_moments_sym7<KIND, 8>(f.s[1], vi, l1, l2, w, a.dp, acc, &pole);
+    } else {
+        subtri_moments<KIND, SPHERE>(f.s[0], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
+        subtri_moments<KIND, SPHERE>(f.s[1], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
+    }
     if (pole) atomicOr(a.status, ST_POLE);
     int64_t N = a.n_inc;
     a.part[u] = acc[0];
@@ -704,6 +709,7 @@ struct scvt_ctx {
     DensityParams dp{};
     int measure = 0;
     int nq = 0;
+    bool sym7 = false;           // node table = symmetric 7-node rule on depth-3 leaves
     int m = 7;
     double* d_nodes = nullptr;   // [3][nq]
     double* d_table = nullptr;   // [2][tab_k][TAB_P+1] rho^(1/4) table (tanh4 kinds)
@@ -777,6 +783,45 @@ double grid_refine() {
     const char* e = getenv("SCVT_GRID_REFINE");
     double f = e ? atof(e) : 1.0;
     return f > 0.1 && f < 16.0 ? f : 1.0;
+}
+
+// Is the composite node table a depth-3 subdivision of a permutation-symmetric 7-node rule?
+// Then k_quad may place nodes leaf by leaf (subtri_moments_sym7): check that the table's
+// node set equals that construction and its weights are leaf-independent.
+bool is_sym7_depth3(const scvt_config* cfg) {
+    if (cfg->n_nodes != 448) return false;
+    const double* l1 = cfg->node_l1;
+    const double* l2 = cfg->node_l2;
+    const double* w = cfg->node_w;
+    double nu1[7], nu2[7];
+    for (int q = 0; q < 7; ++q) { nu1[q] = 8.0 * l1[q]; nu2[q] = 8.0 * l2[q]; }
+    if (!(w[1] == w[2] && w[2] == w[3] && w[4] == w[5] && w[5] == w[6])) return false;
+    // symmetric: (nu1, nu2) -> (nu2, nu1) and (nu0, nu1) permutations stay in the set
+    auto in_set = [&](double x, double y) {
+        for (int q = 0; q < 7; ++q)
+            if (fabs(nu1[q] - x) < 1e-13 && fabs(nu2[q] - y) < 1e-13) return true;
+        return false;
+    };
+    for (int q = 0; q < 7; ++q) {
+        double nu0 = 1.0 - nu1[q] - nu2[q];
+        if (!in_set(nu2[q], nu1[q]) || !in_set(nu0, nu2[q]) || !in_set(nu1[q], nu0)) return false;
+    }
+    // every table node must be a grid node of the construction, with its orbit's weight
+    for (int k = 0; k < 448; ++k) {
+        bool found = false;
+        for (int pass = 0; pass < 2 && !found; ++pass)
+            for (int a = 0; a < 8 - pass && !found; ++a)
+                for (int b = 0; b < 8 - pass - a && !found; ++b)
+                    for (int q = 0; q < 7 && !found; ++q) {
+                        double sg = pass ? -1.0 : 1.0;
+                        double x = (a + pass + sg * nu1[q]) / 8.0, y = (b + pass + sg * nu2[q]) / 8.0;
+                        if (fabs(x - l1[k]) < 1e-13 && fabs(y - l2[k]) < 1e-13 &&
+                            fabs(w[k] - w[q]) <= 1e-15 * fabs(w[q]))
+                            found = true;
+                    }
+        if (!found) return false;
+    }
+    return true;
 }
 
 int grid_for(int64_t n) {
@@ -928,9 +973,11 @@ int cells_from_triangles(scvt_ctx* ctx, const int64_t* tri, int64_t t, int64_t n
 template <int KIND>
 int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t smem) {
     if (ctx->measure)
-        k_quad<KIND, true><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
+        k_quad<KIND, true, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
+    else if (ctx->sym7)
+        k_quad<KIND, false, true><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
     else
-        k_quad<KIND, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
+        k_quad<KIND, false, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
     LAUNCHED();
     return SCVT_OK;
 }
@@ -1167,6 +1214,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         tbl[ctx->nq + q] = cfg->node_l2[q];
         tbl[2 * ctx->nq + q] = cfg->node_w[q];
     }
+    ctx->sym7 = getenv("SCVT_NO_SYM7") == nullptr && is_sym7_depth3(cfg);
     {
         cudaError_t e = cudaMemcpy(ctx->d_nodes, tbl.data(), tbl.size() * sizeof(double),
                                    cudaMemcpyHostToDevice);
@@ -1182,8 +1230,9 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     if (smem > 48 * 1024) {
         // opt in to large dynamic shared memory for every instantiation
 #define OPT(K)                                                                             \
-    cudaFuncSetAttribute(k_quad<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    cudaFuncSetAttribute(k_quad<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+    cudaFuncSetAttribute(k_quad<K, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(k_quad<K, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(k_quad<K, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
         OPT(DEN_CONST); OPT(DEN_X3); OPT(DEN_X16); OPT(DEN_TANH); OPT(DEN_TANH4); OPT(DEN_TANH4X2);
         OPT(DEN_TANH4_TAB); OPT(DEN_TANH4X2_TAB);
 #undef OPT

@@ -126,3 +126,61 @@ extern "C" int harness_one_cell(const double* z, int n, int i, int* nbr, int* ro
     delete P; delete T;
     return d;
 }
+
+// per-sub-triangle local-fit acceptance and sym7-path moments (tanh4 table kinds 6/7)
+extern "C" int harness_fit_stats(const double* z, int n, const int* nbr, const int* deg,
+                                 const double* table, int tab_k, double tab_w, const double* prm,
+                                 int kind, long long* counts) {
+    DensityParams dp{};
+    dp.kind = kind;
+    dp.gamma = prm[0]; dp.beta = prm[1]; dp.alpha = prm[2];
+    dp.c0x = prm[3]; dp.c0y = prm[4]; dp.c0z = prm[5];
+    dp.c1x = prm[6]; dp.c1y = prm[7]; dp.c1z = prm[8];
+    dp.tab = table; dp.tab_k = tab_k; dp.tab_invw = 1.0 / tab_w;
+    long long ok = 0, tot = 0;
+    for (int i = 0; i < n; ++i) {
+        const int* row = nbr + (int64_t)i * MAXDEG;
+        for (int t = 0; t < deg[i]; ++t) {
+            int j = row[t], k = row[(t + 1) % deg[i]];
+            FanPair f = fan_pair(load3(z, i), load3(z, j), load3(z, k), i, j, k);
+            for (int s = 0; s < 2; ++s) {
+                LocalFit lf;
+                bool a = local_fit(dp, f.s[s], v3(dp.c0x, dp.c0y, dp.c0z), lf);
+                if (a && kind == 7) a = local_fit(dp, f.s[s], v3(dp.c1x, dp.c1y, dp.c1z), lf);
+                ok += a;
+                ++tot;
+            }
+        }
+    }
+    counts[0] = ok;
+    counts[1] = tot;
+    return 0;
+}
+
+extern "C" int harness_quad_sym7(const double* z, int n, const int* nbr, const int* deg,
+                                 const double* l1, const double* l2, const double* w,
+                                 const double* table, int tab_k, double tab_w, const double* prm,
+                                 int kind, double* out) {
+    DensityParams dp{};
+    dp.kind = kind;
+    dp.gamma = prm[0]; dp.beta = prm[1]; dp.alpha = prm[2];
+    dp.c0x = prm[3]; dp.c0y = prm[4]; dp.c0z = prm[5];
+    dp.c1x = prm[6]; dp.c1y = prm[7]; dp.c1z = prm[8];
+    dp.tab = table; dp.tab_k = tab_k; dp.tab_invw = tab_w > 0 ? 1.0 / tab_w : 0.0;
+    int pole = 0;
+    for (int i = 0; i < n; ++i) {
+        double acc[5] = {0, 0, 0, 0, 0};
+        const int* row = nbr + (int64_t)i * MAXDEG;
+        for (int t = 0; t < deg[i]; ++t) {
+            int j = row[t], k = row[(t + 1) % deg[i]];
+            FanPair f = fan_pair(load3(z, i), load3(z, j), load3(z, k), i, j, k);
+            for (int s = 0; s < 2; ++s) {
+                if (kind == 6) subtri_moments_sym7<6, 8>(f.s[s], load3(z, i), l1, l2, w, dp, acc, &pole);
+                else if (kind == 7) subtri_moments_sym7<7, 8>(f.s[s], load3(z, i), l1, l2, w, dp, acc, &pole);
+                else subtri_moments_sym7<0, 8>(f.s[s], load3(z, i), l1, l2, w, dp, acc, &pole);
+            }
+        }
+        for (int c = 0; c < 5; ++c) out[5 * (int64_t)i + c] = acc[c];
+    }
+    return pole;
+}

@@ -311,3 +311,19 @@ def test_sharded_errors_raise_consistently():
     zt = torch.from_numpy(z).cuda()
     with _ev("const", "4pt", 0) as ev, pytest.raises(P.InsufficientPointsError):
         emulate_shards(CudaShardBackend(ev), zt, 2)
+
+
+@pytest.mark.parametrize("cfg", ["const", "c4", "c5"])
+def test_sym7_fast_path_matches_generic(cfg, monkeypatch):
+    """Leaf-grid placement of the symmetric 7-point rule (subtri_moments_sym7) against the
+    generic composite-table loop (SCVT_NO_SYM7=1 at context creation)."""
+    z = (P.random_sphere_points(40962, 0) if cfg == "const"
+         else P.sample_by_density(P.density_preset(cfg), 40962, 0))
+    with _ev(cfg, "7pt", 3) as a:
+        ra = a.evaluate(z)
+    monkeypatch.setenv("SCVT_NO_SYM7", "1")
+    with _ev(cfg, "7pt", 3) as b:
+        rb = b.evaluate(z)
+    assert rel(ra.mass, rb.mass) <= 1e-13
+    assert rel(ra.first, rb.first) <= 1e-13
+    assert abs(ra.energy - rb.energy) <= 1e-13 * rb.energy

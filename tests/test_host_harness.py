@@ -173,3 +173,36 @@ def test_density_kinds_vs_golden(h, gold, cfg):
     p = f"uniform_{cfg}_4pt_d0_"
     assert rel(out[:, 1:4], g[p + "first"]) <= 1e-13
     assert rel(out[:, 0], g[p + "mass"]) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg,which", [("const", "uniform"), ("c4", "uniform"), ("c5", "uniform"),
+                                       ("c4", "sampled"), ("c5", "sampled")])
+def test_sym7_fit_path_vs_golden(h, gold, cfg, which):
+    """Leaf-grid 7-point placement + per-patch local fit of rho^(1/4) (the k_quad fast path)
+    against the reference's 7pt/depth-3 moments."""
+    from paper_1709_06924_b200 import density as D, geometry as G
+
+    g = gold("c1_eval") if cfg == "const" else gold("density_eval")
+    z = g["z"] if cfg == "const" else g[f"{which}_{cfg}_z" if which == "sampled" else "uniform_z"]
+    pref = "7pt_d3_" if cfg == "const" else (f"sampled_{cfg}_7pt_d3_" if which == "sampled"
+                                            else f"uniform_{cfg}_7pt_d3_")
+    f = D.density_preset(cfg)
+    _, nbr, deg, _ = cells(h, z)
+    l1, l2, w = G.composite_nodes(G.QUADRATURE_RULES["7pt"], 3)
+    p = D.device_params(f)
+    prm = np.zeros(15)
+    prm[0:3] = [p["gamma"], p["beta"], p["alpha"]]
+    prm[3:9] = p["center"]
+    if p["table"] is not None:
+        co, wd = p["table"]
+        co = np.ascontiguousarray(co)
+        kind = 7 if f.variant == "tanh4x2" else 6
+    else:
+        co, wd, kind = np.zeros(1), 0.0, 0
+    out = np.zeros((len(z), 5))
+    h.harness_quad_sym7(dp(np.ascontiguousarray(z)), len(z), ip(nbr), ip(deg), dp(l1), dp(l2),
+                        dp(w), dp(co), co.shape[1] if co.ndim == 3 else 0, ctypes.c_double(wd),
+                        dp(prm), kind, dp(out))
+    assert rel(out[:, 0], g[pref + "mass"]) <= 1e-13
+    assert rel(out[:, 1:4], g[pref + "first"]) <= 1e-13
+    assert abs(out[:, 4].sum() - g[pref + "energy"]) <= 1e-13 * g[pref + "energy"]
