@@ -76,7 +76,9 @@ __device__ __forceinline__ int wpoly_clip(WPoly& P, int lane, double ax, double 
     line_meet(eax, eay, eb, ax, ay, b, &Ax, &Ay);
     line_meet(ax, ay, b, lax, lay, lb, &Bx, &By);
     // surviving edges last, last+1, ..., ein (cyclic) -> lanes 0..m-2; new edge -> lane m-1
-    const int src = (last + lane) % n;
+    int src = last + lane;                       // (last + lane) mod n for lanes < m
+    if (src >= n) src -= n;
+    if (src >= n) src = 0;
     double nax = __shfl_sync(FULL, P.ax, src), nay = __shfl_sync(FULL, P.ay, src);
     double nb = __shfl_sync(FULL, P.b, src);
     double nvx = __shfl_sync(FULL, P.vx, src), nvy = __shfl_sync(FULL, P.vy, src);
@@ -95,8 +97,11 @@ __device__ __forceinline__ double wpoly_R2(const WPoly& P, int lane, bool* box) 
     double q = lane < P.n ? P.vx * P.vx + P.vy * P.vy : 0.0;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) q = fmax(q, __shfl_xor_sync(FULL, q, off));
-    double s = sqrt(1.0 + q);
-    return 2.0 * q / (s * (s + 1.0));
+    // chord^2 = 2q / (s (s + 1)), s = sqrt(1 + q); branch-free, ~1 ulp (only compared with
+    // candidate distances, and rounded up by the callers' (1 + 1e-12) factors)
+    const double is = fast_rsqrt(1.0 + q);
+    const double sq = (1.0 + q) * is;
+    return 2.0 * q * is * fast_rcp(sq + 1.0) * (1.0 + 1e-15);
 }
 
 // local point density from the 3x3 bucket neighbourhood of `key` (same face only)
@@ -162,7 +167,7 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
     double lo_c2 = -1.0;                       // exclusive lower bound on c2
     double R2 = 8.0;
     bool box = true;
-    int status = 0, rounds = 0, passes = 0, sweep_visits = 0;
+    int status = 0, rounds = 0, passes = 0, sweep_visits = 0, scanned = 0, ncands = 0, nclips = 0;
     const unsigned lt_mask = (1u << lane) - 1u;
     while (true) {
         ++passes;
@@ -193,6 +198,7 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
                         if (acc && c2 == 0.0) { status |= ST_DUPLICATE; acc = false; }
                     }
                     unsigned ma = __ballot_sync(FULL, acc);
+                    scanned += min(32, p1 - base);
                     int pos = count + __popc(ma & lt_mask);
                     if (acc && pos < WCAND) { s_c2[pos] = c2; s_j[pos] = j; s_p[pos] = p; }
                     count += __popc(ma);
@@ -224,9 +230,11 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
             for (int h = 0; h < 2; ++h)
                 if (rk[h] >= 0) { s_c2[rk[h]] = kc[h]; s_j[rk[h]] = kj[h]; s_p[rk[h]] = kp[h]; }
             __syncwarp();
+            ncands += count;
             for (int t = 0; t < count; ++t) {
                 double c2 = s_c2[t];
                 if (c2 >= 4.0 * R2 * (1.0 + 1e-12)) break;
+                ++nclips;
                 int j = s_j[t];
                 const double* q = g.zs + 4 * (int64_t)s_p[t];
                 V3 zj = v3(q[0], q[1], q[2]);
@@ -356,6 +364,9 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
     st->rounds = rounds;
     st->passes = passes;
     st->sweep_visits = sweep_visits;
+    st->scanned = scanned;
+    st->cands = ncands;
+    st->clips = nclips;
     st->tie_breaks = __reduce_add_sync(FULL, cc.tie_breaks);
     if (status) return -status;
     const int n = P.n;

@@ -73,6 +73,21 @@ SCVT_HD double fast_rsqrt(double a) {
 #endif
 }
 
+// 1/a for finite nonzero a without the special-case branches of the IEEE division:
+// hardware approximation + two Newton steps (~1 ulp).
+SCVT_HD double fast_rcp(double a) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    double e = fma(-a, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-a, y, 1.0);
+    return fma(y, e, y);
+#else
+    return 1.0 / a;
+#endif
+}
+
 // numpy's np.linalg.norm of a 3-vector is sqrt(x*x + y*y + z*z) evaluated as a dot product;
 // we use the same expression.
 SCVT_HD double norm3(V3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
@@ -135,8 +150,10 @@ SCVT_HD bool cap_face_range(const CapBox& cb, int face, int G, int* iu0, int* iu
     float vmin = fminf(cb.lo[cc] / t_lo, cb.lo[cc] / t_hi), vmax = fmaxf(cb.hi[cc] / t_lo, cb.hi[cc] / t_hi);
     umin = fmaxf(umin, -1.0f); umax = fminf(umax, 1.0f);
     vmin = fmaxf(vmin, -1.0f); vmax = fminf(vmax, 1.0f);
-    int a0 = bucket_index_1d(umin, G) - 1, a1 = bucket_index_1d(umax, G) + 1;
-    int b0 = bucket_index_1d(vmin, G) - 1, b1 = bucket_index_1d(vmax, G) + 1;
+    // no +-1 widening: the 2e-4 rad cap margin (cap_box) is ~30x the FP32 error of the bucket
+    // index of a point, so every point of the cap lies in the returned rectangle
+    int a0 = bucket_index_1d(umin, G), a1 = bucket_index_1d(umax, G);
+    int b0 = bucket_index_1d(vmin, G), b1 = bucket_index_1d(vmax, G);
     *iu0 = a0 < 0 ? 0 : a0; *iu1 = a1 >= G ? G - 1 : a1;
     *iv0 = b0 < 0 ? 0 : b0; *iv1 = b1 >= G ? G - 1 : b1;
     return true;
@@ -280,7 +297,7 @@ SCVT_HD void poly_init(Poly& P) {
 SCVT_HD void line_meet(double a1x, double a1y, double b1, double a2x, double a2y, double b2,
                        double* x, double* y) {
     double det = a1x * a2y - a1y * a2x;
-    double inv = 1.0 / det;
+    double inv = fast_rcp(det);
     *x = (b1 * a2y - b2 * a1y) * inv;
     *y = (a1x * b2 - a2x * b1) * inv;
 }
@@ -391,7 +408,7 @@ struct GridView {
 
 constexpr int CAND = 48;    // nearest-first candidate list per pass
 
-struct CellStats { int rounds; int passes; int tie_breaks; int sweep_visits; };
+struct CellStats { int rounds; int passes; int tie_breaks; int sweep_visits; int scanned; int cands; int clips; };
 
 // Build the Voronoi cell of generator i by nearest-first half-plane clipping with a
 // security-radius certificate: a point j can cut the cell only if |z_j - z_i| < 2R with R
@@ -524,6 +541,7 @@ SCVT_HD int build_cell(const GridView& g, int i, V3 zi, int* nbr_out, CellStats*
     st->passes = passes;
     st->tie_breaks = cc.tie_breaks;
     st->sweep_visits = 0;
+    st->scanned = st->cands = st->clips = 0;
     if (status) return -status;
     int n = cur->n;
     if (n > MAXDEG) return -ST_DEG_OVERFLOW;

@@ -70,7 +70,8 @@ __global__ void k_gather_sorted(const double* __restrict__ z, const int* __restr
 // Fast path: one warp per generator (bucket order), polygon in registers.
 __global__ void __launch_bounds__(CELL_WARPS * 32, 4)
 k_cells_warp(GridView g, int p_lo, int p_hi, int* __restrict__ nbr, int* __restrict__ deg,
-             int* __restrict__ status, int* __restrict__ stats) {
+             int* __restrict__ status, int* __restrict__ stats,
+             unsigned long long* __restrict__ diag) {
     __shared__ double s_c2[CELL_WARPS][WCAND];
     __shared__ int s_j[CELL_WARPS][WCAND];
     __shared__ int s_p[CELL_WARPS][WCAND];
@@ -99,6 +100,14 @@ k_cells_warp(GridView g, int p_lo, int p_hi, int* __restrict__ nbr, int* __restr
         if (cs.sweep_visits) {
             atomicAdd(&stats[6], 1);
             atomicAdd(&stats[7], cs.sweep_visits >> 5);
+        }
+        if (diag) {
+            atomicAdd(&diag[0], 1ull);
+            atomicAdd(&diag[1], (unsigned long long)cs.passes);
+            atomicAdd(&diag[2], (unsigned long long)cs.scanned);
+            atomicAdd(&diag[3], (unsigned long long)cs.cands);
+            atomicAdd(&diag[4], (unsigned long long)cs.clips);
+            atomicAdd(&diag[5], (unsigned long long)cs.rounds);
         }
     }
 }
@@ -743,6 +752,7 @@ struct scvt_ctx {
     bool prof = false;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     double prof_ms[4] = {0, 0, 0, 0};
+    unsigned long long* d_diag = nullptr;   // cell-builder work counters (profiling only)
     int64_t prof_n[4] = {0, 0, 0, 0};
 };
 
@@ -929,7 +939,8 @@ int build_cells_range(scvt_ctx* ctx, const GridView& g, int64_t lo, int64_t hi) 
     if (cnt <= 0) return SCVT_OK;
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], s));
     k_cells_warp<<<blocks_for(cnt, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
-        g, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
+        g, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8,
+        ctx->prof ? ctx->d_diag : nullptr);
     LAUNCHED();
     k_cells<<<blocks_for(cnt, CELL_THREADS), CELL_THREADS, 0, s>>>(
         g, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
@@ -1101,6 +1112,13 @@ int scvt_profile_enable(scvt_ctx* ctx, int on) {
     return SCVT_OK;
 }
 
+int scvt_profile_counters(scvt_ctx* ctx, int64_t* out8, int reset) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    CK(cudaMemcpy(out8, ctx->d_diag, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (reset) CK(cudaMemset(ctx->d_diag, 0, 8 * sizeof(int64_t)));
+    return SCVT_OK;
+}
+
 int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int reset) {
     if (!ctx) return SCVT_ERR_CONFIG;
     for (int k = 0; k < 3; ++k) {
@@ -1190,6 +1208,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_partials, (int64_t)MAX_SLOTS * RED_BLOCKS);
     AL(d_scal, MAX_SLOTS);
     AL(d_status, 16);
+    AL(d_diag, 8);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -1246,7 +1265,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
-    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
+    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
                    ctx->d_obt, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, ctx->d_partials,
