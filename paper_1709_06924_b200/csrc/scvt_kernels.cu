@@ -216,7 +216,7 @@ struct QuadArgs {
 };
 
 template <int KIND, bool SPHERE, bool SYM7>
-__global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? 5 : 1)
+__global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? (KIND == DEN_TANH4X2_TAB ? 3 : 5) : 1)
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
     for (int q = threadIdx.x; q < 3 * a.nq; q += blockDim.x) s_nodes[q] = a.nodes[q];
