@@ -101,6 +101,10 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
                      uint8_t* flags_out, int64_t* stats_host);
 
 /* evaluation ---------------------------------------------------------------------------
+ * Consecutive evaluations of the same n reuse the previous cycles when the robust certificate
+ * (consistency, orientation, local Delaunay on every edge) still holds at the new positions;
+ * failing neighbourhoods are rebuilt, so the result is always THE Delaunay triangulation
+ * (env SCVT_NO_REUSE=1 disables the reuse).
  * Replaces MeshEvaluator.evaluate (pipeline.py:261-279) = triangulation + Voronoi fans
  * (delaunay.py:337-380) + depth-d subdivision (383-407) + cell_quadrature
  * (cvt_core.py:55-117) + gradient assembly.  Outputs (device): grad (n,3) =
@@ -188,7 +192,8 @@ int scvt_normalize_rows(scvt_ctx* ctx, double* z, int64_t n);
 int scvt_profile_enable(scvt_ctx* ctx, int on);
 int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int reset);
 /* cell-builder work counters accumulated while profiling is enabled:
- * out8 = {cells, candidate passes, points scanned, candidates sorted, clips, radius rounds, 0, 0} */
+ * out8 = {cells, candidate passes, points scanned, candidates sorted, clips, radius rounds,
+ *         evaluations whose previous cycles were certified and reused, cells rebuilt by reuse} */
 int scvt_profile_counters(scvt_ctx* ctx, int64_t* out8, int reset);
 /* measured FP64 DFMA throughput of `device` in TFLOP/s (2 FLOPs per FMA): the FP64
  * roofline denominator, which MEASURED_PEAKS.json does not carry */

@@ -69,15 +69,23 @@ __global__ void k_gather_sorted(const double* __restrict__ z, const int* __restr
 
 // Fast path: one warp per generator (bucket order), polygon in registers.
 __global__ void __launch_bounds__(CELL_WARPS * 32, 4)
-k_cells_warp(GridView g, int p_lo, int p_hi, int* __restrict__ nbr, int* __restrict__ deg,
+k_cells_warp(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
+             const int* __restrict__ list_n, int* __restrict__ nbr, int* __restrict__ deg,
              int* __restrict__ status, int* __restrict__ stats,
              unsigned long long* __restrict__ diag) {
     __shared__ double s_c2[CELL_WARPS][WCAND];
     __shared__ int s_j[CELL_WARPS][WCAND];
     __shared__ int s_p[CELL_WARPS][WCAND];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t p = p_lo + (int64_t)blockIdx.x * CELL_WARPS + w;
-    if (p >= p_hi) return;   // warp-uniform
+    const int64_t idx = (int64_t)blockIdx.x * CELL_WARPS + w;
+    int64_t p;
+    if (list) {                 // rebuild of a compacted list of sorted slots
+        if (idx >= *list_n) return;
+        p = list[idx];
+    } else {
+        p = p_lo + idx;
+        if (p >= p_hi) return;   // warp-uniform
+    }
     const int i = g.ids[p];
     const double* q = g.zs + 4 * p;
     V3 zi = v3(q[0], q[1], q[2]);
@@ -114,10 +122,18 @@ k_cells_warp(GridView g, int p_lo, int p_hi, int* __restrict__ nbr, int* __restr
 
 // Fallback: one thread per generator the warp builder handed back (deg == -1).
 __global__ void __launch_bounds__(CELL_THREADS)
-k_cells(GridView g, int p_lo, int p_hi, int* __restrict__ nbr, int* __restrict__ deg,
+k_cells(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
+        const int* __restrict__ list_n, int* __restrict__ nbr, int* __restrict__ deg,
         int* __restrict__ status, int* __restrict__ stats) {
-    int p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= p_hi) return;
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    int p;
+    if (list) {
+        if (idx >= *list_n) return;
+        p = list[idx];
+    } else {
+        p = p_lo + idx;
+        if (p >= p_hi) return;
+    }
     int i = g.ids[p];
     if (deg[i] != -1) return;
     V3 zi = v3(g.zs[4 * (int64_t)p], g.zs[4 * (int64_t)p + 1], g.zs[4 * (int64_t)p + 2]);
@@ -140,34 +156,61 @@ __device__ __forceinline__ int find_in_cycle(const int* __restrict__ row, int d,
     return -1;
 }
 
-// consistency of adjacent cycles + local Delaunay filter (edge (i, n_t) with triangles
-// (i, n_t, n_{t+1}) and (i, n_{t-1}, n_t))
+// Certificate of a set of cycles at positions z, per edge (i, n_t) with triangles
+// (i, n_t, n_{t+1}) and (i, n_{t-1}, n_t): (1) consistency — the triangle appears in n_t's
+// cycle as (n_t, n_{t+1}, i); (2) positive orientation det[z_i, z_a, z_b] > 0; (3) local
+// Delaunay — orient(z_i, z_a, z_b, z_c) < 0 decided by the robust predicate (FP64 filter ->
+// double-double -> SoS).  Consistent + positively oriented + locally Delaunay everywhere
+// means the cycles are THE (SoS-)Delaunay triangulation, however they were produced.
+// mode 0: failures set status bits (certificate of a fresh build);
+// mode 1: failures mark the cells of the offending triangle/quad in bad[] (reuse check).
+__device__ __forceinline__ void mark_bad(int mode, int* status, int bit, int* bad, int* nbad,
+                                         int i, int a, int b, int c) {
+    if (mode == 0) { atomicOr(status, bit); return; }
+    const int v[4] = {i, a, b, c};
+    for (int k = 0; k < 4; ++k)
+        if (v[k] >= 0 && atomicExch(&bad[v[k]], 1) == 0) atomicAdd(nbad, 1);
+}
+
 __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ ids, int p_lo,
                          int p_hi, const int* __restrict__ nbr, const int* __restrict__ deg,
                          uint8_t* __restrict__ amb, int* __restrict__ status,
-                         int* __restrict__ stats) {
+                         int* __restrict__ stats, int mode, int* __restrict__ bad,
+                         int* __restrict__ nbad) {
     int p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= p_hi) return;
     int i = ids[p];
     int d = deg[i];
     const int* row = nbr + (int64_t)i * MAXDEG;
-    if (d < 3) { atomicOr(status, ST_INCONSISTENT); return; }
+    if (d < 3 || d > MAXDEG) { mark_bad(mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1); return; }
     V3 zi = load3(z, i);
     int namb = 0;
     for (int t = 0; t < d; ++t) {
         int a = row[t], b = row[t + 1 == d ? 0 : t + 1], c = row[t == 0 ? d - 1 : t - 1];
         int da = deg[a];
         const int* ra = nbr + (int64_t)a * MAXDEG;
-        int p = find_in_cycle(ra, da, i);
-        bool ok = p >= 0 && ra[p == 0 ? da - 1 : p - 1] == b;
-        if (!ok) atomicOr(status, ST_INCONSISTENT);
-        bool am;
-        int s = insphere_sign(zi, load3(z, a), load3(z, b), load3(z, c), &am);
-        amb[(int64_t)i * MAXDEG + t] = am ? 1 : 0;
-        if (am) ++namb;
-        else if (s >= 0) atomicOr(status, ST_NOT_DELAUNAY);
+        int q = da >= 3 && da <= MAXDEG ? find_in_cycle(ra, da, i) : -1;
+        bool ok = q >= 0 && ra[q == 0 ? da - 1 : q - 1] == b;
+        if (!ok) mark_bad(mode, status, ST_INCONSISTENT, bad, nbad, i, a, b, -1);
+        V3 za = load3(z, a), zb = load3(z, b), zc = load3(z, c);
+        if (mode == 1) {   // reused cycles: the triangle must still face outward
+            int tier;
+            if (orient_robust(v3(0, 0, 0), zi, za, zb, -1, i, a, b, &tier) <= 0)
+                mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, -1);
+        }
+        int tier;
+        int sgn = orient_robust(zi, za, zb, zc, i, a, b, c, &tier);
+        amb[(int64_t)i * MAXDEG + t] = tier > 0 ? 1 : 0;
+        namb += tier > 0;
+        if (sgn > 0) mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, c);
     }
     if (namb) atomicAdd(&stats[3], namb);
+}
+
+__global__ void k_flag_slots(int n, const int* __restrict__ ids, const int* __restrict__ bad,
+                             uint8_t* __restrict__ flags) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) flags[p] = bad[ids[p]] ? 1 : 0;
 }
 
 // incidence CSR in bucket (spatial) order: sorted slot p -> generator ids[p]
@@ -753,6 +796,10 @@ struct scvt_ctx {
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     double prof_ms[4] = {0, 0, 0, 0};
     unsigned long long* d_diag = nullptr;   // cell-builder work counters (profiling only)
+    // cycle reuse across evaluations
+    int64_t cycles_n = -1;                  // n of the certified cycles held in d_nbr/d_deg
+    int* d_bad = nullptr; int* d_nbad = nullptr; uint8_t* d_slotflag = nullptr; int* d_list = nullptr;
+    int64_t reuse_stats[4] = {0, 0, 0, 0};  // checks, bad cells, evaluations fully reused
     int64_t prof_n[4] = {0, 0, 0, 0};
 };
 
@@ -939,31 +986,82 @@ int build_cells_range(scvt_ctx* ctx, const GridView& g, int64_t lo, int64_t hi) 
     if (cnt <= 0) return SCVT_OK;
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], s));
     k_cells_warp<<<blocks_for(cnt, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
-        g, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8,
-        ctx->prof ? ctx->d_diag : nullptr);
+        g, (int)lo, (int)hi, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+        ctx->d_status + 8, ctx->prof ? ctx->d_diag : nullptr);
     LAUNCHED();
     k_cells<<<blocks_for(cnt, CELL_THREADS), CELL_THREADS, 0, s>>>(
-        g, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_status, ctx->d_status + 8);
+        g, (int)lo, (int)hi, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+        ctx->d_status + 8);
     LAUNCHED();
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
     return SCVT_OK;
 }
 
-int verify_range(scvt_ctx* ctx, const double* z, int64_t lo, int64_t hi) {
+int verify_range(scvt_ctx* ctx, const double* z, int64_t lo, int64_t hi, int mode = 0) {
     int64_t cnt = hi - lo;
     if (cnt <= 0) return SCVT_OK;
     k_verify<<<blocks_for(cnt, 128), 128, 0, ctx->stream>>>(
         z, ctx->d_ids, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_amb, ctx->d_status,
-        ctx->d_status + 8);
+        ctx->d_status + 8, mode, ctx->d_bad, ctx->d_nbad);
     LAUNCHED();
+    return SCVT_OK;
+}
+
+bool reuse_enabled() { return getenv("SCVT_NO_REUSE") == nullptr; }
+
+// Reuse the previous evaluation's cycles when they are still a certified Delaunay
+// triangulation of the new positions; rebuild (grid method) only the cells of failing
+// triangles/quads, re-certify, and escalate to a full rebuild when churn is large.
+int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView& g, bool* done) {
+    cudaStream_t s = ctx->stream;
+    *done = false;
+    for (int round = 0; round < 4; ++round) {
+        CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
+        CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
+        TRY(verify_range(ctx, z, 0, n, 1));
+        int nbad = 0;
+        CK(cudaMemcpyAsync(&nbad, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ctx->reuse_stats[0] += 1;
+        ctx->reuse_stats[1] += nbad;
+        if (nbad == 0) { *done = true; return SCVT_OK; }
+        if (nbad > (3 * n) / 4 || round == 3) return SCVT_OK;   // caller rebuilds everything
+        // compact the bad generators' sorted slots and rebuild those cells
+        k_flag_slots<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_bad,
+                                                        ctx->d_slotflag);
+        LAUNCHED();
+        size_t tb = ctx->cub_bytes;
+        cub::CountingInputIterator<int> it(0);
+        CK(cub::DeviceSelect::Flagged(ctx->d_cub, tb, it, ctx->d_slotflag, ctx->d_list,
+                                      ctx->d_nbad, (int)n, s));
+        k_cells_warp<<<blocks_for(nbad, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
+            g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+            ctx->d_status + 8, ctx->prof ? ctx->d_diag : nullptr);
+        LAUNCHED();
+        k_cells<<<blocks_for(nbad, CELL_THREADS), CELL_THREADS, 0, s>>>(
+            g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+            ctx->d_status + 8);
+        LAUNCHED();
+    }
     return SCVT_OK;
 }
 
 int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
     GridView g;
     TRY(build_grid(ctx, z, n, &g));
+    if (ctx->cycles_n == n && reuse_enabled()) {
+        if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        bool done = false;
+        TRY(build_cells_reuse(ctx, z, n, g, &done));
+        if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (done) {
+            ctx->reuse_stats[2] += 1;
+            return SCVT_OK;
+        }
+        CK(cudaMemsetAsync(ctx->d_status + 8, 0, 8 * sizeof(int), ctx->stream));
+    }
     TRY(build_cells_range(ctx, g, 0, n));
-    return verify_range(ctx, z, 0, n);
+    return verify_range(ctx, z, 0, n, 0);
 }
 
 int cells_from_triangles(scvt_ctx* ctx, const int64_t* tri, int64_t t, int64_t n) {
@@ -1114,8 +1212,13 @@ int scvt_profile_enable(scvt_ctx* ctx, int on) {
 
 int scvt_profile_counters(scvt_ctx* ctx, int64_t* out8, int reset) {
     if (!ctx) return SCVT_ERR_CONFIG;
-    CK(cudaMemcpy(out8, ctx->d_diag, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-    if (reset) CK(cudaMemset(ctx->d_diag, 0, 8 * sizeof(int64_t)));
+    CK(cudaMemcpy(out8, ctx->d_diag, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    out8[6] = ctx->reuse_stats[2];   // evaluations whose cycles were certified by reuse
+    out8[7] = ctx->reuse_stats[1];   // cells rebuilt by reuse rounds
+    if (reset) {
+        CK(cudaMemset(ctx->d_diag, 0, 8 * sizeof(int64_t)));
+        ctx->reuse_stats[0] = ctx->reuse_stats[1] = ctx->reuse_stats[2] = 0;
+    }
     return SCVT_OK;
 }
 
@@ -1209,6 +1312,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_scal, MAX_SLOTS);
     AL(d_status, 16);
     AL(d_diag, 8);
+    AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -1224,7 +1328,12 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     cub::DeviceRadixSort::SortPairs(nullptr, b1, ctx->d_keys, ctx->d_skeys, ctx->d_vals,
                                     ctx->d_ids, (int)n, 0, 32);
     cub::DeviceScan::ExclusiveSum(nullptr, b2, ctx->d_deg, ctx->d_inc_start, (int)n + 1);
-    ctx->cub_bytes = std::max(b1, b2);
+    size_t b3 = 0;
+    {
+        cub::CountingInputIterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, b3, it, ctx->d_slotflag, ctx->d_list, ctx->d_nbad, (int)n);
+    }
+    ctx->cub_bytes = std::max(std::max(b1, b2), b3);
     if ((r = dalloc(ctx, (char**)&ctx->d_cub, ctx->cub_bytes))) return bail(r);
     // node table
     std::vector<double> tbl(3 * (size_t)ctx->nq);
@@ -1265,7 +1374,8 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
-    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
+    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
+                   ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
                    ctx->d_obt, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, ctx->d_partials,
@@ -1285,6 +1395,7 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
                      uint8_t* flags_out, int64_t* stats_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
     TRY(reset_status(ctx));
+    ctx->cycles_n = -1;
     TRY(build_cells(ctx, z, n));
     cudaStream_t s = ctx->stream;
     // canonical triangles: count per min-id generator, scan, emit sorted
@@ -1316,6 +1427,7 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
     if (total != 2 * n - 4)
         return fail(ctx, SCVT_ERR_COVERAGE, "triangulation not closed: K=%lld, T=%d (want %lld)",
                     (long long)n, total, (long long)(2 * n - 4));
+    ctx->cycles_n = n;
     if (stats_host && flags_out) {
         // flagged triangle count
         std::vector<uint8_t> f((size_t)total);
@@ -1333,8 +1445,10 @@ int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, doubl
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
     ctx->prof_n[3] = 0;
     TRY(reset_status(ctx));
-    TRY(build_cells(ctx, z, n));
-    return moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
+    int rc = build_cells(ctx, z, n);
+    if (rc == SCVT_OK) rc = moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
+    ctx->cycles_n = rc == SCVT_OK ? n : -1;   // certified cycles may seed the next evaluation
+    return rc;
 }
 
 int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const int64_t* tri,
@@ -1345,6 +1459,7 @@ int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const 
     if (t != 2 * n - 4) return fail(ctx, SCVT_ERR_COVERAGE, "T=%lld != 2n-4", (long long)t);
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
     ctx->prof_n[3] = 1;   // no cell-construction pair on this path
+    ctx->cycles_n = -1;
     TRY(reset_status(ctx));
     TRY(cells_from_triangles(ctx, tri, t, n));
     return moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
@@ -1362,6 +1477,7 @@ int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int n
         return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
     ctx->prof_n[3] = 0;
+    ctx->cycles_n = -1;
     TRY(reset_status(ctx));
     GridView g;
     TRY(build_grid(ctx, z, n, &g));

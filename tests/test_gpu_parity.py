@@ -327,3 +327,19 @@ def test_sym7_fast_path_matches_generic(cfg, monkeypatch):
     assert rel(ra.mass, rb.mass) <= 1e-13
     assert rel(ra.first, rb.first) <= 1e-13
     assert abs(ra.energy - rb.energy) <= 1e-13 * rb.energy
+
+
+def test_cycle_reuse_matches_fresh_build(monkeypatch):
+    """Certified reuse of the previous cycles (plus local rebuilds) gives exactly the fresh
+    triangulation along an optimizer trajectory with heavy early churn."""
+    z0 = P.sample_by_density(P.density_preset("c4"), 40962, 0)
+    with _ev("c4", "4pt", 0) as ev, _ev("c4", "4pt", 0) as fresh:
+        st = P.Minimizer(torch.from_numpy(z0).cuda(), "lloyd-plbfgs", ev, 7)
+        for _ in range(6):
+            st.step()
+            t_reuse = ev.triangulation(st.z).triangles          # reuse path (same n as before)
+            monkeypatch.setenv("SCVT_NO_REUSE", "1")
+            t_fresh = fresh.triangulation(st.z).triangles
+            monkeypatch.delenv("SCVT_NO_REUSE")
+            assert np.array_equal(t_reuse, t_fresh)
+            assert np.array_equal(t_fresh, O.convex_hull_delaunay(st.z.cpu().numpy()))
