@@ -823,7 +823,8 @@ SCVT_HD bool local_fit(const DensityParams& p, const SubTri& st, V3 c, LocalFit&
     const double lo = smin - margin, hi = smax + margin;
     if (!(lo > 0.0)) return false;
     const double hw = 0.5 * (hi - lo), sc = 0.5 * (hi + lo);
-    if (hw > 0.02 * sc) return false;           // (hw/sc)^7 bounds the sqrt-singularity term
+    if (hw > 0.1 * sc) return false;            // hopeless near the s = 0 singularity; the
+                                                // check points below are the accuracy guard
     double u[7];
 #pragma unroll
     for (int j = 0; j < 7; ++j) {

@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -1031,7 +1032,7 @@ int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView&
                                                         ctx->d_slotflag);
         LAUNCHED();
         size_t tb = ctx->cub_bytes;
-        cub::CountingInputIterator<int> it(0);
+        thrust::counting_iterator<int> it(0);
         CK(cub::DeviceSelect::Flagged(ctx->d_cub, tb, it, ctx->d_slotflag, ctx->d_list,
                                       ctx->d_nbad, (int)n, s));
         k_cells_warp<<<blocks_for(nbad, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
@@ -1330,7 +1331,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     cub::DeviceScan::ExclusiveSum(nullptr, b2, ctx->d_deg, ctx->d_inc_start, (int)n + 1);
     size_t b3 = 0;
     {
-        cub::CountingInputIterator<int> it(0);
+        thrust::counting_iterator<int> it(0);
         cub::DeviceSelect::Flagged(nullptr, b3, it, ctx->d_slotflag, ctx->d_list, ctx->d_nbad, (int)n);
     }
     ctx->cub_bytes = std::max(std::max(b1, b2), b3);
