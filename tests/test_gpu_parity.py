@@ -343,3 +343,57 @@ def test_cycle_reuse_matches_fresh_build(monkeypatch):
             monkeypatch.delenv("SCVT_NO_REUSE")
             assert np.array_equal(t_reuse, t_fresh)
             assert np.array_equal(t_fresh, O.convex_hull_delaunay(st.z.cpu().numpy()))
+
+
+def _oracle_cells(z, tri, density_name, rule, depth, gens):
+    """Oracle moments of the cells of `gens` only (reference fans restricted to those cells)."""
+    dens = O.density_for(density_name)
+    keep = np.isin(tri, gens).any(axis=1)
+    t = tri[keep]
+    f = O.build_fans(z, t)
+    sel = np.isin(f.cells, gens)
+    f = O.Fans(f.verts[sel], f.cells[sel], f.edge_other[sel], f.signed_area[sel], 0)
+    mass = np.zeros(len(z))
+    first = np.zeros((len(z), 3))
+    for s in range(0, len(f.cells), 8192):
+        sub = O.subdivide(O.Fans(f.verts[s:s + 8192], f.cells[s:s + 8192],
+                                 f.edge_other[s:s + 8192], f.signed_area[s:s + 8192], 0), depth)
+        m, c, _ = O.cell_quadrature(z, sub, dens, O.RULES[rule], len(z))
+        mass += m
+        first += c
+    return mass[gens], first[gens]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,n", [("c3", 163842), ("c4", 655362), ("c5", 2621442)])
+def test_full_size_sampled_cell_parity(cfg, n):
+    """BASELINE sizes: GPU moments of 1500 random cells against the oracle's (Qhull hull +
+    reference fans + depth-3 subdivision + 7-pt rule), per generator at 1e-12."""
+    z = P.sample_by_density(P.density_preset(cfg), n, 0)
+    tri = O.convex_hull_delaunay(z)
+    gens = np.sort(np.random.default_rng(5).choice(n, 1500, replace=False))
+    om, oc = _oracle_cells(z, tri, cfg, "7pt", 3, gens)
+    with _ev(cfg, "7pt", 3) as ev:
+        r = ev.evaluate(z)
+        t = ev.triangulation(z)
+    assert np.array_equal(t.triangles, tri)
+    assert np.max(np.abs(r.mass[gens] - om) / np.abs(om)) <= 1e-12
+    assert np.max(np.linalg.norm(r.first[gens] - oc, axis=1) / np.linalg.norm(oc, axis=1)) <= 1e-12
+
+
+@pytest.mark.slow
+def test_c3_first_iterations_vs_oracle():
+    """c3 (N=163,842, tanh^4 gamma=1/16, m=7): first 3 iterations against the oracle
+    optimizer (4-pt rule to keep the CPU oracle fast)."""
+    z = P.sample_by_density(P.density_preset("c3"), 163842, 0)
+    crit = P.StoppingCriteria(max_iterations=3, movement_tol=1e-300, grad_tol=1e-300,
+                              stall_tol=1e-300)
+    ref = O.minimize(z, "lloyd-plbfgs", O.Evaluator(O.density_for("c3"), "4pt", 0),
+                     O.StoppingCriteria(3, 1e-300, 1e-300, 1e-300), corrections=7)
+    with _ev("c3", "4pt", 0) as ev:
+        res = P.minimize(z, "lloyd-plbfgs", ev, crit, corrections=7)
+    e = np.array([r.energy for r in res.records])
+    eo = np.array([r.energy for r in ref.records])
+    assert np.max(np.abs(e - eo) / eo) <= 1e-10
+    assert [r.fevals for r in res.records] == [r.fevals for r in ref.records]
+    assert rel(res.points, ref.points) <= 1e-10
