@@ -13,8 +13,8 @@ from .geometry import (QUADRATURE_RULES, QuadratureRule, composite_nodes, icosah
                        normalize, random_sphere_points)
 from .optimizer import IterationRecord, MinimizeResult, Minimizer, StoppingCriteria, minimize
 from .parallel import ShardedMeshEvaluator
-from .pipeline import (EvalResult, MeshEvaluator, SphericalTriangulation, bisect,
-                       bisection_ladder, parallel_iteration)
+from .pipeline import (EvalResult, LevelResult, MeshEvaluator, RunPlan, RunResult,
+                       SphericalTriangulation, bisect, bisection_ladder, parallel_iteration, run)
 
 __version__ = "0.1.0"
 
@@ -40,5 +40,9 @@ __all__ = [
     "parallel_iteration",
     "bisect",
     "bisection_ladder",
+    "RunPlan",
+    "RunResult",
+    "LevelResult",
+    "run",
     "__version__",
 ]

@@ -301,3 +301,142 @@ def bisection_ladder(target: int, floor: int = 200) -> list[int]:
     while ladder[0] > floor and (ladder[0] + 6) % 4 == 0:
         ladder.insert(0, (ladder[0] + 6) // 4)
     return ladder
+
+
+# ---------------------------------------------------------------------- ladder driver (§8(f)1)
+def default_quadrature(density_name: str) -> str:
+    """pipeline.py:56-59."""
+    return "9pt" if density_name == "x64" else "4pt"
+
+
+def default_partitions(k: int) -> int:
+    """pipeline.py:48-53 (kept for API parity; the GPU always runs the global path)."""
+    return max(8, min(64, k // 160))
+
+
+@dataclass
+class RunPlan:
+    """pipeline.py:318-363, plus ``subdivision`` (depth-d fans, DECISIONS.md D2) and the
+    BASELINE densities/rules (`density_preset` c3/c4/c5, "7pt")."""
+
+    points: int
+    density_name: str = "const"
+    method: str = "lloyd-plbfgs"
+    seed: int = 1
+    workers: int = 1
+    backend: str = "process"
+    partitions: int | None = None
+    quadrature: str | None = None
+    ladder: list | None = None
+    criteria: object = None
+    intermediate_movement_tol: float = 1e-3
+    measure: str = "flat"
+    density_overrides: dict = None
+    eps_proj: float = EPS_PROJ
+    subdivision: int = 0
+    corrections: int = 7
+
+    def __post_init__(self):
+        from .errors import ConfigError
+        from .optimizer import StoppingCriteria
+
+        if self.criteria is None:
+            self.criteria = StoppingCriteria()
+        if self.density_overrides is None:
+            self.density_overrides = {}
+        if self.points < 4:
+            raise ConfigError("need at least 4 generators")
+        if self.ladder is None:
+            self.ladder = [self.points]
+        if self.ladder[-1] != self.points:
+            raise ConfigError(
+                f"ladder must end at the target point count {self.points}, got {self.ladder}")
+        for a, b in zip(self.ladder, self.ladder[1:]):
+            if b != 4 * a - 6:
+                raise ConfigError(f"ladder step {a} -> {b} violates the bisection arithmetic "
+                                  f"(expect {4 * a - 6})")
+        if self.quadrature is None:
+            self.quadrature = default_quadrature(self.density_name)
+        if self.quadrature not in QUADRATURE_RULES:
+            raise ConfigError(f"unknown quadrature {self.quadrature!r}")
+
+    def density(self) -> DensityField:
+        from .density import density_preset
+
+        d = density_preset(self.density_name)
+        if self.density_overrides:
+            d = d.with_overrides(**self.density_overrides)
+        return d
+
+    def rule(self) -> QuadratureRule:
+        return QUADRATURE_RULES[self.quadrature]
+
+
+@dataclass
+class LevelResult:
+    k: int
+    result: object
+    wall_time: float
+
+
+@dataclass
+class RunResult:
+    plan: RunPlan
+    points: np.ndarray
+    triangulation: SphericalTriangulation
+    levels: list
+    covering: object
+    wall_time: float
+
+    @property
+    def final(self):
+        return self.levels[-1].result.final
+
+
+def run(plan: RunPlan, initial_points=None, progress=None) -> RunResult:
+    """Optimise-bisect ladder (pipeline.py:396-455) on the GPU: every level is minimised by
+    the GPU optimizer, triangulated on the GPU, and bisected (K -> 4K - 6) to seed the next."""
+    import time
+    from dataclasses import replace
+
+    from .density import sample_by_density
+    from .errors import ConfigError, ScvtError
+    from .optimizer import minimize
+
+    t0 = time.perf_counter()
+    density = plan.density()
+    rule = plan.rule()
+    if initial_points is not None:
+        z = normalize(np.asarray(initial_points, dtype=float))
+        if len(z) != plan.ladder[0]:
+            raise ConfigError(f"initial points ({len(z)}) do not match the first ladder level "
+                              f"({plan.ladder[0]})")
+    else:
+        z = sample_by_density(density, plan.ladder[0], plan.seed)
+    if plan.method.startswith("laplacian"):
+        raise ConfigError("the Laplacian preconditioner is outside this hot path")
+    levels = []
+    tri = None
+    for li, k in enumerate(plan.ladder):
+        last = li == len(plan.ladder) - 1
+        criteria = plan.criteria if last else replace(
+            plan.criteria, movement_tol=plan.intermediate_movement_tol)
+        t_level = time.perf_counter()
+        with MeshEvaluator(density, rule, None, workers=plan.workers, backend=plan.backend,
+                           measure=plan.measure, eps_proj=plan.eps_proj,
+                           subdivision=plan.subdivision) as ev:
+            result = minimize(z, plan.method, ev, criteria, corrections=plan.corrections,
+                              callback=progress)
+            z = result.points
+            tri = ev.triangulation(z)
+        levels.append(LevelResult(k=k, result=result, wall_time=time.perf_counter() - t_level))
+        logger.info("level K=%d: %d iterations, F=%.6e, |grad|=%.3e (%s)", k,
+                    len(result.records), result.final.energy, result.final.grad_norm,
+                    result.reason)
+        if not last:
+            z = bisect(z, tri)
+            if len(z) != plan.ladder[li + 1]:
+                raise ScvtError(f"bisection produced {len(z)} points; ladder expected "
+                                f"{plan.ladder[li + 1]}")
+    return RunResult(plan=plan, points=z, triangulation=tri, levels=levels, covering=None,
+                     wall_time=time.perf_counter() - t0)

@@ -338,11 +338,28 @@ def case_medium_slim():
     save("medium", **out)
 
 
+def case_run_ladder():
+    """pipeline.run: optimise-bisect ladder 162 -> 642 (x3 density, 4-pt rule, global path:
+    partitions=64 keeps K < 16 p so no covering is used)."""
+    _DEPTH["d"] = 0
+    plan = pipeline.RunPlan(points=642, density_name="x3", method="lloyd-plbfgs", seed=1,
+                            partitions=64, quadrature="4pt", ladder=[162, 642],
+                            criteria=optimizer.StoppingCriteria(max_iterations=25))
+    res = pipeline.run(plan)
+    out = {"final_z": res.points, "triangles": res.triangulation.triangles}
+    for li, lv in enumerate(res.levels):
+        out[f"level{li}_energy"] = np.array([r.energy for r in lv.result.records])
+        out[f"level{li}_points"] = lv.result.points
+        out[f"level{li}_reason"] = np.array(lv.result.reason)
+    save("run_ladder", **out)
+
+
 CASES = {
     "rules": case_rules, "c1_eval": case_c1_eval, "density_eval": case_density_eval,
     "sampler": case_sampler, "medium": case_medium, "small_sets": case_small_sets,
     "traj_fast": case_traj_fast, "traj_slow": case_traj_slow,
     "traj_fallback": case_traj_fallback, "medium_slim": case_medium_slim,
+    "run_ladder": case_run_ladder,
 }
 
 if __name__ == "__main__":

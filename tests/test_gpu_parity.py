@@ -397,3 +397,18 @@ def test_c3_first_iterations_vs_oracle():
     assert np.max(np.abs(e - eo) / eo) <= 1e-10
     assert [r.fevals for r in res.records] == [r.fevals for r in ref.records]
     assert rel(res.points, ref.points) <= 1e-10
+
+
+def test_run_ladder_matches_reference(gold):
+    """pipeline.run optimise-bisect ladder 162 -> 642 (x3, 4-pt) against the reference."""
+    g = gold("run_ladder")
+    plan = P.RunPlan(points=642, density_name="x3", method="lloyd-plbfgs", seed=1,
+                     partitions=64, quadrature="4pt", ladder=[162, 642],
+                     criteria=P.StoppingCriteria(max_iterations=25))
+    res = P.run(plan)
+    for li in range(2):
+        e = np.array([r.energy for r in res.levels[li].result.records])
+        assert np.max(np.abs(e - g[f"level{li}_energy"]) / g[f"level{li}_energy"]) <= 1e-10
+        assert res.levels[li].result.reason == str(g[f"level{li}_reason"])
+    assert rel(res.points, g["final_z"]) <= 1e-10
+    assert np.array_equal(res.triangulation.triangles, g["triangles"])

@@ -152,3 +152,14 @@ def test_unknown_method_and_laplacian_rejected():
         P.MeshEvaluator(P.density_preset("const"), "4pt", laplacian="a6")
     with pytest.raises(ValueError):
         P.MeshEvaluator(P.density_preset("const"), "4pt", measure="bogus")
+
+
+def test_runplan_validation():
+    with pytest.raises(P.ConfigError):
+        P.RunPlan(points=642, ladder=[160, 642])
+    with pytest.raises(P.ConfigError):
+        P.RunPlan(points=3)
+    with pytest.raises(P.ConfigError):
+        P.RunPlan(points=642, quadrature="5pt")
+    p = P.RunPlan(points=642, density_name="x64")
+    assert p.quadrature == "9pt" and p.ladder == [642]
