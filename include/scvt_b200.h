@@ -164,6 +164,14 @@ int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new,
  * qg_host = q.g (caller raises NonDescentError when >= 0). */
 int scvt_lbfgs_direction(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
                          double gamma, int64_t n, double* q_out, double* qg_host);
+/* Fused two_loop_direction + tangent projection (optimizer.py:147-167, 322-333) in Gram form:
+ * one pass computes s_i.g, y_i.H0 g, y_i.H0 y_j, g.H0 g (y_i.s_j is kept from the pushes), a
+ * one-block kernel runs the scalar recursion, one pass forms q, q3 = q - (q.z)z and the sums.
+ * out_host[0] = q.g (descent test), out_host[1] = dphi0 = sum g.q3.  h0 as for
+ * scvt_lbfgs_direction (lloyd_diag != NULL: LloydDiagonal, else gamma*I). */
+int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
+                                 double gamma, const double* z, int64_t n, double* q3_out,
+                                 double* out_host);
 /* q3 = q - (q.z) z rowwise (optimizer.py:322-323); dphi0_host = sum g.q3 (333) */
 int scvt_tangent_project(scvt_ctx* ctx, const double* q, const double* z, const double* g,
                          int64_t n, double* q3_out, double* dphi0_host);

@@ -515,6 +515,174 @@ k_absdiff_stage1(const double* __restrict__ a, const double* __restrict__ b, int
     if (threadIdx.x == 0) partials[blockIdx.x] = v;
 }
 
+// ------------------------------------------------------------------ Gram-form two-loop
+// two_loop_direction (optimizer.py:147-167) needs, besides the host-side y_i.s_j matrix kept up
+// to date at push time, only s_i.g, y_i.H0 g, y_i.H0 y_j and g.H0 g: one fused pass over the
+// history computes them all; one block runs the scalar recursion; one combine pass forms
+// q = -(H0 (g - sum a_j y_j) + sum c_l s_l), projects it to the tangent planes and reduces
+// q.g and g.q3.  Mathematically the reference's two loops; 2K+3 vector reads instead of 4K.
+constexpr int MAXM = 16;
+
+struct HistPtrs {
+    const double* S[MAXM];   // ordered oldest -> newest
+    const double* Y[MAXM];
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+constexpr int GRAM_THREADS = 128;
+
+template <int K>
+__global__ void __launch_bounds__(GRAM_THREADS)
+k_gram(const double* __restrict__ g, const double* __restrict__ diag, double gamma, HistPtrs h,
+       int64_t n, double* __restrict__ partials) {
+    constexpr int A = 2 * K + K * (K + 1) / 2 + 1;
+    double acc[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) acc[a] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * GRAM_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * GRAM_THREADS) {
+        const double hw = diag ? 1.0 / diag[i] : gamma;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int64_t e = 3 * i + c;
+            const double ge = g[e];
+            double yv[K > 0 ? K : 1];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                yv[k] = h.Y[k][e];
+                acc[k] += h.S[k][e] * ge;               // s_k . g
+                acc[K + k] += yv[k] * (hw * ge);        // y_k . H0 g
+            }
+            int a = 2 * K;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int l = k; l < K; ++l) acc[a++] += yv[k] * (hw * yv[l]);   // y_k . H0 y_l
+            acc[A - 1] += ge * (hw * ge);                                      // g . H0 g
+        }
+    }
+    __shared__ double sh[GRAM_THREADS / 32][A];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        double v = warp_sum(acc[a]);
+        if (lane == 0) sh[w][a] = v;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < A; a += GRAM_THREADS) {
+        double v = 0.0;
+        for (int q = 0; q < GRAM_THREADS / 32; ++q) v += sh[q][a];
+        partials[(int64_t)a * RED_BLOCKS + blockIdx.x] = v;
+    }
+}
+
+struct GramScalars {
+    double ys[MAXM][MAXM];   // y_i . s_j, ordered oldest -> newest
+    double rho[MAXM];
+};
+
+// one block: fixed-order sums of the Gram partials, then the scalar two-loop recursion
+__global__ void k_gram_recursion(const double* __restrict__ partials, int K, GramScalars gs,
+                                 double* __restrict__ coef) {
+    __shared__ double val[2 * MAXM + MAXM * (MAXM + 1) / 2 + 1];
+    const int A = 2 * K + K * (K + 1) / 2 + 1;
+    for (int a = threadIdx.x; a < A; a += blockDim.x) {
+        double v = 0.0;
+        for (int b = 0; b < RED_BLOCKS; ++b) v += partials[(int64_t)a * RED_BLOCKS + b];
+        val[a] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    auto yhy = [&](int i, int j) {   // packed upper triangle, i <= j
+        if (i > j) { int t = i; i = j; j = t; }
+        return val[2 * K + i * K - i * (i - 1) / 2 + (j - i)];
+    };
+    double a[MAXM], c[MAXM];
+    for (int i = K - 1; i >= 0; --i) {               // backward: newest -> oldest
+        double sq = val[i];                          // s_i . g
+        for (int j = i + 1; j < K; ++j) sq -= a[j] * gs.ys[j][i];   // - a_j s_i . y_j
+        a[i] = gs.rho[i] * sq;
+    }
+    for (int i = 0; i < K; ++i) {                    // forward: oldest -> newest
+        double yr = val[K + i];                      // y_i . H0 g
+        for (int j = 0; j < K; ++j) yr -= a[j] * yhy(i, j);
+        for (int l = 0; l < i; ++l) yr += c[l] * gs.ys[i][l];
+        c[i] = a[i] - gs.rho[i] * yr;
+    }
+    for (int i = 0; i < K; ++i) { coef[i] = a[i]; coef[MAXM + i] = c[i]; }
+}
+
+// q = -(H0 (g - sum_j a_j y_j) + sum_l c_l s_l); q3 = q - (q.z) z; partials of q.g and g.q3
+template <int K>
+__global__ void __launch_bounds__(RED_THREADS)
+k_combine(const double* __restrict__ g, const double* __restrict__ diag, double gamma,
+          HistPtrs h, const double* __restrict__ coef, const double* __restrict__ z, int64_t n,
+          double* __restrict__ q3, double* __restrict__ partials) {
+    double ca[K > 0 ? K : 1], cc[K > 0 ? K : 1];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { ca[k] = coef[k]; cc[k] = coef[MAXM + k]; }
+    double qg = 0.0, gq3 = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        const double hw = diag ? 1.0 / diag[i] : gamma;
+        double q[3], gg[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int64_t e = 3 * i + c;
+            double v = g[e];
+            gg[c] = v;
+#pragma unroll
+            for (int k = K - 1; k >= 0; --k) v -= ca[k] * h.Y[k][e];
+            v *= hw;
+#pragma unroll
+            for (int k = 0; k < K; ++k) v += cc[k] * h.S[k][e];
+            q[c] = -v;
+        }
+        const double zx = z[3 * i], zy = z[3 * i + 1], zz = z[3 * i + 2];
+        const double qd = q[0] * zx + q[1] * zy + q[2] * zz;
+        const double ax = q[0] - qd * zx, ay = q[1] - qd * zy, az = q[2] - qd * zz;
+        q3[3 * i] = ax; q3[3 * i + 1] = ay; q3[3 * i + 2] = az;
+        qg += q[0] * gg[0] + q[1] * gg[1] + q[2] * gg[2];
+        gq3 += gg[0] * ax + gg[1] * ay + gg[2] * az;
+    }
+    qg = block_reduce<0>(qg);
+    gq3 = block_reduce<0>(gq3);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = qg;
+        partials[RED_BLOCKS + blockIdx.x] = gq3;
+    }
+}
+
+// y_new . s_j and y_j . s_new against the K stored pairs (partials, 2K slots)
+template <int K>
+__global__ void __launch_bounds__(RED_THREADS)
+k_cross(const double* __restrict__ sn, const double* __restrict__ yn, HistPtrs h, int64_t len,
+        double* __restrict__ partials) {
+    double a1[K > 0 ? K : 1], a2[K > 0 ? K : 1];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { a1[k] = 0.0; a2[k] = 0.0; }
+    for (int64_t e = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; e < len;
+         e += (int64_t)RED_BLOCKS * RED_THREADS) {
+        const double s = sn[e], y = yn[e];
+#pragma unroll
+        for (int k = 0; k < K; ++k) { a1[k] += y * h.S[k][e]; a2[k] += h.Y[k][e] * s; }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double v1 = block_reduce<0>(a1[k]);
+        double v2 = block_reduce<0>(a2[k]);
+        if (threadIdx.x == 0) {
+            partials[(int64_t)(4 + k) * RED_BLOCKS + blockIdx.x] = v1;
+            partials[(int64_t)(4 + K + k) * RED_BLOCKS + blockIdx.x] = v2;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ LBFGS vector kernels
 __global__ void k_copy(const double* __restrict__ x, int64_t len, double* __restrict__ y) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len;
@@ -790,6 +958,8 @@ struct scvt_ctx {
     double* d_S = nullptr; double* d_Y = nullptr;   // [m][3 n_max]
     double* d_alpha = nullptr;                      // [m]
     std::vector<double> rho, ys, yy;
+    double YS[16][16] = {};            // y_slot_i . s_slot_j of the stored pairs (host)
+    double* d_coef = nullptr;          // two-loop coefficients a[MAXM], c[MAXM] (device)
     int hist_head = 0, hist_count = 0;
     double* d_tmp_s = nullptr; double* d_tmp_y = nullptr;   // staging for push
     // live per-kernel timing (bench roofline): pairs {cells, quad, evaluate}
@@ -1194,6 +1364,61 @@ inline void shard_range(int64_t n, int shard, int nshards, int64_t* lo, int64_t*
 
 }  // namespace
 
+namespace {
+
+// ---------------------------------------------------------------------- Gram dispatch
+HistPtrs hist_ptrs(scvt_ctx* ctx) {
+    HistPtrs hp;
+    const int64_t stride = 3 * ctx->n_max;
+    for (int k = 0; k < MAXM; ++k) {
+        const int slot = (ctx->hist_head + k) % ctx->m;
+        hp.S[k] = k < ctx->hist_count ? ctx->d_S + slot * stride : nullptr;
+        hp.Y[k] = k < ctx->hist_count ? ctx->d_Y + slot * stride : nullptr;
+    }
+    return hp;
+}
+
+#define SCVT_K_CASES(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) \
+    X(13) X(14) X(15) X(16)
+
+int launch_gram(scvt_ctx* ctx, int K, const double* g, const double* diag, double gamma,
+                const HistPtrs& hp, int64_t n) {
+    switch (K) {
+#define G(k) case k: k_gram<k><<<RED_BLOCKS, GRAM_THREADS, 0, ctx->stream>>>(g, diag, gamma, hp, n, ctx->d_partials); break;
+        SCVT_K_CASES(G)
+#undef G
+        default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
+    }
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int launch_combine(scvt_ctx* ctx, int K, const double* g, const double* diag, double gamma,
+                   const HistPtrs& hp, const double* z, int64_t n, double* q3) {
+    switch (K) {
+#define C(k) case k: k_combine<k><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(g, diag, gamma, hp, ctx->d_coef, z, n, q3, ctx->d_partials); break;
+        SCVT_K_CASES(C)
+#undef C
+        default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
+    }
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int launch_cross(scvt_ctx* ctx, int K, const HistPtrs& hp, int64_t len) {
+    if (K == 0) return SCVT_OK;
+    switch (K) {
+#define X_(k) case k: k_cross<k><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(ctx->d_tmp_s, ctx->d_tmp_y, hp, len, ctx->d_partials); break;
+        SCVT_K_CASES(X_)
+#undef X_
+        default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
+    }
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+}  // namespace
+
 // ====================================================================== C ABI
 extern "C" {
 
@@ -1253,7 +1478,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         return bail(fail(ctx, SCVT_ERR_CONFIG, "bad node table (n_nodes=%d)", cfg->n_nodes));
     if (cfg->density_kind < 0 || cfg->density_kind > 5)
         return bail(fail(ctx, SCVT_ERR_CONFIG, "bad density kind %d", cfg->density_kind));
-    if (cfg->lbfgs_m < 1 || cfg->lbfgs_m > 32)
+    if (cfg->lbfgs_m < 1 || cfg->lbfgs_m > MAXM)
         return bail(fail(ctx, SCVT_ERR_CONFIG, "lbfgs_m=%d out of range", cfg->lbfgs_m));
     {
         cudaError_t e = cudaSetDevice(device);
@@ -1317,6 +1542,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
+    AL(d_coef, 2 * MAXM);
 #undef AL
     {
         cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_SLOTS * sizeof(double));
@@ -1381,7 +1607,7 @@ int scvt_destroy(scvt_ctx* ctx) {
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
                    ctx->d_obt, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, ctx->d_partials,
                    ctx->d_scal, ctx->d_status, ctx->d_S, ctx->d_Y, ctx->d_alpha,
-                   ctx->d_tmp_s, ctx->d_tmp_y};
+                   ctx->d_tmp_s, ctx->d_tmp_y, ctx->d_coef};
     for (void* p : dev)
         if (p) cudaFree(p);
     for (cudaEvent_t e : ctx->ev)
@@ -1583,9 +1809,17 @@ int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new, c
     k_history_pair<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(
         z_old, z_new, g_old, g_new, len, ctx->d_tmp_s, ctx->d_tmp_y, ctx->d_partials);
     LAUNCHED();
+    const int K = ctx->hist_count;
+    HistPtrs hp = hist_ptrs(ctx);
+    TRY(launch_cross(ctx, K, hp, len));
     k_history_finish<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials, ctx->d_scal);
     LAUNCHED();
-    TRY(readback(ctx, 4));
+    if (K) {
+        k_reduce_stage2<0><<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials + 4 * RED_BLOCKS,
+                                                               2 * K, ctx->d_scal + 4);
+        LAUNCHED();
+    }
+    TRY(readback(ctx, 4 + 2 * K));
     double ys = ctx->h_scal[0], ss = ctx->h_scal[1], yy = ctx->h_scal[2];
     *movement_host = ctx->h_scal[3];
     if (ys <= 1e-14 * sqrt(ss) * sqrt(yy)) {   // optimizer.py:98-104
@@ -1601,9 +1835,41 @@ int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new, c
     ctx->rho[slot] = 1.0 / ys;
     ctx->ys[slot] = ys;
     ctx->yy[slot] = yy;
+    for (int k = 0; k < K; ++k) {                 // cross products with the kept pairs
+        const int sk = (ctx->hist_head + k) % ctx->m;
+        if (sk == slot) continue;                 // the pair being overwritten
+        ctx->YS[slot][sk] = ctx->h_scal[4 + k];       // y_new . s_k
+        ctx->YS[sk][slot] = ctx->h_scal[4 + K + k];   // y_k . s_new
+    }
+    ctx->YS[slot][slot] = ys;
     if (ctx->hist_count < ctx->m) ++ctx->hist_count;
     else ctx->hist_head = (ctx->hist_head + 1) % ctx->m;
     *pushed_host = 1;
+    return SCVT_OK;
+}
+
+int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
+                                 double gamma, const double* z, int64_t n, double* q3,
+                                 double* out_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    const int K = ctx->hist_count;
+    HistPtrs hp = hist_ptrs(ctx);
+    if (K) {
+        TRY(launch_gram(ctx, K, g, lloyd_diag, gamma, hp, n));
+        GramScalars gs;
+        for (int i = 0; i < K; ++i) {
+            const int si = (ctx->hist_head + i) % ctx->m;
+            gs.rho[i] = ctx->rho[si];
+            for (int j = 0; j < K; ++j) gs.ys[i][j] = ctx->YS[si][(ctx->hist_head + j) % ctx->m];
+        }
+        k_gram_recursion<<<1, 128, 0, ctx->stream>>>(ctx->d_partials, K, gs, ctx->d_coef);
+        LAUNCHED();
+    }
+    TRY(launch_combine(ctx, K, g, lloyd_diag, gamma, hp, z, n, q3));
+    TRY(finish_slots(ctx, 2));
+    TRY(readback(ctx, 2));
+    out_host[0] = ctx->h_scal[0];   // q . g
+    out_host[1] = ctx->h_scal[1];   // dphi0 = g . q3
     return SCVT_OK;
 }
 

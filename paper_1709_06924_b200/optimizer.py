@@ -159,6 +159,12 @@ class _DeviceOps:
                       _lib.dptr(q), ctypes.byref(qg))
         return qg.value
 
+    def direction_tangent(self, g, diag, gamma, z, q3):
+        out = (ctypes.c_double * 2)()
+        self.ctx.call("scvt_lbfgs_direction_tangent", _lib.dptr(g), _lib.dptr(diag),
+                      float(gamma), _lib.dptr(z), self.n, _lib.dptr(q3), out)
+        return out[0], out[1]
+
     def tangent(self, q, z, g, q3) -> float:
         d = ctypes.c_double()
         self.ctx.call("scvt_tangent_project", _lib.dptr(q), _lib.dptr(z), _lib.dptr(g), self.n,
@@ -266,15 +272,16 @@ class Minimizer:
                 else:
                     diag = res.lloyd_diag
             q, q3 = self.q, self.q3
-            qg = ops.direction(res.grad, diag, gamma, q)         # two_loop_direction
+            # two_loop_direction + projection (optimizer.py:147-167, 322-333), fused on device
+            qg, dphi0 = ops.direction_tangent(res.grad, diag, gamma, z, q3)
             if qg >= 0.0:
                 logger.warning("non-descent direction at iteration %d; history reset", n)
                 ops.history_clear()
                 self.resets += 1
-                qg = ops.direction(res.grad, diag, gamma, q)
+                qg, dphi0 = ops.direction_tangent(res.grad, diag, gamma, z, q3)
                 if qg >= 0.0:
                     ops.scale(-ops.gamma(), res.grad, q)          # q = -hist.gamma() * g
-            dphi0 = ops.tangent(q, z, res.grad, q3)              # optimizer.py:322-333
+                    dphi0 = ops.tangent(q, z, res.grad, q3)
 
             def phi(alpha, z=z, q3=q3):
                 zt = torch.empty_like(z)
