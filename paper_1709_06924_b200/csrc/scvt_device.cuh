@@ -777,11 +777,11 @@ SCVT_HD double tab_u_chord(const DensityParams& p, double x, int br) {
 
 struct LocalFit {
     double sc;          // centre of the s interval
-    double b[7];        // u(s) = sum_k b[k] (s - sc)^k
+    double b[7];        // rho(s) = sum_k b[k] (s - sc)^k
     V3 sgc;             // sigma * c
 };
 
-// Fit u over the patch of sub-triangle `st` (nodes y = normalize(v0 + l1 e1 + l2 e2)).
+// Fit rho = u^4 over the patch of sub-triangle `st` (nodes y = normalize(v0 + l1 e1 + l2 e2)).
 // Returns false (caller falls back to per-node table evaluation) when the patch straddles
 // 90 deg from c, comes too close to the sqrt singularity at s = 0, or the fit misses the table
 // by more than 4e-15 relative at any check point (the table itself is within 1.6e-15 of the
@@ -825,11 +825,13 @@ SCVT_HD bool local_fit(const DensityParams& p, const SubTri& st, V3 c, LocalFit&
     const double hw = 0.5 * (hi - lo), sc = 0.5 * (hi + lo);
     if (hw > 0.1 * sc) return false;            // hopeless near the s = 0 singularity; the
                                                 // check points below are the accuracy guard
-    double u[7];
+    double u[7];   // rho = (table u)^4 at the Chebyshev points: the fit is of rho itself
 #pragma unroll
     for (int j = 0; j < 7; ++j) {
         const double sj = fma(hw, CHEB_V[j], sc);
-        u[j] = tab_u_chord(p, sj * fast_rsqrt(sj), br);
+        const double uj = tab_u_chord(p, sj * fast_rsqrt(sj), br);
+        const double u2 = uj * uj;
+        u[j] = u2 * u2;
     }
     double a[7];
 #pragma unroll
@@ -855,8 +857,9 @@ SCVT_HD bool local_fit(const DensityParams& p, const SubTri& st, V3 c, LocalFit&
 #pragma unroll
         for (int k = 5; k >= 0; --k) pv = fma(pv, v, b[k]);
         const double sq = fma(hw, v, sc);
-        const double ex = tab_u_chord(p, sq * fast_rsqrt(sq), br);
-        if (!(fabs(pv - ex) <= 4e-15 * ex)) return false;   // fit rounding floor ~1e-15
+        const double eu = tab_u_chord(p, sq * fast_rsqrt(sq), br);
+        const double e2 = eu * eu, ex = e2 * e2;
+        if (!(fabs(pv - ex) <= 1.6e-14 * ex)) return false;   // = 4e-15 on u = rho^(1/4)
     }
     const double ih = 1.0 / hw;
     double sc_k = 1.0;
@@ -924,10 +927,8 @@ SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const 
             const double inv = fast_rsqrt(r2);
             double rho;
             if (TAB && fitted) {
-                double u = fit_u(f0, x, inv);
-                if (KIND == DEN_TANH4X2_TAB) u = fmax(u, fit_u(f1, x, inv));
-                const double u2 = u * u;
-                rho = u2 * u2;
+                rho = fit_u(f0, x, inv);                        // the fit is of rho = u^4
+                if (KIND == DEN_TANH4X2_TAB) rho = fmax(rho, fit_u(f1, x, inv));
             } else {
                 rho = density_x<KIND>(dp, x, inv, t0, t1, pole);
             }
