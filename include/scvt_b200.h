@@ -113,6 +113,14 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
 int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
                   double* mass, double* lloyd_diag, double* scalars_host);
 
+/* scvt_evaluate plus, in the same fixed-shape reduction: scalars_host[3] = min lloyd_diag (the
+ * nonpositive-diagonal test of cvt_core.py:184) and, when q3/norms are given (a line-search
+ * trial at v = z + alpha q3, norms = |v|), scalars_host[4] = sum g.(q3/|v|) (optimizer.py:330).
+ * scalars_host must hold 5 doubles. */
+int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                     double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                     double* scalars_host);
+
 /* Moments only over an externally supplied canonical triangulation (T,3) int64 — used by
  * parity tests to isolate the quadrature from the triangulation. Same outputs as above. */
 int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n,
@@ -145,6 +153,11 @@ int scvt_shard_status(scvt_ctx* ctx, int32_t status);
 int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                       const double* res_all, double* grad, double* first, double* mass,
                       double* lloyd_diag, double* scalars_host);
+/* as scvt_shard_finish with the extra scalars of scvt_evaluate_ex (5 doubles) */
+int scvt_shard_finish_ex(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                         const double* res_all, double* grad, double* first, double* mass,
+                         double* lloyd_diag, const double* q3, const double* norms,
+                         double* scalars_host);
 
 /* optimizer vector algebra -------------------------------------------------------------
  * CorrectionHistory (optimizer.py:79-114): ring of at most lbfgs_m (s, y) pairs held on

@@ -59,6 +59,8 @@ SIGNATURES = {
     "scvt_version": (ctypes.c_char_p, []),
     "scvt_triangulate": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _c_i64_p]),
     "scvt_evaluate": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _c_dbl_p]),
+    "scvt_evaluate_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        _c_dbl_p]),
     "scvt_evaluate_on_triangles": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
                                                   _vp, _vp, _vp, _vp, _c_dbl_p]),
     "scvt_shard_rows": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int]),
@@ -68,6 +70,8 @@ SIGNATURES = {
     "scvt_shard_status": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "scvt_shard_finish": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp,
                                          _vp, _vp, _c_dbl_p]),
+    "scvt_shard_finish_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp,
+                                            _vp, _vp, _vp, _vp, _vp, _c_dbl_p]),
     "scvt_history_clear": (ctypes.c_int, [_vp]),
     "scvt_history_size": (ctypes.c_int, [_vp, _c_i32_p]),
     "scvt_history_gamma": (ctypes.c_int, [_vp, _c_dbl_p]),

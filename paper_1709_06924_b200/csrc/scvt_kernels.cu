@@ -683,6 +683,48 @@ k_cross(const double* __restrict__ sn, const double* __restrict__ yn, HistPtrs h
     }
 }
 
+// ------------------------------------------------------------------ evaluation scalars
+// One pass over the per-generator arrays: sum E_i, sum |g_i|^2, obtuse count, min lloyd_diag
+// (the nonpositive-diagonal test of cvt_core.py:184) and, for a line-search trial, the
+// directional derivative sum g.(q3/|v|) (optimizer.py:330).  Fixed shape -> bitwise repeatable.
+__global__ void __launch_bounds__(RED_THREADS)
+k_eval_reduce(const double* __restrict__ e_gen, const double* __restrict__ g2_gen,
+              const double* __restrict__ ob_gen, const double* __restrict__ diag,
+              const double* __restrict__ grad, const double* __restrict__ q3,
+              const double* __restrict__ norms, int64_t n, double* __restrict__ partials) {
+    double se = 0.0, sg = 0.0, so = 0.0, mn = INFINITY, sd = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        se += e_gen[i];
+        sg += g2_gen[i];
+        so += ob_gen[i];
+        mn = fmin(mn, diag[i]);
+        if (q3) {
+            const double nr = norms[i];
+            sd += grad[3 * i] * (q3[3 * i] / nr) + grad[3 * i + 1] * (q3[3 * i + 1] / nr) +
+                  grad[3 * i + 2] * (q3[3 * i + 2] / nr);
+        }
+    }
+    se = block_reduce<0>(se); sg = block_reduce<0>(sg); so = block_reduce<0>(so);
+    mn = block_reduce<2>(mn); sd = block_reduce<0>(sd);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = se;
+        partials[RED_BLOCKS + blockIdx.x] = sg;
+        partials[2 * RED_BLOCKS + blockIdx.x] = so;
+        partials[3 * RED_BLOCKS + blockIdx.x] = mn;
+        partials[4 * RED_BLOCKS + blockIdx.x] = sd;
+    }
+}
+
+__global__ void k_eval_reduce2(const double* __restrict__ partials, double* __restrict__ out) {
+    double se = finish_partials<0>(partials);
+    double sg = finish_partials<0>(partials + RED_BLOCKS);
+    double so = finish_partials<0>(partials + 2 * RED_BLOCKS);
+    double mn = finish_partials<2>(partials + 3 * RED_BLOCKS);
+    double sd = finish_partials<0>(partials + 4 * RED_BLOCKS);
+    if (threadIdx.x == 0) { out[0] = se; out[1] = sg; out[2] = so; out[3] = mn; out[4] = sd; }
+}
+
 // ------------------------------------------------------------------ LBFGS vector kernels
 __global__ void k_copy(const double* __restrict__ x, int64_t len, double* __restrict__ y) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len;
@@ -1312,19 +1354,16 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
 
 // fixed-shape reductions of E_i, |g_i|^2, obtuse_i over ALL n generators (id order), so the
 // scalars are bitwise identical whatever the shard count; reads back and checks status
-int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host) {
+int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* diag,
+                  const double* grad, const double* q3, const double* norms, int nsc) {
     cudaStream_t s = ctx->stream;
-    k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_egen, n, ctx->d_partials);
+    k_eval_reduce<<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_egen, ctx->d_g2gen, ctx->d_obgen,
+                                                      diag, grad, q3, norms, n, ctx->d_partials);
     LAUNCHED();
-    k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_g2gen, n,
-                                                          ctx->d_partials + RED_BLOCKS);
+    k_eval_reduce2<<<1, RED_THREADS, 0, s>>>(ctx->d_partials, ctx->d_scal);
     LAUNCHED();
-    k_reduce_stage1<0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_obgen, n,
-                                                          ctx->d_partials + 2 * RED_BLOCKS);
-    LAUNCHED();
-    TRY(finish_slots(ctx, 3));
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[5], s));
-    TRY(readback(ctx, 3));
+    TRY(readback(ctx, 5));
     if (ctx->prof) {
         float a = 0.f, b = 0.f, c = 0.f;
         CK(cudaEventElapsedTime(&b, ctx->ev[2], ctx->ev[3]));
@@ -1341,11 +1380,14 @@ int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host) {
     scalars_host[0] = ctx->h_scal[0];
     scalars_host[1] = sqrt(ctx->h_scal[1]);
     scalars_host[2] = ctx->h_scal[2];
+    if (nsc > 3) scalars_host[3] = ctx->h_scal[3];
+    if (nsc > 4) scalars_host[4] = q3 ? ctx->h_scal[4] : 0.0;
     return SCVT_OK;
 }
 
 int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
-            double* mass, double* diag, double* scalars_host) {
+            double* mass, double* diag, double* scalars_host, const double* q3 = nullptr,
+            const double* norms = nullptr, int nsc = 3) {
     int64_t n_inc = 6 * n - 12;   // Euler: a closed triangulation has exactly 6n-12 incidences
     TRY(incidences_range(ctx, 0, n, n_inc));
     TRY(quad_range(ctx, z, n, 0, n, n_inc));
@@ -1353,7 +1395,7 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
         z, (int)n, (int)n, ctx->d_inc_start, ctx->d_inc_base, ctx->d_deg, ctx->d_part, ctx->d_obt,
         n_inc, ctx->d_status, grad, first, mass, diag, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen);
     LAUNCHED();
-    return reduce_finish(ctx, n, scalars_host);
+    return reduce_finish(ctx, n, scalars_host, diag, grad, q3, norms, nsc);
 }
 
 inline void shard_range(int64_t n, int shard, int nshards, int64_t* lo, int64_t* hi) {
@@ -1668,12 +1710,26 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
 
 int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
                   double* mass, double* lloyd_diag, double* scalars_host) {
+    double sc[5];
+    int rc = scvt_evaluate_ex(ctx, z, n, grad, first, mass, lloyd_diag, nullptr, nullptr, sc);
+    if (rc == SCVT_OK)
+        for (int k = 0; k < 3; ++k) scalars_host[k] = sc[k];
+    return rc;
+}
+
+int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                     double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                     double* scalars_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
     ctx->prof_n[3] = 0;
     TRY(reset_status(ctx));
+    const int nsc = q3 ? 5 : (norms ? 4 : 3);
     int rc = build_cells(ctx, z, n);
-    if (rc == SCVT_OK) rc = moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host);
+    if (rc == SCVT_OK)
+        rc = moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host, q3, norms,
+                     q3 ? 5 : 4);
+    (void)nsc;
     ctx->cycles_n = rc == SCVT_OK ? n : -1;   // certified cycles may seed the next evaluation
     return rc;
 }
@@ -1760,6 +1816,18 @@ int scvt_shard_status(scvt_ctx* ctx, int32_t status) {
 int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                       const double* res_all, double* grad, double* first, double* mass,
                       double* lloyd_diag, double* scalars_host) {
+    double sc[5];
+    int rc = scvt_shard_finish_ex(ctx, z, n, nshards, res_all, grad, first, mass, lloyd_diag,
+                                  nullptr, nullptr, sc);
+    if (rc == SCVT_OK)
+        for (int k = 0; k < 3; ++k) scalars_host[k] = sc[k];
+    return rc;
+}
+
+int scvt_shard_finish_ex(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                         const double* res_all, double* grad, double* first, double* mass,
+                         double* lloyd_diag, const double* q3, const double* norms,
+                         double* scalars_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
     cudaStream_t s = ctx->stream;
     int64_t cap = scvt_shard_rows(n, nshards);
@@ -1768,7 +1836,7 @@ int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
         res_all, (int)(cap * nshards), (int)n, z, grad, first, mass, lloyd_diag, ctx->d_egen,
         ctx->d_g2gen, ctx->d_obgen, ctx->d_status + 13);
     LAUNCHED();
-    TRY(reduce_finish(ctx, n, scalars_host));
+    TRY(reduce_finish(ctx, n, scalars_host, lloyd_diag, grad, q3, norms, q3 ? 5 : 4));
     int seen = 0;
     CK(cudaMemcpy(&seen, ctx->d_status + 13, sizeof(int), cudaMemcpyDeviceToHost));
     if (seen != n)

@@ -267,7 +267,7 @@ class Minimizer:
             diag = None
             gamma = ops.gamma()
             if self.method == "lloyd-plbfgs":
-                if ops.minimum(res.lloyd_diag) <= 0.0:
+                if res.min_diag <= 0.0:                          # lloyd_preconditioner raises
                     logger.warning("nonpositive Lloyd diagonal; falling back to gamma identity")
                 else:
                     diag = res.lloyd_diag
@@ -287,9 +287,8 @@ class Minimizer:
                 zt = torch.empty_like(z)
                 norms = torch.empty(k, dtype=torch.float64, device=z.device)
                 ops.trial(z, q3, alpha, zt, norms)
-                r = ev.evaluate_device(zt)
-                d = ops.dirderiv(r.grad, q3, norms)
-                return r.energy, d, (zt, r)
+                r = ev.evaluate_device(zt, q3, norms)            # derivative fused in
+                return r.energy, r.dirderiv, (zt, r)
 
             try:
                 alpha, _, payload, evals, exhausted = wolfe_line_search(phi, res.energy, dphi0)

@@ -68,7 +68,7 @@ class CudaShardBackend:
         rc = ctx.lib.scvt_shard_status(ctx.ptr, int(status))
         _lib.check(rc, ctx.ptr, "evaluate (sharded)")
 
-    def finish(self, z, nshards, res_all) -> EvalResult:
+    def finish(self, z, nshards, res_all, q3=None, norms=None) -> EvalResult:
         import torch
 
         n = z.shape[0]
@@ -77,12 +77,14 @@ class CudaShardBackend:
         first = torch.empty_like(z)
         mass = torch.empty(n, dtype=torch.float64, device=z.device)
         diag = torch.empty(n, dtype=torch.float64, device=z.device)
-        sc = (ctypes.c_double * 3)()
-        ctx.call("scvt_shard_finish", _lib.dptr(z), n, nshards, _lib.dptr(res_all),
-                 _lib.dptr(grad), _lib.dptr(first), _lib.dptr(mass), _lib.dptr(diag), sc,
-                 what="shard_finish")
+        sc = (ctypes.c_double * 5)()
+        ctx.call("scvt_shard_finish_ex", _lib.dptr(z), n, nshards, _lib.dptr(res_all),
+                 _lib.dptr(grad), _lib.dptr(first), _lib.dptr(mass), _lib.dptr(diag),
+                 _lib.dptr(q3), _lib.dptr(norms), sc, what="shard_finish")
         return EvalResult(energy=float(sc[0]), grad=grad, grad_norm=float(sc[1]),
-                          lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]))
+                          lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]),
+                          min_diag=float(sc[3]),
+                          dirderiv=float(sc[4]) if q3 is not None else float("nan"))
 
     def buffers(self, n, nshards, device):
         import torch
@@ -105,7 +107,8 @@ def _all_gather(out, inp, group):
         dist.all_gather(parts, inp, group=group)
 
 
-def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=None):
+def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=None,
+                     q3=None, norms=None):
     """One evaluation on rank `rank` of `world` (collectives through torch.distributed)."""
     import torch
     import torch.distributed as dist
@@ -120,10 +123,12 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
     if int(st.item()):
         backend.raise_status(int(st.item()))
     _all_gather(res_all, res_send, group)
-    return backend.finish(z, world, res_all)
+    if q3 is None:
+        return backend.finish(z, world, res_all)
+    return backend.finish(z, world, res_all, q3, norms)
 
 
-def emulate_shards(backend, z, nshards: int):
+def emulate_shards(backend, z, nshards: int, q3=None, norms=None):
     """All shards of one evaluation run back to back in one process (no collectives): the
     exchange buffers are filled slice by slice.  Used to test the sharded path on one GPU."""
     n = z.shape[0]
@@ -138,7 +143,9 @@ def emulate_shards(backend, z, nshards: int):
         res_all[s * r:(s + 1) * r] = res_send
     if worst:
         backend.raise_status(worst)
-    return backend.finish(z, nshards, res_all)
+    if q3 is None:
+        return backend.finish(z, nshards, res_all)
+    return backend.finish(z, nshards, res_all, q3, norms)
 
 
 class ShardedMeshEvaluator(MeshEvaluator):
@@ -158,11 +165,12 @@ class ShardedMeshEvaluator(MeshEvaluator):
             self.rank, self.world = 0, 1
         self.backend = backend or CudaShardBackend(self)
 
-    def evaluate_device(self, z) -> EvalResult:
+    def evaluate_device(self, z, q3=None, norms=None) -> EvalResult:
         if self.world == 1:
-            r = emulate_shards(self.backend, z, 1)
+            r = emulate_shards(self.backend, z, 1, q3, norms)
         else:
-            r = sharded_evaluate(self.backend, z, self.rank, self.world, self.group)
+            r = sharded_evaluate(self.backend, z, self.rank, self.world, self.group, q3=q3,
+                                 norms=norms)
         self.evaluations += 1
         return r
 

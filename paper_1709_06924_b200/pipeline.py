@@ -44,6 +44,8 @@ class EvalResult:
     laplacian: object = None
     mass: object = None
     obtuse_count: int = 0
+    min_diag: float = float("nan")      # min lloyd_diag (cvt_core.py:184 test), device path
+    dirderiv: float = float("nan")      # sum g.(q3/|v|) when evaluated as a line-search trial
 
 
 @dataclass(frozen=True)
@@ -197,8 +199,10 @@ class MeshEvaluator:
             raise ValueError("points must be (K, 3)")
         return torch.from_numpy(arr).to(f"cuda:{self._device_index()}"), True
 
-    def evaluate_device(self, z) -> EvalResult:
-        """Device-resident evaluation: ``z`` is a contiguous float64 CUDA tensor (K, 3)."""
+    def evaluate_device(self, z, q3=None, norms=None) -> EvalResult:
+        """Device-resident evaluation: ``z`` is a contiguous float64 CUDA tensor (K, 3).
+        With ``q3``/``norms`` (a line-search trial z = v/|v|, v = z0 + alpha q3) the result also
+        carries the directional derivative sum g.(q3/|v|) (optimizer.py:330)."""
         torch = _torch()
         n = z.shape[0]
         ctx = self._ensure_ctx(n)
@@ -206,12 +210,15 @@ class MeshEvaluator:
         first = torch.empty_like(z)
         mass = torch.empty(n, dtype=torch.float64, device=z.device)
         diag = torch.empty(n, dtype=torch.float64, device=z.device)
-        sc = (ctypes.c_double * 3)()
-        ctx.call("scvt_evaluate", _lib.dptr(z), n, _lib.dptr(grad), _lib.dptr(first),
-                 _lib.dptr(mass), _lib.dptr(diag), sc, what="evaluate")
+        sc = (ctypes.c_double * 5)()
+        ctx.call("scvt_evaluate_ex", _lib.dptr(z), n, _lib.dptr(grad), _lib.dptr(first),
+                 _lib.dptr(mass), _lib.dptr(diag), _lib.dptr(q3), _lib.dptr(norms), sc,
+                 what="evaluate")
         self.evaluations += 1
         return EvalResult(energy=float(sc[0]), grad=grad, grad_norm=float(sc[1]),
-                          lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]))
+                          lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]),
+                          min_diag=float(sc[3]),
+                          dirderiv=float(sc[4]) if q3 is not None else float("nan"))
 
     def evaluate(self, points) -> EvalResult:
         """pipeline.py:261-279.  NumPy in -> NumPy out; CUDA tensor in -> tensors out."""

@@ -26,10 +26,10 @@ for name in ("gamma", "direction", "direction_tangent", "tangent", "trial", "dir
 ev_f = P.MeshEvaluator.evaluate_device
 
 
-def ev_wrap(self, z):
+def ev_wrap(self, z, *a):
     torch.cuda.synchronize()
     t = time.perf_counter()
-    r = ev_f(self, z)
+    r = ev_f(self, z, *a)
     torch.cuda.synchronize()
     acc["evaluate"] += time.perf_counter() - t
     cnt["evaluate"] += 1
