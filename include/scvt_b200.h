@@ -213,9 +213,11 @@ int scvt_normalize_rows(scvt_ctx* ctx, double* z, int64_t n);
 int scvt_profile_enable(scvt_ctx* ctx, int on);
 int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int reset);
 /* cell-builder work counters accumulated while profiling is enabled:
- * out8 = {cells, candidate passes, points scanned, candidates sorted, clips, radius rounds,
- *         evaluations whose previous cycles were certified and reused, cells rebuilt by reuse} */
-int scvt_profile_counters(scvt_ctx* ctx, int64_t* out8, int reset);
+ * out12 = {cells, candidate passes, points scanned, candidates sorted, clips, radius rounds,
+ *          max 32-point sweep batches of one cell, max clips of one cell,
+ *          evaluations whose previous cycles were certified and reused, cells rebuilt by
+ *          reuse, certificate passes run by reuse, 0} */
+int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset);
 /* measured FP64 DFMA throughput of `device` in TFLOP/s (2 FLOPs per FMA): the FP64
  * roofline denominator, which MEASURED_PEAKS.json does not carry */
 int scvt_fp64_peak(int device, double* tflops_out);

@@ -151,6 +151,25 @@ __device__ __forceinline__ void block_cap(int face, int G, int ua, int ub, int v
     *rad = sqrtf(r2) * 1.0001f + 1e-5f;
 }
 
+// Per-lane vertex circumdisk on the sphere (float, conservative): a point can cut the cell
+// only inside some disk |y - y_k| < R_k.  Box vertices (and idle lanes) cover everything.
+__device__ __forceinline__ void vertex_disk(const WPoly& P, int lane, V3 zi, V3 e1, V3 e2,
+                                            float* vyx, float* vyy, float* vyz, float* vR) {
+    if (lane < P.n && P.lab >= 0) {
+        double x = zi.x + P.vx * e1.x + P.vy * e2.x;
+        double y = zi.y + P.vx * e1.y + P.vy * e2.y;
+        double w = zi.z + P.vx * e1.z + P.vy * e2.z;
+        double inv = rsqrt(x * x + y * y + w * w);
+        x *= inv; y *= inv; w *= inv;
+        double rx = x - zi.x, ry = y - zi.y, rz = w - zi.z;
+        *vyx = (float)x; *vyy = (float)y; *vyz = (float)w;
+        *vR = (float)sqrt(rx * rx + ry * ry + rz * rz);
+    } else {
+        *vyx = *vyy = *vyz = 0.f;
+        *vR = lane < P.n ? 3.0f : 0.f;
+    }
+}
+
 // Returns valence > 0, -ST_* for genuine failures, or -ST_POLY_OVERFLOW to request the
 // single-thread fallback.  All lanes return the same value.
 __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double* s_c2,
@@ -168,6 +187,7 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
     double R2 = 8.0;
     bool box = true;
     int status = 0, rounds = 0, passes = 0, sweep_visits = 0, scanned = 0, ncands = 0, nclips = 0;
+    int shrinks = 0;
     const unsigned lt_mask = (1u << lane) - 1u;
     while (true) {
         ++passes;
@@ -208,6 +228,15 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
         status = __reduce_or_sync(FULL, status);
         if (status) break;
         __syncwarp();
+        if (count > WCAND && shrinks < 4) {
+            // annulus denser than expected (a coarse cell next to the plateau, or a far
+            // vertex that inflated R2): narrow it and clip nearest-first instead of sweeping;
+            // the sweep, if still needed, then starts from a tighter polygon
+            ++shrinks;
+            r2 = lo_c2 < 0.0 ? 0.25 * r2 : lo_c2 + 0.25 * (r2 - lo_c2);
+            continue;
+        }
+        shrinks = 0;
         if (count <= WCAND) {
             // ---- rank sort by (c2, id), then clip nearest-first with early exit
             double kc[2];
@@ -258,20 +287,8 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
                 const int bu0 = iu0 >> 3, bu1 = iu1 >> 3, bv0 = iv0 >> 3, bv1 = iv1 >> 3;
                 const int nbv = bv1 - bv0 + 1, nblk = (bu1 - bu0 + 1) * nbv;
                 for (int b0 = 0; b0 < nblk && !status; b0 += 32) {
-                    if (dirty) {   // per-lane vertex circumdisk on the sphere (float, conservative)
-                        if (lane < P.n && P.lab >= 0) {
-                            double x = zi.x + P.vx * e1.x + P.vy * e2.x;
-                            double y = zi.y + P.vx * e1.y + P.vy * e2.y;
-                            double w = zi.z + P.vx * e1.z + P.vy * e2.z;
-                            double inv = rsqrt(x * x + y * y + w * w);
-                            x *= inv; y *= inv; w *= inv;
-                            double rx = x - zi.x, ry = y - zi.y, rz = w - zi.z;
-                            vyx = (float)x; vyy = (float)y; vyz = (float)w;
-                            vR = (float)sqrt(rx * rx + ry * ry + rz * rz);
-                        } else {
-                            vyx = vyy = vyz = 0.f;
-                            vR = 3.0f;       // box vertex: covers everything
-                        }
+                    if (dirty) {
+                        vertex_disk(P, lane, zi, e1, e2, &vyx, &vyy, &vyz, &vR);
                         dirty = false;
                     }
                     const int bk = b0 + lane;
@@ -297,6 +314,18 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
                         mb &= mb - 1u;
                         const int bua = __shfl_sync(FULL, ua, src), bub = __shfl_sync(FULL, ub, src);
                         const int bva = __shfl_sync(FULL, va, src), bvb = __shfl_sync(FULL, vb, src);
+                        if (dirty) {
+                            // the polygon shrank since this batch was tested: re-test the
+                            // block against the current vertex disks before scanning it
+                            vertex_disk(P, lane, zi, e1, e2, &vyx, &vyy, &vyz, &vR);
+                            dirty = false;
+                            const float bx = __shfl_sync(FULL, cx, src), by = __shfl_sync(FULL, cy, src);
+                            const float bz = __shfl_sync(FULL, cz, src), br = __shfl_sync(FULL, crad, src);
+                            const float dx = vyx - bx, dy = vyy - by, dz = vyz - bz;
+                            const float lim2 = vR + br + 1e-4f;
+                            const bool h = lane < P.n && dx * dx + dy * dy + dz * dz < lim2 * lim2;
+                            if (!__any_sync(FULL, h)) continue;
+                        }
                         for (int iu = bua; iu <= bub && !status; ++iu) {
                             int rowbase = (face * g.G + iu) * g.G;
                             int p0 = g.start[rowbase + bva], p1 = g.start[rowbase + bvb + 1];

@@ -117,6 +117,8 @@ k_cells_warp(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
             atomicAdd(&diag[3], (unsigned long long)cs.cands);
             atomicAdd(&diag[4], (unsigned long long)cs.clips);
             atomicAdd(&diag[5], (unsigned long long)cs.rounds);
+            atomicMax(&diag[6], (unsigned long long)(cs.sweep_visits >> 5));
+            atomicMax(&diag[7], (unsigned long long)cs.clips);
         }
     }
 }
@@ -1235,7 +1237,7 @@ int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView&
         int nbad = 0;
         CK(cudaMemcpyAsync(&nbad, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        ctx->reuse_stats[0] += 1;
+        ctx->reuse_stats[0] += 1;                   // certificate passes run
         ctx->reuse_stats[1] += nbad;
         if (nbad == 0) { *done = true; return SCVT_OK; }
         if (nbad > (3 * n) / 4 || round == 3) return SCVT_OK;   // caller rebuilds everything
@@ -1478,11 +1480,13 @@ int scvt_profile_enable(scvt_ctx* ctx, int on) {
     return SCVT_OK;
 }
 
-int scvt_profile_counters(scvt_ctx* ctx, int64_t* out8, int reset) {
+int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset) {
     if (!ctx) return SCVT_ERR_CONFIG;
-    CK(cudaMemcpy(out8, ctx->d_diag, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-    out8[6] = ctx->reuse_stats[2];   // evaluations whose cycles were certified by reuse
-    out8[7] = ctx->reuse_stats[1];   // cells rebuilt by reuse rounds
+    CK(cudaMemcpy(out12, ctx->d_diag, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    out12[8] = ctx->reuse_stats[2];   // evaluations whose cycles were certified by reuse
+    out12[9] = ctx->reuse_stats[1];   // cells rebuilt by reuse rounds
+    out12[10] = ctx->reuse_stats[0];  // certificate passes run by the reuse path
+    out12[11] = 0;
     if (reset) {
         CK(cudaMemset(ctx->d_diag, 0, 8 * sizeof(int64_t)));
         ctx->reuse_stats[0] = ctx->reuse_stats[1] = ctx->reuse_stats[2] = 0;

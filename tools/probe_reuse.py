@@ -15,8 +15,8 @@ z = P.sample_by_density(P.density_preset(cfg), n, 0) if cfg != "const" else P.ra
 with P.MeshEvaluator(P.density_preset(cfg), "7pt", subdivision=3) as ev:
     st = P.Minimizer(torch.from_numpy(z).cuda(), "lloyd-plbfgs", ev, 7)
     lib.scvt_profile_enable(ev.context.ptr, 1)
-    for it in range(1, 13):
-        c = (ctypes.c_int64 * 8)()
+    for it in range(1, 1 + (int(sys.argv[3]) if len(sys.argv) > 3 else 12)):
+        c = (ctypes.c_int64 * 12)()
         lib.scvt_profile_counters(ev.context.ptr, c, 1)
         ms = (ctypes.c_double * 3)(); cnt = (ctypes.c_int64 * 3)()
         lib.scvt_profile_read(ev.context.ptr, ms, cnt, 1)
@@ -25,5 +25,5 @@ with P.MeshEvaluator(P.density_preset(cfg), "7pt", subdivision=3) as ev:
         lib.scvt_profile_counters(ev.context.ptr, c, 0)
         lib.scvt_profile_read(ev.context.ptr, ms, cnt, 0)
         print(f"iter {it}: evals {cnt[2]} cells_ms/eval {ms[0]/max(cnt[0],1):.2f} quad_ms/eval "
-              f"{ms[1]/max(cnt[1],1):.2f} eval_ms {ms[2]/max(cnt[2],1):.2f} reused {c[6]} "
-              f"rebuilt cells {c[7]}", flush=True)
+              f"{ms[1]/max(cnt[1],1):.2f} eval_ms {ms[2]/max(cnt[2],1):.2f} reused {c[8]} cert_passes {c[10]} "
+              f"rebuilt cells {c[9]} max_sweep_batches {c[6]} max_clips {c[7]}", flush=True)
