@@ -892,24 +892,15 @@ SCVT_HD double density_x(const DensityParams& dp, V3 x, double inv, TabCache& t0
     return density_eval<KIND>(dp, v3(x.x * inv, x.y * inv, x.z * inv), pole);
 }
 
-template <int KIND, int L>
-SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const double* l2,
-                                 const double* w, const DensityParams& dp, double* acc,
-                                 int* pole) {
-    V3 o[7];
-#pragma unroll
-    for (int q = 0; q < 7; ++q) o[q] = add(mul(s.e1, l1[q]), mul(s.e2, l2[q]));
-    const double w0 = w[0], w1 = w[1], w2 = w[4];
+// Leaf sweep of one sub-triangle; FIT selects the per-patch fit (loop-invariant, so the two
+// density paths are separate loops: the table path's per-lane caches are not live in the
+// fitted loop).
+template <int KIND, int L, bool FIT>
+SCVT_HD void sym7_leaves(const SubTri& s, V3 z, const V3* o, double w0, double w1, double w2,
+                         const DensityParams& dp, const LocalFit& f0, const LocalFit& f1,
+                         double* mo, int* pole) {
     TabCache t0, t1;
-    t0.key = -1; t1.key = -1;
-    const bool TAB = KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB;
-    LocalFit f0, f1;
-    bool fitted = false;
-    if (TAB) {
-        fitted = local_fit(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f0);
-        if (fitted && KIND == DEN_TANH4X2_TAB)
-            fitted = local_fit(dp, s, v3(dp.c1x, dp.c1y, dp.c1z), f1);
-    }
+    if (!FIT) { t0.key = -1; t1.key = -1; }
     double m = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, e = 0.0;
     const double invL = 1.0 / (double)L;
     for (int pass = 0; pass < 2; ++pass) {          // 0: up-leaves, 1: down-leaves
@@ -926,7 +917,7 @@ SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const 
             const double r2 = x.x * x.x + x.y * x.y + x.z * x.z;
             const double inv = fast_rsqrt(r2);
             double rho;
-            if (TAB && fitted) {
+            if (FIT) {
                 rho = fit_u(f0, x, inv);                        // the fit is of rho = u^4
                 if (KIND == DEN_TANH4X2_TAB) rho = fmax(rho, fit_u(f1, x, inv));
             } else {
@@ -941,9 +932,185 @@ SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const 
         }
     }
     }
-    acc[0] += s.area * m;
-    acc[1] += s.area * cx; acc[2] += s.area * cy; acc[3] += s.area * cz;
-    acc[4] += s.area * e;
+    mo[0] = m; mo[1] = cx; mo[2] = cy; mo[3] = cz; mo[4] = e;
+}
+
+// Fitted-density sweep, rule node outermost: for node q of every leaf,
+//   x = v0 + ((a+pass)/L + sg l1_q) e1 + ((b+pass)/L + sg l2_q) e2 = row_base(a) + (b/L) e2,
+// so a node costs 3 FMA to place (the leaf-outer loop recomputes o_q, which does not fit in
+// registers), the rule weight is applied once per q, and with the patch's fit of rho in
+// s = |y - sigma c|^2 = 2 - 2 y.(sigma c) (|y| = |c| = 1):  s - sc = (2 - sc) + inv x.(-2 sigma c).
+// SERIES: 1/|x| = (1 - delta)^(-1/2) = 1 + delta/2 + 3 delta^2/8 + 5 delta^3/16 with
+// delta = 1 - |x|^2 <= 1e-4 on the patch (truncation <= 35/128 delta^4 < 3e-17), else the
+// MUFU seed + cubic refinement.  31 FP64 instructions per node (one centre).
+struct FitEval {
+    double b[7];   // rho = sum_k b[k] ds^k
+    V3 m2c;        // -2 sigma c
+    double k0;     // 2 - sc
+};
+
+SCVT_HD FitEval fit_eval(const LocalFit& f) {
+    FitEval r;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) r.b[k] = f.b[k];
+    r.m2c = mul(f.sgc, -2.0);
+    r.k0 = 2.0 - f.sc;
+    return r;
+}
+
+SCVT_HD double fit_rho(const FitEval& f, V3 x, double inv) {
+    const double t = x.x * f.m2c.x + x.y * f.m2c.y + x.z * f.m2c.z;
+    const double ds = fma(inv, t, f.k0);
+    double acc = f.b[6];
+#pragma unroll
+    for (int k = 5; k >= 0; --k) acc = fma(acc, ds, f.b[k]);
+    return acc;
+}
+
+SCVT_HD void fit_rho2(const FitEval& f, V3 x0, double inv0, V3 x1, double inv1, double* r0,
+                      double* r1) {
+    const double t0 = fma(x0.z, f.m2c.z, fma(x0.y, f.m2c.y, x0.x * f.m2c.x));
+    const double t1 = fma(x1.z, f.m2c.z, fma(x1.y, f.m2c.y, x1.x * f.m2c.x));
+    const double s0 = fma(inv0, t0, f.k0), s1 = fma(inv1, t1, f.k0);
+#ifdef FIT_ESTRIN
+    // Estrin: depth 4 instead of Horner's 6 (one more FMA)
+    const double q0 = s0 * s0, q1 = s1 * s1;
+    const double l0 = fma(f.b[1], s0, f.b[0]), l1 = fma(f.b[1], s1, f.b[0]);
+    const double m0 = fma(f.b[3], s0, f.b[2]), m1 = fma(f.b[3], s1, f.b[2]);
+    double h0 = fma(f.b[5], s0, f.b[4]), h1 = fma(f.b[5], s1, f.b[4]);
+    h0 = fma(f.b[6], q0, h0); h1 = fma(f.b[6], q1, h1);
+    *r0 = fma(fma(h0, q0, m0), q0, l0);
+    *r1 = fma(fma(h1, q1, m1), q1, l1);
+#else
+    double a0 = f.b[6], a1 = f.b[6];
+#pragma unroll
+    for (int k = 5; k >= 0; --k) { a0 = fma(a0, s0, f.b[k]); a1 = fma(a1, s1, f.b[k]); }
+    *r0 = a0; *r1 = a1;
+#endif
+}
+
+template <int KIND, int L, bool SERIES>
+SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const double* l2,
+                             const double* w, const LocalFit& lf0, const LocalFit& lf1,
+                             double* acc) {
+    const FitEval f0 = fit_eval(lf0);
+    FitEval f1;
+    if (KIND == DEN_TANH4X2_TAB) f1 = fit_eval(lf1);
+    const double invL = 1.0 / (double)L;
+    for (int pass = 0; pass < 2; ++pass) {          // 0: up-leaves, 1: down-leaves
+        const double sg = pass ? -1.0 : 1.0;
+        const int M = L - pass;
+#pragma unroll 1
+        for (int q = 0; q < 7; ++q) {
+            const double ga = fma(sg, l1[q], pass * invL), gb = fma(sg, l2[q], pass * invL);
+            const V3 r0 = v3(fma(gb, s.e2.x, s.v0.x), fma(gb, s.e2.y, s.v0.y),
+                             fma(gb, s.e2.z, s.v0.z));
+            double mq = 0.0, xq = 0.0, yq = 0.0, zq = 0.0, eq = 0.0;
+            for (int a = 0; a < M; ++a) {
+                const double fa = fma((double)a, invL, ga);
+                const V3 base = v3(fma(fa, s.e1.x, r0.x), fma(fa, s.e1.y, r0.y),
+                                   fma(fa, s.e1.z, r0.z));
+                const int nb = M - a;
+                int b = 0;
+                double fb = 0.0;
+                // two nodes per step, interleaved stage by stage in the source: ptxas keeps
+                // the order, and the two dependency chains hide the DFMA latency
+                for (; b + 1 < nb; b += 2, fb += 2.0 * invL) {
+                    const double fb1 = fb + invL;
+                    const V3 x0 = v3(fma(fb, s.e2.x, base.x), fma(fb, s.e2.y, base.y),
+                                     fma(fb, s.e2.z, base.z));
+                    const V3 x1 = v3(fma(fb1, s.e2.x, base.x), fma(fb1, s.e2.y, base.y),
+                                     fma(fb1, s.e2.z, base.z));
+                    double inv0, inv1;
+                    if (SERIES) {
+                        const double d0 = fma(-x0.z, x0.z, fma(-x0.y, x0.y, fma(-x0.x, x0.x, 1.0)));
+                        const double d1 = fma(-x1.z, x1.z, fma(-x1.y, x1.y, fma(-x1.x, x1.x, 1.0)));
+                        const double p0 = fma(d0, 0.3125, 0.375), p1 = fma(d1, 0.3125, 0.375);
+                        const double q0 = fma(d0, p0, 0.5), q1 = fma(d1, p1, 0.5);
+                        inv0 = fma(d0, q0, 1.0); inv1 = fma(d1, q1, 1.0);
+                    } else {
+                        inv0 = fast_rsqrt(x0.x * x0.x + x0.y * x0.y + x0.z * x0.z);
+                        inv1 = fast_rsqrt(x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+                    }
+                    double rho0, rho1;
+                    fit_rho2(f0, x0, inv0, x1, inv1, &rho0, &rho1);
+                    if (KIND == DEN_TANH4X2_TAB) {
+                        double r0b, r1b;
+                        fit_rho2(f1, x0, inv0, x1, inv1, &r0b, &r1b);
+                        rho0 = fmax(rho0, r0b); rho1 = fmax(rho1, r1b);
+                    }
+                    const double ri0 = rho0 * inv0, ri1 = rho1 * inv1;
+                    const double dx0 = fma(x0.x, inv0, -z.x), dx1 = fma(x1.x, inv1, -z.x);
+                    const double dy0 = fma(x0.y, inv0, -z.y), dy1 = fma(x1.y, inv1, -z.y);
+                    const double dz0 = fma(x0.z, inv0, -z.z), dz1 = fma(x1.z, inv1, -z.z);
+                    const double e0 = fma(dz0, dz0, fma(dy0, dy0, dx0 * dx0));
+                    const double e1 = fma(dz1, dz1, fma(dy1, dy1, dx1 * dx1));
+                    mq += rho0 + rho1;
+                    xq = fma(ri1, x1.x, fma(ri0, x0.x, xq));
+                    yq = fma(ri1, x1.y, fma(ri0, x0.y, yq));
+                    zq = fma(ri1, x1.z, fma(ri0, x0.z, zq));
+                    eq = fma(rho1, e1, fma(rho0, e0, eq));
+                }
+                if (b < nb) {
+                    const V3 x = v3(fma(fb, s.e2.x, base.x), fma(fb, s.e2.y, base.y),
+                                    fma(fb, s.e2.z, base.z));
+                    double inv;
+                    if (SERIES) {
+                        const double dl = fma(-x.z, x.z, fma(-x.y, x.y, fma(-x.x, x.x, 1.0)));
+                        inv = fma(dl, fma(dl, fma(dl, 0.3125, 0.375), 0.5), 1.0);
+                    } else {
+                        inv = fast_rsqrt(x.x * x.x + x.y * x.y + x.z * x.z);
+                    }
+                    double rho = fit_rho(f0, x, inv);
+                    if (KIND == DEN_TANH4X2_TAB) rho = fmax(rho, fit_rho(f1, x, inv));
+                    const double ri = rho * inv;
+                    mq += rho;
+                    xq = fma(ri, x.x, xq); yq = fma(ri, x.y, yq); zq = fma(ri, x.z, zq);
+                    const double dx = fma(x.x, inv, -z.x), dy = fma(x.y, inv, -z.y),
+                                 dz = fma(x.z, inv, -z.z);
+                    eq = fma(rho, dx * dx + dy * dy + dz * dz, eq);
+                }
+            }
+            const double wq = s.area * w[q == 0 ? 0 : (q < 4 ? 1 : 4)];
+            acc[0] = fma(wq, mq, acc[0]);
+            acc[1] = fma(wq, xq, acc[1]); acc[2] = fma(wq, yq, acc[2]);
+            acc[3] = fma(wq, zq, acc[3]);
+            acc[4] = fma(wq, eq, acc[4]);
+        }
+    }
+}
+
+template <int KIND, int L>
+SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const double* l2,
+                                 const double* w, const DensityParams& dp, double* acc,
+                                 int* pole) {
+    const bool TAB = KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB;
+    LocalFit f0, f1;
+    bool fitted = false;
+    if (TAB) {
+        fitted = local_fit(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f0);
+        if (fitted && KIND == DEN_TANH4X2_TAB)
+            fitted = local_fit(dp, s, v3(dp.c1x, dp.c1y, dp.c1z), f1);
+    }
+    if (TAB && fitted) {
+        // 1 - |x|^2 <= 1 - dist(origin, plane)^2 on the patch
+        const V3 nv = cross(s.e1, s.e2);
+        const double nn = dot(nv, nv), h = dot(nv, s.v0);
+        if (nn > 0.0 && nn - h * h <= 1e-4 * nn)
+            sym7_fit_leaves<KIND, L, true>(s, z, l1, l2, w, f0, f1, acc);
+        else
+            sym7_fit_leaves<KIND, L, false>(s, z, l1, l2, w, f0, f1, acc);
+        return;
+    }
+    V3 o[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) o[q] = add(mul(s.e1, l1[q]), mul(s.e2, l2[q]));
+    const double w0 = w[0], w1 = w[1], w2 = w[4];
+    double mo[5];
+    sym7_leaves<KIND, L, false>(s, z, o, w0, w1, w2, dp, f0, f1, mo, pole);
+    acc[0] += s.area * mo[0];
+    acc[1] += s.area * mo[1]; acc[2] += s.area * mo[2]; acc[3] += s.area * mo[3];
+    acc[4] += s.area * mo[4];
 }
 
 }  // namespace scvt

@@ -37,6 +37,12 @@ constexpr int RED_BLOCKS = 296;      // 2 x 148 SMs: fixed reduction shape
 constexpr int RED_THREADS = 256;
 constexpr int VEC_THREADS = 256;
 constexpr int QUAD_THREADS = 128;
+#ifndef QUAD_MINB
+#define QUAD_MINB 4      // k_quad fast path: CTAs per SM the register budget must allow
+#endif
+#ifndef QUAD_MINB2
+#define QUAD_MINB2 3     // two-centre fast path
+#endif
 constexpr int CELL_THREADS = 64;
 constexpr int MAX_SLOTS = 64;        // partial-sum slots
 
@@ -262,7 +268,7 @@ struct QuadArgs {
 };
 
 template <int KIND, bool SPHERE, bool SYM7>
-__global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? (KIND == DEN_TANH4X2_TAB ? 3 : 5) : 1)
+__global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? (KIND == DEN_TANH4X2_TAB ? QUAD_MINB2 : QUAD_MINB) : 1)
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
     for (int q = threadIdx.x; q < 3 * a.nq; q += blockDim.x) s_nodes[q] = a.nodes[q];
