@@ -182,12 +182,20 @@ __device__ __forceinline__ void mark_bad(int mode, int* status, int bit, int* ba
 }
 
 __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ ids, int p_lo,
-                         int p_hi, const int* __restrict__ nbr, const int* __restrict__ deg,
+                         int p_hi, const int* __restrict__ list, const int* __restrict__ list_n,
+                         const int* __restrict__ nbr, const int* __restrict__ deg,
                          uint8_t* __restrict__ amb, int* __restrict__ status,
                          int* __restrict__ stats, int mode, int* __restrict__ bad,
                          int* __restrict__ nbad) {
-    int p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= p_hi) return;
+    int p;
+    if (list) {                 // re-certification of a compacted list of sorted slots
+        const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+        if (idx >= *list_n) return;
+        p = list[idx];
+    } else {
+        p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
+        if (p >= p_hi) return;
+    }
     int i = ids[p];
     int d = deg[i];
     const int* row = nbr + (int64_t)i * MAXDEG;
@@ -220,6 +228,22 @@ __global__ void k_flag_slots(int n, const int* __restrict__ ids, const int* __re
                              uint8_t* __restrict__ flags) {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p < n) flags[p] = bad[ids[p]] ? 1 : 0;
+}
+
+// Cells whose certificate verdict can change once the listed cells are rebuilt: the listed
+// cells and their current (pre-rebuild) neighbours.  A cell that passed lists only neighbours
+// that list it back, so a passing cell outside this set reads no rebuilt cycle.
+__global__ void k_mark_recheck(const int* __restrict__ list, const int* __restrict__ list_n,
+                               const int* __restrict__ ids, const int* __restrict__ nbr,
+                               const int* __restrict__ deg, int* __restrict__ recheck) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= *list_n) return;
+    const int i = ids[list[idx]];
+    recheck[i] = 1;
+    const int d = deg[i];
+    if (d < 3 || d > MAXDEG) return;
+    const int* row = nbr + (int64_t)i * MAXDEG;
+    for (int t = 0; t < d; ++t) recheck[row[t]] = 1;
 }
 
 // incidence CSR in bucket (spatial) order: sorted slot p -> generator ids[p]
@@ -1020,6 +1044,7 @@ struct scvt_ctx {
     // cycle reuse across evaluations
     int64_t cycles_n = -1;                  // n of the certified cycles held in d_nbr/d_deg
     int* d_bad = nullptr; int* d_nbad = nullptr; uint8_t* d_slotflag = nullptr; int* d_list = nullptr;
+    int* d_recheck = nullptr; int* d_nlist = nullptr;   // reuse: cells to re-certify
     int64_t reuse_stats[4] = {0, 0, 0, 0};  // checks, bad cells, evaluations fully reused
     int64_t prof_n[4] = {0, 0, 0, 0};
 };
@@ -1222,9 +1247,21 @@ int verify_range(scvt_ctx* ctx, const double* z, int64_t lo, int64_t hi, int mod
     int64_t cnt = hi - lo;
     if (cnt <= 0) return SCVT_OK;
     k_verify<<<blocks_for(cnt, 128), 128, 0, ctx->stream>>>(
-        z, ctx->d_ids, (int)lo, (int)hi, ctx->d_nbr, ctx->d_deg, ctx->d_amb, ctx->d_status,
-        ctx->d_status + 8, mode, ctx->d_bad, ctx->d_nbad);
+        z, ctx->d_ids, (int)lo, (int)hi, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
+        ctx->d_status, ctx->d_status + 8, mode, ctx->d_bad, ctx->d_nbad);
     LAUNCHED();
+    return SCVT_OK;
+}
+
+// compact the sorted slots p in [0, n) whose generator has flag[ids[p]] != 0 into d_list
+int compact_slots(scvt_ctx* ctx, int64_t n, const int* flag, int* count_dev) {
+    cudaStream_t s = ctx->stream;
+    k_flag_slots<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, flag, ctx->d_slotflag);
+    LAUNCHED();
+    size_t tb = ctx->cub_bytes;
+    thrust::counting_iterator<int> it(0);
+    CK(cub::DeviceSelect::Flagged(ctx->d_cub, tb, it, ctx->d_slotflag, ctx->d_list, count_dev,
+                                  (int)n, s));
     return SCVT_OK;
 }
 
@@ -1236,10 +1273,18 @@ bool reuse_enabled() { return getenv("SCVT_NO_REUSE") == nullptr; }
 int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView& g, bool* done) {
     cudaStream_t s = ctx->stream;
     *done = false;
+    int nlist = (int)n;                          // cells the next pass must certify
     for (int round = 0; round < 4; ++round) {
         CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
         CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
-        TRY(verify_range(ctx, z, 0, n, 1));
+        if (round == 0) {
+            TRY(verify_range(ctx, z, 0, n, 1));
+        } else if (nlist > 0) {
+            k_verify<<<blocks_for(nlist, 128), 128, 0, s>>>(
+                z, ctx->d_ids, 0, (int)n, ctx->d_list, ctx->d_nlist, ctx->d_nbr, ctx->d_deg,
+                ctx->d_amb, ctx->d_status, ctx->d_status + 8, 1, ctx->d_bad, ctx->d_nbad);
+            LAUNCHED();
+        }
         int nbad = 0;
         CK(cudaMemcpyAsync(&nbad, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1247,14 +1292,12 @@ int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView&
         ctx->reuse_stats[1] += nbad;
         if (nbad == 0) { *done = true; return SCVT_OK; }
         if (nbad > (3 * n) / 4 || round == 3) return SCVT_OK;   // caller rebuilds everything
-        // compact the bad generators' sorted slots and rebuild those cells
-        k_flag_slots<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_bad,
-                                                        ctx->d_slotflag);
+        // the bad cells' slots; what the next pass must re-certify; then rebuild them
+        TRY(compact_slots(ctx, n, ctx->d_bad, ctx->d_nbad));
+        CK(cudaMemsetAsync(ctx->d_recheck, 0, n * sizeof(int), s));
+        k_mark_recheck<<<blocks_for(nbad, 256), 256, 0, s>>>(ctx->d_list, ctx->d_nbad, ctx->d_ids,
+                                                              ctx->d_nbr, ctx->d_deg, ctx->d_recheck);
         LAUNCHED();
-        size_t tb = ctx->cub_bytes;
-        thrust::counting_iterator<int> it(0);
-        CK(cub::DeviceSelect::Flagged(ctx->d_cub, tb, it, ctx->d_slotflag, ctx->d_list,
-                                      ctx->d_nbad, (int)n, s));
         k_cells_warp<<<blocks_for(nbad, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
             g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
             ctx->d_status + 8, ctx->prof ? ctx->d_diag : nullptr);
@@ -1263,6 +1306,9 @@ int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView&
             g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
             ctx->d_status + 8);
         LAUNCHED();
+        TRY(compact_slots(ctx, n, ctx->d_recheck, ctx->d_nlist));
+        CK(cudaMemcpyAsync(&nlist, ctx->d_nlist, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
     }
     return SCVT_OK;
 }
@@ -1590,7 +1636,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_scal, MAX_SLOTS);
     AL(d_status, 16);
     AL(d_diag, 8);
-    AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n);
+    AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -1654,6 +1700,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
+                   ctx->d_recheck, ctx->d_nlist,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
