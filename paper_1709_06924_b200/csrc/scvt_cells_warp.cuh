@@ -231,12 +231,13 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
         if (count > WCAND && shrinks < 4) {
             // annulus denser than expected (a coarse cell next to the plateau, or a far
             // vertex that inflated R2): narrow it and clip nearest-first instead of sweeping;
-            // the sweep, if still needed, then starts from a tighter polygon
+            // the sweep, if still needed, then starts from a tighter polygon.  Capped per
+            // cell: a coarse cell whose security disk covers a dense region would otherwise
+            // crawl through it in thin annuli (the culled sweep is the right tool there)
             ++shrinks;
             r2 = lo_c2 < 0.0 ? 0.25 * r2 : lo_c2 + 0.25 * (r2 - lo_c2);
             continue;
         }
-        shrinks = 0;
         if (count <= WCAND) {
             // ---- rank sort by (c2, id), then clip nearest-first with early exit
             double kc[2];
