@@ -216,7 +216,8 @@ int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int re
  * out12 = {cells, candidate passes, points scanned, candidates sorted, clips, radius rounds,
  *          max 32-point sweep batches of one cell, max clips of one cell,
  *          evaluations whose previous cycles were certified and reused, cells rebuilt by
- *          reuse, certificate passes run by reuse, 0} */
+ *          reuse, certificate passes run by reuse,
+ *          max points scanned by one cell | (max candidate passes of one cell << 40)} */
 int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset);
 /* measured FP64 DFMA throughput of `device` in TFLOP/s (2 FLOPs per FMA): the FP64
  * roofline denominator, which MEASURED_PEAKS.json does not carry */

@@ -170,6 +170,9 @@ __device__ __forceinline__ void vertex_disk(const WPoly& P, int lane, V3 zi, V3 
     }
 }
 
+// cap rectangles above this many buckets go to the culled sweep once the polygon is bounded
+constexpr int SWEEP_BUCKETS = 8192;
+
 // Returns valence > 0, -ST_* for genuine failures, or -ST_POLY_OVERFLOW to request the
 // single-thread fallback.  All lanes return the same value.
 __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double* s_c2,
@@ -195,6 +198,18 @@ __device__ int build_cell_warp(const GridView& g, int i, V3 zi, int lane, double
         CapBox cb = cap_box(zi, sqrt(r2));
         double lim = 4.0 * R2 * (1.0 + 1e-12);
         int count = 0;
+        if (!box) {
+            // a bounded polygon with a large security disk (a far vertex, or a coarse cell
+            // next to a dense region): the plain gather would rescan every bucket of the cap,
+            // inner disk included; the sweep culls 8x8-bucket blocks by the vertex disks
+            int nbk = 0;
+            for (int face = 0; face < 6; ++face) {
+                int iu0, iu1, iv0, iv1;
+                if (cap_face_range(cb, face, g.G, &iu0, &iu1, &iv0, &iv1))
+                    nbk += (iu1 - iu0 + 1) * (iv1 - iv0 + 1);
+            }
+            if (nbk > SWEEP_BUCKETS) count = WCAND + 1;
+        }
         // ---- gather candidates in (lo_c2, r2] that can still cut the cell
         for (int face = 0; face < 6 && count <= WCAND; ++face) {
             int iu0, iu1, iv0, iv1;

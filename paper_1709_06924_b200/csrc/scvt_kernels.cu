@@ -125,6 +125,8 @@ k_cells_warp(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
             atomicAdd(&diag[5], (unsigned long long)cs.rounds);
             atomicMax(&diag[6], (unsigned long long)(cs.sweep_visits >> 5));
             atomicMax(&diag[7], (unsigned long long)cs.clips);
+            atomicMax(&diag[8], (unsigned long long)cs.scanned);
+            atomicMax(&diag[9], (unsigned long long)cs.passes);
         }
     }
 }
@@ -1538,9 +1540,11 @@ int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset) {
     out12[8] = ctx->reuse_stats[2];   // evaluations whose cycles were certified by reuse
     out12[9] = ctx->reuse_stats[1];   // cells rebuilt by reuse rounds
     out12[10] = ctx->reuse_stats[0];  // certificate passes run by the reuse path
-    out12[11] = 0;
+    unsigned long long mx[2];
+    CK(cudaMemcpy(mx, ctx->d_diag + 8, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    out12[11] = (int64_t)mx[0] | ((int64_t)mx[1] << 40);   // max scanned | max passes << 40
     if (reset) {
-        CK(cudaMemset(ctx->d_diag, 0, 8 * sizeof(int64_t)));
+        CK(cudaMemset(ctx->d_diag, 0, 10 * sizeof(int64_t)));
         ctx->reuse_stats[0] = ctx->reuse_stats[1] = ctx->reuse_stats[2] = 0;
     }
     return SCVT_OK;
@@ -1635,7 +1639,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_partials, (int64_t)MAX_SLOTS * RED_BLOCKS);
     AL(d_scal, MAX_SLOTS);
     AL(d_status, 16);
-    AL(d_diag, 8);
+    AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);

@@ -26,4 +26,4 @@ with P.MeshEvaluator(P.density_preset(cfg), "7pt", subdivision=3) as ev:
         lib.scvt_profile_read(ev.context.ptr, ms, cnt, 0)
         print(f"iter {it}: evals {cnt[2]} cells_ms/eval {ms[0]/max(cnt[0],1):.2f} quad_ms/eval "
               f"{ms[1]/max(cnt[1],1):.2f} eval_ms {ms[2]/max(cnt[2],1):.2f} reused {c[8]} cert_passes {c[10]} "
-              f"rebuilt cells {c[9]} max_sweep_batches {c[6]} max_clips {c[7]}", flush=True)
+              f"rebuilt cells {c[9]} max_sweep_batches {c[6]} max_clips {c[7]} max_scanned {c[11] & ((1 << 40) - 1)} max_passes {c[11] >> 40}", flush=True)
