@@ -147,8 +147,36 @@ int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n,
 int64_t scvt_shard_rows(int64_t n, int nshards);
 int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                      int32_t* cyc_send);
+/* cyc_all may be NULL after the reuse rounds below certified the context's cycles */
 int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                        const int32_t* cyc_all, double* res_send, int32_t* status_host);
+
+/* sharded cycle reuse: the single-GPU reuse loop (previous evaluation's cycles certified at
+ * the new positions, failing cells rebuilt, re-certified) split at its exchanges.  After a
+ * successful evaluation every rank holds all n certified cycles, identically.  Per round r:
+ *   scvt_shard_recheck  r = 0: grid (replicated) and the certificate of the owned cells
+ *                       against the held cycles; r > 0: the owned cells of the last plan's
+ *                       re-check list.  bad_out int32[n]: 1 for every generator of a failing
+ *                       triangle seen by this shard.  *ready_host = 0 at r = 0 when the context
+ *                       holds no cycles for n points (take the scvt_shard_cells path).
+ *   <caller all-reduces bad_out (max) -> bad_all>
+ *   scvt_shard_plan     bad set, the next round's re-check list (bad cells and their
+ *                       current neighbours) and counts_host int64[nshards+1] = bad cells per
+ *                       shard, total.  Identical on every rank.  Total 0: certified, call
+ *                       scvt_shard_moments(cyc_all = NULL).
+ *   scvt_shard_rebuild  rebuild this shard's bad cells -> rows_send int32[cap][34] (cap = max
+ *                       per-shard count; padding id -1)
+ *   <caller all-gathers rows_send -> rows [nshards*cap][34]>
+ *   scvt_shard_install  write the gathered rows into the held cycles
+ * Bad set, re-check lists and rebuilt cells equal the single-GPU loop's, so the certified
+ * triangulation (unique) and every output are bitwise those of scvt_evaluate. */
+int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                       int round, int32_t* bad_out, int32_t* ready_host);
+int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_all,
+                    int64_t* counts_host);
+int scvt_shard_rebuild(scvt_ctx* ctx, int64_t n, int shard, int nshards, int64_t cap,
+                       int32_t* rows_send);
+int scvt_shard_install(scvt_ctx* ctx, int64_t n, const int32_t* rows, int64_t nrows);
 int scvt_shard_status(scvt_ctx* ctx, int32_t status);
 int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                       const double* res_all, double* grad, double* first, double* mass,

@@ -67,6 +67,12 @@ SIGNATURES = {
     "scvt_shard_cells": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp]),
     "scvt_shard_moments": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                           _vp, _vp, _c_i32_p]),
+    "scvt_shard_recheck": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, _vp, _c_i32_p]),
+    "scvt_shard_plan": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, _vp, _c_i64_p]),
+    "scvt_shard_rebuild": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int64, _vp]),
+    "scvt_shard_install": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64]),
     "scvt_shard_status": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "scvt_shard_finish": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp,
                                          _vp, _vp, _c_dbl_p]),

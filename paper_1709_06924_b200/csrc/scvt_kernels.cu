@@ -194,6 +194,7 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
         const int idx = blockIdx.x * blockDim.x + threadIdx.x;
         if (idx >= *list_n) return;
         p = list[idx];
+        if (p < p_lo || p >= p_hi) return;     // sharded re-check: owned slots only
     } else {
         p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
         if (p >= p_hi) return;
@@ -417,6 +418,23 @@ __global__ void k_unpack_cycles(const int* __restrict__ rows, int nrows, int n,
     for (int t = 0; t < d && t < MAXDEG; ++t) nbr[(int64_t)i * MAXDEG + t] = row[2 + t];
     atomicAdd(degsum, d);
 }
+
+// rebuilt cells of a slot list packed as exchange rows (cap rows, padding id = -1)
+__global__ void k_pack_list(const int* __restrict__ list, const int* __restrict__ cnt_dev,
+                            int cap, const int* __restrict__ ids, const int* __restrict__ nbr,
+                            const int* __restrict__ deg, int* __restrict__ out) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= cap) return;
+    int* row = out + (int64_t)q * CYC_ROW;
+    if (q >= *cnt_dev) { row[0] = -1; row[1] = 0; return; }
+    int i = ids[list[q]];
+    int d = deg[i];
+    row[0] = i;
+    row[1] = d;
+    for (int t = 0; t < MAXDEG; ++t) row[2 + t] = t < d ? nbr[(int64_t)i * MAXDEG + t] : -1;
+}
+
+__global__ void k_set_int(int* p, int v) { *p = v; }
 
 // owned slots: fixed-order incidence sums packed as exchange rows
 __global__ void k_gather_pack(int p_lo, int cnt, int cap, const int* __restrict__ ids,
@@ -1047,6 +1065,10 @@ struct scvt_ctx {
     int64_t cycles_n = -1;                  // n of the certified cycles held in d_nbr/d_deg
     int* d_bad = nullptr; int* d_nbad = nullptr; uint8_t* d_slotflag = nullptr; int* d_list = nullptr;
     int* d_recheck = nullptr; int* d_nlist = nullptr;   // reuse: cells to re-certify
+    int* d_list2 = nullptr; int* d_nlist2 = nullptr;    // sharded reuse: re-check slot list
+    int* d_cnt = nullptr;                               // sharded reuse: owned rebuild count
+    GridView gv;                                        // grid of the current evaluation
+    std::vector<int64_t> plan_counts;                   // bad cells per shard (last plan)
     int64_t reuse_stats[4] = {0, 0, 0, 0};  // checks, bad cells, evaluations fully reused
     int64_t prof_n[4] = {0, 0, 0, 0};
 };
@@ -1224,6 +1246,7 @@ int build_grid(scvt_ctx* ctx, const double* z, int64_t n, GridView* gv) {
     LAUNCHED();
     gv->zs = ctx->d_zs; gv->ids = ctx->d_ids; gv->start = ctx->d_start; gv->z = z; gv->G = G;
     gv->n = n;
+    ctx->gv = *gv;
     return SCVT_OK;
 }
 
@@ -1641,6 +1664,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_status, 16);
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
+    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -1704,7 +1728,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
-                   ctx->d_recheck, ctx->d_nlist,
+                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
@@ -1834,6 +1858,126 @@ int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int n
     return SCVT_OK;
 }
 
+// ---- sharded cycle reuse: the single-GPU reuse loop split at its two exchanges
+int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                       int round, int32_t* bad_out, int32_t* ready_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (nshards < 1 || shard < 0 || shard >= nshards)
+        return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
+    cudaStream_t s = ctx->stream;
+    *ready_host = 0;
+    if (round == 0) {
+        if (ctx->cycles_n != n || !reuse_enabled()) return SCVT_OK;   // caller: full path
+        if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], s));
+        ctx->prof_n[3] = 0;
+        TRY(reset_status(ctx));
+        GridView g;
+        TRY(build_grid(ctx, z, n, &g));
+    }
+    int64_t lo, hi;
+    shard_range(n, shard, nshards, &lo, &hi);
+    CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
+    CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
+    if (round == 0) {
+        TRY(verify_range(ctx, z, lo, hi, 1));
+    } else {
+        int nl = 0;
+        CK(cudaMemcpyAsync(&nl, ctx->d_nlist2, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (nl > 0) {
+            k_verify<<<blocks_for(nl, 128), 128, 0, s>>>(
+                z, ctx->d_ids, (int)lo, (int)hi, ctx->d_list2, ctx->d_nlist2, ctx->d_nbr,
+                ctx->d_deg, ctx->d_amb, ctx->d_status, ctx->d_status + 8, 1, ctx->d_bad,
+                ctx->d_nbad);
+            LAUNCHED();
+        }
+    }
+    CK(cudaMemcpyAsync(bad_out, ctx->d_bad, n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    *ready_host = 1;
+    return SCVT_OK;
+}
+
+int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_all,
+                    int64_t* counts_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (nshards < 1) return fail(ctx, SCVT_ERR_CONFIG, "bad shard count %d", nshards);
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->d_bad, bad_all, n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    TRY(compact_slots(ctx, n, ctx->d_bad, ctx->d_nbad));       // bad slots, ascending
+    int nbad = 0;
+    CK(cudaMemcpyAsync(&nbad, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->reuse_stats[0] += 1;
+    ctx->reuse_stats[1] += nbad;
+    ctx->plan_counts.assign(nshards, 0);
+    if (nbad > 0) {
+        // re-check set of the next round, and the bad cells per shard (slot ranges)
+        CK(cudaMemsetAsync(ctx->d_recheck, 0, n * sizeof(int), s));
+        k_mark_recheck<<<blocks_for(nbad, 256), 256, 0, s>>>(ctx->d_list, ctx->d_nbad, ctx->d_ids,
+                                                              ctx->d_nbr, ctx->d_deg, ctx->d_recheck);
+        LAUNCHED();
+        std::vector<int> slots(nbad);
+        CK(cudaMemcpyAsync(slots.data(), ctx->d_list, nbad * sizeof(int), cudaMemcpyDeviceToHost, s));
+        // compact the re-check flags into d_list2 (d_list stays: the shards' rebuild lists)
+        k_flag_slots<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_recheck,
+                                                        ctx->d_slotflag);
+        LAUNCHED();
+        size_t tb = ctx->cub_bytes;
+        thrust::counting_iterator<int> it(0);
+        CK(cub::DeviceSelect::Flagged(ctx->d_cub, tb, it, ctx->d_slotflag, ctx->d_list2,
+                                      ctx->d_nlist2, (int)n, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t cap = scvt_shard_rows(n, nshards);
+        for (int p : slots) ctx->plan_counts[std::min<int64_t>(p / cap, nshards - 1)] += 1;
+    } else {
+        ctx->reuse_stats[2] += 1;                 // certified: the evaluation reuses all cycles
+    }
+    for (int k = 0; k < nshards; ++k) counts_host[k] = ctx->plan_counts[k];
+    counts_host[nshards] = nbad;
+    return SCVT_OK;
+}
+
+int scvt_shard_rebuild(scvt_ctx* ctx, int64_t n, int shard, int nshards, int64_t cap,
+                       int32_t* rows_send) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if ((int)ctx->plan_counts.size() != nshards || shard < 0 || shard >= nshards)
+        return fail(ctx, SCVT_ERR_CONFIG, "scvt_shard_rebuild without a matching plan");
+    cudaStream_t s = ctx->stream;
+    int64_t off = 0;
+    for (int k = 0; k < shard; ++k) off += ctx->plan_counts[k];
+    const int cnt = (int)ctx->plan_counts[shard];
+    if (cap < cnt) return fail(ctx, SCVT_ERR_CONFIG, "cap %lld < %d rebuilt cells",
+                               (long long)cap, cnt);
+    k_set_int<<<1, 1, 0, s>>>(ctx->d_cnt, cnt);
+    LAUNCHED();
+    const int* list = ctx->d_list + off;
+    if (cnt > 0) {
+        k_cells_warp<<<blocks_for(cnt, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
+            ctx->gv, 0, (int)n, list, ctx->d_cnt, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+            ctx->d_status + 8, ctx->prof ? ctx->d_diag : nullptr);
+        LAUNCHED();
+        k_cells<<<blocks_for(cnt, CELL_THREADS), CELL_THREADS, 0, s>>>(
+            ctx->gv, 0, (int)n, list, ctx->d_cnt, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+            ctx->d_status + 8);
+        LAUNCHED();
+    }
+    if (cap > 0) {
+        k_pack_list<<<blocks_for(cap, 128), 128, 0, s>>>(list, ctx->d_cnt, (int)cap, ctx->d_ids,
+                                                          ctx->d_nbr, ctx->d_deg, rows_send);
+        LAUNCHED();
+    }
+    return SCVT_OK;
+}
+
+int scvt_shard_install(scvt_ctx* ctx, int64_t n, const int32_t* rows, int64_t nrows) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (nrows <= 0) return SCVT_OK;
+    k_unpack_cycles<<<blocks_for(nrows, 128), 128, 0, ctx->stream>>>(
+        rows, (int)nrows, (int)n, ctx->d_nbr, ctx->d_deg, ctx->d_status + 13, ctx->d_status);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
 int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                        const int32_t* cyc_all, double* res_send, int32_t* status_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
@@ -1841,16 +1985,20 @@ int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
     int64_t lo, hi, cap = scvt_shard_rows(n, nshards);
     shard_range(n, shard, nshards, &lo, &hi);
     // every rank gets every cycle: needed to certify its own cells against their neighbours
-    CK(cudaMemsetAsync(ctx->d_status + 13, 0, sizeof(int), s));
-    k_unpack_cycles<<<blocks_for(cap * nshards, 128), 128, 0, s>>>(
-        cyc_all, (int)(cap * nshards), (int)n, ctx->d_nbr, ctx->d_deg, ctx->d_status + 13,
-        ctx->d_status);
-    LAUNCHED();
-    TRY(verify_range(ctx, z, lo, hi));
+    // (cyc_all == NULL: the cycles were certified by the sharded reuse rounds)
+    if (cyc_all) {
+        CK(cudaMemsetAsync(ctx->d_status + 13, 0, sizeof(int), s));
+        k_unpack_cycles<<<blocks_for(cap * nshards, 128), 128, 0, s>>>(
+            cyc_all, (int)(cap * nshards), (int)n, ctx->d_nbr, ctx->d_deg, ctx->d_status + 13,
+            ctx->d_status);
+        LAUNCHED();
+        TRY(verify_range(ctx, z, lo, hi));
+    }
     TRY(incidences_range(ctx, lo, hi, 6 * n));
-    int tot[2] = {0, 0};
+    int tot[2] = {0, (int)(6 * n - 12)};
     CK(cudaMemcpyAsync(&tot[0], ctx->d_inc_start + (hi - lo), sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tot[1], ctx->d_status + 13, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (cyc_all)
+        CK(cudaMemcpyAsync(&tot[1], ctx->d_status + 13, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (tot[1] != 6 * n - 12) {
         CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1903,6 +2051,8 @@ int scvt_shard_finish_ex(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
     if (seen != n)
         return fail(ctx, SCVT_ERR_COVERAGE, "shard results cover %d of %lld generators", seen,
                     (long long)n);
+    // every rank now holds all n certified cycles: the next evaluation may reuse them
+    ctx->cycles_n = n;
     return SCVT_OK;
 }
 

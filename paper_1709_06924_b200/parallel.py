@@ -12,6 +12,11 @@ exchanges are two all-gathers per evaluation:
                 all-gathered, scattered to id order and reduced by the same fixed-shape kernel
                 on every rank.
 
+From the second evaluation on, the previous cycles are reused exactly as on one GPU: each
+rank certifies its owned cells at the new positions, the bad flags are all-reduced (max),
+every rank derives the same bad set and re-check list, rebuilds its own bad cells, and only
+those cycles are all-gathered; up to four rounds, then the full path above.
+
 Positions and LBFGS state are replicated, so every rank runs the identical optimizer control
 flow, and the outputs are bitwise identical to the single-GPU `scvt_evaluate` for any rank
 count (tests/test_gpu_parity.py emulates 2/3/8 shards on one GPU).  Errors are agreed on by an
@@ -59,9 +64,37 @@ class CudaShardBackend:
         ctx = self.ev._ensure_ctx(z.shape[0])
         st = ctypes.c_int32(0)
         ctx.call("scvt_shard_moments", _lib.dptr(z), z.shape[0], shard, nshards,
-                 _lib.dptr(cyc_all), _lib.dptr(res_send), ctypes.byref(st),
-                 what="shard_moments")
+                 _lib.dptr(cyc_all) if cyc_all is not None else None, _lib.dptr(res_send),
+                 ctypes.byref(st), what="shard_moments")
         return int(st.value)
+
+    # ---- cycle reuse (include/scvt_b200.h: scvt_shard_recheck / plan / rebuild / install)
+    def recheck(self, z, shard, nshards, rnd, bad) -> bool:
+        ctx = self.ev._ensure_ctx(z.shape[0])
+        ready = ctypes.c_int32(0)
+        ctx.call("scvt_shard_recheck", _lib.dptr(z), z.shape[0], shard, nshards, rnd,
+                 _lib.dptr(bad), ctypes.byref(ready), what="shard_recheck")
+        return bool(ready.value)
+
+    def plan(self, n, nshards, bad_all):
+        ctx = self.ev._ensure_ctx(n)
+        counts = (ctypes.c_int64 * (nshards + 1))()
+        ctx.call("scvt_shard_plan", n, nshards, _lib.dptr(bad_all), counts, what="shard_plan")
+        return [int(c) for c in counts]
+
+    def rebuild(self, n, shard, nshards, cap, rows_send):
+        ctx = self.ev._ensure_ctx(n)
+        ctx.call("scvt_shard_rebuild", n, shard, nshards, cap, _lib.dptr(rows_send),
+                 what="shard_rebuild")
+
+    def install(self, n, rows, nrows):
+        ctx = self.ev._ensure_ctx(n)
+        ctx.call("scvt_shard_install", n, _lib.dptr(rows), nrows, what="shard_install")
+
+    def bad_buffer(self, n, device):
+        import torch
+
+        return torch.empty(n, dtype=torch.int32, device=device)
 
     def raise_status(self, status: int):
         ctx = self.ev._ensure_ctx(1)
@@ -107,6 +140,47 @@ def _all_gather(out, inp, group):
         dist.all_gather(parts, inp, group=group)
 
 
+REUSE_ROUNDS = 4   # certificate passes before a full rebuild (same as the single-GPU loop)
+
+
+def _reuse_cycles(backend, z, shards, nshards, bad, cyc_send, cyc_all, reduce_bad, gather_rows):
+    """The single-GPU reuse loop split at its exchanges (include/scvt_b200.h).  `shards` are
+    the shards this process runs (one under torch.distributed, all when emulating);
+    `reduce_bad(bad_of_each_shard) -> bad_all` and `gather_rows(rows_of_each_shard, cap)`
+    are the two collectives.  True when the held cycles were certified for z."""
+    n = z.shape[0]
+    if not hasattr(backend, "recheck"):
+        return False
+    for rnd in range(REUSE_ROUNDS):
+        local = []
+        for s in shards:
+            if not backend.recheck(z, s, nshards, rnd, bad):
+                return False                          # no previous cycles: identical on all ranks
+            local.append(bad.clone() if len(shards) > 1 else bad)
+        bad_all = reduce_bad(local)
+        counts = backend.plan(n, nshards, bad_all)
+        nbad = counts[nshards]
+        if nbad == 0:
+            return True
+        if nbad > (3 * n) // 4 or rnd == REUSE_ROUNDS - 1:
+            return False                              # churn too large: full rebuild
+        cap = max(counts[:nshards])
+        rows = []
+        for s in shards:
+            backend.rebuild(n, s, nshards, cap, cyc_send)
+            rows.append(cyc_send[:cap].clone() if len(shards) > 1 else cyc_send[:cap])
+        gather_rows(rows, cap)
+        backend.install(n, cyc_all, nshards * cap)
+    return False
+
+
+def _all_reduce_max(t, group):
+    import torch.distributed as dist
+
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
 def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=None,
                      q3=None, norms=None):
     """One evaluation on rank `rank` of `world` (collectives through torch.distributed)."""
@@ -114,10 +188,23 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
     import torch.distributed as dist
 
     n = z.shape[0]
-    cyc_send, cyc_all, res_send, res_all = backend.buffers(n, world, comm_device or z.device)
-    backend.cells(z, rank, world, cyc_send)
-    _all_gather(cyc_all, cyc_send, group)
-    status = backend.moments(z, rank, world, cyc_all, res_send)
+    dev = comm_device or z.device
+    cyc_send, cyc_all, res_send, res_all = backend.buffers(n, world, dev)
+    reused = False
+    if hasattr(backend, "recheck"):
+        bad = backend.bad_buffer(n, dev)
+
+        def gather_rows(rows, cap):
+            _all_gather(cyc_all[:world * cap], rows[0], group)
+
+        reused = _reuse_cycles(backend, z, [rank], world, bad, cyc_send, cyc_all,
+                               lambda local: _all_reduce_max(local[0], group), gather_rows)
+    if reused:
+        status = backend.moments(z, rank, world, None, res_send)
+    else:
+        backend.cells(z, rank, world, cyc_send)
+        _all_gather(cyc_all, cyc_send, group)
+        status = backend.moments(z, rank, world, cyc_all, res_send)
     st = torch.tensor([status], dtype=torch.int32, device=cyc_send.device)
     dist.all_reduce(st, op=dist.ReduceOp.MAX, group=group)   # everyone raises, or no one
     if int(st.item()):
@@ -134,12 +221,29 @@ def emulate_shards(backend, z, nshards: int, q3=None, norms=None):
     n = z.shape[0]
     cyc_send, cyc_all, res_send, res_all = backend.buffers(n, nshards, z.device)
     r = shard_rows(n, nshards)
-    for s in range(nshards):
-        backend.cells(z, s, nshards, cyc_send)
-        cyc_all[s * r:(s + 1) * r] = cyc_send
+    reused = False
+    if hasattr(backend, "recheck"):
+        bad = backend.bad_buffer(n, z.device)
+
+        def reduce_bad(local):
+            out = local[0]
+            for b in local[1:]:
+                out = out.maximum(b)
+            return out
+
+        def gather_rows(rows, cap):
+            for s, rw in enumerate(rows):
+                cyc_all[s * cap:(s + 1) * cap] = rw
+
+        reused = _reuse_cycles(backend, z, list(range(nshards)), nshards, bad, cyc_send,
+                               cyc_all, reduce_bad, gather_rows)
+    if not reused:
+        for s in range(nshards):
+            backend.cells(z, s, nshards, cyc_send)
+            cyc_all[s * r:(s + 1) * r] = cyc_send
     worst = 0
     for s in range(nshards):
-        worst = max(worst, backend.moments(z, s, nshards, cyc_all, res_send))
+        worst = max(worst, backend.moments(z, s, nshards, None if reused else cyc_all, res_send))
         res_all[s * r:(s + 1) * r] = res_send
     if worst:
         backend.raise_status(worst)

@@ -8,6 +8,8 @@ Tolerances (DECISIONS.md D7, the parity contract):
   * trajectories: positions and energies within 1e-10 relative.
 """
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -343,6 +345,52 @@ def test_cycle_reuse_matches_fresh_build(monkeypatch):
             monkeypatch.delenv("SCVT_NO_REUSE")
             assert np.array_equal(t_reuse, t_fresh)
             assert np.array_equal(t_fresh, O.convex_hull_delaunay(st.z.cpu().numpy()))
+
+
+def _reuse_counters(ev):
+    c = (ctypes.c_int64 * 12)()
+    ev.context.lib.scvt_profile_counters(ev.context.ptr, c, 0)
+    return {"reused_evals": c[8], "rebuilt": c[9], "passes": c[10]}
+
+
+@pytest.mark.parametrize("nshards", [2, 3, 8])
+def test_sharded_cycle_reuse_is_bitwise_identical(nshards):
+    """Sharded reuse (scvt_shard_recheck/plan/rebuild/install, shards emulated back to back
+    with the bad flags max-reduced and the rebuilt rows gathered slice by slice) along an
+    optimizer trajectory: every evaluation bitwise equal to single-GPU scvt_evaluate, and
+    the reuse path actually taken (certified evaluations, local rebuilds)."""
+    from paper_1709_06924_b200.parallel import ShardedMeshEvaluator, CudaShardBackend, emulate_shards
+
+    z0 = P.sample_by_density(P.density_preset("c4"), 40962, 0)
+    with _ev("c4", "7pt", 3) as ev, _ev("c4", "7pt", 3) as one:
+        be = CudaShardBackend(ev)
+        st = P.Minimizer(torch.from_numpy(z0).cuda(), "lloyd-plbfgs", one, 7)
+        emulate_shards(be, st.z, nshards)                  # full path: holds the cycles
+        for _ in range(4):
+            st.step()
+            sh = emulate_shards(be, st.z, nshards)
+            ref = one.evaluate_device(st.z)
+            assert sh.energy == ref.energy and sh.grad_norm == ref.grad_norm
+            assert torch.equal(sh.grad, ref.grad) and torch.equal(sh.first, ref.first)
+            assert torch.equal(sh.lloyd_diag, ref.lloyd_diag)
+        cnt = _reuse_counters(ev)
+    assert cnt["reused_evals"] == 4 and cnt["rebuilt"] > 0
+
+
+def test_sharded_trajectory_matches_single_gpu():
+    """A whole P-LBFGS run through ShardedMeshEvaluator (world size 1: the sharded code path
+    with reuse) is bitwise the single-GPU run."""
+    from paper_1709_06924_b200.parallel import ShardedMeshEvaluator
+
+    z0 = P.sample_by_density(P.density_preset("c3"), 10242 * 4, 0)
+    crit = P.StoppingCriteria(max_iterations=12)
+    with _ev("c3", "7pt", 3) as a, \
+            ShardedMeshEvaluator(P.density_preset("c3"), "7pt", subdivision=3) as b:
+        ra = P.minimize(z0, "lloyd-plbfgs", a, crit, corrections=7)
+        rb = P.minimize(z0, "lloyd-plbfgs", b, crit, corrections=7)
+    assert np.array_equal(np.asarray(ra.points), np.asarray(rb.points))
+    assert [h.energy for h in ra.records] == [h.energy for h in rb.records]
+    assert ra.fevals == rb.fevals and ra.reason == rb.reason
 
 
 def _oracle_cells(z, tri, density_name, rule, depth, gens):

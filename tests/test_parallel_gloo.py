@@ -18,11 +18,82 @@ import oracle as O
 from paper_1709_06924_b200.parallel import CYC_ROW, RES_ROW, shard_range, shard_rows, sharded_evaluate
 
 
+def _true_cycles(z):
+    """Delaunay cycles of every generator (Qhull via the oracle), CCW from the min id."""
+    n = len(z)
+    nxt = [dict() for _ in range(n)]
+    for a, b, c in O.convex_hull_delaunay(z):
+        nxt[a][b] = c
+        nxt[b][c] = a
+        nxt[c][a] = b
+    out = []
+    for i in range(n):
+        start = min(nxt[i])
+        cyc, cur = [], start
+        while True:
+            cyc.append(cur)
+            cur = nxt[i][cur]
+            if cur == start:
+                break
+        out.append(cyc)
+    return out
+
+
 class NumpyShardBackend:
     def __init__(self, density="const", rule="4pt", fail_on=None):
         self.density = O.density_for(density)
         self.rule = O.RULES[rule]
         self.fail_on = fail_on
+        self.held = None          # cycles of the last evaluation (all generators)
+        self.rounds = []          # bad-set sizes of the reuse rounds (test introspection)
+
+    # ---- cycle reuse, same protocol as CudaShardBackend (certificate stand-in: the held
+    # cycle differs from the Delaunay cycle at the new positions)
+    def bad_buffer(self, n, device):
+        return torch.zeros(n, dtype=torch.int32)
+
+    def recheck(self, z, shard, nshards, rnd, bad):
+        zz = z.numpy()
+        n = len(zz)
+        if rnd == 0:
+            if self.held is None or len(self.held) != n:
+                return False
+            self.truth = _true_cycles(zz)
+        lo, hi = shard_range(n, shard, nshards)
+        bad.zero_()
+        for i in range(lo, hi):
+            if rnd > 0 and not self.recheck_set[i]:
+                continue
+            if self.held[i] != self.truth[i]:
+                bad[i] = 1
+                bad[self.held[i]] = 1
+        return True
+
+    def plan(self, n, nshards, bad_all):
+        b = np.nonzero(bad_all.numpy())[0]
+        self.bad_set = b
+        rs = np.zeros(n, dtype=bool)
+        rs[b] = True
+        for i in b:
+            rs[self.held[i]] = True
+        self.recheck_set = rs
+        self.rounds.append(len(b))
+        cap = shard_rows(n, nshards)
+        return [int(np.sum((b >= s * cap) & (b < (s + 1) * cap))) for s in range(nshards)] + [len(b)]
+
+    def rebuild(self, n, shard, nshards, cap, rows_send):
+        lo, hi = shard_range(n, shard, nshards)
+        rows_send[:cap].fill_(-1)
+        for q, i in enumerate(i for i in self.bad_set if lo <= i < hi):
+            cyc = self.truth[i]
+            rows_send[q, 0] = int(i)
+            rows_send[q, 1] = len(cyc)
+            rows_send[q, 2:2 + len(cyc)] = torch.tensor(cyc, dtype=torch.int32)
+
+    def install(self, n, rows, nrows):
+        for r in rows[:nrows].numpy():
+            if r[0] >= 0:
+                self.held[r[0]] = [int(v) for v in r[2:2 + r[1]]]
 
     def buffers(self, n, nshards, device):
         r = shard_rows(n, nshards)
@@ -57,11 +128,20 @@ class NumpyShardBackend:
     def moments(self, z, shard, nshards, cyc_all, res_send):
         zz = z.numpy()
         n = len(zz)
-        rows = cyc_all.numpy()
-        rows = rows[rows[:, 0] >= 0]
-        ids = np.sort(rows[:, 0])
-        if not np.array_equal(ids, np.arange(n)):
-            return 1 << 4                                   # ST_INCONSISTENT
+        if cyc_all is None:                                 # cycles certified by reuse
+            rows = np.full((n, CYC_ROW), -1, dtype=np.int64)
+            for i, cyc in enumerate(self.held):
+                rows[i, 0], rows[i, 1] = i, len(cyc)
+                rows[i, 2:2 + len(cyc)] = cyc
+        else:
+            rows = cyc_all.numpy()
+            rows = rows[rows[:, 0] >= 0]
+            ids = np.sort(rows[:, 0])
+            if not np.array_equal(ids, np.arange(n)):
+                return 1 << 4                               # ST_INCONSISTENT
+            self.held = [None] * n
+            for r in rows:
+                self.held[r[0]] = [int(v) for v in r[2:2 + r[1]]]
         tris = []
         for r in rows:
             i, d = r[0], r[1]
@@ -113,24 +193,34 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, fail_on, out):
+def _moved(z0, scale=0.001, seed=9):
+    rng = np.random.default_rng(seed)
+    z = z0 + scale * rng.standard_normal(z0.shape)
+    return z / np.linalg.norm(z, axis=1, keepdims=True)
+
+
+def _worker(rank, world, port, fail_on, out, second):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        z = torch.from_numpy(O.random_sphere_points(1202, 5))
+        z0 = O.random_sphere_points(1202, 5)
+        be = NumpyShardBackend(fail_on=fail_on)
         try:
-            r = sharded_evaluate(NumpyShardBackend(fail_on=fail_on), z, rank, world)
-            out[rank] = {"energy": r["energy"], "first": r["first"], "covered": r["covered"]}
+            r = sharded_evaluate(be, torch.from_numpy(z0), rank, world)
+            if second:        # same backend, moved points: the reuse rounds
+                r = sharded_evaluate(be, torch.from_numpy(_moved(z0)), rank, world)
+            out[rank] = {"energy": r["energy"], "first": r["first"], "covered": r["covered"],
+                         "rounds": list(be.rounds)}
         except RuntimeError as exc:
             out[rank] = {"error": str(exc)}
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, fail_on=None):
+def _run(world, fail_on=None, second=False):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), fail_on, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), fail_on, out, second), nprocs=world, join=True)
     return dict(out)
 
 
@@ -149,3 +239,19 @@ def test_gloo_two_ranks_match_single_process():
 def test_gloo_error_on_one_rank_raises_on_all():
     out = _run(2, fail_on=1)
     assert "error" in out[0] and "error" in out[1]
+
+
+def test_gloo_cycle_reuse_rounds():
+    """Second evaluation at moved points: the reuse protocol (per-shard certificate, max
+    all-reduce of the bad flags, identical plan on both ranks, rebuilt rows all-gathered)
+    must end with the Delaunay cycles of the new positions on both ranks."""
+    out = _run(2, second=True)
+    z = _moved(O.random_sphere_points(1202, 5))
+    ref = O.Evaluator(O.density_for("const"), "4pt", 0).evaluate(z)
+    assert out[0]["rounds"] == out[1]["rounds"]
+    assert out[0]["rounds"][0] > 0 and out[0]["rounds"][-1] == 0   # some churn, then certified
+    for rank in (0, 1):
+        assert out[rank]["covered"] == 1202
+        np.testing.assert_allclose(out[rank]["first"], ref.first, rtol=0, atol=1e-15)
+        assert abs(out[rank]["energy"] - ref.energy) <= 1e-14 * ref.energy
+    np.testing.assert_array_equal(out[0]["first"], out[1]["first"])
