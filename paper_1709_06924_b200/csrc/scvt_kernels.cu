@@ -79,12 +79,22 @@ __global__ void __launch_bounds__(CELL_WARPS * 32, 4)
 k_cells_warp(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
              const int* __restrict__ list_n, int* __restrict__ nbr, int* __restrict__ deg,
              int* __restrict__ status, int* __restrict__ stats,
-             unsigned long long* __restrict__ diag) {
+             unsigned long long* __restrict__ diag, int* __restrict__ queue = nullptr) {
     __shared__ double s_c2[CELL_WARPS][WCAND];
     __shared__ int s_j[CELL_WARPS][WCAND];
     __shared__ int s_p[CELL_WARPS][WCAND];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t idx = (int64_t)blockIdx.x * CELL_WARPS + w;
+    // a host-sized grid runs one trip; a fixed (resident) grid serves a list whose length
+    // only the device knows by pulling cells from an atomic queue (dynamic balance: cell
+    // costs vary by orders of magnitude)
+    auto next = [&](int64_t cur) -> int64_t {
+        if (!queue) return cur < 0 ? (int64_t)blockIdx.x * CELL_WARPS + w
+                                   : cur + (int64_t)gridDim.x * CELL_WARPS;
+        int t = 0;
+        if (lane == 0) t = atomicAdd(queue, 1);
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
+    for (int64_t idx = next(-1);; idx = next(idx)) {
     int64_t p;
     if (list) {                 // rebuild of a compacted list of sorted slots
         if (idx >= *list_n) return;
@@ -129,6 +139,8 @@ k_cells_warp(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
             atomicMax(&diag[9], (unsigned long long)cs.passes);
         }
     }
+    __syncwarp();
+    }
 }
 
 // Fallback: one thread per generator the warp builder handed back (deg == -1).
@@ -136,7 +148,7 @@ __global__ void __launch_bounds__(CELL_THREADS)
 k_cells(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
         const int* __restrict__ list_n, int* __restrict__ nbr, int* __restrict__ deg,
         int* __restrict__ status, int* __restrict__ stats) {
-    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x;; idx += gridDim.x * blockDim.x) {
     int p;
     if (list) {
         if (idx >= *list_n) return;
@@ -146,7 +158,7 @@ k_cells(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
         if (p >= p_hi) return;
     }
     int i = g.ids[p];
-    if (deg[i] != -1) return;
+    if (deg[i] != -1) continue;
     V3 zi = v3(g.zs[4 * (int64_t)p], g.zs[4 * (int64_t)p + 1], g.zs[4 * (int64_t)p + 2]);
     Poly P, T;
     CellStats cs;
@@ -159,6 +171,7 @@ k_cells(GridView g, int p_lo, int p_hi, const int* __restrict__ list,
         atomicMax(&stats[0], d);
     }
     if (cs.tie_breaks) atomicAdd(&stats[4], cs.tie_breaks);
+    }
 }
 
 __device__ __forceinline__ int find_in_cycle(const int* __restrict__ row, int d, int x) {
@@ -189,20 +202,20 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
                          uint8_t* __restrict__ amb, int* __restrict__ status,
                          int* __restrict__ stats, int mode, int* __restrict__ bad,
                          int* __restrict__ nbad) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x;; idx += gridDim.x * blockDim.x) {
     int p;
     if (list) {                 // re-certification of a compacted list of sorted slots
-        const int idx = blockIdx.x * blockDim.x + threadIdx.x;
         if (idx >= *list_n) return;
         p = list[idx];
-        if (p < p_lo || p >= p_hi) return;     // sharded re-check: owned slots only
+        if (p < p_lo || p >= p_hi) continue;   // sharded re-check: owned slots only
     } else {
-        p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
+        p = p_lo + idx;
         if (p >= p_hi) return;
     }
     int i = ids[p];
     int d = deg[i];
     const int* row = nbr + (int64_t)i * MAXDEG;
-    if (d < 3 || d > MAXDEG) { mark_bad(mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1); return; }
+    if (d < 3 || d > MAXDEG) { mark_bad(mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1); continue; }
     V3 zi = load3(z, i);
     int namb = 0;
     for (int t = 0; t < d; ++t) {
@@ -225,6 +238,7 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
         if (sgn > 0) mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, c);
     }
     if (namb) atomicAdd(&stats[3], namb);
+    }
 }
 
 __global__ void k_flag_slots(int n, const int* __restrict__ ids, const int* __restrict__ bad,
@@ -239,14 +253,14 @@ __global__ void k_flag_slots(int n, const int* __restrict__ ids, const int* __re
 __global__ void k_mark_recheck(const int* __restrict__ list, const int* __restrict__ list_n,
                                const int* __restrict__ ids, const int* __restrict__ nbr,
                                const int* __restrict__ deg, int* __restrict__ recheck) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= *list_n) return;
-    const int i = ids[list[idx]];
-    recheck[i] = 1;
-    const int d = deg[i];
-    if (d < 3 || d > MAXDEG) return;
-    const int* row = nbr + (int64_t)i * MAXDEG;
-    for (int t = 0; t < d; ++t) recheck[row[t]] = 1;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < *list_n; idx += gridDim.x * blockDim.x) {
+        const int i = ids[list[idx]];
+        recheck[i] = 1;
+        const int d = deg[i];
+        if (d < 3 || d > MAXDEG) continue;
+        const int* row = nbr + (int64_t)i * MAXDEG;
+        for (int t = 0; t < d; ++t) recheck[row[t]] = 1;
+    }
 }
 
 // incidence CSR in bucket (spatial) order: sorted slot p -> generator ids[p]
@@ -1048,6 +1062,9 @@ struct scvt_ctx {
     int* d_status = nullptr;           // [1 + 4 stats]
     double* h_scal = nullptr;          // pinned [MAX_SLOTS]
     int* h_status = nullptr;           // pinned [8]
+    int* h_small = nullptr;            // pinned [16]: small readbacks (reuse counts)
+    int* d_rcount = nullptr;           // per-round bad counts of the chained reuse rounds
+    int* d_queue = nullptr;            // work queue of the fixed-grid cell rebuilds
     // LBFGS history
     double* d_S = nullptr; double* d_Y = nullptr;   // [m][3 n_max]
     double* d_alpha = nullptr;                      // [m]
@@ -1295,46 +1312,86 @@ bool reuse_enabled() { return getenv("SCVT_NO_REUSE") == nullptr; }
 // Reuse the previous evaluation's cycles when they are still a certified Delaunay
 // triangulation of the new positions; rebuild (grid method) only the cells of failing
 // triangles/quads, re-certify, and escalate to a full rebuild when churn is large.
+// fixed grids for lists whose length only the device knows: the resident capacity
+constexpr int SPEC_CELL_BLOCKS = 148 * 4;     // k_cells_warp: 4 CTAs x 4 warps per SM
+constexpr int SPEC_BLOCKS = 148 * 8;          // thread-per-item kernels
+
+// One rebuild round on the device, no host round trip: the bad cells of the last pass are
+// compacted, their re-check set marked, rebuilt (grid-stride over the device count), and the
+// re-check list certified; the new bad count lands in d_nbad.
+// nbad_host >= 0: the bad count is known on the host (exact grids, hardware block
+// scheduling); -1: device-only count (resident grid pulling from a work queue).
+int reuse_round_device(scvt_ctx* ctx, const double* z, int64_t n, const GridView& g,
+                       int nbad_host) {
+    cudaStream_t s = ctx->stream;
+    TRY(compact_slots(ctx, n, ctx->d_bad, ctx->d_nbad));
+    CK(cudaMemsetAsync(ctx->d_recheck, 0, n * sizeof(int), s));
+    const bool known = nbad_host >= 0;
+    const int nb = known ? std::max(nbad_host, 1) : 0;
+    k_mark_recheck<<<known ? blocks_for(nb, 256) : SPEC_BLOCKS, 256, 0, s>>>(
+        ctx->d_list, ctx->d_nbad, ctx->d_ids, ctx->d_nbr, ctx->d_deg, ctx->d_recheck);
+    LAUNCHED();
+    if (known) {
+        k_cells_warp<<<blocks_for(nb, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
+            g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+            ctx->d_status + 8, ctx->prof ? ctx->d_diag : nullptr);
+    } else {
+        CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int), s));
+        k_cells_warp<<<SPEC_CELL_BLOCKS, CELL_WARPS * 32, 0, s>>>(
+            g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+            ctx->d_status + 8, ctx->prof ? ctx->d_diag : nullptr, ctx->d_queue);
+    }
+    LAUNCHED();
+    k_cells<<<known ? blocks_for(nb, CELL_THREADS) : SPEC_BLOCKS, CELL_THREADS, 0, s>>>(
+        g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
+        ctx->d_status + 8);
+    LAUNCHED();
+    TRY(compact_slots(ctx, n, ctx->d_recheck, ctx->d_nlist));
+    CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
+    CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
+    k_verify<<<SPEC_BLOCKS, 128, 0, s>>>(z, ctx->d_ids, 0, (int)n, ctx->d_list, ctx->d_nlist,
+                                          ctx->d_nbr, ctx->d_deg, ctx->d_amb, ctx->d_status,
+                                          ctx->d_status + 8, 1, ctx->d_bad, ctx->d_nbad);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+// Reuse the previous evaluation's cycles when they are still a certified Delaunay
+// triangulation of the new positions; rebuild (grid method) only the cells of failing
+// triangles, re-certify those cells and their previous neighbours, at most 4 passes, and
+// escalate to a full rebuild when churn is large.  Pass 0 (every cell) is read back on the
+// host (certified evaluations stop there); passes 1-2 with their rebuild rounds are chained
+// on the device and read back once.
 int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView& g, bool* done) {
     cudaStream_t s = ctx->stream;
     *done = false;
-    int nlist = (int)n;                          // cells the next pass must certify
-    for (int round = 0; round < 4; ++round) {
-        CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
-        CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
-        if (round == 0) {
-            TRY(verify_range(ctx, z, 0, n, 1));
-        } else if (nlist > 0) {
-            k_verify<<<blocks_for(nlist, 128), 128, 0, s>>>(
-                z, ctx->d_ids, 0, (int)n, ctx->d_list, ctx->d_nlist, ctx->d_nbr, ctx->d_deg,
-                ctx->d_amb, ctx->d_status, ctx->d_status + 8, 1, ctx->d_bad, ctx->d_nbad);
-            LAUNCHED();
-        }
-        int nbad = 0;
-        CK(cudaMemcpyAsync(&nbad, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        ctx->reuse_stats[0] += 1;                   // certificate passes run
-        ctx->reuse_stats[1] += nbad;
-        if (nbad == 0) { *done = true; return SCVT_OK; }
-        if (nbad > (3 * n) / 4 || round == 3) return SCVT_OK;   // caller rebuilds everything
-        // the bad cells' slots; what the next pass must re-certify; then rebuild them
-        TRY(compact_slots(ctx, n, ctx->d_bad, ctx->d_nbad));
-        CK(cudaMemsetAsync(ctx->d_recheck, 0, n * sizeof(int), s));
-        k_mark_recheck<<<blocks_for(nbad, 256), 256, 0, s>>>(ctx->d_list, ctx->d_nbad, ctx->d_ids,
-                                                              ctx->d_nbr, ctx->d_deg, ctx->d_recheck);
-        LAUNCHED();
-        k_cells_warp<<<blocks_for(nbad, CELL_WARPS), CELL_WARPS * 32, 0, s>>>(
-            g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
-            ctx->d_status + 8, ctx->prof ? ctx->d_diag : nullptr);
-        LAUNCHED();
-        k_cells<<<blocks_for(nbad, CELL_THREADS), CELL_THREADS, 0, s>>>(
-            g, 0, (int)n, ctx->d_list, ctx->d_nbad, ctx->d_nbr, ctx->d_deg, ctx->d_status,
-            ctx->d_status + 8);
-        LAUNCHED();
-        TRY(compact_slots(ctx, n, ctx->d_recheck, ctx->d_nlist));
-        CK(cudaMemcpyAsync(&nlist, ctx->d_nlist, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+    CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
+    CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
+    TRY(verify_range(ctx, z, 0, n, 1));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int nbad = ctx->h_small[0];
+    ctx->reuse_stats[0] += 1;                       // certificate passes run
+    ctx->reuse_stats[1] += nbad;
+    if (nbad == 0) { *done = true; return SCVT_OK; }
+    if (nbad > (3 * n) / 4) return SCVT_OK;         // caller rebuilds everything
+    for (int r = 0; r < 2; ++r) {
+        TRY(reuse_round_device(ctx, z, n, g, r == 0 ? nbad : -1));
+        CK(cudaMemcpyAsync(ctx->d_rcount + r, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToDevice, s));
     }
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_rcount, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->reuse_stats[0] += 2;
+    ctx->reuse_stats[1] += ctx->h_small[0] + ctx->h_small[1];
+    nbad = ctx->h_small[1];
+    if (nbad == 0) { *done = true; return SCVT_OK; }
+    if (nbad > (3 * n) / 4) return SCVT_OK;
+    TRY(reuse_round_device(ctx, z, n, g, nbad));    // fourth and last pass
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->reuse_stats[0] += 1;
+    ctx->reuse_stats[1] += ctx->h_small[0];
+    if (ctx->h_small[0] == 0) *done = true;
     return SCVT_OK;
 }
 
@@ -1664,7 +1721,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_status, 16);
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
-    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1);
+    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -1673,7 +1730,8 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     {
         cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_SLOTS * sizeof(double));
         cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
-        if (e1 != cudaSuccess || e2 != cudaSuccess)
+        cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 16 * sizeof(int));
+        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
             return bail(fail(ctx, SCVT_ERR_CUDA, "cudaMallocHost failed"));
     }
     // CUB temp storage: max of radix sort (n) and scan (n+1)
@@ -1728,7 +1786,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
-                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt,
+                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
@@ -1741,6 +1799,7 @@ int scvt_destroy(scvt_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
     if (ctx->h_status) cudaFreeHost(ctx->h_status);
+    if (ctx->h_small) cudaFreeHost(ctx->h_small);
     delete ctx;
     return SCVT_OK;
 }
