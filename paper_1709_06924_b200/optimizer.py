@@ -24,7 +24,7 @@ from .errors import (
     LineSearchFailure,
     NonDescentError,
 )
-from .pipeline import EvalResult, MeshEvaluator
+from .pipeline import EvalResult, MeshEvaluator, to_numpy
 
 logger = logging.getLogger(__name__)
 
@@ -209,11 +209,14 @@ class _DeviceOps:
         self.ctx.call("scvt_normalize_rows", _lib.dptr(z), self.n)
 
 
-def _to_host(res: EvalResult) -> EvalResult:
-    return EvalResult(energy=res.energy, grad=res.grad.cpu().numpy(), grad_norm=res.grad_norm,
-                      lloyd_diag=res.lloyd_diag.cpu().numpy(), first=res.first.cpu().numpy(),
-                      migration=res.migration, mass=res.mass.cpu().numpy(),
-                      obtuse_count=res.obtuse_count)
+def _to_host(res: EvalResult, z=None):
+    """NumPy copy of a device result (and of the positions `z`), one pinned transfer."""
+    ts = [res.grad, res.lloyd_diag, res.first, res.mass] + ([z] if z is not None else [])
+    arr = to_numpy(*ts)
+    out = EvalResult(energy=res.energy, grad=arr[0], grad_norm=res.grad_norm,
+                     lloyd_diag=arr[1], first=arr[2], migration=res.migration, mass=arr[3],
+                     obtuse_count=res.obtuse_count)
+    return (out, arr[4]) if z is not None else out
 
 
 class Minimizer:
@@ -342,9 +345,9 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
             break
     st.torch.cuda.current_stream().synchronize()
     wall = time.perf_counter() - t0
-    return MinimizeResult(points=st.z.cpu().numpy(), records=records, reason=reason,
-                          fevals=st.fevals, resets=st.resets, wall_time=wall,
-                          final=_to_host(st.res))
+    final, points = _to_host(st.res, st.z)
+    return MinimizeResult(points=points, records=records, reason=reason,
+                          fevals=st.fevals, resets=st.resets, wall_time=wall, final=final)
 
 
 def lloyd_step(points, first_moments) -> np.ndarray:

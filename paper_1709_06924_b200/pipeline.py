@@ -31,6 +31,18 @@ def _torch():
     return torch
 
 
+def to_numpy(*tensors):
+    """Device tensors -> NumPy arrays through pinned host tensors (torch's caching host
+    allocator: full PCIe rate, no per-call page-locking after the first), one sync.  Each
+    array keeps its pinned tensor alive."""
+    torch = _torch()
+    outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in tensors]
+    for o, t in zip(outs, tensors):
+        o.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return [o.numpy() for o in outs]
+
+
 @dataclass
 class EvalResult:
     """optimizer.py:66-76 (+ mass).  Arrays are NumPy or CUDA tensors (see module doc)."""
@@ -225,10 +237,8 @@ class MeshEvaluator:
         z, host = self._as_device(points)
         r = self.evaluate_device(z)
         if host:
-            r.grad = r.grad.cpu().numpy()
-            r.first = r.first.cpu().numpy()
-            r.mass = r.mass.cpu().numpy()
-            r.lloyd_diag = r.lloyd_diag.cpu().numpy()
+            r.grad, r.first, r.mass, r.lloyd_diag = to_numpy(r.grad, r.first, r.mass,
+                                                             r.lloyd_diag)
         return r
 
     def evaluate_on_triangles(self, points, triangles) -> EvalResult:
@@ -249,8 +259,8 @@ class MeshEvaluator:
         r = EvalResult(energy=float(sc[0]), grad=grad, grad_norm=float(sc[1]), lloyd_diag=diag,
                        first=first, mass=mass, obtuse_count=int(sc[2]))
         if host:
-            r.grad, r.first = r.grad.cpu().numpy(), r.first.cpu().numpy()
-            r.mass, r.lloyd_diag = r.mass.cpu().numpy(), r.lloyd_diag.cpu().numpy()
+            r.grad, r.first, r.mass, r.lloyd_diag = to_numpy(r.grad, r.first, r.mass,
+                                                             r.lloyd_diag)
         return r
 
     def triangulate_device(self, z):
