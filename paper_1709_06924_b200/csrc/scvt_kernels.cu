@@ -45,6 +45,7 @@ constexpr int QUAD_THREADS = 128;
 #endif
 constexpr int CELL_THREADS = 64;
 constexpr int MAX_SLOTS = 64;        // partial-sum slots
+constexpr int MAX_SHARDS = 256;      // sharded evaluation: ranks per evaluation
 
 // ------------------------------------------------------------------ grid kernels
 __global__ void k_bucket_keys(const double* __restrict__ z, int n, int G,
@@ -449,6 +450,26 @@ __global__ void k_pack_list(const int* __restrict__ list, const int* __restrict_
 }
 
 __global__ void k_set_int(int* p, int v) { *p = v; }
+
+// per-shard counts of an ascending slot list (shard s owns slots [s*cap, (s+1)*cap)):
+// counts[s] = lower_bound((s+1)*cap) - lower_bound(s*cap); counts[nshards] = total
+__global__ void k_shard_counts(const int* __restrict__ list, const int* __restrict__ list_n,
+                               int nshards, int64_t cap, int* __restrict__ counts) {
+    __shared__ int bound[MAX_SHARDS + 1];
+    const int total = *list_n;
+    for (int b = threadIdx.x; b <= nshards; b += blockDim.x) {
+        const int64_t key = (int64_t)b * cap;
+        int lo = 0, hi = total;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (list[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        bound[b] = b == nshards ? total : lo;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nshards; b += blockDim.x) counts[b] = bound[b + 1] - bound[b];
+    if (threadIdx.x == 0) counts[nshards] = total;
+}
 
 // owned slots: fixed-order incidence sums packed as exchange rows
 __global__ void k_gather_pack(int p_lo, int cnt, int cap, const int* __restrict__ ids,
@@ -1065,6 +1086,8 @@ struct scvt_ctx {
     int* h_small = nullptr;            // pinned [16]: small readbacks (reuse counts)
     int* d_rcount = nullptr;           // per-round bad counts of the chained reuse rounds
     int* d_queue = nullptr;            // work queue of the fixed-grid cell rebuilds
+    int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
+    int* h_counts = nullptr;           // pinned copy
     // LBFGS history
     double* d_S = nullptr; double* d_Y = nullptr;   // [m][3 n_max]
     double* d_alpha = nullptr;                      // [m]
@@ -1721,7 +1744,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_status, 16);
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
-    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1);
+    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_counts, MAX_SHARDS + 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -1731,7 +1754,8 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_SLOTS * sizeof(double));
         cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
         cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 16 * sizeof(int));
-        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+        cudaError_t e4 = cudaMallocHost((void**)&ctx->h_counts, (MAX_SHARDS + 1) * sizeof(int));
+        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess)
             return bail(fail(ctx, SCVT_ERR_CUDA, "cudaMallocHost failed"));
     }
     // CUB temp storage: max of radix sort (n) and scan (n+1)
@@ -1786,7 +1810,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
-                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue,
+                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_counts,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
@@ -1800,6 +1824,7 @@ int scvt_destroy(scvt_ctx* ctx) {
     if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
     if (ctx->h_status) cudaFreeHost(ctx->h_status);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
     delete ctx;
     return SCVT_OK;
 }
@@ -1939,17 +1964,12 @@ int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
     CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
     if (round == 0) {
         TRY(verify_range(ctx, z, lo, hi, 1));
-    } else {
-        int nl = 0;
-        CK(cudaMemcpyAsync(&nl, ctx->d_nlist2, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (nl > 0) {
-            k_verify<<<blocks_for(nl, 128), 128, 0, s>>>(
-                z, ctx->d_ids, (int)lo, (int)hi, ctx->d_list2, ctx->d_nlist2, ctx->d_nbr,
-                ctx->d_deg, ctx->d_amb, ctx->d_status, ctx->d_status + 8, 1, ctx->d_bad,
-                ctx->d_nbad);
-            LAUNCHED();
-        }
+    } else {                    // the plan's re-check list; its length stays on the device
+        k_verify<<<SPEC_BLOCKS, 128, 0, s>>>(
+            z, ctx->d_ids, (int)lo, (int)hi, ctx->d_list2, ctx->d_nlist2, ctx->d_nbr,
+            ctx->d_deg, ctx->d_amb, ctx->d_status, ctx->d_status + 8, 1, ctx->d_bad,
+            ctx->d_nbad);
+        LAUNCHED();
     }
     CK(cudaMemcpyAsync(bad_out, ctx->d_bad, n * sizeof(int), cudaMemcpyDeviceToDevice, s));
     *ready_host = 1;
@@ -1959,39 +1979,36 @@ int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
 int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_all,
                     int64_t* counts_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
-    if (nshards < 1) return fail(ctx, SCVT_ERR_CONFIG, "bad shard count %d", nshards);
+    if (nshards < 1 || nshards > MAX_SHARDS)
+        return fail(ctx, SCVT_ERR_CONFIG, "bad shard count %d (max %d)", nshards, MAX_SHARDS);
     cudaStream_t s = ctx->stream;
     CK(cudaMemcpyAsync(ctx->d_bad, bad_all, n * sizeof(int), cudaMemcpyDeviceToDevice, s));
     TRY(compact_slots(ctx, n, ctx->d_bad, ctx->d_nbad));       // bad slots, ascending
-    int nbad = 0;
-    CK(cudaMemcpyAsync(&nbad, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    // re-check set of the next round (bad cells and their current neighbours) -> d_list2
+    CK(cudaMemsetAsync(ctx->d_recheck, 0, n * sizeof(int), s));
+    k_mark_recheck<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_list, ctx->d_nbad, ctx->d_ids, ctx->d_nbr,
+                                                ctx->d_deg, ctx->d_recheck);
+    LAUNCHED();
+    k_flag_slots<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_recheck,
+                                                    ctx->d_slotflag);
+    LAUNCHED();
+    size_t tb = ctx->cub_bytes;
+    thrust::counting_iterator<int> it(0);
+    CK(cub::DeviceSelect::Flagged(ctx->d_cub, tb, it, ctx->d_slotflag, ctx->d_list2,
+                                  ctx->d_nlist2, (int)n, s));
+    // bad cells per shard: boundaries of the ascending slot list, found on the device
+    k_shard_counts<<<1, 256, 0, s>>>(ctx->d_list, ctx->d_nbad, nshards,
+                                     scvt_shard_rows(n, nshards), ctx->d_counts);
+    LAUNCHED();
+    CK(cudaMemcpyAsync(ctx->h_counts, ctx->d_counts, (nshards + 1) * sizeof(int),
+                       cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const int nbad = ctx->h_counts[nshards];
     ctx->reuse_stats[0] += 1;
     ctx->reuse_stats[1] += nbad;
-    ctx->plan_counts.assign(nshards, 0);
-    if (nbad > 0) {
-        // re-check set of the next round, and the bad cells per shard (slot ranges)
-        CK(cudaMemsetAsync(ctx->d_recheck, 0, n * sizeof(int), s));
-        k_mark_recheck<<<blocks_for(nbad, 256), 256, 0, s>>>(ctx->d_list, ctx->d_nbad, ctx->d_ids,
-                                                              ctx->d_nbr, ctx->d_deg, ctx->d_recheck);
-        LAUNCHED();
-        std::vector<int> slots(nbad);
-        CK(cudaMemcpyAsync(slots.data(), ctx->d_list, nbad * sizeof(int), cudaMemcpyDeviceToHost, s));
-        // compact the re-check flags into d_list2 (d_list stays: the shards' rebuild lists)
-        k_flag_slots<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_ids, ctx->d_recheck,
-                                                        ctx->d_slotflag);
-        LAUNCHED();
-        size_t tb = ctx->cub_bytes;
-        thrust::counting_iterator<int> it(0);
-        CK(cub::DeviceSelect::Flagged(ctx->d_cub, tb, it, ctx->d_slotflag, ctx->d_list2,
-                                      ctx->d_nlist2, (int)n, s));
-        CK(cudaStreamSynchronize(s));
-        const int64_t cap = scvt_shard_rows(n, nshards);
-        for (int p : slots) ctx->plan_counts[std::min<int64_t>(p / cap, nshards - 1)] += 1;
-    } else {
-        ctx->reuse_stats[2] += 1;                 // certified: the evaluation reuses all cycles
-    }
-    for (int k = 0; k < nshards; ++k) counts_host[k] = ctx->plan_counts[k];
+    if (nbad == 0) ctx->reuse_stats[2] += 1;   // certified: the evaluation reuses all cycles
+    ctx->plan_counts.assign(ctx->h_counts, ctx->h_counts + nshards);
+    for (int k = 0; k < nshards; ++k) counts_host[k] = ctx->h_counts[k];
     counts_host[nshards] = nbad;
     return SCVT_OK;
 }
