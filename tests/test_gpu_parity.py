@@ -460,3 +460,32 @@ def test_run_ladder_matches_reference(gold):
         assert res.levels[li].result.reason == str(g[f"level{li}_reason"])
     assert rel(res.points, g["final_z"]) <= 1e-10
     assert np.array_equal(res.triangulation.triangles, g["triangles"])
+
+
+def _unit(a):
+    return a / np.linalg.norm(a, axis=1, keepdims=True)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", ["cluster", "band", "icosahedral"])
+def test_adversarial_triangulations_match_qhull(case):
+    """Cell builder + certificate on inputs that stress it (tools/stress_cells.py): a dense
+    cluster (256x the background density) inside a sparse background, a thin great-circle band
+    (huge elongated cells), the exact icosahedral bisection lattice at N=163,842."""
+    rng = np.random.default_rng(3)
+    if case == "cluster":
+        c = _unit(np.array([[0.3, -0.5, 0.8]]))
+        t = rng.standard_normal((65536, 3)) * 0.05
+        z = np.vstack([_unit(c + t - (t @ c.T) * c), P.random_sphere_points(200000, 1)])
+    elif case == "band":
+        b = rng.standard_normal((300000, 3))
+        b[:, 2] *= 0.01
+        z = _unit(b)
+    else:
+        z = P.icosahedron_vertices()
+        with _ev("const", "4pt", 0) as ev:
+            while len(z) < 163842:
+                z = P.bisect(z, ev.triangulation(z))
+    with _ev("const", "4pt", 0) as ev:
+        t = ev.triangulation(z).triangles
+    assert np.array_equal(t, O.convex_hull_delaunay(z))
