@@ -134,10 +134,16 @@ def _all_gather(out, inp, group):
 
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, inp, group=group)
-    else:                                   # gloo (CPU tests): list form
-        r = inp.shape[0]
-        parts = [out[k * r:(k + 1) * r] for k in range(out.shape[0] // r)]
-        dist.all_gather(parts, inp, group=group)
+        return
+    # gloo (CPU tests; CUDA tensors staged through host memory): list form
+    host = out.device.type != "cpu"
+    src = inp.cpu() if host else inp
+    dst = out.cpu() if host else out
+    r = src.shape[0]
+    parts = [dst[k * r:(k + 1) * r] for k in range(dst.shape[0] // r)]
+    dist.all_gather(parts, src, group=group)
+    if host:
+        out.copy_(dst)
 
 
 REUSE_ROUNDS = 4   # certificate passes before a full rebuild (same as the single-GPU loop)
@@ -177,6 +183,11 @@ def _reuse_cycles(backend, z, shards, nshards, bad, cyc_send, cyc_all, reduce_ba
 def _all_reduce_max(t, group):
     import torch.distributed as dist
 
+    if dist.get_backend(group) != "nccl" and t.device.type != "cpu":
+        h = t.cpu()                          # gloo: staged through host memory
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(h)
+        return t
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t
 
@@ -185,7 +196,6 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
                      q3=None, norms=None):
     """One evaluation on rank `rank` of `world` (collectives through torch.distributed)."""
     import torch
-    import torch.distributed as dist
 
     n = z.shape[0]
     dev = comm_device or z.device
@@ -206,7 +216,7 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
         _all_gather(cyc_all, cyc_send, group)
         status = backend.moments(z, rank, world, cyc_all, res_send)
     st = torch.tensor([status], dtype=torch.int32, device=cyc_send.device)
-    dist.all_reduce(st, op=dist.ReduceOp.MAX, group=group)   # everyone raises, or no one
+    _all_reduce_max(st, group)                                # everyone raises, or no one
     if int(st.item()):
         backend.raise_status(int(st.item()))
     _all_gather(res_all, res_send, group)
