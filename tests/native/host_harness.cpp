@@ -137,16 +137,26 @@ extern "C" int harness_fit_stats(const double* z, int n, const int* nbr, const i
     dp.c0x = prm[3]; dp.c0y = prm[4]; dp.c0z = prm[5];
     dp.c1x = prm[6]; dp.c1y = prm[7]; dp.c1z = prm[8];
     dp.tab = table; dp.tab_k = tab_k; dp.tab_invw = 1.0 / tab_w;
-    long long ok = 0, tot = 0;
+    // counts: {fitted, sub-triangles, fitted on the 1/|x| series path, fitted and
+    //          single-centre dominated (two-centre kind)}
+    long long ok = 0, tot = 0, series = 0, dom = 0;
     for (int i = 0; i < n; ++i) {
         const int* row = nbr + (int64_t)i * MAXDEG;
         for (int t = 0; t < deg[i]; ++t) {
             int j = row[t], k = row[(t + 1) % deg[i]];
             FanPair f = fan_pair(load3(z, i), load3(z, j), load3(z, k), i, j, k);
             for (int s = 0; s < 2; ++s) {
-                LocalFit lf;
+                LocalFit lf, lf1;
                 bool a = local_fit(dp, f.s[s], v3(dp.c0x, dp.c0y, dp.c0z), lf);
-                if (a && kind == 7) a = local_fit(dp, f.s[s], v3(dp.c1x, dp.c1y, dp.c1z), lf);
+                if (a && kind == 7) {
+                    a = local_fit(dp, f.s[s], v3(dp.c1x, dp.c1y, dp.c1z), lf1);
+                    if (a) dom += lf1.rmax < lf.rmin * (1.0 - 1e-13) || lf.rmax < lf1.rmin * (1.0 - 1e-13);
+                }
+                if (a) {
+                    const V3 nv = cross(f.s[s].e1, f.s[s].e2);
+                    const double nn = dot(nv, nv), h = dot(nv, f.s[s].v0);
+                    series += nn > 0.0 && nn - h * h <= 1e-4 * nn;
+                }
                 ok += a;
                 ++tot;
             }
@@ -154,6 +164,8 @@ extern "C" int harness_fit_stats(const double* z, int n, const int* nbr, const i
     }
     counts[0] = ok;
     counts[1] = tot;
+    counts[2] = series;
+    counts[3] = dom;
     return 0;
 }
 
