@@ -678,10 +678,16 @@ __global__ void k_gram_recursion(const double* __restrict__ partials, int K, Gra
                                  double* __restrict__ coef) {
     __shared__ double val[2 * MAXM + MAXM * (MAXM + 1) / 2 + 1];
     const int A = 2 * K + K * (K + 1) / 2 + 1;
-    for (int a = threadIdx.x; a < A; a += blockDim.x) {
+    // one warp per value: lanes sum a fixed stride of the block partials (independent loads,
+    // not one 296-long dependent chain), then a fixed shuffle tree: deterministic
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int a = warp; a < A; a += nw) {
+        const double* pa = partials + (int64_t)a * RED_BLOCKS;
         double v = 0.0;
-        for (int b = 0; b < RED_BLOCKS; ++b) v += partials[(int64_t)a * RED_BLOCKS + b];
-        val[a] = v;
+        for (int b = lane; b < RED_BLOCKS; b += 32) v += pa[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) val[a] = v;
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
@@ -2217,7 +2223,7 @@ int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* l
             gs.rho[i] = ctx->rho[si];
             for (int j = 0; j < K; ++j) gs.ys[i][j] = ctx->YS[si][(ctx->hist_head + j) % ctx->m];
         }
-        k_gram_recursion<<<1, 128, 0, ctx->stream>>>(ctx->d_partials, K, gs, ctx->d_coef);
+        k_gram_recursion<<<1, 1024, 0, ctx->stream>>>(ctx->d_partials, K, gs, ctx->d_coef);
         LAUNCHED();
     }
     TRY(launch_combine(ctx, K, g, lloyd_diag, gamma, hp, z, n, q3));

@@ -10,8 +10,10 @@ sys.path.insert(0, ".")
 import paper_1709_06924_b200 as P  # noqa: E402
 
 cfg, n, steps = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
-z0 = torch.from_numpy(P.sample_by_density(P.density_preset(cfg), n, 0)).cuda()
-with P.MeshEvaluator(P.density_preset(cfg), "7pt", subdivision=3) as ev:
+dens = {"c1": "const", "c2": "const"}.get(cfg, cfg)
+z0 = torch.from_numpy(P.random_sphere_points(n, 0) if dens == "const"
+                      else P.sample_by_density(P.density_preset(dens), n, 0)).cuda()
+with P.MeshEvaluator(P.density_preset(dens), "7pt", subdivision=3) as ev:
     st = P.Minimizer(z0, "lloyd-plbfgs", ev, 7)
     for _ in range(4):
         st.step()
