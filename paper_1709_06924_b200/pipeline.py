@@ -95,10 +95,17 @@ class _Context:
             _lib.check(rc, None, f"scvt_create: {msg}")
         self.n_max = n_max
         self.device = device
+        self._stream = None
+        torch = _torch()
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        self._current_stream = ((lambda: raw(device)) if raw is not None else
+                                (lambda: torch.cuda.current_stream(device).cuda_stream))
 
     def call(self, name: str, *args, what: str | None = None):
-        torch = _torch()
-        self.lib.scvt_set_stream(self.ptr, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        s = self._current_stream()          # calls are ordered on the caller's current stream
+        if s != self._stream:
+            self.lib.scvt_set_stream(self.ptr, ctypes.c_void_p(s))
+            self._stream = s
         rc = getattr(self.lib, name)(self.ptr, *args)
         if rc:
             _lib.check(rc, self.ptr, what or name)
