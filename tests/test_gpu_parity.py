@@ -530,3 +530,30 @@ def test_two_processes_sharded_run_matches_single_gpu():
         assert np.array_equal(out[rank]["points"], ref.points)
         assert out[rank]["energies"] == [h.energy for h in ref.records]
         assert out[rank]["fevals"] == ref.fevals
+
+
+@pytest.mark.parametrize("sharded", [False, True])
+def test_reuse_escalates_to_full_rebuild_under_large_moves(sharded):
+    """Positions moved by about a cell spacing between evaluations (most certificates fail):
+    the reuse loop must escalate to the full rebuild (more than 3n/4 bad, or the pass limit)
+    and still return exactly the fresh triangulation and moments."""
+    from paper_1709_06924_b200.parallel import CudaShardBackend, emulate_shards
+
+    n = 40962
+    z0 = P.sample_by_density(P.density_preset("c4"), n, 0)
+    rng = np.random.default_rng(11)
+    z1 = _unit(z0 + 0.01 * rng.standard_normal(z0.shape))
+    with _ev("c4", "7pt", 3) as ev, _ev("c4", "7pt", 3) as fresh:
+        if sharded:
+            be = CudaShardBackend(ev)
+            emulate_shards(be, torch.from_numpy(z0).cuda(), 3)
+            r = emulate_shards(be, torch.from_numpy(z1).cuda(), 3)
+        else:
+            ev.evaluate(z0)
+            r = ev.evaluate_device(torch.from_numpy(z1).cuda())
+            assert np.array_equal(ev.triangulation(z1).triangles, O.convex_hull_delaunay(z1))
+        ref = fresh.evaluate_device(torch.from_numpy(z1).cuda())
+        cnt = _reuse_counters(ev)
+    assert cnt["reused_evals"] == 0 and cnt["passes"] >= 1      # escalated, not certified
+    assert r.energy == ref.energy and torch.equal(r.grad, ref.grad)
+    assert torch.equal(r.first, ref.first) and torch.equal(r.mass, ref.mass)
