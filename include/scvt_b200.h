@@ -187,6 +187,52 @@ int scvt_shard_finish_ex(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                          double* lloyd_diag, const double* q3, const double* norms,
                          double* scalars_host);
 
+/* arithmetic-layout slices (multi-GPU optimizer algebra) -----------------------------------
+ * The generator ids are cut into SCVT_CHUNKS fixed chunks of ceil(n / SCVT_CHUNKS) ids; rank r
+ * of W (W divides SCVT_CHUNKS) owns the chunks [r C/W, (r+1) C/W), i.e. the ids [lo, hi) of
+ * scvt_slice_range.  Its LBFGS vectors (grad, first, lloyd_diag, q3, norms, the history ring)
+ * hold only those rows (slice-local: index 0 = id lo); positions stay replicated.  Every
+ * reduction of the optimizer is written per chunk into a caller-owned partials buffer
+ * red f64 [nval][SCVT_CHUNKS] that is zero outside the owned chunks; the caller sums the
+ * buffers over the ranks (all-reduce SUM — each entry has exactly one non-zero contributor,
+ * so the sum is exact) and the next call reduces the SCVT_CHUNKS partials in a fixed order.
+ * Every scalar is therefore bitwise the same for any W, and the single-GPU entry points run
+ * the same kernels with W = 1.  Replaces the paper's distributed LBFGS dot products
+ * (the reference's optimizer.py:147-167 and 340-355 on one process).
+ *   evaluation   scvt_slice_finish (5 values) -> <sum> -> scvt_slice_scalars
+ *   direction    scvt_slice_gram (nval values, 0 with an empty history) -> <sum> ->
+ *                scvt_slice_combine (2 values: q.g, g.q3) -> <sum> -> scvt_reduce_chunks
+ *   fallback     scvt_slice_tangent (1 value: g.q3) -> <sum> -> scvt_reduce_chunks
+ *   history      scvt_slice_history_pair (nval = 4 + 2K values) -> <sum> ->
+ *                scvt_slice_history_commit (curvature test, ring commit, movement)
+ *   trial point  scvt_trial_point on the slice rows, then the caller all-gathers z_t. */
+#define SCVT_CHUNKS 1184
+int scvt_slice_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
+/* scatter of the gathered shard results (res_all of scvt_shard_moments) to this slice,
+ * gradient epilogue; 5 values: E, |g|^2, obtuse, min lloyd_diag, sum g.(q3/norms) */
+int scvt_slice_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                      const double* res_all, int rank, int world, double* grad, double* first,
+                      double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                      double* red);
+/* scalars_host[5] = {energy, |g|, obtuse, min lloyd_diag, dphi} (as scvt_evaluate_ex) */
+int scvt_slice_scalars(scvt_ctx* ctx, const double* red, double* scalars_host);
+int scvt_slice_gram(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
+                    int64_t n, int rank, int world, double* red, int32_t* nval_host);
+/* red may alias red_gram (the recursion consumes it first, stream-ordered) */
+int scvt_slice_combine(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
+                       const double* z, int64_t n, int rank, int world, const double* red_gram,
+                       double* q3, double* red);
+int scvt_slice_tangent(scvt_ctx* ctx, const double* q, const double* z, const double* g,
+                       int64_t n, int rank, int world, double* q3, double* red);
+int scvt_slice_history_pair(scvt_ctx* ctx, const double* z_old, const double* z_new,
+                            const double* g_old, const double* g_new, int64_t n, int rank,
+                            int world, double* red, int32_t* nval_host);
+int scvt_slice_history_commit(scvt_ctx* ctx, const double* red, int64_t n, int rank, int world,
+                              int32_t* pushed_host, double* movement_host);
+/* fixed-order reduction of nval values (ops[v]: 0 sum, 1 max, 2 min; NULL = all sums) */
+int scvt_reduce_chunks(scvt_ctx* ctx, const double* red, int32_t nval, const uint8_t* ops,
+                       double* out_host);
+
 /* optimizer vector algebra -------------------------------------------------------------
  * CorrectionHistory (optimizer.py:79-114): ring of at most lbfgs_m (s, y) pairs held on
  * the device inside ctx. */

@@ -78,6 +78,23 @@ SIGNATURES = {
                                          _vp, _vp, _c_dbl_p]),
     "scvt_shard_finish_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp,
                                             _vp, _vp, _vp, _vp, _vp, _c_dbl_p]),
+    "scvt_slice_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _c_i64_p,
+                                        _c_i64_p]),
+    "scvt_slice_finish": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp,
+                                         ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                         _vp]),
+    "scvt_slice_scalars": (ctypes.c_int, [_vp, _vp, _c_dbl_p]),
+    "scvt_slice_gram": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int64,
+                                       ctypes.c_int, ctypes.c_int, _vp, _c_i32_p]),
+    "scvt_slice_combine": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _vp, ctypes.c_int64,
+                                          ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "scvt_slice_tangent": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int,
+                                          ctypes.c_int, _vp, _vp]),
+    "scvt_slice_history_pair": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, ctypes.c_int64,
+                                               ctypes.c_int, ctypes.c_int, _vp, _c_i32_p]),
+    "scvt_slice_history_commit": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int,
+                                                 ctypes.c_int, _c_i32_p, _c_dbl_p]),
+    "scvt_reduce_chunks": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _c_dbl_p]),
     "scvt_history_clear": (ctypes.c_int, [_vp]),
     "scvt_history_size": (ctypes.c_int, [_vp, _c_i32_p]),
     "scvt_history_gamma": (ctypes.c_int, [_vp, _c_dbl_p]),

@@ -34,6 +34,13 @@ using namespace scvt;
 namespace {
 
 constexpr int RED_BLOCKS = 296;      // 2 x 148 SMs: fixed reduction shape
+// The optimizer's reductions run over a fixed partition of the generator ids into CHUNKS
+// chunks of ceil(n / CHUNKS) ids (include/scvt_b200.h, SCVT_CHUNKS): one block per chunk, one
+// partial per chunk and value, then a fixed-order pass over the CHUNKS partials.  A rank of an
+// arithmetic-layout run owns a contiguous range of whole chunks, so the same partials come out
+// whatever the rank count.
+constexpr int CHUNKS = SCVT_CHUNKS;
+constexpr int MAX_RED_VALS = 176;    // >= 2K + K(K+1)/2 + 1 for K <= 16
 constexpr int RED_THREADS = 256;
 constexpr int VEC_THREADS = 256;
 constexpr int QUAD_THREADS = 128;
@@ -543,6 +550,35 @@ __global__ void k_unpack_results(const double* __restrict__ rows, int nrows, int
     atomicAdd(seen, 1);
 }
 
+// arithmetic-layout finish: the rows of ids in [lo, hi) -> slice-local outputs (index i - lo);
+// E_i, |g_i|^2, obtuse_i by id (the caller NaN-fills E of the slice first: coverage check)
+__global__ void k_unpack_slice(const double* __restrict__ rows, int nrows, int64_t lo,
+                               int64_t hi, const double* __restrict__ z, double* __restrict__ grad,
+                               double* __restrict__ first, double* __restrict__ mass,
+                               double* __restrict__ diag, double* __restrict__ e_gen,
+                               double* __restrict__ g2_gen, double* __restrict__ ob_gen) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const double* row = rows + (int64_t)r * RES_ROW;
+    if (row[0] < 0.0) return;
+    const int64_t i = (int64_t)row[0];
+    if (i < lo || i >= hi) return;
+    const int64_t k = i - lo;
+    const double cx = row[2], cy = row[3], cz = row[4];
+    V3 zi = load3(z, (int)i);
+    const double czd = cx * zi.x + cy * zi.y + cz * zi.z;
+    const double gx = 2.0 * czd * zi.x - 2.0 * cx;
+    const double gy = 2.0 * czd * zi.y - 2.0 * cy;
+    const double gz = 2.0 * czd * zi.z - 2.0 * cz;
+    grad[3 * k] = gx; grad[3 * k + 1] = gy; grad[3 * k + 2] = gz;
+    diag[k] = 2.0 * czd;
+    g2_gen[i] = gx * gx + gy * gy + gz * gz;
+    first[3 * k] = cx; first[3 * k + 1] = cy; first[3 * k + 2] = cz;
+    if (mass) mass[k] = row[1];
+    e_gen[i] = row[5];
+    ob_gen[i] = row[6];
+}
+
 // ------------------------------------------------------------------ deterministic reductions
 // op 0 = sum, 1 = max, 2 = min.  Stage 1 writes RED_BLOCKS partials per array.
 template <int OP>
@@ -638,6 +674,23 @@ struct HistPtrs {
     const double* Y[MAXM];
 };
 
+// A slice of the generator ids [lo, lo + len) made of the chunks [c_lo, c_lo + nc); block b of a
+// chunked launch (grid = nc) owns the slice-local ids [b ch, min(len, (b + 1) ch)).  Pointers
+// handed to the kernels are slice-local (index 0 = id lo).
+struct Chunks {
+    int64_t lo, len, ch;
+    int c_lo, nc;
+};
+
+__device__ __forceinline__ void chunk_span(const Chunks& c, int64_t* b, int64_t* e) {
+    *b = (int64_t)blockIdx.x * c.ch;
+    *e = min(c.len, *b + c.ch);
+}
+
+__device__ __forceinline__ double* chunk_slot(double* red, const Chunks& c, int v) {
+    return red + (int64_t)v * CHUNKS + c.c_lo + blockIdx.x;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -646,16 +699,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 constexpr int GRAM_THREADS = 128;
 
+// Gram pass of the two-loop (one read of the history): per chunk, s_k.g, y_k.H0 g, y_k.H0 y_l
+// (packed upper triangle) and g.H0 g
 template <int K>
 __global__ void __launch_bounds__(GRAM_THREADS)
 k_gram(const double* __restrict__ g, const double* __restrict__ diag, double gamma, HistPtrs h,
-       int64_t n, double* __restrict__ partials) {
+       Chunks ck, double* __restrict__ red) {
     constexpr int A = 2 * K + K * (K + 1) / 2 + 1;
     double acc[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) acc[a] = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * GRAM_THREADS + threadIdx.x; i < n;
-         i += (int64_t)RED_BLOCKS * GRAM_THREADS) {
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += GRAM_THREADS) {
         const double hw = diag ? 1.0 / diag[i] : gamma;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -687,7 +743,7 @@ k_gram(const double* __restrict__ g, const double* __restrict__ diag, double gam
     for (int a = threadIdx.x; a < A; a += GRAM_THREADS) {
         double v = 0.0;
         for (int q = 0; q < GRAM_THREADS / 32; ++q) v += sh[q][a];
-        partials[(int64_t)a * RED_BLOCKS + blockIdx.x] = v;
+        *chunk_slot(red, ck, a) = v;
     }
 }
 
@@ -696,20 +752,26 @@ struct GramScalars {
     double rho[MAXM];
 };
 
+// fixed-order reduction of one value's CHUNKS partials by one warp (lane-strided, then a fixed
+// butterfly): the same bits on every rank and for every rank count
+template <int OP>
+__device__ __forceinline__ double warp_chunks(const double* __restrict__ pv) {
+    const int lane = threadIdx.x & 31;
+    double v = red_identity<OP>();
+    for (int b = lane; b < CHUNKS; b += 32) v = red_op<OP>(v, pv[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = red_op<OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 // one block: fixed-order sums of the Gram partials, then the scalar two-loop recursion
-__global__ void k_gram_recursion(const double* __restrict__ partials, int K, GramScalars gs,
+__global__ void k_gram_recursion(const double* __restrict__ red, int K, GramScalars gs,
                                  double* __restrict__ coef) {
     __shared__ double val[2 * MAXM + MAXM * (MAXM + 1) / 2 + 1];
     const int A = 2 * K + K * (K + 1) / 2 + 1;
-    // one warp per value: lanes sum a fixed stride of the block partials (independent loads,
-    // not one 296-long dependent chain), then a fixed shuffle tree: deterministic
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int a = warp; a < A; a += nw) {
-        const double* pa = partials + (int64_t)a * RED_BLOCKS;
-        double v = 0.0;
-        for (int b = lane; b < RED_BLOCKS; b += 32) v += pa[b];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const double v = warp_chunks<0>(red + (int64_t)a * CHUNKS);
         if (lane == 0) val[a] = v;
     }
     __syncthreads();
@@ -733,18 +795,19 @@ __global__ void k_gram_recursion(const double* __restrict__ partials, int K, Gra
     for (int i = 0; i < K; ++i) { coef[i] = a[i]; coef[MAXM + i] = c[i]; }
 }
 
-// q = -(H0 (g - sum_j a_j y_j) + sum_l c_l s_l); q3 = q - (q.z) z; partials of q.g and g.q3
+// q = -(H0 (g - sum_j a_j y_j) + sum_l c_l s_l); q3 = q - (q.z) z; chunk partials of q.g, g.q3
 template <int K>
 __global__ void __launch_bounds__(RED_THREADS)
 k_combine(const double* __restrict__ g, const double* __restrict__ diag, double gamma,
-          HistPtrs h, const double* __restrict__ coef, const double* __restrict__ z, int64_t n,
-          double* __restrict__ q3, double* __restrict__ partials) {
+          HistPtrs h, const double* __restrict__ coef, const double* __restrict__ z, Chunks ck,
+          double* __restrict__ q3, double* __restrict__ red) {
     double ca[K > 0 ? K : 1], cc[K > 0 ? K : 1];
 #pragma unroll
     for (int k = 0; k < K; ++k) { ca[k] = coef[k]; cc[k] = coef[MAXM + k]; }
     double qg = 0.0, gq3 = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
-         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
         const double hw = diag ? 1.0 / diag[i] : gamma;
         double q[3], gg[3];
 #pragma unroll
@@ -769,21 +832,45 @@ k_combine(const double* __restrict__ g, const double* __restrict__ diag, double 
     qg = block_reduce<0>(qg);
     gq3 = block_reduce<0>(gq3);
     if (threadIdx.x == 0) {
-        partials[blockIdx.x] = qg;
-        partials[RED_BLOCKS + blockIdx.x] = gq3;
+        *chunk_slot(red, ck, 0) = qg;
+        *chunk_slot(red, ck, 1) = gq3;
     }
 }
 
-// y_new . s_j and y_j . s_new against the K stored pairs (partials, 2K slots)
+// s = z_new - z_old, y = g_new - g_old (staged); chunk partials of y.s, s.s, y.y, max|s|
+__global__ void __launch_bounds__(RED_THREADS)
+k_history_pair(const double* __restrict__ zo, const double* __restrict__ zn,
+               const double* __restrict__ go, const double* __restrict__ gn, Chunks ck,
+               double* __restrict__ s, double* __restrict__ y, double* __restrict__ red) {
+    double ys = 0, ss = 0, yy = 0, mv = 0;
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t k = 3 * i0 + threadIdx.x; k < 3 * i1; k += RED_THREADS) {
+        double sk = zn[k] - zo[k], yk = gn[k] - go[k];
+        s[k] = sk; y[k] = yk;
+        ys += yk * sk; ss += sk * sk; yy += yk * yk; mv = fmax(mv, fabs(sk));
+    }
+    ys = block_reduce<0>(ys); ss = block_reduce<0>(ss); yy = block_reduce<0>(yy);
+    mv = block_reduce<1>(mv);
+    if (threadIdx.x == 0) {
+        *chunk_slot(red, ck, 0) = ys;
+        *chunk_slot(red, ck, 1) = ss;
+        *chunk_slot(red, ck, 2) = yy;
+        *chunk_slot(red, ck, 3) = mv;
+    }
+}
+
+// y_new . s_j and y_j . s_new against the K stored pairs (values 4 .. 4 + 2K)
 template <int K>
 __global__ void __launch_bounds__(RED_THREADS)
-k_cross(const double* __restrict__ sn, const double* __restrict__ yn, HistPtrs h, int64_t len,
-        double* __restrict__ partials) {
+k_cross(const double* __restrict__ sn, const double* __restrict__ yn, HistPtrs h, Chunks ck,
+        double* __restrict__ red) {
     double a1[K > 0 ? K : 1], a2[K > 0 ? K : 1];
 #pragma unroll
     for (int k = 0; k < K; ++k) { a1[k] = 0.0; a2[k] = 0.0; }
-    for (int64_t e = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; e < len;
-         e += (int64_t)RED_BLOCKS * RED_THREADS) {
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t e = 3 * i0 + threadIdx.x; e < 3 * i1; e += RED_THREADS) {
         const double s = sn[e], y = yn[e];
 #pragma unroll
         for (int k = 0; k < K; ++k) { a1[k] += y * h.S[k][e]; a2[k] += h.Y[k][e] * s; }
@@ -793,24 +880,26 @@ k_cross(const double* __restrict__ sn, const double* __restrict__ yn, HistPtrs h
         double v1 = block_reduce<0>(a1[k]);
         double v2 = block_reduce<0>(a2[k]);
         if (threadIdx.x == 0) {
-            partials[(int64_t)(4 + k) * RED_BLOCKS + blockIdx.x] = v1;
-            partials[(int64_t)(4 + K + k) * RED_BLOCKS + blockIdx.x] = v2;
+            *chunk_slot(red, ck, 4 + k) = v1;
+            *chunk_slot(red, ck, 4 + K + k) = v2;
         }
     }
 }
 
 // ------------------------------------------------------------------ evaluation scalars
-// One pass over the per-generator arrays: sum E_i, sum |g_i|^2, obtuse count, min lloyd_diag
-// (the nonpositive-diagonal test of cvt_core.py:184) and, for a line-search trial, the
-// directional derivative sum g.(q3/|v|) (optimizer.py:330).  Fixed shape -> bitwise repeatable.
+// Per chunk: sum E_i, sum |g_i|^2, obtuse count, min lloyd_diag (the nonpositive-diagonal test
+// of cvt_core.py:184) and, for a line-search trial, the directional derivative
+// sum g.(q3/|v|) (optimizer.py:330).  e_gen, g2_gen, ob_gen, diag, grad, q3, norms are
+// slice-local.  A missing generator (NaN E) poisons the energy: the coverage check.
 __global__ void __launch_bounds__(RED_THREADS)
 k_eval_reduce(const double* __restrict__ e_gen, const double* __restrict__ g2_gen,
               const double* __restrict__ ob_gen, const double* __restrict__ diag,
               const double* __restrict__ grad, const double* __restrict__ q3,
-              const double* __restrict__ norms, int64_t n, double* __restrict__ partials) {
+              const double* __restrict__ norms, Chunks ck, double* __restrict__ red) {
     double se = 0.0, sg = 0.0, so = 0.0, mn = INFINITY, sd = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
-         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
         se += e_gen[i];
         sg += g2_gen[i];
         so += ob_gen[i];
@@ -824,21 +913,29 @@ k_eval_reduce(const double* __restrict__ e_gen, const double* __restrict__ g2_ge
     se = block_reduce<0>(se); sg = block_reduce<0>(sg); so = block_reduce<0>(so);
     mn = block_reduce<2>(mn); sd = block_reduce<0>(sd);
     if (threadIdx.x == 0) {
-        partials[blockIdx.x] = se;
-        partials[RED_BLOCKS + blockIdx.x] = sg;
-        partials[2 * RED_BLOCKS + blockIdx.x] = so;
-        partials[3 * RED_BLOCKS + blockIdx.x] = mn;
-        partials[4 * RED_BLOCKS + blockIdx.x] = sd;
+        *chunk_slot(red, ck, 0) = se;
+        *chunk_slot(red, ck, 1) = sg;
+        *chunk_slot(red, ck, 2) = so;
+        *chunk_slot(red, ck, 3) = mn;
+        *chunk_slot(red, ck, 4) = sd;
     }
 }
 
-__global__ void k_eval_reduce2(const double* __restrict__ partials, double* __restrict__ out) {
-    double se = finish_partials<0>(partials);
-    double sg = finish_partials<0>(partials + RED_BLOCKS);
-    double so = finish_partials<0>(partials + 2 * RED_BLOCKS);
-    double mn = finish_partials<2>(partials + 3 * RED_BLOCKS);
-    double sd = finish_partials<0>(partials + 4 * RED_BLOCKS);
-    if (threadIdx.x == 0) { out[0] = se; out[1] = sg; out[2] = so; out[3] = mn; out[4] = sd; }
+// fixed-order pass over the chunk partials of nval values (op per value: 0 sum, 1 max, 2 min)
+struct RedOps {
+    unsigned char op[MAX_RED_VALS];
+};
+
+__global__ void k_reduce_chunks(const double* __restrict__ red, int nval, RedOps ops,
+                                double* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int v = warp; v < nval; v += nw) {
+        const double* pv = red + (int64_t)v * CHUNKS;
+        const int op = ops.op[v];
+        const double r = op == 0 ? warp_chunks<0>(pv) : (op == 1 ? warp_chunks<1>(pv)
+                                                                 : warp_chunks<2>(pv));
+        if (lane == 0) out[v] = r;
+    }
 }
 
 // ------------------------------------------------------------------ LBFGS vector kernels
@@ -891,44 +988,15 @@ __global__ void k_apply_h0(double* __restrict__ q, const double* __restrict__ di
     }
 }
 
-// s = z_new - z_old, y = g_new - g_old; stage-1 partials of y.s, s.s, y.y and max|s|
-__global__ void __launch_bounds__(RED_THREADS)
-k_history_pair(const double* __restrict__ zo, const double* __restrict__ zn,
-               const double* __restrict__ go, const double* __restrict__ gn, int64_t len,
-               double* __restrict__ s, double* __restrict__ y, double* __restrict__ partials) {
-    double ys = 0, ss = 0, yy = 0, mv = 0;
-    for (int64_t k = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < len;
-         k += (int64_t)RED_BLOCKS * RED_THREADS) {
-        double sk = zn[k] - zo[k], yk = gn[k] - go[k];
-        s[k] = sk; y[k] = yk;
-        ys += yk * sk; ss += sk * sk; yy += yk * yk; mv = fmax(mv, fabs(sk));
-    }
-    ys = block_reduce<0>(ys); ss = block_reduce<0>(ss); yy = block_reduce<0>(yy);
-    mv = block_reduce<1>(mv);
-    if (threadIdx.x == 0) {
-        partials[blockIdx.x] = ys;
-        partials[RED_BLOCKS + blockIdx.x] = ss;
-        partials[2 * RED_BLOCKS + blockIdx.x] = yy;
-        partials[3 * RED_BLOCKS + blockIdx.x] = mv;
-    }
-}
-
-__global__ void k_history_finish(const double* __restrict__ partials, double* __restrict__ out) {
-    double ys = finish_partials<0>(partials);
-    double ss = finish_partials<0>(partials + RED_BLOCKS);
-    double yy = finish_partials<0>(partials + 2 * RED_BLOCKS);
-    double mv = finish_partials<1>(partials + 3 * RED_BLOCKS);
-    if (threadIdx.x == 0) { out[0] = ys; out[1] = ss; out[2] = yy; out[3] = mv; }
-}
-
-// q3 = q - (q.z) z per row; partials of g.q3
+// q3 = q - (q.z) z per row; chunk partials of g.q3
 __global__ void __launch_bounds__(RED_THREADS)
 k_tangent(const double* __restrict__ q, const double* __restrict__ z,
-          const double* __restrict__ g, int64_t n, double* __restrict__ q3,
-          double* __restrict__ partials) {
+          const double* __restrict__ g, Chunks ck, double* __restrict__ q3,
+          double* __restrict__ red) {
     double v = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
-         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
         double qx = q[3 * i], qy = q[3 * i + 1], qz = q[3 * i + 2];
         double zx = z[3 * i], zy = z[3 * i + 1], zz = z[3 * i + 2];
         double qd = qx * zx + qy * zy + qz * zz;
@@ -937,7 +1005,7 @@ k_tangent(const double* __restrict__ q, const double* __restrict__ z,
         v += g[3 * i] * ax + g[3 * i + 1] * ay + g[3 * i + 2] * az;
     }
     v = block_reduce<0>(v);
-    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+    if (threadIdx.x == 0) *chunk_slot(red, ck, 0) = v;
 }
 
 __global__ void k_trial(const double* __restrict__ z, const double* __restrict__ q3, double alpha,
@@ -955,16 +1023,17 @@ __global__ void k_trial(const double* __restrict__ z, const double* __restrict__
 
 __global__ void __launch_bounds__(RED_THREADS)
 k_dirderiv(const double* __restrict__ g, const double* __restrict__ q3,
-           const double* __restrict__ norms, int64_t n, double* __restrict__ partials) {
+           const double* __restrict__ norms, Chunks ck, double* __restrict__ red) {
     double v = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
-         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
         double nr = norms[i];
         v += g[3 * i] * (q3[3 * i] / nr) + g[3 * i + 1] * (q3[3 * i + 1] / nr) +
              g[3 * i + 2] * (q3[3 * i + 2] / nr);
     }
     v = block_reduce<0>(v);
-    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+    if (threadIdx.x == 0) *chunk_slot(red, ck, 0) = v;
 }
 
 __global__ void k_lloyd(const double* __restrict__ c, int64_t n, double* __restrict__ z,
@@ -1107,10 +1176,10 @@ struct scvt_ctx {
     double* d_part = nullptr; uint8_t* d_obt = nullptr;
     double* d_egen = nullptr; double* d_g2gen = nullptr; double* d_obgen = nullptr;
     // reductions and status
-    double* d_partials = nullptr;      // [MAX_SLOTS][RED_BLOCKS]
-    double* d_scal = nullptr;          // [MAX_SLOTS]
+    double* d_partials = nullptr;      // [MAX_SLOTS][RED_BLOCKS] and [MAX_RED_VALS][CHUNKS]
+    double* d_scal = nullptr;          // [MAX_RED_VALS]
     int* d_status = nullptr;           // [1 + 4 stats]
-    double* h_scal = nullptr;          // pinned [MAX_SLOTS]
+    double* h_scal = nullptr;          // pinned [MAX_RED_VALS]
     int* h_status = nullptr;           // pinned [8]
     int* h_small = nullptr;            // pinned [16]: small readbacks (reuse counts)
     int* d_rcount = nullptr;           // per-round bad counts of the chained reuse rounds
@@ -1289,6 +1358,37 @@ int dot_to_slot(scvt_ctx* ctx, const double* a, const double* b, int64_t len, in
 // sum(slots) -> d_scal[0..nslots) -> host
 int finish_slots(scvt_ctx* ctx, int nslots) {
     k_reduce_stage2<0><<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials, nslots, ctx->d_scal);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+// ---------------------------------------------------------------------- chunked reductions
+// rank `rank` of `world` (world divides CHUNKS) owns chunks [rank C/W, (rank+1) C/W)
+int make_chunks(scvt_ctx* ctx, int64_t n, int rank, int world, Chunks* c) {
+    if (world < 1 || rank < 0 || rank >= world || CHUNKS % world)
+        return fail(ctx, SCVT_ERR_CONFIG, "slice %d of %d: the world size must divide %d", rank,
+                    world, CHUNKS);
+    c->ch = std::max<int64_t>(1, (n + CHUNKS - 1) / CHUNKS);
+    c->nc = CHUNKS / world;
+    c->c_lo = rank * c->nc;
+    c->lo = std::min<int64_t>(n, (int64_t)c->c_lo * c->ch);
+    c->len = std::min<int64_t>(n, (int64_t)(c->c_lo + c->nc) * c->ch) - c->lo;
+    return SCVT_OK;
+}
+
+// partial buffers of a slice: zero outside the owned chunks (the cross-rank SUM is then exact)
+int prep_red(scvt_ctx* ctx, double* red, int nval, const Chunks& c) {
+    if (c.nc < CHUNKS && nval > 0)
+        CK(cudaMemsetAsync(red, 0, (size_t)nval * CHUNKS * sizeof(double), ctx->stream));
+    return SCVT_OK;
+}
+
+// fixed-order reduction of nval values' chunk partials -> d_scal (device)
+int reduce_chunks(scvt_ctx* ctx, const double* red, int nval, const unsigned char* ops) {
+    if (nval > MAX_RED_VALS) return fail(ctx, SCVT_ERR_CONFIG, "%d values > %d", nval, MAX_RED_VALS);
+    RedOps ro;
+    for (int v = 0; v < nval; ++v) ro.op[v] = ops ? ops[v] : 0;
+    k_reduce_chunks<<<1, 1024, 0, ctx->stream>>>(red, nval, ro, ctx->d_scal);
     LAUNCHED();
     return SCVT_OK;
 }
@@ -1545,16 +1645,18 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
     return SCVT_OK;
 }
 
-// fixed-shape reductions of E_i, |g_i|^2, obtuse_i over ALL n generators (id order), so the
+// fixed-chunk reductions of E_i, |g_i|^2, obtuse_i over ALL n generators (id order), so the
 // scalars are bitwise identical whatever the shard count; reads back and checks status
 int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* diag,
                   const double* grad, const double* q3, const double* norms, int nsc) {
     cudaStream_t s = ctx->stream;
-    k_eval_reduce<<<RED_BLOCKS, RED_THREADS, 0, s>>>(ctx->d_egen, ctx->d_g2gen, ctx->d_obgen,
-                                                      diag, grad, q3, norms, n, ctx->d_partials);
+    Chunks ck;
+    TRY(make_chunks(ctx, n, 0, 1, &ck));
+    k_eval_reduce<<<ck.nc, RED_THREADS, 0, s>>>(ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, diag,
+                                                 grad, q3, norms, ck, ctx->d_partials);
     LAUNCHED();
-    k_eval_reduce2<<<1, RED_THREADS, 0, s>>>(ctx->d_partials, ctx->d_scal);
-    LAUNCHED();
+    static const unsigned char ops[5] = {0, 0, 0, 2, 0};
+    TRY(reduce_chunks(ctx, ctx->d_partials, 5, ops));
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[5], s));
     TRY(readback(ctx, 5));
     if (ctx->prof) {
@@ -1618,9 +1720,9 @@ HistPtrs hist_ptrs(scvt_ctx* ctx) {
     X(13) X(14) X(15) X(16)
 
 int launch_gram(scvt_ctx* ctx, int K, const double* g, const double* diag, double gamma,
-                const HistPtrs& hp, int64_t n) {
+                const HistPtrs& hp, const Chunks& ck, double* red) {
     switch (K) {
-#define G(k) case k: k_gram<k><<<RED_BLOCKS, GRAM_THREADS, 0, ctx->stream>>>(g, diag, gamma, hp, n, ctx->d_partials); break;
+#define G(k) case k: k_gram<k><<<ck.nc, GRAM_THREADS, 0, ctx->stream>>>(g, diag, gamma, hp, ck, red); break;
         SCVT_K_CASES(G)
 #undef G
         default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
@@ -1630,9 +1732,9 @@ int launch_gram(scvt_ctx* ctx, int K, const double* g, const double* diag, doubl
 }
 
 int launch_combine(scvt_ctx* ctx, int K, const double* g, const double* diag, double gamma,
-                   const HistPtrs& hp, const double* z, int64_t n, double* q3) {
+                   const HistPtrs& hp, const double* z, const Chunks& ck, double* q3, double* red) {
     switch (K) {
-#define C(k) case k: k_combine<k><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(g, diag, gamma, hp, ctx->d_coef, z, n, q3, ctx->d_partials); break;
+#define C(k) case k: k_combine<k><<<ck.nc, RED_THREADS, 0, ctx->stream>>>(g, diag, gamma, hp, ctx->d_coef, z, ck, q3, red); break;
         SCVT_K_CASES(C)
 #undef C
         default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
@@ -1641,14 +1743,105 @@ int launch_combine(scvt_ctx* ctx, int K, const double* g, const double* diag, do
     return SCVT_OK;
 }
 
-int launch_cross(scvt_ctx* ctx, int K, const HistPtrs& hp, int64_t len) {
+int launch_cross(scvt_ctx* ctx, int K, const HistPtrs& hp, const Chunks& ck, double* red) {
     if (K == 0) return SCVT_OK;
     switch (K) {
-#define X_(k) case k: k_cross<k><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(ctx->d_tmp_s, ctx->d_tmp_y, hp, len, ctx->d_partials); break;
+#define X_(k) case k: k_cross<k><<<ck.nc, RED_THREADS, 0, ctx->stream>>>(ctx->d_tmp_s, ctx->d_tmp_y, hp, ck, red); break;
         SCVT_K_CASES(X_)
 #undef X_
         default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
     }
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+inline int gram_values(int K) { return K ? 2 * K + K * (K + 1) / 2 + 1 : 0; }
+
+// two-loop, phase 1: the Gram partials of the slice (nothing when the history is empty)
+int gram_phase(scvt_ctx* ctx, const double* g, const double* diag, double gamma,
+               const Chunks& ck, double* red) {
+    const int K = ctx->hist_count;
+    if (!K) return SCVT_OK;
+    TRY(prep_red(ctx, red, gram_values(K), ck));
+    return launch_gram(ctx, K, g, diag, gamma, hist_ptrs(ctx), ck, red);
+}
+
+// two-loop, phase 2: recursion on the (rank-summed) Gram partials, then the combine pass of the
+// slice with the tangent projection; 2 values (q.g, g.q3) into red (may alias red_gram)
+int combine_phase(scvt_ctx* ctx, const double* g, const double* diag, double gamma,
+                  const double* z, const Chunks& ck, const double* red_gram, double* q3,
+                  double* red) {
+    const int K = ctx->hist_count;
+    if (K) {
+        GramScalars gs;
+        for (int i = 0; i < K; ++i) {
+            const int si = (ctx->hist_head + i) % ctx->m;
+            gs.rho[i] = ctx->rho[si];
+            for (int j = 0; j < K; ++j) gs.ys[i][j] = ctx->YS[si][(ctx->hist_head + j) % ctx->m];
+        }
+        k_gram_recursion<<<1, 1024, 0, ctx->stream>>>(red_gram, K, gs, ctx->d_coef);
+        LAUNCHED();
+    }
+    TRY(prep_red(ctx, red, 2, ck));
+    return launch_combine(ctx, K, g, diag, gamma, hist_ptrs(ctx), z, ck, q3, red);
+}
+
+// history push, phase 1: stage s, y of the slice; 4 + 2K values (y.s, s.s, y.y, max|s|, cross)
+int pair_phase(scvt_ctx* ctx, const double* zo, const double* zn, const double* go,
+               const double* gn, const Chunks& ck, double* red, int* nval) {
+    const int K = ctx->hist_count;
+    *nval = 4 + 2 * K;
+    TRY(prep_red(ctx, red, *nval, ck));
+    k_history_pair<<<ck.nc, RED_THREADS, 0, ctx->stream>>>(zo, zn, go, gn, ck, ctx->d_tmp_s,
+                                                          ctx->d_tmp_y, red);
+    LAUNCHED();
+    return launch_cross(ctx, K, hist_ptrs(ctx), ck, red);
+}
+
+// history push, phase 2: fixed-order scalars, curvature test (optimizer.py:98-104), commit of
+// the staged slice into the ring slot and of the cross products into the host y.s matrix
+int commit_phase(scvt_ctx* ctx, const double* red, int64_t len, int32_t* pushed_host,
+                 double* movement_host) {
+    const int K = ctx->hist_count;
+    unsigned char ops[4 + 2 * MAXM];
+    for (int v = 0; v < 4 + 2 * K; ++v) ops[v] = v == 3 ? 1 : 0;
+    TRY(reduce_chunks(ctx, red, 4 + 2 * K, ops));
+    TRY(readback(ctx, 4 + 2 * K));
+    double ys = ctx->h_scal[0], ss = ctx->h_scal[1], yy = ctx->h_scal[2];
+    *movement_host = ctx->h_scal[3];
+    if (ys <= 1e-14 * sqrt(ss) * sqrt(yy)) {
+        *pushed_host = 0;
+        return SCVT_OK;
+    }
+    const int slot = (ctx->hist_head + ctx->hist_count) % ctx->m;
+    CK(cudaMemcpyAsync(ctx->d_S + (int64_t)slot * 3 * ctx->n_max, ctx->d_tmp_s,
+                       3 * len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_Y + (int64_t)slot * 3 * ctx->n_max, ctx->d_tmp_y,
+                       3 * len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->launches += 2;
+    ctx->rho[slot] = 1.0 / ys;
+    ctx->ys[slot] = ys;
+    ctx->yy[slot] = yy;
+    for (int k = 0; k < K; ++k) {                 // cross products with the kept pairs
+        const int sk = (ctx->hist_head + k) % ctx->m;
+        if (sk == slot) continue;                 // the pair being overwritten
+        ctx->YS[slot][sk] = ctx->h_scal[4 + k];       // y_new . s_k
+        ctx->YS[sk][slot] = ctx->h_scal[4 + K + k];   // y_k . s_new
+    }
+    ctx->YS[slot][slot] = ys;
+    if (ctx->hist_count < ctx->m) ++ctx->hist_count;
+    else ctx->hist_head = (ctx->hist_head + 1) % ctx->m;
+    *pushed_host = 1;
+    return SCVT_OK;
+}
+
+// evaluation scalars of a slice: 5 values (E, |g|^2, obtuse, min diag, dirderiv) into red
+int eval_scalars_phase(scvt_ctx* ctx, const Chunks& ck, const double* diag, const double* grad,
+                       const double* q3, const double* norms, double* red) {
+    TRY(prep_red(ctx, red, 5, ck));
+    k_eval_reduce<<<ck.nc, RED_THREADS, 0, ctx->stream>>>(
+        ctx->d_egen + ck.lo, ctx->d_g2gen + ck.lo, ctx->d_obgen + ck.lo, diag, grad, q3, norms,
+        ck, red);
     LAUNCHED();
     return SCVT_OK;
 }
@@ -1774,8 +1967,8 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_pairs, n * MAXDEG * 2); AL(d_cursor, n + 1);
     AL(d_part, 10 * n_inc); AL(d_obt, n_inc);      // [2][5][n_inc]: split mode uses both
     AL(d_egen, n); AL(d_g2gen, n); AL(d_obgen, n);
-    AL(d_partials, (int64_t)MAX_SLOTS * RED_BLOCKS);
-    AL(d_scal, MAX_SLOTS);
+    AL(d_partials, std::max<int64_t>((int64_t)MAX_SLOTS * RED_BLOCKS, (int64_t)MAX_RED_VALS * CHUNKS));
+    AL(d_scal, MAX_RED_VALS);
     AL(d_status, 16);
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
@@ -1786,7 +1979,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_coef, 2 * MAXM);
 #undef AL
     {
-        cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_SLOTS * sizeof(double));
+        cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_RED_VALS * sizeof(double));
         cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
         cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 16 * sizeof(int));
         cudaError_t e4 = cudaMallocHost((void**)&ctx->h_counts, (MAX_SHARDS + 1) * sizeof(int));
@@ -2167,6 +2360,110 @@ int scvt_shard_finish_ex(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
     return SCVT_OK;
 }
 
+// ---------------------------------------------------------------------- arithmetic-layout slices
+int scvt_slice_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi) {
+    if (world < 1 || rank < 0 || rank >= world || SCVT_CHUNKS % world) return SCVT_ERR_CONFIG;
+    const int64_t ch = std::max<int64_t>(1, (n + SCVT_CHUNKS - 1) / SCVT_CHUNKS);
+    const int64_t nc = SCVT_CHUNKS / world;
+    *lo = std::min<int64_t>(n, rank * nc * ch);
+    *hi = std::min<int64_t>(n, (rank + 1) * nc * ch);
+    return SCVT_OK;
+}
+
+int scvt_slice_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                      const double* res_all, int rank, int world, double* grad, double* first,
+                      double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                      double* red) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, rank, world, &ck));
+    cudaStream_t s = ctx->stream;
+    const int64_t rows = scvt_shard_rows(n, nshards) * nshards;
+    if (ck.len)
+        CK(cudaMemsetAsync(ctx->d_egen + ck.lo, 0xFF, ck.len * sizeof(double), s));   // NaN
+    k_unpack_slice<<<blocks_for(rows, 128), 128, 0, s>>>(
+        res_all, (int)rows, ck.lo, ck.lo + ck.len, z, grad, first, mass, lloyd_diag,
+        ctx->d_egen, ctx->d_g2gen, ctx->d_obgen);
+    LAUNCHED();
+    TRY(eval_scalars_phase(ctx, ck, lloyd_diag, grad, q3, norms, red));
+    ctx->cycles_n = n;   // every rank holds all n certified cycles: the next evaluation may reuse them
+    return SCVT_OK;
+}
+
+int scvt_slice_scalars(scvt_ctx* ctx, const double* red, double* scalars_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    static const unsigned char ops[5] = {0, 0, 0, 2, 0};
+    TRY(reduce_chunks(ctx, red, 5, ops));
+    TRY(readback(ctx, 5));
+    if (ctx->h_status[0]) return status_to_code(ctx, ctx->h_status[0]);
+    if (std::isnan(ctx->h_scal[0]))
+        return fail(ctx, SCVT_ERR_COVERAGE, "shard results do not cover every generator");
+    scalars_host[0] = ctx->h_scal[0];
+    scalars_host[1] = sqrt(ctx->h_scal[1]);
+    scalars_host[2] = ctx->h_scal[2];
+    scalars_host[3] = ctx->h_scal[3];
+    scalars_host[4] = ctx->h_scal[4];
+    return SCVT_OK;
+}
+
+int scvt_slice_gram(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
+                    int64_t n, int rank, int world, double* red, int32_t* nval_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, rank, world, &ck));
+    *nval_host = gram_values(ctx->hist_count);
+    return gram_phase(ctx, g, lloyd_diag, gamma, ck, red);
+}
+
+int scvt_slice_combine(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
+                       const double* z, int64_t n, int rank, int world, const double* red_gram,
+                       double* q3, double* red) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, rank, world, &ck));
+    return combine_phase(ctx, g, lloyd_diag, gamma, z, ck, red_gram, q3, red);
+}
+
+int scvt_slice_tangent(scvt_ctx* ctx, const double* q, const double* z, const double* g,
+                       int64_t n, int rank, int world, double* q3, double* red) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, rank, world, &ck));
+    TRY(prep_red(ctx, red, 1, ck));
+    k_tangent<<<ck.nc, RED_THREADS, 0, ctx->stream>>>(q, z, g, ck, q3, red);
+    LAUNCHED();
+    return SCVT_OK;
+}
+
+int scvt_slice_history_pair(scvt_ctx* ctx, const double* z_old, const double* z_new,
+                            const double* g_old, const double* g_new, int64_t n, int rank,
+                            int world, double* red, int32_t* nval_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, rank, world, &ck));
+    int nval = 0;
+    TRY(pair_phase(ctx, z_old, z_new, g_old, g_new, ck, red, &nval));
+    *nval_host = nval;
+    return SCVT_OK;
+}
+
+int scvt_slice_history_commit(scvt_ctx* ctx, const double* red, int64_t n, int rank, int world,
+                              int32_t* pushed_host, double* movement_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, rank, world, &ck));
+    return commit_phase(ctx, red, ck.len, pushed_host, movement_host);
+}
+
+int scvt_reduce_chunks(scvt_ctx* ctx, const double* red, int32_t nval, const uint8_t* ops,
+                       double* out_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    TRY(reduce_chunks(ctx, red, nval, ops));
+    TRY(readback(ctx, nval));
+    for (int v = 0; v < nval; ++v) out_host[v] = ctx->h_scal[v];
+    return SCVT_OK;
+}
+
 // ---------------------------------------------------------------------- optimizer algebra
 int scvt_history_clear(scvt_ctx* ctx) {
     if (!ctx) return SCVT_ERR_CONFIG;
@@ -2192,71 +2489,23 @@ int scvt_history_gamma(scvt_ctx* ctx, double* gamma_host) {
 int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new, const double* g_old,
                       const double* g_new, int64_t n, int32_t* pushed_host, double* movement_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
-    int64_t len = 3 * n;
-    // candidate slot: the next one in the ring (overwrites the oldest when full)
-    int slot = (ctx->hist_head + ctx->hist_count) % ctx->m;
-    // stage into tmp buffers so a rejected pair never clobbers the oldest stored one
-    k_history_pair<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(
-        z_old, z_new, g_old, g_new, len, ctx->d_tmp_s, ctx->d_tmp_y, ctx->d_partials);
-    LAUNCHED();
-    const int K = ctx->hist_count;
-    HistPtrs hp = hist_ptrs(ctx);
-    TRY(launch_cross(ctx, K, hp, len));
-    k_history_finish<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials, ctx->d_scal);
-    LAUNCHED();
-    if (K) {
-        k_reduce_stage2<0><<<1, RED_THREADS, 0, ctx->stream>>>(ctx->d_partials + 4 * RED_BLOCKS,
-                                                               2 * K, ctx->d_scal + 4);
-        LAUNCHED();
-    }
-    TRY(readback(ctx, 4 + 2 * K));
-    double ys = ctx->h_scal[0], ss = ctx->h_scal[1], yy = ctx->h_scal[2];
-    *movement_host = ctx->h_scal[3];
-    if (ys <= 1e-14 * sqrt(ss) * sqrt(yy)) {   // optimizer.py:98-104
-        *pushed_host = 0;
-        return SCVT_OK;
-    }
-    // swap the staged vectors into the ring slot (pointer-free copy on the device)
-    CK(cudaMemcpyAsync(ctx->d_S + (int64_t)slot * 3 * ctx->n_max, ctx->d_tmp_s,
-                       len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->d_Y + (int64_t)slot * 3 * ctx->n_max, ctx->d_tmp_y,
-                       len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-    ctx->launches += 2;
-    ctx->rho[slot] = 1.0 / ys;
-    ctx->ys[slot] = ys;
-    ctx->yy[slot] = yy;
-    for (int k = 0; k < K; ++k) {                 // cross products with the kept pairs
-        const int sk = (ctx->hist_head + k) % ctx->m;
-        if (sk == slot) continue;                 // the pair being overwritten
-        ctx->YS[slot][sk] = ctx->h_scal[4 + k];       // y_new . s_k
-        ctx->YS[sk][slot] = ctx->h_scal[4 + K + k];   // y_k . s_new
-    }
-    ctx->YS[slot][slot] = ys;
-    if (ctx->hist_count < ctx->m) ++ctx->hist_count;
-    else ctx->hist_head = (ctx->hist_head + 1) % ctx->m;
-    *pushed_host = 1;
-    return SCVT_OK;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, 0, 1, &ck));
+    // staged into tmp buffers so a rejected pair never clobbers the oldest stored one
+    int nval = 0;
+    TRY(pair_phase(ctx, z_old, z_new, g_old, g_new, ck, ctx->d_partials, &nval));
+    return commit_phase(ctx, ctx->d_partials, ck.len, pushed_host, movement_host);
 }
 
 int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
                                  double gamma, const double* z, int64_t n, double* q3,
                                  double* out_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
-    const int K = ctx->hist_count;
-    HistPtrs hp = hist_ptrs(ctx);
-    if (K) {
-        TRY(launch_gram(ctx, K, g, lloyd_diag, gamma, hp, n));
-        GramScalars gs;
-        for (int i = 0; i < K; ++i) {
-            const int si = (ctx->hist_head + i) % ctx->m;
-            gs.rho[i] = ctx->rho[si];
-            for (int j = 0; j < K; ++j) gs.ys[i][j] = ctx->YS[si][(ctx->hist_head + j) % ctx->m];
-        }
-        k_gram_recursion<<<1, 1024, 0, ctx->stream>>>(ctx->d_partials, K, gs, ctx->d_coef);
-        LAUNCHED();
-    }
-    TRY(launch_combine(ctx, K, g, lloyd_diag, gamma, hp, z, n, q3));
-    TRY(finish_slots(ctx, 2));
+    Chunks ck;
+    TRY(make_chunks(ctx, n, 0, 1, &ck));
+    TRY(gram_phase(ctx, g, lloyd_diag, gamma, ck, ctx->d_partials));
+    TRY(combine_phase(ctx, g, lloyd_diag, gamma, z, ck, ctx->d_partials, q3, ctx->d_partials));
+    TRY(reduce_chunks(ctx, ctx->d_partials, 2, nullptr));
     TRY(readback(ctx, 2));
     out_host[0] = ctx->h_scal[0];   // q . g
     out_host[1] = ctx->h_scal[1];   // dphi0 = g . q3
@@ -2303,9 +2552,11 @@ int scvt_lbfgs_direction(scvt_ctx* ctx, const double* g, const double* lloyd_dia
 int scvt_tangent_project(scvt_ctx* ctx, const double* q, const double* z, const double* g,
                          int64_t n, double* q3, double* dphi0_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
-    k_tangent<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(q, z, g, n, q3, ctx->d_partials);
+    Chunks ck;
+    TRY(make_chunks(ctx, n, 0, 1, &ck));
+    k_tangent<<<ck.nc, RED_THREADS, 0, ctx->stream>>>(q, z, g, ck, q3, ctx->d_partials);
     LAUNCHED();
-    TRY(finish_slots(ctx, 1));
+    TRY(reduce_chunks(ctx, ctx->d_partials, 1, nullptr));
     TRY(readback(ctx, 1));
     *dphi0_host = ctx->h_scal[0];
     return SCVT_OK;
@@ -2322,9 +2573,11 @@ int scvt_trial_point(scvt_ctx* ctx, const double* z, const double* q3, double al
 int scvt_directional_derivative(scvt_ctx* ctx, const double* g, const double* q3,
                                 const double* norms, int64_t n, double* d_host) {
     if (!ctx) return SCVT_ERR_CONFIG;
-    k_dirderiv<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(g, q3, norms, n, ctx->d_partials);
+    Chunks ck;
+    TRY(make_chunks(ctx, n, 0, 1, &ck));
+    k_dirderiv<<<ck.nc, RED_THREADS, 0, ctx->stream>>>(g, q3, norms, ck, ctx->d_partials);
     LAUNCHED();
-    TRY(finish_slots(ctx, 1));
+    TRY(reduce_chunks(ctx, ctx->d_partials, 1, nullptr));
     TRY(readback(ctx, 1));
     *d_host = ctx->h_scal[0];
     return SCVT_OK;

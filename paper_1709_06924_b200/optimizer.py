@@ -139,11 +139,29 @@ def wolfe_line_search(phi, f0: float, dphi0: float, c1: float = WOLFE_C1, c2: fl
 
 
 class _DeviceOps:
-    """Thin wrappers over the optimizer entry points of the C ABI."""
+    """Thin wrappers over the optimizer entry points of the C ABI (one GPU: every vector holds
+    all n rows).  `parallel.SliceOps` is the arithmetic-layout counterpart of one rank."""
 
     def __init__(self, ctx, n: int):
         self.ctx = ctx
         self.n = n
+
+    # -- layout: one GPU holds every row
+    def vec3(self, z):
+        """An (owned rows, 3) work vector (q, q3)."""
+        return z.new_empty(z.shape)
+
+    def positions(self, z):
+        """A full (n, 3) position buffer that trial / Lloyd points are written into."""
+        return z.new_empty(z.shape)
+
+    def scalars(self, z):
+        """An (owned rows,) work vector (trial norms)."""
+        return z.new_empty(z.shape[0])
+
+    def full(self, res: EvalResult) -> EvalResult:
+        """The result with every row (the owned rows are all of them here)."""
+        return res
 
     def history_clear(self):
         self.ctx.call("scvt_history_clear")
@@ -239,15 +257,15 @@ class Minimizer:
         self.z = z.clone()
         self.k = self.z.shape[0]
         self.ctx = evaluator._ensure_ctx(self.k, corrections)
-        self.ops = _DeviceOps(self.ctx, self.k)
+        self.ops = evaluator.optimizer_ops(self.ctx, self.k)
         self.ops.normalize(self.z)                               # optimizer.py:290
         self.res = evaluator.evaluate_device(self.z)             # optimizer.py:293
         self.fevals = 1
         self.ops.history_clear()                                 # CorrectionHistory(m)
         self.resets = 0
         self.n = 0
-        self.q = torch.empty_like(self.z)
-        self.q3 = torch.empty_like(self.z)
+        self.q = self.ops.vec3(self.z)
+        self.q3 = self.ops.vec3(self.z)
 
     def step(self):
         """One iteration (optimizer.py:300-366).  Returns (record, movement, z_new, res_new)
@@ -258,7 +276,7 @@ class Minimizer:
         n = self.n
         t_iter = time.perf_counter()
         if self.method == "lloyd":
-            z_new = torch.empty_like(z)
+            z_new = ops.positions(z)
             ops.lloyd(res.first, z_new)                          # optimizer.py:304
             res_new = ev.evaluate_device(z_new)
             self.fevals += 1
@@ -287,8 +305,8 @@ class Minimizer:
                     dphi0 = ops.tangent(q, z, res.grad, q3)
 
             def phi(alpha, z=z, q3=q3):
-                zt = torch.empty_like(z)
-                norms = torch.empty(k, dtype=torch.float64, device=z.device)
+                zt = ops.positions(z)
+                norms = ops.scalars(z)
                 ops.trial(z, q3, alpha, zt, norms)
                 r = ev.evaluate_device(zt, q3, norms)            # derivative fused in
                 return r.energy, r.dirderiv, (zt, r)
@@ -303,7 +321,7 @@ class Minimizer:
                 logger.warning("line search failed at iteration %d (%s); Lloyd fallback", n, exc)
                 ops.history_clear()
                 self.resets += 1
-                z_new = torch.empty_like(z)
+                z_new = ops.positions(z)
                 ops.lloyd(res.first, z_new)
                 res_new = ev.evaluate_device(z_new)
                 fevals_iter = 1
@@ -321,7 +339,9 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
     """Drive one of the iteration methods to a stopping criterion (optimizer.py:278-391).
 
     ``points``: (K, 3) NumPy array or CUDA tensor.  ``callback(n, z_new, res_new)`` receives
-    CUDA tensors (zero-copy).  Returns NumPy ``points`` and ``final``."""
+    CUDA tensors (zero-copy; under a multi-GPU `ShardedMeshEvaluator` the vectors of res_new
+    hold the rank's arithmetic slice, `parallel.SliceOps`).  Returns NumPy ``points`` and
+    ``final`` (all rows)."""
     criteria = criteria or StoppingCriteria()
     t0 = time.perf_counter()
     st = Minimizer(points, method, evaluator, corrections)
@@ -345,7 +365,7 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
             break
     st.torch.cuda.current_stream().synchronize()
     wall = time.perf_counter() - t0
-    final, points = _to_host(st.res, st.z)
+    final, points = _to_host(st.ops.full(st.res), st.z)
     return MinimizeResult(points=points, records=records, reason=reason,
                           fevals=st.fevals, resets=st.resets, wall_time=wall, final=final)
 

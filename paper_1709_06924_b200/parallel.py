@@ -17,10 +17,16 @@ rank certifies its owned cells at the new positions, the bad flags are all-reduc
 every rank derives the same bad set and re-check list, rebuilds its own bad cells, and only
 those cycles are all-gathered; up to four rounds, then the full path above.
 
-Positions and LBFGS state are replicated, so every rank runs the identical optimizer control
-flow, and the outputs are bitwise identical to the single-GPU `scvt_evaluate` for any rank
-count (tests/test_gpu_parity.py emulates 2/3/8 shards on one GPU).  Errors are agreed on by an
-all-reduce of the status word before anyone raises, so no rank is left in a collective.
+Positions are replicated; the optimizer's vectors are in arithmetic layout (`SliceOps`): rank r
+owns a contiguous range of whole chunks of the generator ids (include/scvt_b200.h,
+SCVT_CHUNKS) and holds only those rows of the gradient, first moments, Lloyd diagonal, search
+direction and LBFGS history.  Every dot product is reduced per chunk, the partial buffers are
+summed over the ranks by one all-reduce per phase (each entry has a single non-zero
+contributor, so the sum is exact), and every rank reduces the chunk partials in the same fixed
+order: all ranks see the same scalars, run the identical control flow, and the run is bitwise
+the single-GPU run for any rank count.  New positions are computed per slice and
+all-gathered.  Errors are agreed on by an all-reduce of the status word before anyone raises,
+so no rank is left in a collective.
 
 `ShardedMeshEvaluator` is backend-agnostic: `CudaShardBackend` drives the C ABI; the CPU test
 suite plugs a NumPy backend into the same orchestration under gloo (tests/test_parallel_gloo.py).
@@ -119,6 +125,28 @@ class CudaShardBackend:
                           min_diag=float(sc[3]),
                           dirderiv=float(sc[4]) if q3 is not None else float("nan"))
 
+    def finish_slice(self, z, nshards, res_all, rank, world, red, reduce_sum, q3=None,
+                     norms=None) -> EvalResult:
+        """Arithmetic-layout finish: the rank's rows of every output, the evaluation scalars
+        reduced over the chunks of all ranks (include/scvt_b200.h scvt_slice_finish)."""
+        n = z.shape[0]
+        lo, hi = slice_range(n, rank, world)
+        ctx = self.ev._ensure_ctx(n)
+        grad = z.new_empty((hi - lo, 3))
+        first = z.new_empty((hi - lo, 3))
+        mass = z.new_empty(hi - lo)
+        diag = z.new_empty(hi - lo)
+        ctx.call("scvt_slice_finish", _lib.dptr(z), n, nshards, _lib.dptr(res_all), rank, world,
+                 _lib.dptr(grad), _lib.dptr(first), _lib.dptr(mass), _lib.dptr(diag),
+                 _lib.dptr(q3), _lib.dptr(norms), _lib.dptr(red), what="slice_finish")
+        reduce_sum(red[:5 * CHUNKS])
+        sc = (ctypes.c_double * 5)()
+        ctx.call("scvt_slice_scalars", _lib.dptr(red), sc, what="evaluate (sharded)")
+        return EvalResult(energy=float(sc[0]), grad=grad, grad_norm=float(sc[1]),
+                          lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]),
+                          min_diag=float(sc[3]),
+                          dirderiv=float(sc[4]) if q3 is not None else float("nan"))
+
     def buffers(self, n, nshards, device):
         import torch
 
@@ -127,6 +155,191 @@ class CudaShardBackend:
                 torch.empty((nshards * r, CYC_ROW), dtype=torch.int32, device=device),
                 torch.empty((r, RES_ROW), dtype=torch.float64, device=device),
                 torch.empty((nshards * r, RES_ROW), dtype=torch.float64, device=device))
+
+
+CHUNKS = 1184         # include/scvt_b200.h SCVT_CHUNKS
+MAX_RED_VALS = 176    # partial values per phase (Gram pass with m <= 16)
+
+
+def slice_range(n: int, rank: int, world: int):
+    """Owned generator ids [lo, hi) of the arithmetic layout (include/scvt_b200.h
+    scvt_slice_range): whole chunks [rank C/W, (rank+1) C/W) of ceil(n/C) ids."""
+    if world < 1 or CHUNKS % world:
+        raise ValueError(f"the world size must divide {CHUNKS}, got {world}")
+    ch = max(1, -(-n // CHUNKS))
+    nc = CHUNKS // world
+    return min(n, rank * nc * ch), min(n, (rank + 1) * nc * ch)
+
+
+def slice_pad(n: int, world: int) -> int:
+    """Rows per rank in a gathered buffer: the slices laid end to end, the last one padded."""
+    return (CHUNKS // world) * max(1, -(-n // CHUNKS))
+
+
+def _padded_view(t, rows: int):
+    """The (rows, ...) tensor over the whole storage of a [:n] view made by `_padded`."""
+    import torch
+
+    full = torch.empty(0, dtype=t.dtype, device=t.device)
+    return full.set_(t.untyped_storage(), 0, (rows,) + tuple(t.shape[1:]))
+
+
+def _padded(n: int, world: int, cols, like):
+    """A [:n] view of a (world * pad, cols) buffer: the layout the slice all-gather fills."""
+    import torch
+
+    shape = (world * slice_pad(n, world),) + ((cols,) if cols else ())
+    return torch.empty(shape, dtype=like.dtype, device=like.device)[:n]
+
+
+def _gather_slices(full, rank: int, world: int, group):
+    """All-gather the owned block of every rank into `full` (a [:n] view from `_padded`)."""
+    n = full.shape[0]
+    pad = slice_pad(n, world)
+    buf = _padded_view(full, world * pad)
+    _all_gather(buf, buf[rank * pad:(rank + 1) * pad].clone(), group)
+    return full
+
+
+def _all_reduce_sum(t, group):
+    import torch.distributed as dist
+
+    if dist.get_backend(group) != "nccl" and t.device.type != "cpu":
+        h = t.cpu()                          # gloo: staged through host memory
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+        return t
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+class SliceOps:
+    """The optimizer's vector algebra on one rank of the arithmetic layout (include/scvt_b200.h
+    "arithmetic-layout slices"): the same methods as `optimizer._DeviceOps`, each a chunked
+    C call, one all-reduce SUM of the chunk partials, and the fixed-order finish.  Positions
+    stay replicated; trial and Lloyd points are computed on the owned rows and all-gathered."""
+
+    def __init__(self, ctx, n: int, rank: int, world: int, group=None, reduce_sum=None,
+                 gather=None):
+        import torch
+
+        self.ctx, self.n, self.rank, self.world, self.group = ctx, n, rank, world, group
+        self.lo, self.hi = slice_range(n, rank, world)
+        self.len = self.hi - self.lo
+        self.red = torch.zeros(MAX_RED_VALS * CHUNKS, dtype=torch.float64,
+                               device=f"cuda:{ctx.device}")
+        self._reduce_sum = reduce_sum or (lambda t: _all_reduce_sum(t, group))
+        self._gather = gather or (lambda full: _gather_slices(full, rank, world, group))
+
+    def _sum(self, nval: int):
+        if nval:
+            self._reduce_sum(self.red[:nval * CHUNKS])
+
+    def _rows(self, t):
+        return t[self.lo:self.hi]
+
+    # -- layout
+    def vec3(self, z):
+        return z.new_empty((self.len, 3))
+
+    def scalars(self, z):
+        return z.new_empty(self.len)
+
+    def positions(self, z):
+        return _padded(self.n, self.world, 3, z)
+
+    def full(self, res: EvalResult) -> EvalResult:
+        def g(t, cols):
+            out = _padded(self.n, self.world, cols, t)
+            out[self.lo:self.hi] = t
+            return self._gather(out)
+
+        return EvalResult(energy=res.energy, grad=g(res.grad, 3), grad_norm=res.grad_norm,
+                          lloyd_diag=g(res.lloyd_diag, 0), first=g(res.first, 3),
+                          migration=res.migration, mass=g(res.mass, 0),
+                          obtuse_count=res.obtuse_count, min_diag=res.min_diag,
+                          dirderiv=res.dirderiv)
+
+    # -- history
+    def history_clear(self):
+        self.ctx.call("scvt_history_clear")
+
+    def gamma(self) -> float:
+        g = ctypes.c_double()
+        self.ctx.call("scvt_history_gamma", ctypes.byref(g))
+        return g.value
+
+    def push(self, z_old, z_new, g_old, g_new):
+        nval = ctypes.c_int32()
+        red = _lib.dptr(self.red)
+        self.ctx.call("scvt_slice_history_pair", _lib.dptr(self._rows(z_old)),
+                      _lib.dptr(self._rows(z_new)), _lib.dptr(g_old), _lib.dptr(g_new), self.n,
+                      self.rank, self.world, red, ctypes.byref(nval))
+        self._sum(nval.value)
+        pushed = ctypes.c_int32()
+        mv = ctypes.c_double()
+        self.ctx.call("scvt_slice_history_commit", red, self.n, self.rank, self.world,
+                      ctypes.byref(pushed), ctypes.byref(mv))
+        return bool(pushed.value), mv.value
+
+    # -- directions
+    def _reduce(self, nval: int):
+        out = (ctypes.c_double * nval)()
+        self.ctx.call("scvt_reduce_chunks", _lib.dptr(self.red), nval, None, out)
+        return list(out)
+
+    def direction_tangent(self, g, diag, gamma, z, q3):
+        nval = ctypes.c_int32()
+        red = _lib.dptr(self.red)
+        self.ctx.call("scvt_slice_gram", _lib.dptr(g), _lib.dptr(diag), float(gamma), self.n,
+                      self.rank, self.world, red, ctypes.byref(nval))
+        self._sum(nval.value)
+        self.ctx.call("scvt_slice_combine", _lib.dptr(g), _lib.dptr(diag), float(gamma),
+                      _lib.dptr(self._rows(z)), self.n, self.rank, self.world, red,
+                      _lib.dptr(q3), red)
+        self._sum(2)
+        qg, dphi0 = self._reduce(2)
+        return qg, dphi0
+
+    def scale(self, a, x, y):
+        self.ctx.call("scvt_scale", float(a), _lib.dptr(x), x.numel(), _lib.dptr(y))
+
+    def tangent(self, q, z, g, q3) -> float:
+        self.ctx.call("scvt_slice_tangent", _lib.dptr(q), _lib.dptr(self._rows(z)), _lib.dptr(g),
+                      self.n, self.rank, self.world, _lib.dptr(q3), _lib.dptr(self.red))
+        self._sum(1)
+        return self._reduce(1)[0]
+
+    # -- new positions (owned rows, then all-gathered)
+    def trial(self, z, q3, alpha, zt, norms):
+        self.ctx.call("scvt_trial_point", _lib.dptr(self._rows(z)), _lib.dptr(q3), float(alpha),
+                      self.len, _lib.dptr(self._rows(zt)), _lib.dptr(norms))
+        self._gather(zt)
+
+    def lloyd(self, first, z_out):
+        import torch
+
+        from .errors import CentroidAtOriginError
+
+        bad = torch.zeros(CHUNKS, dtype=torch.float64, device=z_out.device)
+        try:
+            self.ctx.call("scvt_lloyd_step", _lib.dptr(first), self.len,
+                          _lib.dptr(self._rows(z_out)), what="lloyd_step")
+        except CentroidAtOriginError:
+            bad[self.rank] = 1.0
+        self._reduce_sum(bad)                        # everyone raises, or no one
+        if float(bad.sum()) > 0.0:
+            raise CentroidAtOriginError("a first moment is ~0 (Lloyd step)")
+        self._gather(z_out)
+
+    # -- replicated positions: computed identically on every rank
+    def max_abs_diff(self, a, b) -> float:
+        m = ctypes.c_double()
+        self.ctx.call("scvt_max_abs_diff", _lib.dptr(a), _lib.dptr(b), a.numel(), ctypes.byref(m))
+        return m.value
+
+    def normalize(self, z):
+        self.ctx.call("scvt_normalize_rows", _lib.dptr(z), self.n)
 
 
 def _all_gather(out, inp, group):
@@ -193,8 +406,9 @@ def _all_reduce_max(t, group):
 
 
 def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=None,
-                     q3=None, norms=None):
-    """One evaluation on rank `rank` of `world` (collectives through torch.distributed)."""
+                     q3=None, norms=None, finish=None):
+    """One evaluation on rank `rank` of `world` (collectives through torch.distributed).
+    `finish(res_all)`, when given, replaces the replicated finish (arithmetic layout)."""
     import torch
 
     n = z.shape[0]
@@ -220,6 +434,8 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
     if int(st.item()):
         backend.raise_status(int(st.item()))
     _all_gather(res_all, res_send, group)
+    if finish is not None:
+        return finish(res_all)
     if q3 is None:
         return backend.finish(z, world, res_all)
     return backend.finish(z, world, res_all, q3, norms)
@@ -279,15 +495,50 @@ class ShardedMeshEvaluator(MeshEvaluator):
             self.rank, self.world = 0, 1
         self.backend = backend or CudaShardBackend(self)
 
+        self._red = None
+
+    def optimizer_ops(self, ctx, n: int):
+        """One GPU: the all-rows algebra; several: this rank's arithmetic slice."""
+        if self.world == 1:
+            return super().optimizer_ops(ctx, n)
+        return SliceOps(ctx, n, self.rank, self.world, self.group)
+
+    def _sum(self, t):
+        return _all_reduce_sum(t, self.group)
+
     def evaluate_device(self, z, q3=None, norms=None) -> EvalResult:
+        """World size 1: all rows.  Several ranks: the vectors of the result hold this rank's
+        arithmetic slice (`slice_range`); the scalars are global."""
         if self.world == 1:
             r = emulate_shards(self.backend, z, 1, q3, norms)
         else:
-            r = sharded_evaluate(self.backend, z, self.rank, self.world, self.group, q3=q3,
-                                 norms=norms)
+            import torch
+
+            if self._red is None:
+                self._red = torch.zeros(MAX_RED_VALS * CHUNKS, dtype=torch.float64,
+                                        device=z.device)
+            r = sharded_evaluate(
+                self.backend, z, self.rank, self.world, self.group, q3=q3, norms=norms,
+                finish=lambda res_all: self.backend.finish_slice(
+                    z, self.world, res_all, self.rank, self.world, self._red, self._sum, q3,
+                    norms))
         self.evaluations += 1
         return r
 
+    def evaluate(self, points) -> EvalResult:
+        """pipeline.py:261-279 with every row on every rank."""
+        from .pipeline import to_numpy
 
-__all__ = ["ShardedMeshEvaluator", "CudaShardBackend", "sharded_evaluate", "emulate_shards",
-           "shard_rows", "shard_range"]
+        z, host = self._as_device(points)
+        r = self.evaluate_device(z)
+        if self.world > 1:
+            r = SliceOps(self._ensure_ctx(z.shape[0]), z.shape[0], self.rank, self.world,
+                         self.group).full(r)
+        if host:
+            r.grad, r.first, r.mass, r.lloyd_diag = to_numpy(r.grad, r.first, r.mass,
+                                                             r.lloyd_diag)
+        return r
+
+
+__all__ = ["ShardedMeshEvaluator", "CudaShardBackend", "SliceOps", "sharded_evaluate",
+           "emulate_shards", "shard_rows", "shard_range", "slice_range"]

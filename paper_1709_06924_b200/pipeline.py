@@ -205,6 +205,12 @@ class MeshEvaluator:
         """No decomposition state on the global GPU path (pipeline.py:157-162)."""
         return None
 
+    def optimizer_ops(self, ctx, n: int):
+        """The optimizer's vector algebra for this evaluator's layout (one GPU: all rows)."""
+        from .optimizer import _DeviceOps
+
+        return _DeviceOps(ctx, n)
+
     # -- evaluation -------------------------------------------------------------------
     def _as_device(self, points):
         torch = _torch()

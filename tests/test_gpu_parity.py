@@ -504,15 +504,18 @@ def _two_rank_worker(rank, world, port, z0, out):
         with ShardedMeshEvaluator(P.density_preset("c4"), "7pt", subdivision=3) as ev:
             r = P.minimize(z0, "lloyd-plbfgs", ev, crit, corrections=7)
         out[rank] = {"points": r.points, "energies": [h.energy for h in r.records],
-                     "fevals": r.fevals}
+                     "fevals": r.fevals, "grad": r.final.grad, "diag": r.final.lloyd_diag}
     finally:
         dist.destroy_process_group()
 
 
-def test_two_processes_sharded_run_matches_single_gpu():
-    """Two real ranks (separate processes and contexts, gloo collectives staged through host
-    memory, both on cuda:0 — host-mediated exchanges, no kernel waits on another rank) run
-    the sharded P-LBFGS path incl. cycle reuse; bitwise equal to the single-GPU run."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_two_processes_sharded_run_matches_single_gpu(world):
+    """Real ranks (separate processes and contexts, gloo collectives staged through host
+    memory, all on cuda:0 — host-mediated exchanges, no kernel waits on another rank) run
+    the sharded P-LBFGS path: cells sharded with cycle reuse, the optimizer's vectors in
+    arithmetic layout (parallel.SliceOps: chunk partials summed over the ranks); bitwise equal
+    to the single-GPU run."""
     import socket
 
     import torch.multiprocessing as mp
@@ -522,14 +525,16 @@ def test_two_processes_sharded_run_matches_single_gpu():
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     out = mp.Manager().dict()
-    mp.spawn(_two_rank_worker, args=(2, port, z0, out), nprocs=2, join=True)
+    mp.spawn(_two_rank_worker, args=(world, port, z0, out), nprocs=world, join=True)
     with _ev("c4", "7pt", 3) as ev:
         ref = P.minimize(z0, "lloyd-plbfgs", ev, P.StoppingCriteria(max_iterations=6),
                          corrections=7)
-    for rank in (0, 1):
+    for rank in range(world):
         assert np.array_equal(out[rank]["points"], ref.points)
         assert out[rank]["energies"] == [h.energy for h in ref.records]
         assert out[rank]["fevals"] == ref.fevals
+        assert np.array_equal(out[rank]["grad"], ref.final.grad)
+        assert np.array_equal(out[rank]["diag"], ref.final.lloyd_diag)
 
 
 @pytest.mark.parametrize("sharded", [False, True])
