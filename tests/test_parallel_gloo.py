@@ -255,3 +255,68 @@ def test_gloo_cycle_reuse_rounds():
         np.testing.assert_allclose(out[rank]["first"], ref.first, rtol=0, atol=1e-15)
         assert abs(out[rank]["energy"] - ref.energy) <= 1e-14 * ref.energy
     np.testing.assert_array_equal(out[0]["first"], out[1]["first"])
+
+
+# ---- arithmetic layout (parallel.SliceOps): partition, exact chunk-partial exchange, gathers
+def _chunk_dots(a, b, n, lo, hi, world):
+    """NumPy stand-in of a chunked dot-product phase (include/scvt_b200.h slices): per chunk
+    partials of the owned rows, zeros elsewhere."""
+    from paper_1709_06924_b200.parallel import CHUNKS
+
+    ch = max(1, -(-n // CHUNKS))
+    red = np.zeros(CHUNKS)
+    for c in range(CHUNKS):
+        c0, c1 = max(lo, c * ch), min(hi, (c + 1) * ch)
+        if c0 < c1:
+            red[c] = float(np.sum(a[c0:c1] * b[c0:c1]))
+    return red
+
+
+def _slice_worker(rank, world, port, out):
+    from paper_1709_06924_b200.parallel import (_all_reduce_sum, _gather_slices, _padded,
+                                                slice_range)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 40962
+        rng = np.random.default_rng(3)
+        a, b = rng.standard_normal(n), rng.standard_normal(n)
+        lo, hi = slice_range(n, rank, world)
+        red = torch.from_numpy(_chunk_dots(a, b, n, lo, hi, world))
+        _all_reduce_sum(red, None)
+        z = torch.from_numpy(rng.standard_normal((n, 3)))
+        full = _padded(n, world, 3, z)
+        full[lo:hi] = z[lo:hi]                     # only the owned rows are valid locally
+        _gather_slices(full, rank, world, None)
+        out[rank] = {"red": red.numpy().copy(), "lohi": (lo, hi), "full": full.numpy().copy(),
+                     "z": z.numpy()}
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_arithmetic_slices(world):
+    """Rank slices tile [0, n) with whole chunks; the all-reduced chunk partials equal the
+    single-process partials bitwise (one non-zero contributor per entry); the padded
+    all-gather reassembles the owned rows of every rank."""
+    from paper_1709_06924_b200.parallel import CHUNKS, slice_range
+
+    for n in (4, 2562, 40962, 655362, 2621442):
+        for w in (1, 2, 4, 8):
+            bounds = [slice_range(n, r, w) for r in range(w)]
+            assert bounds[0][0] == 0 and bounds[-1][1] == n
+            assert all(bounds[r][1] == bounds[r + 1][0] for r in range(w - 1))
+    with pytest.raises(ValueError):
+        slice_range(100, 0, 3)                    # 3 does not divide the chunk count
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_slice_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    n = 40962
+    rng = np.random.default_rng(3)
+    a, b = rng.standard_normal(n), rng.standard_normal(n)
+    ref = _chunk_dots(a, b, n, 0, n, 1)
+    for r in range(world):
+        assert np.array_equal(out[r]["red"], ref)
+        assert np.array_equal(out[r]["full"], out[r]["z"])
+    assert len(ref) == CHUNKS
