@@ -51,6 +51,7 @@ constexpr int QUAD_THREADS = 128;
 #define QUAD_MINB2 3     // two-centre fast path
 #endif
 constexpr int CELL_THREADS = 64;
+constexpr int PART_ROW = 10;         // per-incidence partials: [half][m, cx, cy, cz, E]
 constexpr int MAX_SLOTS = 64;        // partial-sum slots
 constexpr int MAX_SHARDS = 256;      // sharded evaluation: ranks per evaluation
 
@@ -311,7 +312,7 @@ struct QuadArgs {
     const double* table;  // device rho^(1/4) table (tanh4 kinds) or null
     int nq;
     DensityParams dp;
-    double* part;         // [5][n_inc] SoA; split mode: [2][5][n_inc] (sub-triangle 0, 1)
+    double* part;         // [n_inc][PART_ROW]: per incidence, sub-triangle 0 then 1 (split mode)
     uint8_t* obtuse;      // [n_inc]
     int* status;
 };
@@ -359,13 +360,11 @@ k_quad(QuadArgs a) {
         subtri_moments<KIND, SPHERE>(f.s[1], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
     }
     if (pole) atomicOr(a.status, ST_POLE);
-    int64_t N = a.n_inc;
-    double* out = a.part + (SPLIT && half ? 5 * N : 0);
-    out[u] = acc[0];
-    out[N + u] = acc[1];
-    out[2 * N + u] = acc[2];
-    out[3 * N + u] = acc[3];
-    out[4 * N + u] = acc[4];
+    // incidence-major: [u][half][m, cx, cy, cz, E] (80 B per incidence, one contiguous run
+    // of 80 * valence bytes per generator for the gathers)
+    double* out = a.part + (int64_t)u * PART_ROW + (SPLIT && half ? 5 : 0);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) out[c] = acc[c];
     if (!SPLIT || half == 0) a.obtuse[u] = (f.obtuse && i < j && i < k) ? 1 : 0;
 }
 
@@ -383,38 +382,45 @@ __device__ __forceinline__ void epilogue(const double* __restrict__ z, int i, do
     g2[i] = gx * gx + gy * gy + gz * gz;
 }
 
-// per generator: fixed-order sum over its incidences, then the gradient epilogue
+// per generator (id order: coalesced outputs): fixed-order sum over its incidences — one
+// contiguous run of 80 * valence bytes of the incidence-major partials — then the gradient
+// epilogue.
+__device__ __forceinline__ void incidence_sums(const double* __restrict__ part, int u0, int u1,
+                                               int split, double* v5) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) v5[c] = 0.0;
+    for (int u = u0; u < u1; ++u) {
+        const double2* r = reinterpret_cast<const double2*>(part + (int64_t)u * PART_ROW);
+        const double2 a0 = r[0], a1 = r[1], a2 = r[2], a3 = r[3], a4 = r[4];
+        const double h0[5] = {a0.x, a0.y, a1.x, a1.y, a2.x};
+        const double h1[5] = {a2.y, a3.x, a3.y, a4.x, a4.y};
+        if (split) {
+#pragma unroll
+            for (int c = 0; c < 5; ++c) v5[c] += h0[c] + h1[c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 5; ++c) v5[c] += h0[c];
+        }
+    }
+}
+
 __global__ void k_gather(const double* __restrict__ z, int n, int cnt,
                          const int* __restrict__ inc_start,
                          const int* __restrict__ inc_base, const int* __restrict__ deg,
                          const double* __restrict__ part, const uint8_t* __restrict__ obtuse,
-                         int64_t n_inc, const int* __restrict__ status, double* __restrict__ grad,
-                         double* __restrict__ first, double* __restrict__ mass,
-                         double* __restrict__ diag, double* __restrict__ e_gen,
-                         double* __restrict__ g2_gen, double* __restrict__ ob_gen, int split) {
+                         int64_t n_inc, double* __restrict__ grad, double* __restrict__ first,
+                         double* __restrict__ mass, double* __restrict__ diag,
+                         double* __restrict__ e_gen, double* __restrict__ g2_gen,
+                         double* __restrict__ ob_gen, int split) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double m = 0, cx = 0, cy = 0, cz = 0, e = 0, ob = 0;
+    double v5[5] = {0, 0, 0, 0, 0}, ob = 0;
     if (inc_start[cnt] == n_inc) {
         const int u0 = inc_base[i], u1 = u0 + deg[i];
-        for (int u = u0; u < u1; ++u) {
-            if (split) {
-                const double* p2 = part + 5 * n_inc;
-                m += part[u] + p2[u];
-                cx += part[n_inc + u] + p2[n_inc + u];
-                cy += part[2 * n_inc + u] + p2[2 * n_inc + u];
-                cz += part[3 * n_inc + u] + p2[3 * n_inc + u];
-                e += part[4 * n_inc + u] + p2[4 * n_inc + u];
-            } else {
-                m += part[u];
-                cx += part[n_inc + u];
-                cy += part[2 * n_inc + u];
-                cz += part[3 * n_inc + u];
-                e += part[4 * n_inc + u];
-            }
-            ob += obtuse[u];
-        }
+        incidence_sums(part, u0, u1, split, v5);
+        for (int u = u0; u < u1; ++u) ob += obtuse[u];
     }
+    const double m = v5[0], cx = v5[1], cy = v5[2], cz = v5[3], e = v5[4];
     epilogue(z, i, cx, cy, cz, grad, diag, g2_gen);
     first[3 * (int64_t)i] = cx; first[3 * (int64_t)i + 1] = cy; first[3 * (int64_t)i + 2] = cz;
     if (mass) mass[i] = m;
@@ -492,7 +498,8 @@ __global__ void k_shard_counts(const int* __restrict__ list, const int* __restri
     if (threadIdx.x == 0) counts[nshards] = total;
 }
 
-// owned slots: fixed-order incidence sums packed as exchange rows
+// owned slots: fixed-order incidence sums packed as exchange rows (slot order: the rows and
+// the incidence runs are both contiguous)
 __global__ void k_gather_pack(int p_lo, int cnt, int cap, const int* __restrict__ ids,
                               const int* __restrict__ inc_base, const int* __restrict__ deg,
                               const double* __restrict__ part, const uint8_t* __restrict__ obtuse,
@@ -506,27 +513,12 @@ __global__ void k_gather_pack(int p_lo, int cnt, int cap, const int* __restrict_
         return;
     }
     int i = ids[p_lo + q];
-    double m = 0, cx = 0, cy = 0, cz = 0, e = 0, ob = 0;
     const int u0 = inc_base[i], u1 = u0 + deg[i];
-    for (int u = u0; u < u1; ++u) {
-        if (split) {
-            const double* p2 = part + 5 * n_inc;
-            m += part[u] + p2[u];
-            cx += part[n_inc + u] + p2[n_inc + u];
-            cy += part[2 * n_inc + u] + p2[2 * n_inc + u];
-            cz += part[3 * n_inc + u] + p2[3 * n_inc + u];
-            e += part[4 * n_inc + u] + p2[4 * n_inc + u];
-        } else {
-            m += part[u];
-            cx += part[n_inc + u];
-            cy += part[2 * n_inc + u];
-            cz += part[3 * n_inc + u];
-            e += part[4 * n_inc + u];
-        }
-        ob += obtuse[u];
-    }
-    row[0] = (double)i; row[1] = m; row[2] = cx; row[3] = cy; row[4] = cz; row[5] = e;
-    row[6] = ob; row[7] = 0.0;
+    double v5[5], ob = 0;
+    incidence_sums(part, u0, u1, split, v5);
+    for (int u = u0; u < u1; ++u) ob += obtuse[u];
+    row[0] = (double)i; row[1] = v5[0]; row[2] = v5[1]; row[3] = v5[2]; row[4] = v5[3];
+    row[5] = v5[4]; row[6] = ob; row[7] = 0.0;
 }
 
 __global__ void k_unpack_results(const double* __restrict__ rows, int nrows, int n,
@@ -1687,8 +1679,8 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
     TRY(incidences_range(ctx, 0, n, n_inc));
     TRY(quad_range(ctx, z, n, 0, n, n_inc));
     k_gather<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
-        z, (int)n, (int)n, ctx->d_inc_start, ctx->d_inc_base, ctx->d_deg, ctx->d_part, ctx->d_obt,
-        n_inc, ctx->d_status, grad, first, mass, diag, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen,
+        z, (int)n, (int)n, ctx->d_inc_start, ctx->d_inc_base, ctx->d_deg, ctx->d_part,
+        ctx->d_obt, n_inc, grad, first, mass, diag, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen,
         ctx->split);
     LAUNCHED();
     return reduce_finish(ctx, n, scalars_host, diag, grad, q3, norms, nsc);
@@ -1965,7 +1957,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_nbr, n * MAXDEG); AL(d_deg, n + 1); AL(d_amb, n * MAXDEG);
     AL(d_inc_start, n + 1); AL(d_inc_gen, n_inc); AL(d_inc_base, n);
     AL(d_pairs, n * MAXDEG * 2); AL(d_cursor, n + 1);
-    AL(d_part, 10 * n_inc); AL(d_obt, n_inc);      // [2][5][n_inc]: split mode uses both
+    AL(d_part, PART_ROW * n_inc); AL(d_obt, n_inc);   // [n_inc][2][5]: split mode uses both halves
     AL(d_egen, n); AL(d_g2gen, n); AL(d_obgen, n);
     AL(d_partials, std::max<int64_t>((int64_t)MAX_SLOTS * RED_BLOCKS, (int64_t)MAX_RED_VALS * CHUNKS));
     AL(d_scal, MAX_RED_VALS);
