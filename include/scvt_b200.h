@@ -233,6 +233,17 @@ int scvt_slice_history_commit(scvt_ctx* ctx, const double* red, int64_t n, int r
 int scvt_reduce_chunks(scvt_ctx* ctx, const double* red, int32_t nval, const uint8_t* ops,
                        double* out_host);
 
+/* covering migration (region-mode bookkeeping; partition.py:123-164, pipeline.py:163-167,
+ * 244-259, optimizer.py:377-381) ----------------------------------------------------------
+ * geometric cell of every point = argmax_c z.centers[c] (ties to the lowest index).
+ * fresh != 0: arithmetic[i] = geometric cell (assign_points without a frozen layout);
+ * otherwise *class_host = 0 in-place, 1 neighbor-move (every moved point's geometric cell is a
+ * one-level neighbour of its arithmetic cell: bit (a, g) of the row-major p x ceil(p/32)
+ * uint32 `adjacency` bitmap), 2 out-of-range (detect_migration). */
+int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* centers, int32_t p,
+                   const uint32_t* adjacency, int32_t* arithmetic, int32_t fresh,
+                   int32_t* class_host);
+
 /* optimizer vector algebra -------------------------------------------------------------
  * CorrectionHistory (optimizer.py:79-114): ring of at most lbfgs_m (s, y) pairs held on
  * the device inside ctx. */

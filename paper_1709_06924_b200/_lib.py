@@ -95,6 +95,8 @@ SIGNATURES = {
     "scvt_slice_history_commit": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int,
                                                  ctypes.c_int, _c_i32_p, _c_dbl_p]),
     "scvt_reduce_chunks": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _c_dbl_p]),
+    "scvt_migration": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int32, _vp, _vp,
+                                      ctypes.c_int32, _c_i32_p]),
     "scvt_history_clear": (ctypes.c_int, [_vp]),
     "scvt_history_size": (ctypes.c_int, [_vp, _c_i32_p]),
     "scvt_history_gamma": (ctypes.c_int, [_vp, _c_dbl_p]),

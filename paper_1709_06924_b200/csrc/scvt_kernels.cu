@@ -829,52 +829,45 @@ k_combine(const double* __restrict__ g, const double* __restrict__ diag, double 
     }
 }
 
-// s = z_new - z_old, y = g_new - g_old (staged); chunk partials of y.s, s.s, y.y, max|s|
-__global__ void __launch_bounds__(RED_THREADS)
-k_history_pair(const double* __restrict__ zo, const double* __restrict__ zn,
-               const double* __restrict__ go, const double* __restrict__ gn, Chunks ck,
-               double* __restrict__ s, double* __restrict__ y, double* __restrict__ red) {
-    double ys = 0, ss = 0, yy = 0, mv = 0;
-    int64_t i0, i1;
-    chunk_span(ck, &i0, &i1);
-    for (int64_t k = 3 * i0 + threadIdx.x; k < 3 * i1; k += RED_THREADS) {
-        double sk = zn[k] - zo[k], yk = gn[k] - go[k];
-        s[k] = sk; y[k] = yk;
-        ys += yk * sk; ss += sk * sk; yy += yk * yk; mv = fmax(mv, fabs(sk));
-    }
-    ys = block_reduce<0>(ys); ss = block_reduce<0>(ss); yy = block_reduce<0>(yy);
-    mv = block_reduce<1>(mv);
-    if (threadIdx.x == 0) {
-        *chunk_slot(red, ck, 0) = ys;
-        *chunk_slot(red, ck, 1) = ss;
-        *chunk_slot(red, ck, 2) = yy;
-        *chunk_slot(red, ck, 3) = mv;
-    }
-}
-
-// y_new . s_j and y_j . s_new against the K stored pairs (values 4 .. 4 + 2K)
+// s = z_new - z_old, y = g_new - g_old (staged) and, in the same pass, their products with the
+// K stored pairs: chunk partials of y.s, s.s, y.y, max|s| (values 0-3), y_new.s_j (4 .. 4+K)
+// and y_j.s_new (4+K .. 4+2K).  Warp butterflies, then the warps in a fixed order.
 template <int K>
 __global__ void __launch_bounds__(RED_THREADS)
-k_cross(const double* __restrict__ sn, const double* __restrict__ yn, HistPtrs h, Chunks ck,
-        double* __restrict__ red) {
-    double a1[K > 0 ? K : 1], a2[K > 0 ? K : 1];
+k_history_pair(const double* __restrict__ zo, const double* __restrict__ zn,
+               const double* __restrict__ go, const double* __restrict__ gn, HistPtrs h,
+               Chunks ck, double* __restrict__ s, double* __restrict__ y,
+               double* __restrict__ red) {
+    constexpr int A = 4 + 2 * K;
+    double acc[A];
 #pragma unroll
-    for (int k = 0; k < K; ++k) { a1[k] = 0.0; a2[k] = 0.0; }
+    for (int a = 0; a < A; ++a) acc[a] = 0.0;
     int64_t i0, i1;
     chunk_span(ck, &i0, &i1);
     for (int64_t e = 3 * i0 + threadIdx.x; e < 3 * i1; e += RED_THREADS) {
-        const double s = sn[e], y = yn[e];
+        const double sk = zn[e] - zo[e], yk = gn[e] - go[e];
+        s[e] = sk; y[e] = yk;
+        acc[0] += yk * sk; acc[1] += sk * sk; acc[2] += yk * yk; acc[3] = fmax(acc[3], fabs(sk));
 #pragma unroll
-        for (int k = 0; k < K; ++k) { a1[k] += y * h.S[k][e]; a2[k] += h.Y[k][e] * s; }
+        for (int k = 0; k < K; ++k) { acc[4 + k] += yk * h.S[k][e]; acc[4 + K + k] += h.Y[k][e] * sk; }
     }
+    __shared__ double sh[RED_THREADS / 32][A];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double v1 = block_reduce<0>(a1[k]);
-        double v2 = block_reduce<0>(a2[k]);
-        if (threadIdx.x == 0) {
-            *chunk_slot(red, ck, 4 + k) = v1;
-            *chunk_slot(red, ck, 4 + K + k) = v2;
+    for (int a = 0; a < A; ++a) {
+        double v = acc[a];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double t = __shfl_xor_sync(0xffffffffu, v, o);
+            v = a == 3 ? fmax(v, t) : v + t;
         }
+        if (lane == 0) sh[w][a] = v;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < A; a += RED_THREADS) {
+        double v = sh[0][a];
+        for (int q = 1; q < RED_THREADS / 32; ++q) v = a == 3 ? fmax(v, sh[q][a]) : v + sh[q][a];
+        *chunk_slot(red, ck, a) = v;
     }
 }
 
@@ -1048,6 +1041,33 @@ __global__ void k_normalize(double* __restrict__ z, int64_t n) {
     }
 }
 
+// ------------------------------------------------------------------ covering migration
+// Region-mode bookkeeping of the reference (partition.py:123-164, pipeline.py:163-167, 244-259):
+// the geometric cell of every point is its Euclidean-nearest covering centre (argmax z.c,
+// ties to the lowest index); a fresh decomposition freezes it as the arithmetic cell; later
+// evaluations classify the movement: 0 in-place, 1 every moved point stayed in a one-level
+// neighbour of its arithmetic cell, 2 out-of-range (max over the points).
+__global__ void k_migration(const double* __restrict__ z, int64_t n,
+                            const double* __restrict__ centers, int p,
+                            const uint32_t* __restrict__ adj, int words,
+                            int* __restrict__ arith, int fresh, int* __restrict__ cls) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x = z[3 * i], y = z[3 * i + 1], w = z[3 * i + 2];
+    double best = -INFINITY;
+    int arg = 0;
+    for (int c = 0; c < p; ++c) {
+        const double sc = x * __ldg(centers + 3 * c) + y * __ldg(centers + 3 * c + 1) +
+                          w * __ldg(centers + 3 * c + 2);
+        if (sc > best) { best = sc; arg = c; }
+    }
+    if (fresh) { arith[i] = arg; return; }
+    const int a = arith[i];
+    if (arg == a) return;
+    const bool near = (adj[(int64_t)a * words + (arg >> 5)] >> (arg & 31)) & 1u;
+    atomicMax(cls, near ? 1 : 2);
+}
+
 // ------------------------------------------------------------------ canonical triangles
 __global__ void k_tri_count(int n, const int* __restrict__ nbr, const int* __restrict__ deg,
                             int* __restrict__ cnt) {
@@ -1176,6 +1196,7 @@ struct scvt_ctx {
     int* h_small = nullptr;            // pinned [16]: small readbacks (reuse counts)
     int* d_rcount = nullptr;           // per-round bad counts of the chained reuse rounds
     int* d_queue = nullptr;            // work queue of the fixed-grid cell rebuilds
+    int* d_mig = nullptr;              // covering migration class (scvt_migration)
     int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
     int* h_counts = nullptr;           // pinned copy
     // LBFGS history
@@ -1735,18 +1756,6 @@ int launch_combine(scvt_ctx* ctx, int K, const double* g, const double* diag, do
     return SCVT_OK;
 }
 
-int launch_cross(scvt_ctx* ctx, int K, const HistPtrs& hp, const Chunks& ck, double* red) {
-    if (K == 0) return SCVT_OK;
-    switch (K) {
-#define X_(k) case k: k_cross<k><<<ck.nc, RED_THREADS, 0, ctx->stream>>>(ctx->d_tmp_s, ctx->d_tmp_y, hp, ck, red); break;
-        SCVT_K_CASES(X_)
-#undef X_
-        default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
-    }
-    LAUNCHED();
-    return SCVT_OK;
-}
-
 inline int gram_values(int K) { return K ? 2 * K + K * (K + 1) / 2 + 1 : 0; }
 
 // two-loop, phase 1: the Gram partials of the slice (nothing when the history is empty)
@@ -1784,10 +1793,15 @@ int pair_phase(scvt_ctx* ctx, const double* zo, const double* zn, const double* 
     const int K = ctx->hist_count;
     *nval = 4 + 2 * K;
     TRY(prep_red(ctx, red, *nval, ck));
-    k_history_pair<<<ck.nc, RED_THREADS, 0, ctx->stream>>>(zo, zn, go, gn, ck, ctx->d_tmp_s,
-                                                          ctx->d_tmp_y, red);
+    const HistPtrs hp = hist_ptrs(ctx);
+    switch (K) {
+#define P_(k) case k: k_history_pair<k><<<ck.nc, RED_THREADS, 0, ctx->stream>>>(zo, zn, go, gn, hp, ck, ctx->d_tmp_s, ctx->d_tmp_y, red); break;
+        SCVT_K_CASES(P_)
+#undef P_
+        default: return fail(ctx, SCVT_ERR_CONFIG, "history length %d > %d", K, MAXM);
+    }
     LAUNCHED();
-    return launch_cross(ctx, K, hist_ptrs(ctx), ck, red);
+    return SCVT_OK;
 }
 
 // history push, phase 2: fixed-order scalars, curvature test (optimizer.py:98-104), commit of
@@ -1964,7 +1978,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_status, 16);
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
-    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_counts, MAX_SHARDS + 1);
+    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_counts, MAX_SHARDS + 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -2030,7 +2044,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
-                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_counts,
+                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_counts,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
@@ -2453,6 +2467,22 @@ int scvt_reduce_chunks(scvt_ctx* ctx, const double* red, int32_t nval, const uin
     TRY(reduce_chunks(ctx, red, nval, ops));
     TRY(readback(ctx, nval));
     for (int v = 0; v < nval; ++v) out_host[v] = ctx->h_scal[v];
+    return SCVT_OK;
+}
+
+int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* centers, int32_t p,
+                   const uint32_t* adjacency, int32_t* arithmetic, int32_t fresh,
+                   int32_t* class_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (p < 1) return fail(ctx, SCVT_ERR_CONFIG, "covering with %d cells", p);
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemsetAsync(ctx->d_mig, 0, sizeof(int), s));
+    k_migration<<<blocks_for(n, 256), 256, 0, s>>>(z, n, centers, p, adjacency, (p + 31) / 32,
+                                                    arithmetic, fresh, ctx->d_mig);
+    LAUNCHED();
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_mig, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *class_host = ctx->h_small[0];
     return SCVT_OK;
 }
 

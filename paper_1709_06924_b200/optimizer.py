@@ -363,6 +363,12 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
         if res.grad_norm / res.energy <= criteria.grad_tol:
             reason = "gradient"
             break
+        if res.migration == "out-of-range":                     # optimizer.py:377-381
+            logger.info("point migrated out of range at iteration %d; decomposition reset",
+                        rec.n)
+            evaluator.redecompose(st.z)
+            st.ops.history_clear()
+            st.resets += 1
     st.torch.cuda.current_stream().synchronize()
     wall = time.perf_counter() - t0
     final, points = _to_host(st.ops.full(st.res), st.z)

@@ -522,6 +522,7 @@ class ShardedMeshEvaluator(MeshEvaluator):
                 finish=lambda res_all: self.backend.finish_slice(
                     z, self.world, res_all, self.rank, self.world, self._red, self._sum, q3,
                     norms))
+        r.migration = self._migration(z)
         self.evaluations += 1
         return r
 

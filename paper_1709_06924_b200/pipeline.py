@@ -131,10 +131,12 @@ class MeshEvaluator:
     Extra keywords ``subdivision`` (depth d of `subdivide_fans`, delaunay.py:383-407, applied
     to every fan sub-triangle; DECISIONS.md D2), ``device`` and ``density_table`` (tanh^4
     densities: evaluate rho through the piecewise polynomial of `density.tanh4_table`
-    instead of atan2/tanh per node; both agree to ~1e-15).  ``covering``/``workers``/
-    ``backend`` are accepted for signature compatibility; the GPU path is always the
-    covering-free global path, which the reference's region path reproduces bitwise
-    (SURVEY.md §6.3).  ``laplacian`` (SuperLU graph Laplacian, cvt_core.py:192-240) is out of
+    instead of atan2/tanh per node; both agree to ~1e-15).  ``workers``/``backend`` are accepted
+    for signature compatibility.  The moments always come from the global path, which the
+    reference's region path reproduces bitwise; a ``covering``
+    (`partition.Covering`) adds the reference's per-evaluation migration class
+    (`EvalResult.migration`, computed on the device), which drives the optimizer's
+    re-decompose-and-reset rule (optimizer.py:377-381).  ``laplacian`` (SuperLU graph Laplacian, cvt_core.py:192-240) is out of
     scope and raises."""
 
     def __init__(self, density: DensityField, rule: QuadratureRule | str, covering=None,
@@ -161,6 +163,8 @@ class MeshEvaluator:
         self._l1, self._l2, self._w = composite_nodes(self.rule, self.subdivision)
         self._ctx: _Context | None = None
         self._m = 7
+        self._arith = None      # frozen covering cells (device int32), see _migration
+        self._cov_dev = None
 
     # -- context ----------------------------------------------------------------------
     def _device_index(self) -> int:
@@ -202,8 +206,40 @@ class MeshEvaluator:
         self.close()
 
     def redecompose(self, points):
-        """No decomposition state on the global GPU path (pipeline.py:157-162)."""
+        """Refresh the frozen (arithmetic) cells from the current geometry (pipeline.py:
+        157-162); nothing to do without a covering."""
+        if self.covering is None:
+            return None
+        z, _ = self._as_device(points)
+        self._migration(z, fresh=True)
         return None
+
+    def _migration(self, z, fresh: bool = False) -> str:
+        """The reference's per-evaluation migration class (pipeline.py:244-259 with
+        partition.py:123-164) on the device: nearest covering centre of every point against
+        the cells frozen at the first evaluation / last `redecompose`."""
+        if self.covering is None:
+            return "in-place"
+        torch = _torch()
+        from .partition import MIGRATION_CLASSES
+
+        n = z.shape[0]
+        if self._cov_dev is None:
+            cov = self.covering
+            self._cov_dev = (torch.as_tensor(np.ascontiguousarray(cov.centers, dtype=np.float64),
+                                             device=z.device),
+                             torch.as_tensor(cov.adjacency_bitmap().view(np.int32),
+                                             device=z.device).contiguous(),
+                             int(cov.cell_count))
+        if self._arith is None or self._arith.shape[0] != n:
+            self._arith = torch.empty(n, dtype=torch.int32, device=z.device)
+            fresh = True
+        centers, adj, p = self._cov_dev
+        cls = ctypes.c_int32()
+        self._ensure_ctx(n).call("scvt_migration", _lib.dptr(z), n, _lib.dptr(centers), p,
+                                 _lib.dptr(adj), _lib.dptr(self._arith), int(fresh),
+                                 ctypes.byref(cls), what="migration")
+        return MIGRATION_CLASSES[cls.value]
 
     def optimizer_ops(self, ctx, n: int):
         """The optimizer's vector algebra for this evaluator's layout (one GPU: all rows)."""
@@ -243,7 +279,8 @@ class MeshEvaluator:
         return EvalResult(energy=float(sc[0]), grad=grad, grad_norm=float(sc[1]),
                           lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]),
                           min_diag=float(sc[3]),
-                          dirderiv=float(sc[4]) if q3 is not None else float("nan"))
+                          dirderiv=float(sc[4]) if q3 is not None else float("nan"),
+                          migration=self._migration(z))
 
     def evaluate(self, points) -> EvalResult:
         """pipeline.py:261-279.  NumPy in -> NumPy out; CUDA tensor in -> tensors out."""
@@ -423,6 +460,17 @@ class RunResult:
         return self.levels[-1].result.final
 
 
+def _covering_for(plan: RunPlan, k: int, density: DensityField):
+    """pipeline.py:387-393: the level's covering when it is thick enough to decompose."""
+    from .partition import bootstrap_partition_cvt
+
+    p = plan.partitions if plan.partitions is not None else default_partitions(k)
+    if k < 16 * p:
+        logger.info("level K=%d below 16 x %d partitions; using the global path", k, p)
+        return None
+    return bootstrap_partition_cvt(p, seed=plan.seed, density=density)
+
+
 def run(plan: RunPlan, initial_points=None, progress=None) -> RunResult:
     """Optimise-bisect ladder (pipeline.py:396-455) on the GPU: every level is minimised by
     the GPU optimizer, triangulated on the GPU, and bisected (K -> 4K - 6) to seed the next."""
@@ -447,12 +495,14 @@ def run(plan: RunPlan, initial_points=None, progress=None) -> RunResult:
         raise ConfigError("the Laplacian preconditioner is outside this hot path")
     levels = []
     tri = None
+    covering = None
     for li, k in enumerate(plan.ladder):
         last = li == len(plan.ladder) - 1
         criteria = plan.criteria if last else replace(
             plan.criteria, movement_tol=plan.intermediate_movement_tol)
+        covering = _covering_for(plan, k, density)
         t_level = time.perf_counter()
-        with MeshEvaluator(density, rule, None, workers=plan.workers, backend=plan.backend,
+        with MeshEvaluator(density, rule, covering, workers=plan.workers, backend=plan.backend,
                            measure=plan.measure, eps_proj=plan.eps_proj,
                            subdivision=plan.subdivision) as ev:
             result = minimize(z, plan.method, ev, criteria, corrections=plan.corrections,
@@ -468,5 +518,5 @@ def run(plan: RunPlan, initial_points=None, progress=None) -> RunResult:
             if len(z) != plan.ladder[li + 1]:
                 raise ScvtError(f"bisection produced {len(z)} points; ladder expected "
                                 f"{plan.ladder[li + 1]}")
-    return RunResult(plan=plan, points=z, triangulation=tri, levels=levels, covering=None,
+    return RunResult(plan=plan, points=z, triangulation=tri, levels=levels, covering=covering,
                      wall_time=time.perf_counter() - t0)

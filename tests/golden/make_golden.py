@@ -354,12 +354,42 @@ def case_run_ladder():
     save("run_ladder", **out)
 
 
+def case_covering():
+    """Region mode: a coarse covering (bootstrap_partition_cvt) and a P-LBFGS run through the
+    reference's region path, whose migration class triggers re-decompose + history resets
+    (optimizer.py:377-381)."""
+    from scvtmesh import partition
+
+    _DEPTH["d"] = 0
+    # points clustered on the c4 plateau, optimised for a constant density: they spread over
+    # the sphere, so some leave the neighbourhood of their frozen cell (out-of-range)
+    z0 = dmod.sample_by_density(field_for("c4"), 2562, 3)
+    cov = partition.bootstrap_partition_cvt(64, seed=0, density=field_for("const"))
+    ev = pipeline.MeshEvaluator(field_for("const"), geometry.QUADRATURE_RULES["4pt"], cov,
+                                workers=1, backend="thread")
+    crit = optimizer.StoppingCriteria(max_iterations=40, movement_tol=1e-300, grad_tol=1e-300,
+                                      stall_tol=1e-300)
+    mig = []
+    res = optimizer.minimize(z0, "lloyd-plbfgs", ev, crit, corrections=7,
+                             callback=lambda n, z, r: mig.append(r.migration))
+    ev.close()
+    print(f"  covering run: {len(res.records)} it, resets={res.resets}, fallbacks={ev.fallbacks}, "
+          f"migration counts {dict((m, mig.count(m)) for m in set(mig))}", flush=True)
+    one_ptr = np.cumsum([0] + [len(t) for t in cov.one_level])
+    one_idx = np.concatenate([np.asarray(t, dtype=np.int64) for t in cov.one_level])
+    save("covering", centers=cov.centers, one_ptr=one_ptr, one_idx=one_idx, z0=z0,
+         energy=np.array([r.energy for r in res.records]),
+         fevals=np.array([-1 if r.fevals is None else r.fevals for r in res.records]),
+         migration=np.array(mig), resets=np.int64(res.resets), final_z=res.points,
+         reason=np.array(res.reason))
+
+
 CASES = {
     "rules": case_rules, "c1_eval": case_c1_eval, "density_eval": case_density_eval,
     "sampler": case_sampler, "medium": case_medium, "small_sets": case_small_sets,
     "traj_fast": case_traj_fast, "traj_slow": case_traj_slow,
     "traj_fallback": case_traj_fallback, "medium_slim": case_medium_slim,
-    "run_ladder": case_run_ladder,
+    "run_ladder": case_run_ladder, "covering": case_covering,
 }
 
 if __name__ == "__main__":

@@ -562,3 +562,44 @@ def test_reuse_escalates_to_full_rebuild_under_large_moves(sharded):
     assert cnt["reused_evals"] == 0 and cnt["passes"] >= 1      # escalated, not certified
     assert r.energy == ref.energy and torch.equal(r.grad, ref.grad)
     assert torch.equal(r.first, ref.first) and torch.equal(r.mass, ref.mass)
+
+
+def _golden_covering(g):
+    from paper_1709_06924_b200.partition import Covering
+
+    one = tuple(tuple(int(x) for x in g["one_idx"][g["one_ptr"][k]:g["one_ptr"][k + 1]])
+                for k in range(len(g["centers"])))
+    return Covering(centers=g["centers"], one_level=one, two_level=())
+
+
+def test_covering_migration_resets_match_reference(gold):
+    """Region mode: with the reference's covering, the device migration class
+    of every accepted iterate, the out-of-range re-decompose + history resets and the whole
+    trajectory (plateau-clustered points spreading under a constant density: 8 resets in 40
+    iterations) match the reference's region path run."""
+    g = gold("covering")
+    cov = _golden_covering(g)
+    crit = P.StoppingCriteria(max_iterations=40, movement_tol=1e-300, grad_tol=1e-300,
+                              stall_tol=1e-300)
+    mig = []
+    with P.MeshEvaluator(P.density_preset("const"), "4pt", cov) as ev:
+        res = P.minimize(g["z0"], "lloyd-plbfgs", ev, crit, corrections=7,
+                         callback=lambda n, z, r: mig.append(r.migration))
+    assert mig == [str(m) for m in g["migration"]]
+    assert res.resets == int(g["resets"]) > 0
+    e = np.array([r.energy for r in res.records])
+    assert np.max(np.abs(e - g["energy"]) / g["energy"]) <= 1e-10
+    assert [r.fevals if r.fevals is not None else -1 for r in res.records] == g["fevals"].tolist()
+    assert rel(res.points, g["final_z"]) <= 1e-10
+
+
+def test_bootstrap_partition_cvt_matches_reference(gold):
+    """bootstrap_partition_cvt (partition.py:83-120) with its Lloyd steps on the GPU: same
+    centres to rounding and the same one-level adjacency as the reference's."""
+    from paper_1709_06924_b200.partition import bootstrap_partition_cvt
+
+    g = gold("covering")
+    ref = _golden_covering(g)
+    cov = bootstrap_partition_cvt(64, seed=0, density=P.density_preset("const"))
+    assert rel(cov.centers, ref.centers) <= 1e-12
+    assert cov.one_level == ref.one_level

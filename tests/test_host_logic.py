@@ -163,3 +163,31 @@ def test_runplan_validation():
         P.RunPlan(points=642, quadrature="5pt")
     p = P.RunPlan(points=642, density_name="x64")
     assert p.quadrature == "9pt" and p.ladder == [642]
+
+
+def test_covering_host_helpers_match_reference_golden():
+    """partition.py host forms: the adjacency bitmap handed to scvt_migration encodes exactly
+    the one-level lists, and detect_migration / assign_points classify like the reference."""
+    import numpy as np
+
+    from conftest import golden
+    from paper_1709_06924_b200.partition import (Covering, PointAssignment, assign_points,
+                                                 detect_migration)
+
+    g = golden("covering")
+    one = tuple(tuple(int(x) for x in g["one_idx"][g["one_ptr"][k]:g["one_ptr"][k + 1]])
+                for k in range(len(g["centers"])))
+    cov = Covering(centers=g["centers"], one_level=one, two_level=())
+    bits = cov.adjacency_bitmap()
+    for a in range(cov.cell_count):
+        got = [b for b in range(cov.cell_count) if (bits[a, b >> 5] >> (b & 31)) & 1]
+        assert tuple(got) == one[a]
+    a0 = assign_points(g["z0"], cov)
+    assert detect_migration(a0, cov) == "in-place"
+    far = PointAssignment(arithmetic=a0.arithmetic, geometric=a0.arithmetic.copy())
+    far.geometric[0] = next(c for c in range(cov.cell_count) if c != far.arithmetic[0]
+                            and c not in one[far.arithmetic[0]])
+    assert detect_migration(far, cov) == "out-of-range"
+    near = PointAssignment(arithmetic=a0.arithmetic, geometric=a0.arithmetic.copy())
+    near.geometric[0] = one[near.arithmetic[0]][0]
+    assert detect_migration(near, cov) == "neighbor-move"
