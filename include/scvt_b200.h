@@ -103,8 +103,10 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
 /* evaluation ---------------------------------------------------------------------------
  * Consecutive evaluations of the same n reuse the previous cycles when the robust certificate
  * (consistency, orientation, local Delaunay on every edge) still holds at the new positions;
- * failing neighbourhoods are rebuilt, so the result is always THE Delaunay triangulation
- * (env SCVT_NO_REUSE=1 disables the reuse).
+ * edges failing only the in-circle test are repaired by Lawson edge flips (env SCVT_NO_FLIPS=1:
+ * rebuilt instead), other failing neighbourhoods are rebuilt, and every touched cell is
+ * certified again, so the result is always THE Delaunay triangulation (env SCVT_NO_REUSE=1
+ * disables the reuse).
  * Replaces MeshEvaluator.evaluate (pipeline.py:261-279) = triangulation + Voronoi fans
  * (delaunay.py:337-380) + depth-d subdivision (383-407) + cell_quadrature
  * (cvt_core.py:55-117) + gradient assembly.  Outputs (device): grad (n,3) =
@@ -304,6 +306,9 @@ int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int re
  *          reuse, certificate passes run by reuse,
  *          max points scanned by one cell | (max candidate passes of one cell << 40)} */
 int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset);
+/* flip repair of reused cycles: {evaluations that ran it, flip rounds, flips, evaluations that
+ * left candidates open and rebuilt those cells} since the last reset */
+int scvt_profile_flips(scvt_ctx* ctx, int64_t* out4, int reset);
 /* measured FP64 DFMA throughput of `device` in TFLOP/s (2 FLOPs per FMA): the FP64
  * roofline denominator, which MEASURED_PEAKS.json does not carry */
 int scvt_fp64_peak(int device, double* tflops_out);

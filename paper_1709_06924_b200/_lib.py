@@ -120,6 +120,7 @@ SIGNATURES = {
     "scvt_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
     "scvt_profile_read": (ctypes.c_int, [_vp, _c_dbl_p, _c_i64_p, ctypes.c_int]),
     "scvt_profile_counters": (ctypes.c_int, [_vp, _c_i64_p, ctypes.c_int]),
+    "scvt_profile_flips": (ctypes.c_int, [_vp, _c_i64_p, ctypes.c_int]),
     "scvt_fp64_peak": (ctypes.c_int, [ctypes.c_int, _c_dbl_p]),
 }
 

@@ -205,26 +205,46 @@ __device__ __forceinline__ void mark_bad(int mode, int* status, int bit, int* ba
         if (v[k] >= 0 && atomicExch(&bad[v[k]], 1) == 0) atomicAdd(nbad, 1);
 }
 
+#ifdef SCVT_PROBE_FLIPS
+__device__ unsigned long long g_probe[4];
+#endif
+
+// mode 2 (flip repair): an edge failing only the in-circle test is not marked bad but queued
+// once (from its lower-id end) as a flip candidate {i, a, b, c}: triangles (i, a, b) and
+// (i, c, a) -> (i, c, b) and (c, a, b).  Orientation and consistency failures mark bad as in
+// mode 1.  list_ids: `list` holds generator ids instead of sorted slots.
+struct FlipQueue {
+    int4* cand;
+    int* ncand;
+    int cap;
+};
+
 __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ ids, int p_lo,
                          int p_hi, const int* __restrict__ list, const int* __restrict__ list_n,
                          const int* __restrict__ nbr, const int* __restrict__ deg,
                          uint8_t* __restrict__ amb, int* __restrict__ status,
                          int* __restrict__ stats, int mode, int* __restrict__ bad,
-                         int* __restrict__ nbad) {
+                         int* __restrict__ nbad, FlipQueue fq = FlipQueue{nullptr, nullptr, 0},
+                         int list_ids = 0) {
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x;; idx += gridDim.x * blockDim.x) {
-    int p;
+    int p, i;
     if (list) {                 // re-certification of a compacted list of sorted slots
         if (idx >= *list_n) return;
-        p = list[idx];
-        if (p < p_lo || p >= p_hi) continue;   // sharded re-check: owned slots only
+        if (list_ids) {
+            i = list[idx];
+        } else {
+            p = list[idx];
+            if (p < p_lo || p >= p_hi) continue;   // sharded re-check: owned slots only
+            i = ids[p];
+        }
     } else {
         p = p_lo + idx;
         if (p >= p_hi) return;
+        i = ids[p];
     }
-    int i = ids[p];
     int d = deg[i];
     const int* row = nbr + (int64_t)i * MAXDEG;
-    if (d < 3 || d > MAXDEG) { mark_bad(mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1); continue; }
+    if (d < 3 || d > MAXDEG) { mark_bad(mode > 1 ? 1 : mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1); continue; }
     V3 zi = load3(z, i);
     int namb = 0;
     for (int t = 0; t < d; ++t) {
@@ -235,18 +255,155 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
         bool ok = q >= 0 && ra[q == 0 ? da - 1 : q - 1] == b;
         if (!ok) mark_bad(mode, status, ST_INCONSISTENT, bad, nbad, i, a, b, -1);
         V3 za = load3(z, a), zb = load3(z, b), zc = load3(z, c);
-        if (mode == 1) {   // reused cycles: the triangle must still face outward
+        if (mode >= 1) {   // reused cycles: the triangle must still face outward
             int tier;
-            if (orient_robust(v3(0, 0, 0), zi, za, zb, -1, i, a, b, &tier) <= 0)
+            if (orient_robust(v3(0, 0, 0), zi, za, zb, -1, i, a, b, &tier) <= 0) {
                 mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, -1);
+#ifdef SCVT_PROBE_FLIPS
+                atomicAdd(&g_probe[1], 1);
+#endif
+            }
         }
         int tier;
         int sgn = orient_robust(zi, za, zb, zc, i, a, b, c, &tier);
+#ifdef SCVT_PROBE_FLIPS
+        if (mode >= 1 && sgn > 0) atomicAdd(&g_probe[0], 1);
+        if (mode >= 1 && !ok) atomicAdd(&g_probe[2], 1);
+#endif
         amb[(int64_t)i * MAXDEG + t] = tier > 0 ? 1 : 0;
         namb += tier > 0;
-        if (sgn > 0) mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, c);
+        if (sgn > 0) {
+            if (mode == 2) {
+                if (i < a) {
+                    const int k = atomicAdd(fq.ncand, 1);
+                    if (k < fq.cap) fq.cand[k] = make_int4(i, a, b, c);
+                }
+            } else {
+                mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, c);
+            }
+        }
     }
     if (namb) atomicAdd(&stats[3], namb);
+    }
+}
+
+// ------------------------------------------------------------------ flip repair
+// Lawson flips of the reused cycles (the north star's "repaired by edge flips"): every flip
+// candidate of the detection pass takes a 64-bit ticket {i, a} on its four vertices (atomicMin);
+// the candidates that hold all four tickets form an independent set and flip their edge in the
+// cycles of i, a, b, c (canonical rotation: minimum id first).  The four vertices of every
+// candidate, flipped or not, are re-certified by the next detection pass (the only edges whose
+// status a flip changes are the quad's, whose ends are all among them).  Anything unexpected
+// (degree limits, inconsistent neighbourhoods) marks the four cells bad for the rebuild path.
+__device__ __forceinline__ unsigned long long flip_key(const int4& c) {
+    return ((unsigned long long)(unsigned)c.x << 32) | (unsigned)c.y;
+}
+
+__global__ void k_flip_lock(const int4* __restrict__ cand, const int* __restrict__ ncand,
+                            unsigned long long* __restrict__ lock) {
+    const int nc = *ncand;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+        const int4 c = cand[k];
+        const unsigned long long key = flip_key(c);
+        atomicMin(&lock[c.x], key); atomicMin(&lock[c.y], key);
+        atomicMin(&lock[c.z], key); atomicMin(&lock[c.w], key);
+    }
+}
+
+__device__ __forceinline__ int cyc_pos(const int* __restrict__ row, int d, int x) {
+    for (int k = 0; k < d; ++k)
+        if (row[k] == x) return k;
+    return -1;
+}
+
+// write `tmp` (d entries, cyclic) into `row` rotated so that its minimum comes first
+__device__ __forceinline__ void cyc_store(int* __restrict__ row, const int* tmp, int d) {
+    int m = 0;
+    for (int k = 1; k < d; ++k)
+        if (tmp[k] < tmp[m]) m = k;
+    for (int k = 0; k < d; ++k) row[k] = tmp[(m + k) % d];
+}
+
+__global__ void k_flip_apply(const int4* __restrict__ cand, const int* __restrict__ ncand,
+                             const unsigned long long* __restrict__ lock, int* __restrict__ nbr,
+                             int* __restrict__ deg, int* __restrict__ dflag,
+                             int* __restrict__ next, int* __restrict__ next_n,
+                             int* __restrict__ bad, int* __restrict__ nbad,
+                             int* __restrict__ nflips) {
+    const int nc = *ncand;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+        const int4 c = cand[k];
+        const int v[4] = {c.x, c.y, c.z, c.w};
+        for (int q = 0; q < 4; ++q)
+            if (atomicExch(&dflag[v[q]], 1) == 0) next[atomicAdd(next_n, 1)] = v[q];
+        const unsigned long long key = flip_key(c);
+        if (lock[c.x] != key || lock[c.y] != key || lock[c.z] != key || lock[c.w] != key)
+            continue;                                   // a conflicting flip won this round
+        const int i = c.x, a = c.y, b = c.z, cc = c.w;
+        const int di = deg[i], da = deg[a], db = deg[b], dc = deg[cc];
+        int* ri = nbr + (int64_t)i * MAXDEG;
+        int* ra = nbr + (int64_t)a * MAXDEG;
+        int* rb = nbr + (int64_t)b * MAXDEG;
+        int* rc = nbr + (int64_t)cc * MAXDEG;
+        bool ok = di > 3 && da > 3 && db < MAXDEG && dc < MAXDEG && b != cc;
+        int ti = -1, ta = -1, tb = -1, tc = -1;
+        if (ok) {
+            ti = cyc_pos(ri, di, a); ta = cyc_pos(ra, da, i);
+            tb = cyc_pos(rb, db, i); tc = cyc_pos(rc, dc, a);
+            ok = ti >= 0 && ta >= 0 && tb >= 0 && tc >= 0 &&
+                 ri[(ti + 1) % di] == b && ri[(ti + di - 1) % di] == cc &&    // i: c, a, b
+                 ra[(ta + da - 1) % da] == b && ra[(ta + 1) % da] == cc &&    // a: b, i, c
+                 rb[(tb + 1) % db] == a &&                                  // b: i, a
+                 rc[(tc + 1) % dc] == i &&                                  // c: a, i
+                 cyc_pos(rb, db, cc) < 0 && cyc_pos(rc, dc, b) < 0;          // b-c not an edge
+        }
+        if (!ok) {
+            for (int q = 0; q < 4; ++q)
+                if (atomicExch(&bad[v[q]], 1) == 0) atomicAdd(nbad, 1);
+            continue;
+        }
+        int tmp[MAXDEG];
+        int m = 0;                                       // i: drop a
+        for (int t = 0; t < di; ++t) if (t != ti) tmp[m++] = ri[t];
+        cyc_store(ri, tmp, di - 1); deg[i] = di - 1;
+        m = 0;                                           // a: drop i
+        for (int t = 0; t < da; ++t) if (t != ta) tmp[m++] = ra[t];
+        cyc_store(ra, tmp, da - 1); deg[a] = da - 1;
+        m = 0;                                           // b: i, c, a
+        for (int t = 0; t < db; ++t) { tmp[m++] = rb[t]; if (t == tb) tmp[m++] = cc; }
+        cyc_store(rb, tmp, db + 1); deg[b] = db + 1;
+        m = 0;                                           // c: a, b, i
+        for (int t = 0; t < dc; ++t) { tmp[m++] = rc[t]; if (t == tc) tmp[m++] = b; }
+        cyc_store(rc, tmp, dc + 1); deg[cc] = dc + 1;
+        atomicAdd(nflips, 1);
+    }
+}
+
+__global__ void k_flip_unlock(const int4* __restrict__ cand, const int* __restrict__ ncand,
+                              unsigned long long* __restrict__ lock) {
+    const int nc = *ncand;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+        const int4 c = cand[k];
+        lock[c.x] = ~0ull; lock[c.y] = ~0ull; lock[c.z] = ~0ull; lock[c.w] = ~0ull;
+    }
+}
+
+__global__ void k_clear_flags(const int* __restrict__ list, const int* __restrict__ list_n,
+                              int* __restrict__ flag) {
+    const int nl = *list_n;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nl; k += gridDim.x * blockDim.x)
+        flag[list[k]] = 0;
+}
+
+// the candidates left after the last round: their cells go to the rebuild path
+__global__ void k_cand_bad(const int4* __restrict__ cand, const int* __restrict__ ncand,
+                           int* __restrict__ bad, int* __restrict__ nbad) {
+    const int nc = *ncand;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+        const int4 c = cand[k];
+        const int v[4] = {c.x, c.y, c.z, c.w};
+        for (int q = 0; q < 4; ++q)
+            if (atomicExch(&bad[v[q]], 1) == 0) atomicAdd(nbad, 1);
     }
 }
 
@@ -1197,6 +1354,14 @@ struct scvt_ctx {
     int* d_rcount = nullptr;           // per-round bad counts of the chained reuse rounds
     int* d_queue = nullptr;            // work queue of the fixed-grid cell rebuilds
     int* d_mig = nullptr;              // covering migration class (scvt_migration)
+    // flip repair: candidates {i, a, b, c} (<= 3n), tickets, double-buffered id lists,
+    // counters {ncand, nlist[2], nflips}
+    int4* d_cand = nullptr;
+    unsigned long long* d_lock = nullptr;
+    int* d_flist = nullptr;            // [2][n]
+    int* d_fflag = nullptr;            // [n]
+    int* d_fcnt = nullptr;             // [8]
+    int64_t flip_stats[4] = {0, 0, 0, 0};   // evaluations, rounds, flips, fell back
     int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
     int* h_counts = nullptr;           // pinned copy
     // LBFGS history
@@ -1528,12 +1693,69 @@ int reuse_round_device(scvt_ctx* ctx, const double* z, int64_t n, const GridView
 // escalate to a full rebuild when churn is large.  Pass 0 (every cell) is read back on the
 // host (certified evaluations stop there); passes 1-2 with their rebuild rounds are chained
 // on the device and read back once.
+bool flips_enabled() { return getenv("SCVT_NO_FLIPS") == nullptr; }
+constexpr int FLIP_ROUNDS_PER_SYNC = 3;
+constexpr int FLIP_MAX_ROUNDS = 12;
+
+// Certificate pass over every cell in flip mode, then Lawson flip rounds (detection of the
+// touched cells after each), FLIP_ROUNDS_PER_SYNC rounds chained on the device between host
+// reads.  Leaves d_bad / d_nbad as the rebuild path expects them: the cells of orientation or
+// consistency failures, of rejected flips and of candidates still open after the last round.
+int flip_repair(scvt_ctx* ctx, const double* z, int64_t n) {
+    cudaStream_t s = ctx->stream;
+    int* cnt = ctx->d_fcnt;        // [0] candidates, [1] [2] list lengths, [3] flips
+    CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
+    const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
+    k_verify<<<blocks_for(n, 128), 128, 0, s>>>(
+        z, ctx->d_ids, 0, (int)n, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
+        ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad, fq);
+    LAUNCHED();
+    int cur = 0, rounds = 0;
+    for (;;) {
+        CK(cudaMemcpyAsync(ctx->h_small, cnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (ctx->h_small[0] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
+        for (int r = 0; r < FLIP_ROUNDS_PER_SYNC && rounds < FLIP_MAX_ROUNDS; ++r, ++rounds) {
+            const int nxt = 1 - cur;
+            int* list = ctx->d_flist + (int64_t)nxt * n;
+            CK(cudaMemsetAsync(cnt + 1 + nxt, 0, sizeof(int), s));
+            k_flip_lock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, ctx->d_lock);
+            LAUNCHED();
+            k_flip_apply<<<SPEC_BLOCKS, 128, 0, s>>>(ctx->d_cand, cnt, ctx->d_lock, ctx->d_nbr,
+                                                      ctx->d_deg, ctx->d_fflag, list, cnt + 1 + nxt,
+                                                      ctx->d_bad, ctx->d_nbad, cnt + 3);
+            LAUNCHED();
+            k_flip_unlock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, ctx->d_lock);
+            LAUNCHED();
+            k_clear_flags<<<SPEC_BLOCKS, 256, 0, s>>>(list, cnt + 1 + nxt, ctx->d_fflag);
+            LAUNCHED();
+            CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+            k_verify<<<SPEC_BLOCKS, 128, 0, s>>>(
+                z, ctx->d_ids, 0, (int)n, list, cnt + 1 + nxt, ctx->d_nbr, ctx->d_deg,
+                ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad, fq, 1);
+            LAUNCHED();
+            cur = nxt;
+        }
+    }
+    const bool open = ctx->h_small[0] > 0;
+    if (open) {   // unconverged: those cells are rebuilt
+        k_cand_bad<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, ctx->d_bad, ctx->d_nbad);
+        LAUNCHED();
+    }
+    ctx->flip_stats[0] += 1;
+    ctx->flip_stats[1] += rounds;
+    ctx->flip_stats[2] += ctx->h_small[3];
+    ctx->flip_stats[3] += open ? 1 : 0;
+    return SCVT_OK;
+}
+
 int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView& g, bool* done) {
     cudaStream_t s = ctx->stream;
     *done = false;
     CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
     CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
-    TRY(verify_range(ctx, z, 0, n, 1));
+    if (flips_enabled()) TRY(flip_repair(ctx, z, n));
+    else TRY(verify_range(ctx, z, 0, n, 1));
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     int nbad = ctx->h_small[0];
@@ -1859,6 +2081,17 @@ extern "C" {
 
 const char* scvt_version(void) { return "scvt_b200 0.1.0 (sm_100a)"; }
 
+#ifdef SCVT_PROBE_FLIPS
+// probe build only: {in-circle failures, orientation failures, consistency failures} of the
+// reuse certificate passes since the last read
+int scvt_probe_flips(unsigned long long* out3) {
+    cudaMemcpyFromSymbol(out3, g_probe, 3 * sizeof(unsigned long long));
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_probe, z, sizeof(z));
+    return 0;
+}
+#endif
+
 const char* scvt_last_error(const scvt_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
 int64_t scvt_launch_count(const scvt_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -1883,6 +2116,15 @@ int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset) {
     if (reset) {
         CK(cudaMemset(ctx->d_diag, 0, 10 * sizeof(int64_t)));
         ctx->reuse_stats[0] = ctx->reuse_stats[1] = ctx->reuse_stats[2] = 0;
+    }
+    return SCVT_OK;
+}
+
+int scvt_profile_flips(scvt_ctx* ctx, int64_t* out4, int reset) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    for (int k = 0; k < 4; ++k) {
+        out4[k] = ctx->flip_stats[k];
+        if (reset) ctx->flip_stats[k] = 0;
     }
     return SCVT_OK;
 }
@@ -1978,12 +2220,15 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_status, 16);
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
-    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_counts, MAX_SHARDS + 1);
+    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_cand, 3 * n); AL(d_lock, n); AL(d_flist, 2 * n); AL(d_fflag, n); AL(d_fcnt, 8); AL(d_counts, MAX_SHARDS + 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
     AL(d_coef, 2 * MAXM);
 #undef AL
+    if (cudaMemset(ctx->d_lock, 0xFF, (size_t)n * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(ctx->d_fflag, 0, (size_t)n * sizeof(int)) != cudaSuccess)
+        return bail(fail(ctx, SCVT_ERR_CUDA, "flip buffers init failed"));
     {
         cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_RED_VALS * sizeof(double));
         cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
@@ -2044,7 +2289,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
-                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_counts,
+                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_fcnt, ctx->d_counts,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,

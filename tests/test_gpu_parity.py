@@ -603,3 +603,32 @@ def test_bootstrap_partition_cvt_matches_reference(gold):
     cov = bootstrap_partition_cvt(64, seed=0, density=P.density_preset("const"))
     assert rel(cov.centers, ref.centers) <= 1e-12
     assert cov.one_level == ref.one_level
+
+
+@pytest.mark.parametrize("cfg,n", [("c4", 40962), ("c5", 40962)])
+def test_flip_repair_matches_rebuild(cfg, n, monkeypatch):
+    """Lawson-flip repair of the reused cycles (SCVT_NO_FLIPS unset) against the rebuild-only
+    reuse loop along a P-LBFGS trajectory: bitwise the same iterates and results (the certified
+    Delaunay triangulation is unique and stored canonically), with flips actually applied."""
+    z0 = P.sample_by_density(P.density_preset(cfg), n, 0)
+    crit = P.StoppingCriteria(max_iterations=10, movement_tol=1e-300, grad_tol=1e-300,
+                              stall_tol=1e-300)
+    out = {}
+    for flips in (True, False):
+        if flips:
+            monkeypatch.delenv("SCVT_NO_FLIPS", raising=False)
+        else:
+            monkeypatch.setenv("SCVT_NO_FLIPS", "1")
+        with _ev(cfg, "7pt", 3) as ev:
+            r = P.minimize(z0, "lloyd-plbfgs", ev, crit, corrections=7)
+            fl = (ctypes.c_int64 * 4)()
+            ev.context.lib.scvt_profile_flips(ev.context.ptr, fl, 1)
+            tri = ev.triangulation(r.points).triangles
+        out[flips] = (r, list(fl), tri)
+    (ra, fa, ta), (rb, fb, tb) = out[True], out[False]
+    assert fa[2] > 0 and fb[2] == 0
+    assert np.array_equal(ra.points, rb.points)
+    assert [h.energy for h in ra.records] == [h.energy for h in rb.records]
+    assert np.array_equal(ra.final.grad, rb.final.grad)
+    assert np.array_equal(ta, tb)
+    assert np.array_equal(ta, O.convex_hull_delaunay(ra.points))
