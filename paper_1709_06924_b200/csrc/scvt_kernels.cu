@@ -1694,14 +1694,14 @@ int reuse_round_device(scvt_ctx* ctx, const double* z, int64_t n, const GridView
 // host (certified evaluations stop there); passes 1-2 with their rebuild rounds are chained
 // on the device and read back once.
 bool flips_enabled() { return getenv("SCVT_NO_FLIPS") == nullptr; }
-constexpr int FLIP_ROUNDS_PER_SYNC = 3;
+constexpr int FLIP_ROUNDS_PER_SYNC = 4;
 constexpr int FLIP_MAX_ROUNDS = 12;
 
 // Certificate pass over every cell in flip mode, then Lawson flip rounds (detection of the
 // touched cells after each), FLIP_ROUNDS_PER_SYNC rounds chained on the device between host
 // reads.  Leaves d_bad / d_nbad as the rebuild path expects them: the cells of orientation or
 // consistency failures, of rejected flips and of candidates still open after the last round.
-int flip_repair(scvt_ctx* ctx, const double* z, int64_t n) {
+int flip_repair(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
     cudaStream_t s = ctx->stream;
     int* cnt = ctx->d_fcnt;        // [0] candidates, [1] [2] list lengths, [3] flips
     CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
@@ -1713,6 +1713,7 @@ int flip_repair(scvt_ctx* ctx, const double* z, int64_t n) {
     int cur = 0, rounds = 0;
     for (;;) {
         CK(cudaMemcpyAsync(ctx->h_small, cnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (ctx->h_small[0] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
         for (int r = 0; r < FLIP_ROUNDS_PER_SYNC && rounds < FLIP_MAX_ROUNDS; ++r, ++rounds) {
@@ -1741,7 +1742,10 @@ int flip_repair(scvt_ctx* ctx, const double* z, int64_t n) {
     if (open) {   // unconverged: those cells are rebuilt
         k_cand_bad<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, ctx->d_bad, ctx->d_nbad);
         LAUNCHED();
+        CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
     }
+    *nbad_host = ctx->h_small[4];
     ctx->flip_stats[0] += 1;
     ctx->flip_stats[1] += rounds;
     ctx->flip_stats[2] += ctx->h_small[3];
@@ -1749,20 +1753,32 @@ int flip_repair(scvt_ctx* ctx, const double* z, int64_t n) {
     return SCVT_OK;
 }
 
-int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView& g, bool* done) {
+// The bucket grid is only needed to rebuild cells: it is built on demand (*have_grid), so an
+// evaluation certified by the flip pass keeps the previous slot order (any permutation is
+// valid; outputs do not depend on it).
+int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, GridView& g, bool* have_grid,
+                      bool* done) {
     cudaStream_t s = ctx->stream;
     *done = false;
     CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
     CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
-    if (flips_enabled()) TRY(flip_repair(ctx, z, n));
-    else TRY(verify_range(ctx, z, 0, n, 1));
-    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    int nbad = ctx->h_small[0];
+    int nbad = 0;
+    if (flips_enabled()) {
+        TRY(flip_repair(ctx, z, n, &nbad));
+    } else {
+        TRY(verify_range(ctx, z, 0, n, 1));
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        nbad = ctx->h_small[0];
+    }
     ctx->reuse_stats[0] += 1;                       // certificate passes run
     ctx->reuse_stats[1] += nbad;
     if (nbad == 0) { *done = true; return SCVT_OK; }
     if (nbad > (3 * n) / 4) return SCVT_OK;         // caller rebuilds everything
+    if (!*have_grid) {
+        TRY(build_grid(ctx, z, n, &g));
+        *have_grid = true;
+    }
     for (int r = 0; r < 2; ++r) {
         TRY(reuse_round_device(ctx, z, n, g, r == 0 ? nbad : -1));
         CK(cudaMemcpyAsync(ctx->d_rcount + r, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToDevice, s));
@@ -1785,11 +1801,11 @@ int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, const GridView&
 
 int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
     GridView g;
-    TRY(build_grid(ctx, z, n, &g));
+    bool have_grid = false;
     if (ctx->cycles_n == n && reuse_enabled()) {
         if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         bool done = false;
-        TRY(build_cells_reuse(ctx, z, n, g, &done));
+        TRY(build_cells_reuse(ctx, z, n, g, &have_grid, &done));
         if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (done) {
             ctx->reuse_stats[2] += 1;
@@ -1797,6 +1813,7 @@ int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
         }
         CK(cudaMemsetAsync(ctx->d_status + 8, 0, 8 * sizeof(int), ctx->stream));
     }
+    if (!have_grid) TRY(build_grid(ctx, z, n, &g));
     TRY(build_cells_range(ctx, g, 0, n));
     return verify_range(ctx, z, 0, n, 0);
 }
