@@ -174,6 +174,11 @@ int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
  * triangulation (unique) and every output are bitwise those of scvt_evaluate. */
 int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                        int round, int32_t* bad_out, int32_t* ready_host);
+/* before the rounds: the flip repair of the held cycles, replicated on every rank (the
+ * cycles are replicated and the repair is deterministic, so no exchange is needed).
+ * *nbad_host = 0: certified, call scvt_shard_moments(cyc_all = NULL); > 0: cells left for the
+ * rounds above; -1: no held cycles for n points (or reuse/flips disabled). */
+int scvt_shard_flip(scvt_ctx* ctx, const double* z, int64_t n, int32_t* nbad_host);
 int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_all,
                     int64_t* counts_host);
 int scvt_shard_rebuild(scvt_ctx* ctx, int64_t n, int shard, int nshards, int64_t cap,

@@ -69,6 +69,7 @@ SIGNATURES = {
                                           _vp, _vp, _c_i32_p]),
     "scvt_shard_recheck": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int, _vp, _c_i32_p]),
+    "scvt_shard_flip": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _c_i32_p]),
     "scvt_shard_plan": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, _vp, _c_i64_p]),
     "scvt_shard_rebuild": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int64, _vp]),

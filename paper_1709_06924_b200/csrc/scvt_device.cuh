@@ -593,9 +593,15 @@ SCVT_HD double tab_u(const DensityParams& p, V3 y, V3 c) {
     if (k > p.tab_k - 1) k = p.tab_k - 1;
     double tau = 2.0 * (t - (double)k) - 1.0;
     const double* co = p.tab + (br * p.tab_k + k) * (TAB_P + 1);
+#if defined(__CUDA_ARCH__)
+    double acc = __ldg(co + TAB_P);      // the table lives in global memory (read-only cache)
+#pragma unroll
+    for (int j = TAB_P - 1; j >= 0; --j) acc = fma(acc, tau, __ldg(co + j));
+#else
     double acc = co[TAB_P];
 #pragma unroll
     for (int j = TAB_P - 1; j >= 0; --j) acc = fma(acc, tau, co[j]);
+#endif
     return acc;
 }
 
@@ -773,9 +779,15 @@ SCVT_HD double tab_u_chord(const DensityParams& p, double x, int br) {
     if (k > p.tab_k - 1) k = p.tab_k - 1;
     const double tau = 2.0 * (t - (double)k) - 1.0;
     const double* co = p.tab + (br * p.tab_k + k) * (TAB_P + 1);
+#if defined(__CUDA_ARCH__)
+    double acc = __ldg(co + TAB_P);      // the table lives in global memory (read-only cache)
+#pragma unroll
+    for (int j = TAB_P - 1; j >= 0; --j) acc = fma(acc, tau, __ldg(co + j));
+#else
     double acc = co[TAB_P];
 #pragma unroll
     for (int j = TAB_P - 1; j >= 0; --j) acc = fma(acc, tau, co[j]);
+#endif
     return acc;
 }
 

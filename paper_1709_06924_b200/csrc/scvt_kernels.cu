@@ -482,12 +482,9 @@ __global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? (KIND == DEN_TANH4X2_TAB 
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
     for (int q = threadIdx.x; q < 3 * a.nq; q += blockDim.x) s_nodes[q] = a.nodes[q];
-    if (KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB) {
-        double* s_tab = s_nodes + 3 * a.nq;
-        const int nt = 2 * a.dp.tab_k * (TAB_P + 1);
-        for (int q = threadIdx.x; q < nt; q += blockDim.x) s_tab[q] = a.table[q];
-        a.dp.tab = s_tab;
-    }
+    // the density table (28 KB) is read through the read-only cache, where it stays resident;
+    // staging it in shared memory per CTA cost 1.4-2.7 % of k_quad (c4, c3, c5)
+    if (KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB) a.dp.tab = a.table;
     __syncthreads();
     const int t_id = blockIdx.x * blockDim.x + threadIdx.x;
     const int u = SPLIT ? t_id >> 1 : t_id;
@@ -1880,7 +1877,7 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
     // a finer last wave and shorter per-thread chains (c4 k_quad 9.44 -> 8.84 ms, c3 -11 %)
     ctx->split = ctx->sym7 && !ctx->measure;
     unsigned grid = blocks_for(n_inc, QUAD_THREADS);
-    size_t smem = (3 * (size_t)ctx->nq + 2 * (size_t)ctx->dp.tab_k * (TAB_P + 1)) * sizeof(double);
+    size_t smem = 3 * (size_t)ctx->nq * sizeof(double);
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     switch (ctx->dp.kind) {
         case DEN_CONST: TRY(launch_quad_kind<DEN_CONST>(ctx, a, grid, smem)); break;
@@ -2285,7 +2282,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
                                    cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return bail(fail(ctx, SCVT_ERR_CUDA, "table upload failed"));
     }
-    size_t smem = (3 * (size_t)ctx->nq + 2 * (size_t)dp.tab_k * (TAB_P + 1)) * sizeof(double);
+    size_t smem = 3 * (size_t)ctx->nq * sizeof(double);   // composite node table (quad_range)
     if (smem > 48 * 1024) {
         // opt in to large dynamic shared memory for every instantiation
 #define OPT(K)                                                                             \
@@ -2439,6 +2436,22 @@ int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int n
 }
 
 // ---- sharded cycle reuse: the single-GPU reuse loop split at its two exchanges
+int scvt_shard_flip(scvt_ctx* ctx, const double* z, int64_t n, int32_t* nbad_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    *nbad_host = -1;
+    if (ctx->cycles_n != n || !reuse_enabled() || !flips_enabled()) return SCVT_OK;
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+    ctx->prof_n[3] = 0;
+    TRY(reset_status(ctx));
+    CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), ctx->stream));
+    int nbad = 0;
+    TRY(flip_repair(ctx, z, n, &nbad));
+    if (nbad == 0) ctx->reuse_stats[2] += 1;   // certified: the evaluation reuses all cycles
+    *nbad_host = nbad;
+    return SCVT_OK;
+}
+
 int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                        int round, int32_t* bad_out, int32_t* ready_host) {
     if (!ctx) return SCVT_ERR_CONFIG;

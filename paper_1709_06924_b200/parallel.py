@@ -12,10 +12,12 @@ exchanges are two all-gathers per evaluation:
                 all-gathered, scattered to id order and reduced by the same fixed-shape kernel
                 on every rank.
 
-From the second evaluation on, the previous cycles are reused exactly as on one GPU: each
-rank certifies its owned cells at the new positions, the bad flags are all-reduced (max),
-every rank derives the same bad set and re-check list, rebuilds its own bad cells, and only
-those cycles are all-gathered; up to four rounds, then the full path above.
+From the second evaluation on, the previous cycles are reused exactly as on one GPU: every
+rank runs the same flip repair on its replica of the cycles (deterministic, no exchange);
+cells it cannot repair go through the rounds: each rank certifies its owned cells at the new
+positions, the bad flags are all-reduced (max), every rank derives the same bad set and
+re-check list, rebuilds its own bad cells, and only those cycles are all-gathered; up to
+four rounds, then the full path above.
 
 Positions are replicated; the optimizer's vectors are in arithmetic layout (`SliceOps`): rank r
 owns a contiguous range of whole chunks of the generator ids (include/scvt_b200.h,
@@ -81,6 +83,14 @@ class CudaShardBackend:
         ctx.call("scvt_shard_recheck", _lib.dptr(z), z.shape[0], shard, nshards, rnd,
                  _lib.dptr(bad), ctypes.byref(ready), what="shard_recheck")
         return bool(ready.value)
+
+    def flip(self, z) -> int:
+        """Flip repair of the held cycles, replicated on every rank (no exchange)."""
+        ctx = self.ev._ensure_ctx(z.shape[0])
+        nb = ctypes.c_int32(0)
+        ctx.call("scvt_shard_flip", _lib.dptr(z), z.shape[0], ctypes.byref(nb),
+                 what="shard_flip")
+        return int(nb.value)
 
     def plan(self, n, nshards, bad_all):
         ctx = self.ev._ensure_ctx(n)
@@ -370,6 +380,8 @@ def _reuse_cycles(backend, z, shards, nshards, bad, cyc_send, cyc_all, reduce_ba
     n = z.shape[0]
     if not hasattr(backend, "recheck"):
         return False
+    if hasattr(backend, "flip") and backend.flip(z) == 0:
+        return True                                   # repaired by flips, identically everywhere
     for rnd in range(REUSE_ROUNDS):
         local = []
         for s in shards:

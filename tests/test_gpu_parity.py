@@ -350,7 +350,9 @@ def test_cycle_reuse_matches_fresh_build(monkeypatch):
 def _reuse_counters(ev):
     c = (ctypes.c_int64 * 12)()
     ev.context.lib.scvt_profile_counters(ev.context.ptr, c, 0)
-    return {"reused_evals": c[8], "rebuilt": c[9], "passes": c[10]}
+    f = (ctypes.c_int64 * 4)()
+    ev.context.lib.scvt_profile_flips(ev.context.ptr, f, 0)
+    return {"reused_evals": c[8], "rebuilt": c[9], "passes": c[10], "flips": f[2]}
 
 
 @pytest.mark.parametrize("nshards", [2, 3, 8])
@@ -358,7 +360,8 @@ def test_sharded_cycle_reuse_is_bitwise_identical(nshards):
     """Sharded reuse (scvt_shard_recheck/plan/rebuild/install, shards emulated back to back
     with the bad flags max-reduced and the rebuilt rows gathered slice by slice) along an
     optimizer trajectory: every evaluation bitwise equal to single-GPU scvt_evaluate, and
-    the reuse path actually taken (certified evaluations, local rebuilds)."""
+    the reuse path actually taken (certified evaluations, replicated flip repair, local
+    rebuilds)."""
     from paper_1709_06924_b200.parallel import ShardedMeshEvaluator, CudaShardBackend, emulate_shards
 
     z0 = P.sample_by_density(P.density_preset("c4"), 40962, 0)
@@ -374,7 +377,7 @@ def test_sharded_cycle_reuse_is_bitwise_identical(nshards):
             assert torch.equal(sh.grad, ref.grad) and torch.equal(sh.first, ref.first)
             assert torch.equal(sh.lloyd_diag, ref.lloyd_diag)
         cnt = _reuse_counters(ev)
-    assert cnt["reused_evals"] == 4 and cnt["rebuilt"] > 0
+    assert cnt["reused_evals"] == 4 and cnt["rebuilt"] + cnt["flips"] > 0
 
 
 def test_sharded_trajectory_matches_single_gpu():

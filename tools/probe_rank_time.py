@@ -44,6 +44,9 @@ class Timed(PL.CudaShardBackend):
     def rebuild(self, n_, s, ns, cap, rows):
         return timed("rebuild", s, super().rebuild, n_, s, ns, cap, rows)
 
+    def flip(self, z):
+        return timed("flip", -1, super().flip, z)
+
     def plan(self, n_, ns, bad):
         return timed("plan", -1, super().plan, n_, ns, bad)
 
