@@ -213,6 +213,11 @@ __device__ unsigned long long g_probe[4];
 // once (from its lower-id end) as a flip candidate {i, a, b, c}: triangles (i, a, b) and
 // (i, c, a) -> (i, c, b) and (c, a, b).  Orientation and consistency failures mark bad as in
 // mode 1.  list_ids: `list` holds generator ids instead of sorted slots.
+#ifndef VERIFY_LANES_DEF
+#define VERIFY_LANES_DEF 4
+#endif
+constexpr int VERIFY_LANES = VERIFY_LANES_DEF;   // threads per cell in k_verify
+
 struct FlipQueue {
     int4* cand;
     int* ncand;
@@ -226,7 +231,12 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
                          int* __restrict__ stats, int mode, int* __restrict__ bad,
                          int* __restrict__ nbad, FlipQueue fq = FlipQueue{nullptr, nullptr, 0},
                          int list_ids = 0) {
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x;; idx += gridDim.x * blockDim.x) {
+    // VERIFY_LANES threads per cell, each taking every VERIFY_LANES-th edge of its cycle: the
+    // dependent neighbour-row lookups of different edges run in parallel instead of in one
+    // thread's loop (the pass is memory-latency bound)
+    for (int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;;
+         gidx += (int64_t)gridDim.x * blockDim.x) {
+    const int idx = (int)(gidx / VERIFY_LANES), lane = (int)(gidx % VERIFY_LANES);
     int p, i;
     if (list) {                 // re-certification of a compacted list of sorted slots
         if (idx >= *list_n) return;
@@ -244,10 +254,13 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
     }
     int d = deg[i];
     const int* row = nbr + (int64_t)i * MAXDEG;
-    if (d < 3 || d > MAXDEG) { mark_bad(mode > 1 ? 1 : mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1); continue; }
+    if (d < 3 || d > MAXDEG) {
+        if (lane == 0) mark_bad(mode > 1 ? 1 : mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1);
+        continue;
+    }
     V3 zi = load3(z, i);
     int namb = 0;
-    for (int t = 0; t < d; ++t) {
+    for (int t = lane; t < d; t += VERIFY_LANES) {
         int a = row[t], b = row[t + 1 == d ? 0 : t + 1], c = row[t == 0 ? d - 1 : t - 1];
         int da = deg[a];
         const int* ra = nbr + (int64_t)a * MAXDEG;
@@ -1616,7 +1629,7 @@ int build_cells_range(scvt_ctx* ctx, const GridView& g, int64_t lo, int64_t hi) 
 int verify_range(scvt_ctx* ctx, const double* z, int64_t lo, int64_t hi, int mode = 0) {
     int64_t cnt = hi - lo;
     if (cnt <= 0) return SCVT_OK;
-    k_verify<<<blocks_for(cnt, 128), 128, 0, ctx->stream>>>(
+    k_verify<<<blocks_for(cnt * VERIFY_LANES, 128), 128, 0, ctx->stream>>>(
         z, ctx->d_ids, (int)lo, (int)hi, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
         ctx->d_status, ctx->d_status + 8, mode, ctx->d_bad, ctx->d_nbad);
     LAUNCHED();
@@ -1703,7 +1716,7 @@ int flip_repair(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
     int* cnt = ctx->d_fcnt;        // [0] candidates, [1] [2] list lengths, [3] flips
     CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
     const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
-    k_verify<<<blocks_for(n, 128), 128, 0, s>>>(
+    k_verify<<<blocks_for(n * VERIFY_LANES, 128), 128, 0, s>>>(
         z, ctx->d_ids, 0, (int)n, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
         ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad, fq);
     LAUNCHED();
