@@ -663,8 +663,10 @@ SCVT_HD V3 planar_circumcenter(V3 a, V3 b, V3 c) {
     V3 n = cross(ab, ac);
     double n2 = dot(n, n), ab2 = dot(ab, ab), ac2 = dot(ac, ac);
     V3 num = add(mul(cross(n, ab), ac2), mul(cross(ac, n), ab2));
-    double den = 2.0 * n2;
-    return add(a, v3(num.x / den, num.y / den, num.z / den));
+    // one division, three products (the reference divides each component; the results agree
+    // to an ulp, far inside the 1e-12 parity contract; FP64 divides are long MUFU+Newton chains)
+    const double rden = 1.0 / (2.0 * n2);
+    return add(a, mul(num, rden));
 }
 
 SCVT_HD double signed_area(V3 v0, V3 v1, V3 v2, V3 nhat) {
@@ -682,7 +684,7 @@ SCVT_HD FanPair fan_pair(V3 vi, V3 vj, V3 vk, int i, int j, int k) {
     V3 n = cross(sub(vb, va), sub(vc, va));
     double nn = norm3(n);
     f.degenerate = !(nn > 0.0);
-    n = v3(n.x / nn, n.y / nn, n.z / nn);
+    n = mul(n, 1.0 / nn);
     if (dot(n, add(add(va, vb), vc)) < 0.0) n = mul(n, -1.0);
     V3 mij = mul(add(vi, vj), 0.5);
     V3 mki = mul(add(vk, vi), 0.5);
