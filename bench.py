@@ -183,7 +183,7 @@ def cpu_measure(cfg, steps, warmup, regions=0):
 
 
 def run_reference(a):
-    rank, world, _ = dist_env()
+    rank, _, _ = dist_env()
     if rank != 0:
         return
     n = CONFIGS[a.config][0]

@@ -270,8 +270,7 @@ class Minimizer:
     def step(self):
         """One iteration (optimizer.py:300-366).  Returns (record, movement, z_new, res_new)
         and advances the state; the caller applies the stopping rules."""
-        torch = self.torch
-        ops, ev, z, res, k = self.ops, self.evaluator, self.z, self.res, self.k
+        ops, ev, z, res = self.ops, self.evaluator, self.z, self.res
         self.n += 1
         n = self.n
         t_iter = time.perf_counter()
