@@ -39,7 +39,8 @@ enum scvt_status {
     SCVT_ERR_CONFIG = 9,              /* ConfigError / ValueError                             */
     SCVT_ERR_CAPACITY = 10,           /* n > n_max, valence/polygon capacity exceeded          */
     SCVT_ERR_CUDA = 11,               /* CUDA runtime failure                                  */
-    SCVT_ERR_NCCL = 12                /* collective failure (multi-GPU plumbing)               */
+    SCVT_ERR_NCCL = 12,               /* collective failure (multi-GPU plumbing)               */
+    SCVT_ERR_FACTORIZATION = 13       /* FactorizationError       cvt_core.py:218-236        */
 };
 
 /* density kinds (density.py:116-129 + BASELINE tanh^4 variants, DECISIONS.md D3/D4) */
@@ -250,6 +251,28 @@ int scvt_reduce_chunks(scvt_ctx* ctx, const double* red, int32_t nval, const uin
 int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* centers, int32_t p,
                    const uint32_t* adjacency, int32_t* arithmetic, int32_t fresh,
                    int32_t* class_host);
+
+/* graph Laplacian preconditioner (methods laplacian-a6 / laplacian-m2) ---------------------
+ * LaplacianPreconditioner (cvt_core.py:192-240): a_ij = -int_{T_ij u T_ji} rho over the fan
+ * sub-triangles next to edge ij, zero row sums.  scvt_laplacian, right after the evaluation of
+ * these n points, writes the weights aligned with the context's cycles: wsym (n, 32) f64 =
+ * w_ij + w_ji for the neighbour in cycle slot t, diag (n,) = row sums, and a copy of the
+ * cycles themselves (nbr_out (n, 32) int32, deg_out (n,)) that the solve takes as the matrix's
+ * sparsity.  The caller forms the
+ * perturbed diagonal dpert (m2: 1.01 diag, a6: diag + 1e-6).  scvt_laplacian_solve solves
+ * A_pert x = b for the three coordinate columns of b (n,3) by conjugate gradients with
+ * fixed-order reductions until |r_c| <= tol |b_c| (the reference factors with SuperLU; an
+ * indefinite matrix or no convergence -> SCVT_ERR_FACTORIZATION). */
+int scvt_laplacian(scvt_ctx* ctx, int64_t n, double* wsym, double* diag, int32_t* nbr_out,
+                   int32_t* deg_out);
+int scvt_laplacian_solve(scvt_ctx* ctx, int64_t n, const int32_t* nbr, const int32_t* deg,
+                         const double* wsym, const double* dpert, const double* b, double* x,
+                         double tol, int32_t max_iter, int32_t* iters_host);
+/* two_loop_direction (optimizer.py:147-167) around a general initial inverse: backward loop
+ * (q = g - sum a_k y_k, newest first), caller applies h0, forward loop + negation;
+ * qg_host = q.g */
+int scvt_twoloop_backward(scvt_ctx* ctx, const double* g, int64_t n, double* q);
+int scvt_twoloop_forward(scvt_ctx* ctx, double* q, const double* g, int64_t n, double* qg_host);
 
 /* optimizer vector algebra -------------------------------------------------------------
  * CorrectionHistory (optimizer.py:79-114): ring of at most lbfgs_m (s, y) pairs held on

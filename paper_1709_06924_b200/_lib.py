@@ -98,6 +98,11 @@ SIGNATURES = {
     "scvt_reduce_chunks": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _c_dbl_p]),
     "scvt_migration": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int32, _vp, _vp,
                                       ctypes.c_int32, _c_i32_p]),
+    "scvt_laplacian": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
+    "scvt_laplacian_solve": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                            ctypes.c_double, ctypes.c_int32, _c_i32_p]),
+    "scvt_twoloop_backward": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
+    "scvt_twoloop_forward": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _c_dbl_p]),
     "scvt_history_clear": (ctypes.c_int, [_vp]),
     "scvt_history_size": (ctypes.c_int, [_vp, _c_i32_p]),
     "scvt_history_gamma": (ctypes.c_int, [_vp, _c_dbl_p]),

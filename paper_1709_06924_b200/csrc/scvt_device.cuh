@@ -36,6 +36,7 @@ enum : int {
     ST_POLE = 1 << 7,             // x16 density evaluated within 1e-9 of a pole
     ST_DEGENERATE_TRI = 1 << 8,   // zero-normal triangle in the fan construction
     ST_CENTROID = 1 << 9,         // |c| <= 1e-12 in a Lloyd step
+    ST_INDEFINITE = 1 << 10,      // perturbed Laplacian not positive definite (CG p.Ap <= 0)
 };
 
 constexpr int MAXV = 64;          // polygon edges while clipping

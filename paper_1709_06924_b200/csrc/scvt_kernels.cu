@@ -522,9 +522,14 @@ k_quad(QuadArgs a) {
     const double* w = s_nodes + 2 * a.nq;
     if (SYM7 && !SPHERE && SPLIT) {
         subtri_moments_sym7<KIND, 8>(f.s[half], vi, l1, l2, w, a.dp, acc, &pole);
-    } else {
+    } else {   // both halves in this thread, stored separately (per-sub-triangle masses feed
+               // the graph Laplacian; the gathers add the halves: the same sums as before)
         subtri_moments<KIND, SPHERE>(f.s[0], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
-        subtri_moments<KIND, SPHERE>(f.s[1], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
+        double acc1[5] = {0, 0, 0, 0, 0};
+        subtri_moments<KIND, SPHERE>(f.s[1], vi, l1, l2, w, a.nq, a.dp, acc1, &pole);
+        double* out1 = a.part + (int64_t)u * PART_ROW + 5;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) out1[c] = acc1[c];
     }
     if (pole) atomicOr(a.status, ST_POLE);
     // incidence-major: [u][half][m, cx, cy, cz, E] (80 B per incidence, one contiguous run
@@ -1090,6 +1095,141 @@ __global__ void k_reduce_chunks(const double* __restrict__ red, int nval, RedOps
     }
 }
 
+// ------------------------------------------------------------------ graph Laplacian
+// LaplacianPreconditioner (cvt_core.py:192-229): a_ij = -int over T_ij u T_ji of rho, rows
+// summing to zero, perturbed (m2: diagonal x 1.01, a6: + 1e-6 I).  T_ij, the fan
+// sub-triangles of cell i next to edge (i, j = row[t]), are half 0 of incidence t and half 1
+// of incidence t-1 (delaunay.py:357-361); their masses are the per-half quadrature partials.
+// Stored aligned with the cycles: wsym[i][t] = w_ij + w_ji, diag[i] = sum_t wsym[i][t].
+__global__ void k_lap_dir(int n, const int* __restrict__ inc_base, const int* __restrict__ deg,
+                          const double* __restrict__ part, double* __restrict__ wdir) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int d = deg[i], u0 = inc_base[i];
+    for (int t = 0; t < d; ++t)
+        wdir[(int64_t)i * MAXDEG + t] = part[(int64_t)(u0 + t) * PART_ROW] +
+                                        part[(int64_t)(u0 + (t + d - 1) % d) * PART_ROW + 5];
+}
+
+__global__ void k_lap_sym(int n, const int* __restrict__ nbr, const int* __restrict__ deg,
+                          const double* __restrict__ wdir, double* __restrict__ wsym,
+                          double* __restrict__ diag, int* __restrict__ status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int d = deg[i];
+    const int* row = nbr + (int64_t)i * MAXDEG;
+    double dsum = 0.0;
+    for (int t = 0; t < d; ++t) {
+        const int j = row[t];
+        const int q = find_in_cycle(nbr + (int64_t)j * MAXDEG, deg[j], i);
+        if (q < 0) { atomicOr(status, ST_INCONSISTENT); continue; }
+        const double w = wdir[(int64_t)i * MAXDEG + t] + wdir[(int64_t)j * MAXDEG + q];
+        wsym[(int64_t)i * MAXDEG + t] = w;
+        dsum += w;
+    }
+    diag[i] = dsum;
+}
+
+// Conjugate gradients on the perturbed Laplacian for the three coordinate right-hand sides at
+// once (LaplacianPreconditioner.solve, cvt_core.py:231-236; the reference factors it with
+// SuperLU).  One chunk per block, fixed-order reductions (bitwise repeatable); the scalars
+// live on the device: cg[0..2] r.r, cg[3..5] p.Ap, cg[6..8] new r.r, cg[9..11] b.b.
+__device__ __forceinline__ double lap_row(const int* __restrict__ row, int d,
+                                          const double* __restrict__ wrow, double dp,
+                                          const double* __restrict__ x, int64_t i, int c) {
+    double y = dp * x[3 * i + c];
+    for (int t = 0; t < d; ++t) y -= wrow[t] * x[3 * (int64_t)row[t] + c];
+    return y;
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_cg_spmv(const int* __restrict__ nbr, const int* __restrict__ deg,
+          const double* __restrict__ wsym, const double* __restrict__ dpert,
+          const double* __restrict__ p, double* __restrict__ q, Chunks ck,
+          double* __restrict__ red) {
+    double pq[3] = {0, 0, 0};
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
+        const int d = deg[i];
+        const int* row = nbr + i * MAXDEG;
+        const double* wrow = wsym + i * MAXDEG;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double y = lap_row(row, d, wrow, dpert[i], p, i, c);
+            q[3 * i + c] = y;
+            pq[c] += p[3 * i + c] * y;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double v = block_reduce<0>(pq[c]);
+        if (threadIdx.x == 0) *chunk_slot(red, ck, c) = v;
+    }
+}
+
+// x += alpha p, r -= alpha q (alpha = r.r / p.Ap per coordinate); partials of the new r.r
+__global__ void __launch_bounds__(RED_THREADS)
+k_cg_step(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+          const double* __restrict__ q, const double* __restrict__ cg, Chunks ck,
+          double* __restrict__ red, int* __restrict__ status) {
+    double al[3], rr[3] = {0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        al[c] = cg[3 + c] != 0.0 ? cg[c] / cg[3 + c] : 0.0;
+        if (!(cg[3 + c] > 0.0) && cg[c] > 0.0 && blockIdx.x == 0 && threadIdx.x == 0)
+            atomicOr(status, ST_INDEFINITE);
+    }
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int64_t e = 3 * i + c;
+            x[e] = fma(al[c], p[e], x[e]);
+            const double rv = fma(-al[c], q[e], r[e]);
+            r[e] = rv;
+            rr[c] += rv * rv;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double v = block_reduce<0>(rr[c]);
+        if (threadIdx.x == 0) *chunk_slot(red, ck, c) = v;
+    }
+}
+
+// chunk partials of b.b per coordinate
+__global__ void __launch_bounds__(RED_THREADS)
+k_cg_norms(const double* __restrict__ b, Chunks ck, double* __restrict__ red) {
+    double bb[3] = {0, 0, 0};
+    int64_t i0, i1;
+    chunk_span(ck, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) bb[c] += b[3 * i + c] * b[3 * i + c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double v = block_reduce<0>(bb[c]);
+        if (threadIdx.x == 0) *chunk_slot(red, ck, c) = v;
+    }
+}
+
+// p = r + beta p (beta = new r.r / r.r), then r.r <- new r.r (one thread, after the pass)
+__global__ void k_cg_dir(double* __restrict__ p, const double* __restrict__ r,
+                         double* __restrict__ cg, int64_t len) {
+    double be[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) be[c] = cg[c] != 0.0 ? cg[6 + c] / cg[c] : 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * blockDim.x)
+        p[e] = fma(be[e % 3], p[e], r[e]);
+}
+
+__global__ void k_cg_roll(double* __restrict__ cg) {
+    if (threadIdx.x < 3) cg[threadIdx.x] = cg[6 + threadIdx.x];
+}
+
 // ------------------------------------------------------------------ LBFGS vector kernels
 __global__ void k_copy(const double* __restrict__ x, int64_t len, double* __restrict__ y) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len;
@@ -1367,6 +1507,9 @@ struct scvt_ctx {
     // flip repair: candidates {i, a, b, c} (<= 3n), tickets, double-buffered id lists,
     // counters {ncand, nlist[2], nflips}
     int4* d_cand = nullptr;
+    double* d_wdir = nullptr;          // graph Laplacian: directed pair masses [n][MAXDEG] (lazy)
+    double* d_cgv = nullptr;           // CG work vectors r, p, q: [3][3 n] (lazy)
+    double* d_cg = nullptr;            // CG scalars [16] (lazy)
     unsigned long long* d_lock = nullptr;
     int* d_flist = nullptr;            // [2][n]
     int* d_fflag = nullptr;            // [n]
@@ -1501,6 +1644,8 @@ int status_to_code(scvt_ctx* ctx, int st) {
         return fail(ctx, SCVT_ERR_CENTROID_AT_ORIGIN, "first moment ~0");
     if (st & ST_DEGENERATE_TRI)
         return fail(ctx, SCVT_ERR_DEGENERATE_TRIANGLE, "degenerate triangle in the fan");
+    if (st & ST_INDEFINITE)
+        return fail(ctx, SCVT_ERR_FACTORIZATION, "perturbed Laplacian is numerically indefinite");
     return fail(ctx, SCVT_ERR_COVERAGE,
                 "triangulation certificate failed (status 0x%x: %s%s%s)", st,
                 (st & ST_INCONSISTENT) ? "inconsistent cycles " : "",
@@ -1888,7 +2033,7 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
     if (n_inc <= 0) return SCVT_OK;
     // split mode (thread per fan sub-triangle) on the 7-point fast path: twice the work units,
     // a finer last wave and shorter per-thread chains (c4 k_quad 9.44 -> 8.84 ms, c3 -11 %)
-    ctx->split = ctx->sym7 && !ctx->measure;
+    ctx->split = 1;   // every path stores the two fan sub-triangles of an incidence separately
     unsigned grid = blocks_for(n_inc, QUAD_THREADS);
     size_t smem = 3 * (size_t)ctx->nq * sizeof(double);
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
@@ -2316,7 +2461,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
-                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_fcnt, ctx->d_counts,
+                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_wdir, ctx->d_cgv, ctx->d_cg, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_fcnt, ctx->d_counts,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
@@ -2771,6 +2916,143 @@ int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* cent
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_mig, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     *class_host = ctx->h_small[0];
+    return SCVT_OK;
+}
+
+// ---------------------------------------------------------------------- graph Laplacian
+int scvt_laplacian(scvt_ctx* ctx, int64_t n, double* wsym, double* diag, int32_t* nbr_out,
+                   int32_t* deg_out) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (ctx->cycles_n != n)
+        return fail(ctx, SCVT_ERR_CONFIG, "scvt_laplacian needs the evaluation of these %lld points",
+                    (long long)n);
+    if (!ctx->d_wdir) TRY(dalloc(ctx, &ctx->d_wdir, (size_t)ctx->n_max * MAXDEG));
+    cudaStream_t s = ctx->stream;
+    TRY(reset_status(ctx));
+    k_lap_dir<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_inc_base, ctx->d_deg, ctx->d_part,
+                                                  ctx->d_wdir);
+    LAUNCHED();
+    k_lap_sym<<<blocks_for(n, 256), 256, 0, s>>>((int)n, ctx->d_nbr, ctx->d_deg, ctx->d_wdir,
+                                                  wsym, diag, ctx->d_status);
+    LAUNCHED();
+    // the matrix keeps its own copy of the sparsity (the context's cycles move on with the
+    // next evaluation)
+    CK(cudaMemcpyAsync(nbr_out, ctx->d_nbr, (size_t)n * MAXDEG * sizeof(int),
+                       cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(deg_out, ctx->d_deg, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    ctx->launches += 2;
+    TRY(readback(ctx, 0));
+    if (ctx->h_status[0]) return status_to_code(ctx, ctx->h_status[0]);
+    return SCVT_OK;
+}
+
+int scvt_laplacian_solve(scvt_ctx* ctx, int64_t n, const int32_t* nbr, const int32_t* deg,
+                         const double* wsym, const double* dpert, const double* b, double* x,
+                         double tol, int32_t max_iter, int32_t* iters_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n > n_max");
+    if (!ctx->d_cgv) TRY(dalloc(ctx, &ctx->d_cgv, (size_t)9 * ctx->n_max));
+    if (!ctx->d_cg) TRY(dalloc(ctx, &ctx->d_cg, (size_t)16));
+    cudaStream_t s = ctx->stream;
+    const int64_t len = 3 * n;
+    double* r = ctx->d_cgv;
+    double* pv = r + 3 * ctx->n_max;
+    double* qv = pv + 3 * ctx->n_max;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, 0, 1, &ck));
+    TRY(reset_status(ctx));
+    CK(cudaMemsetAsync(x, 0, len * sizeof(double), s));
+    CK(cudaMemcpyAsync(r, b, len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(pv, b, len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    ctx->launches += 3;
+    RedOps ro;
+    for (int v = 0; v < 3; ++v) ro.op[v] = 0;
+    CK(cudaMemsetAsync(ctx->d_cg, 0, 16 * sizeof(double), s));
+    k_cg_norms<<<ck.nc, RED_THREADS, 0, s>>>(b, ck, ctx->d_partials);              // b.b
+    LAUNCHED();
+    k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg);         // r.r = b.b
+    LAUNCHED();
+    k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg + 9);
+    LAUNCHED();
+    int it = 0;
+    constexpr int CHECK = 8;
+    for (;;) {
+        for (int k = 0; k < CHECK && it < max_iter; ++k, ++it) {
+            k_cg_spmv<<<ck.nc, RED_THREADS, 0, s>>>(nbr, deg, wsym, dpert, pv, qv, ck,
+                                                     ctx->d_partials);
+            LAUNCHED();
+            k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg + 3);   // p.Ap
+            LAUNCHED();
+            k_cg_step<<<ck.nc, RED_THREADS, 0, s>>>(x, r, pv, qv, ctx->d_cg, ck, ctx->d_partials,
+                                                     ctx->d_status);
+            LAUNCHED();
+            k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg + 6);   // new r.r
+            LAUNCHED();
+            k_cg_dir<<<RED_BLOCKS, VEC_THREADS, 0, s>>>(pv, r, ctx->d_cg, len);
+            LAUNCHED();
+            k_cg_roll<<<1, 32, 0, s>>>(ctx->d_cg);
+            LAUNCHED();
+        }
+        CK(cudaMemcpyAsync(ctx->h_scal, ctx->d_cg, 12 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (ctx->h_status[0]) return status_to_code(ctx, ctx->h_status[0]);
+        bool done = true;
+        for (int c = 0; c < 3; ++c) {
+            const double rr = ctx->h_scal[c], bb = ctx->h_scal[9 + c];
+            if (!std::isfinite(rr))
+                return fail(ctx, SCVT_ERR_FACTORIZATION, "Laplacian solve produced non-finite values");
+            if (rr > tol * tol * bb) done = false;
+        }
+        if (done) break;
+        if (it >= max_iter)
+            return fail(ctx, SCVT_ERR_FACTORIZATION, "Laplacian CG did not reach %.1e in %d iterations",
+                        tol, max_iter);
+    }
+    *iters_host = it;
+    return SCVT_OK;
+}
+
+int scvt_twoloop_backward(scvt_ctx* ctx, const double* g, int64_t n, double* q) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    const int64_t len = 3 * n;
+    cudaStream_t s = ctx->stream;
+    k_copy<<<RED_BLOCKS, VEC_THREADS, 0, s>>>(g, len, q);
+    LAUNCHED();
+    const int64_t stride = 3 * ctx->n_max;
+    for (int r = ctx->hist_count - 1; r >= 0; --r) {       // newest -> oldest
+        const int slot = (ctx->hist_head + r) % ctx->m;
+        TRY(dot_to_slot(ctx, ctx->d_S + slot * stride, q, len, 0));
+        k_twoloop_back<<<RED_BLOCKS, RED_THREADS, 0, s>>>(q, ctx->d_Y + slot * stride, len,
+                                                          ctx->d_partials, ctx->rho[slot],
+                                                          ctx->d_alpha + slot);
+        LAUNCHED();
+    }
+    return SCVT_OK;
+}
+
+int scvt_twoloop_forward(scvt_ctx* ctx, double* q, const double* g, int64_t n, double* qg_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    const int64_t len = 3 * n;
+    cudaStream_t s = ctx->stream;
+    const int64_t stride = 3 * ctx->n_max;
+    const int cnt = ctx->hist_count;
+    for (int r = 0; r < cnt; ++r) {                         // oldest -> newest, negate last
+        const int slot = (ctx->hist_head + r) % ctx->m;
+        TRY(dot_to_slot(ctx, ctx->d_Y + slot * stride, q, len, 0));
+        k_twoloop_fwd<<<RED_BLOCKS, RED_THREADS, 0, s>>>(q, ctx->d_S + slot * stride, len,
+                                                         ctx->d_partials, ctx->rho[slot],
+                                                         ctx->d_alpha + slot, r == cnt - 1 ? 1 : 0);
+        LAUNCHED();
+    }
+    if (cnt == 0) {
+        k_scale<<<RED_BLOCKS, VEC_THREADS, 0, s>>>(-1.0, q, len, q);
+        LAUNCHED();
+    }
+    TRY(dot_to_slot(ctx, q, g, len, 0));
+    TRY(finish_slots(ctx, 1));
+    TRY(readback(ctx, 1));
+    *qg_host = ctx->h_scal[0];
     return SCVT_OK;
 }
 

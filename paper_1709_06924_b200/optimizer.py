@@ -33,7 +33,7 @@ WOLFE_C1 = 1e-4              # optimizer.py:33
 WOLFE_C2 = 0.9               # optimizer.py:34
 MAX_LINE_SEARCH_EVALS = 10   # optimizer.py:35
 
-METHODS = ("lloyd", "lbfgs", "lloyd-plbfgs")
+METHODS = ("lloyd", "lbfgs", "lloyd-plbfgs", "laplacian-a6", "laplacian-m2")
 
 
 @dataclass
@@ -183,6 +183,17 @@ class _DeviceOps:
                       float(gamma), _lib.dptr(z), self.n, _lib.dptr(q3), out)
         return out[0], out[1]
 
+    def direction_general(self, g, h0, z, q, q3):
+        """two_loop_direction with a general initial inverse (optimizer.py:147-167; h0 =
+        LaplacianInverse, 137-144) + the tangent projection: returns (q.g, g.q3)."""
+        self.ctx.call("scvt_twoloop_backward", _lib.dptr(g), self.n, _lib.dptr(q))
+        r = h0.solve(q)
+        qg = ctypes.c_double()
+        self.ctx.call("scvt_twoloop_forward", _lib.dptr(r), _lib.dptr(g), self.n,
+                      ctypes.byref(qg))
+        q.copy_(r)
+        return qg.value, self.tangent(q, z, g, q3)
+
     def tangent(self, q, z, g, q3) -> float:
         d = ctypes.c_double()
         self.ctx.call("scvt_tangent_project", _lib.dptr(q), _lib.dptr(z), _lib.dptr(g), self.n,
@@ -292,13 +303,22 @@ class Minimizer:
                 else:
                     diag = res.lloyd_diag
             q, q3 = self.q, self.q3
-            # two_loop_direction + projection (optimizer.py:147-167, 322-333), fused on device
-            qg, dphi0 = ops.direction_tangent(res.grad, diag, gamma, z, q3)
+            if self.method.startswith("laplacian"):                # _initial_inverse
+                if res.laplacian is None:
+                    raise ValueError("evaluator did not supply a Laplacian factorization")
+
+                def direction():
+                    return ops.direction_general(res.grad, res.laplacian, z, q, q3)
+            else:
+                def direction():   # two_loop_direction + projection, fused on the device
+                    return ops.direction_tangent(res.grad, diag, gamma, z, q3)
+            # optimizer.py:147-167, 312-333
+            qg, dphi0 = direction()
             if qg >= 0.0:
                 logger.warning("non-descent direction at iteration %d; history reset", n)
                 ops.history_clear()
                 self.resets += 1
-                qg, dphi0 = ops.direction_tangent(res.grad, diag, gamma, z, q3)
+                qg, dphi0 = direction()
                 if qg >= 0.0:
                     ops.scale(-ops.gamma(), res.grad, q)          # q = -hist.gamma() * g
                     dphi0 = ops.tangent(q, z, res.grad, q3)

@@ -499,6 +499,11 @@ class ShardedMeshEvaluator(MeshEvaluator):
         super().__init__(*args, **kwargs)
         import torch.distributed as dist
 
+        from .errors import ConfigError
+
+        if self.laplacian is not None:
+            raise ConfigError("the graph Laplacian preconditioner runs on one GPU")
+
         self.group = group
         if dist.is_available() and dist.is_initialized():
             self.rank = dist.get_rank(group)

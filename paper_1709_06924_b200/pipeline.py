@@ -60,6 +60,45 @@ class EvalResult:
     dirderiv: float = float("nan")      # sum g.(q3/|v|) when evaluated as a line-search trial
 
 
+class DeviceLaplacian:
+    """LaplacianPreconditioner (cvt_core.py:192-236) on the device: density-weighted graph
+    Laplacian over the Delaunay adjacency of one evaluation (weights and sparsity copied at
+    assembly, C ABI `scvt_laplacian`), perturbed as ``a6`` (+1e-6 I) or ``m2`` (diagonal
+    x 1.01); `solve` runs conjugate gradients on the three coordinate columns
+    (`scvt_laplacian_solve`) where the reference factors with SuperLU."""
+
+    TOL = 1e-14
+    MAX_ITER = 50000
+
+    def __init__(self, ctx, n: int, perturbation: str, device):
+        torch = _torch()
+        if perturbation not in ("a6", "m2"):
+            raise ValueError(f"unknown perturbation {perturbation!r}")
+        self.ctx, self.n, self.perturbation = ctx, n, perturbation
+        self.wsym = torch.empty((n, 32), dtype=torch.float64, device=device)
+        self.diag = torch.empty(n, dtype=torch.float64, device=device)
+        self.nbr = torch.empty((n, 32), dtype=torch.int32, device=device)
+        self.deg = torch.empty(n, dtype=torch.int32, device=device)
+        ctx.call("scvt_laplacian", n, _lib.dptr(self.wsym), _lib.dptr(self.diag),
+                 _lib.dptr(self.nbr), _lib.dptr(self.deg), what="laplacian")
+        self.dpert = self.diag + 1e-6 if perturbation == "a6" else self.diag * (1.0 + 1e-2)
+        self.iterations = 0
+
+    def solve(self, rhs):
+        """Solve A_pert x = rhs for an (n, 3) device tensor (or NumPy array)."""
+        torch = _torch()
+        host = not isinstance(rhs, torch.Tensor)
+        b = torch.as_tensor(np.asarray(rhs, dtype=np.float64) if host else rhs,
+                            device=self.wsym.device).reshape(self.n, 3).contiguous()
+        x = torch.empty_like(b)
+        it = ctypes.c_int32()
+        self.ctx.call("scvt_laplacian_solve", self.n, _lib.dptr(self.nbr), _lib.dptr(self.deg),
+                      _lib.dptr(self.wsym), _lib.dptr(self.dpert), _lib.dptr(b), _lib.dptr(x),
+                      self.TOL, self.MAX_ITER, ctypes.byref(it), what="laplacian solve")
+        self.iterations += it.value
+        return to_numpy(x)[0] if host else x
+
+
 @dataclass(frozen=True)
 class SphericalTriangulation:
     """delaunay.py:50-78: canonical triangles (+ circumcircles) and per-triangle flags
@@ -136,15 +175,16 @@ class MeshEvaluator:
     reference's region path reproduces bitwise; a ``covering``
     (`partition.Covering`) adds the reference's per-evaluation migration class
     (`EvalResult.migration`, computed on the device), which drives the optimizer's
-    re-decompose-and-reset rule (optimizer.py:377-381).  ``laplacian`` (SuperLU graph Laplacian, cvt_core.py:192-240) is out of
-    scope and raises."""
+    re-decompose-and-reset rule (optimizer.py:377-381).  The graph Laplacian preconditioner
+    (cvt_core.py:192-240) is assembled on the device when ``laplacian`` is "a6" or "m2"
+    (`DeviceLaplacian`, `EvalResult.laplacian`)."""
 
     def __init__(self, density: DensityField, rule: QuadratureRule | str, covering=None,
                  workers: int = 1, backend: str = "process", laplacian: str | None = None,
                  measure: str = "flat", eps_proj: float = EPS_PROJ, *, subdivision: int = 0,
                  device: int | None = None, density_table: bool = True):
-        if laplacian is not None:
-            raise ConfigError("the Laplacian preconditioner is outside this hot path")
+        if laplacian not in (None, "a6", "m2"):
+            raise ValueError(f"unknown perturbation {laplacian!r}")
         if measure not in ("flat", "sphere"):
             raise ValueError(f"unknown integration measure {measure!r}")
         self.density = density
@@ -152,7 +192,7 @@ class MeshEvaluator:
         self.covering = covering
         self.workers = max(1, workers)
         self.backend = backend
-        self.laplacian = None
+        self.laplacian = laplacian
         self.measure = measure
         self.eps_proj = eps_proj
         self.subdivision = int(subdivision)
@@ -280,7 +320,9 @@ class MeshEvaluator:
                           lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]),
                           min_diag=float(sc[3]),
                           dirderiv=float(sc[4]) if q3 is not None else float("nan"),
-                          migration=self._migration(z))
+                          migration=self._migration(z),
+                          laplacian=(DeviceLaplacian(ctx, n, self.laplacian, z.device)
+                                     if self.laplacian is not None else None))
 
     def evaluate(self, points) -> EvalResult:
         """pipeline.py:261-279.  NumPy in -> NumPy out; CUDA tensor in -> tensors out."""
@@ -491,8 +533,7 @@ def run(plan: RunPlan, initial_points=None, progress=None) -> RunResult:
                               f"({plan.ladder[0]})")
     else:
         z = sample_by_density(density, plan.ladder[0], plan.seed)
-    if plan.method.startswith("laplacian"):
-        raise ConfigError("the Laplacian preconditioner is outside this hot path")
+    laplacian = {"laplacian-a6": "a6", "laplacian-m2": "m2"}.get(plan.method)
     levels = []
     tri = None
     covering = None
@@ -503,6 +544,7 @@ def run(plan: RunPlan, initial_points=None, progress=None) -> RunResult:
         covering = _covering_for(plan, k, density)
         t_level = time.perf_counter()
         with MeshEvaluator(density, rule, covering, workers=plan.workers, backend=plan.backend,
+                           laplacian=laplacian,
                            measure=plan.measure, eps_proj=plan.eps_proj,
                            subdivision=plan.subdivision) as ev:
             result = minimize(z, plan.method, ev, criteria, corrections=plan.corrections,

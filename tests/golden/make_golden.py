@@ -384,12 +384,41 @@ def case_covering():
          reason=np.array(res.reason))
 
 
+def case_laplacian():
+    """Graph-Laplacian preconditioned LBFGS (laplacian-m2 and laplacian-a6, cvt_core.py:192-240
+    with SuperLU): x3 density, 4-pt rule, N=2562, 20 iterations each; plus one assembled matrix
+    and a solve for the matrix/solve parity tests."""
+    from scvtmesh import cvt_core as cc
+
+    _DEPTH["d"] = 0
+    z0 = geometry.random_sphere_points(2562, 0)
+    out = {"z0": z0}
+    for pert in ("m2", "a6"):
+        ev = pipeline.MeshEvaluator(field_for("x3"), RULES["4pt"], laplacian=pert)
+        crit = optimizer.StoppingCriteria(max_iterations=20, movement_tol=1e-300, grad_tol=1e-300,
+                                          stall_tol=1e-300)
+        res = optimizer.minimize(z0, f"laplacian-{pert}", ev, crit, corrections=7)
+        print(f"  laplacian-{pert}: {len(res.records)} it, {res.fevals} fevals, "
+              f"resets={res.resets}, reason={res.reason}", flush=True)
+        out[f"{pert}_energy"] = np.array([r.energy for r in res.records])
+        out[f"{pert}_fevals"] = np.array([-1 if r.fevals is None else r.fevals for r in res.records])
+        out[f"{pert}_final_z"] = res.points
+        r0 = ev.evaluate(z0)
+        lap = r0.laplacian
+        m = lap.perturbed.tocsr()
+        out[f"{pert}_indptr"], out[f"{pert}_indices"], out[f"{pert}_data"] = m.indptr, m.indices, m.data
+        rhs = np.random.default_rng(1).standard_normal((2562, 3))
+        out[f"{pert}_rhs"], out[f"{pert}_x"] = rhs, lap.solve(rhs)
+        ev.close()
+    save("laplacian", **out)
+
+
 CASES = {
     "rules": case_rules, "c1_eval": case_c1_eval, "density_eval": case_density_eval,
     "sampler": case_sampler, "medium": case_medium, "small_sets": case_small_sets,
     "traj_fast": case_traj_fast, "traj_slow": case_traj_slow,
     "traj_fallback": case_traj_fallback, "medium_slim": case_medium_slim,
-    "run_ladder": case_run_ladder, "covering": case_covering,
+    "run_ladder": case_run_ladder, "covering": case_covering, "laplacian": case_laplacian,
 }
 
 if __name__ == "__main__":

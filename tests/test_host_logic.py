@@ -147,11 +147,20 @@ def test_same_public_names_as_reference():
         assert hasattr(P, name), name
 
 
-def test_unknown_method_and_laplacian_rejected():
-    with pytest.raises(P.ConfigError):
-        P.MeshEvaluator(P.density_preset("const"), "4pt", laplacian="a6")
+def test_unknown_perturbation_and_measure_rejected():
+    """The graph Laplacian perturbations of cvt_core.py:206-214 are "a6" and "m2"; anything else
+    raises like the reference's ValueError; the sharded evaluator keeps it single-GPU."""
+    ev = P.MeshEvaluator(P.density_preset("const"), "4pt", laplacian="a6")
+    assert ev.laplacian == "a6"
+    with pytest.raises(ValueError):
+        P.MeshEvaluator(P.density_preset("const"), "4pt", laplacian="b7")
     with pytest.raises(ValueError):
         P.MeshEvaluator(P.density_preset("const"), "4pt", measure="bogus")
+    with pytest.raises(P.ConfigError):
+        P.ShardedMeshEvaluator(P.density_preset("const"), "4pt", laplacian="m2")
+    from paper_1709_06924_b200.optimizer import METHODS
+
+    assert set(METHODS) == {"lloyd", "lbfgs", "lloyd-plbfgs", "laplacian-a6", "laplacian-m2"}
 
 
 def test_runplan_validation():
