@@ -180,6 +180,18 @@ int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
  * *nbad_host = 0: certified, call scvt_shard_moments(cyc_all = NULL); > 0: cells left for the
  * rounds above; -1: no held cycles for n points (or reuse/flips disabled). */
 int scvt_shard_flip(scvt_ctx* ctx, const double* z, int64_t n, int32_t* nbad_host);
+/* the same repair with the certificate pass sharded: each rank runs the flip-mode certificate
+ * of its owned cells -> cand_send int32 [cap][4] ({i, a, b, c} per non-Delaunay edge) and
+ * counts_host = {candidates (> cap: overflow; -1: no held cycles), bad cells};
+ * <caller all-gathers the counts; any bad cell or overflow -> the rounds above; else it
+ * all-gathers cand_send (padded to the largest count) -> cand_all [nshards*cap][4]>;
+ * scvt_shard_flip_rounds then runs the (replicated, deterministic) flip rounds on the
+ * concatenated candidates; *nbad_host = 0: certified. */
+int scvt_shard_flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                           int32_t* cand_send, int64_t cap, int32_t* counts_host);
+int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                           const int32_t* cand_all, int64_t cap, const int64_t* counts,
+                           int32_t* nbad_host);
 int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_all,
                     int64_t* counts_host);
 int scvt_shard_rebuild(scvt_ctx* ctx, int64_t n, int shard, int nshards, int64_t cap,

@@ -70,6 +70,10 @@ SIGNATURES = {
     "scvt_shard_recheck": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int, _vp, _c_i32_p]),
     "scvt_shard_flip": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _c_i32_p]),
+    "scvt_shard_flip_detect": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int,
+                                              ctypes.c_int, _vp, ctypes.c_int64, _c_i32_p]),
+    "scvt_shard_flip_rounds": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp,
+                                              ctypes.c_int64, _c_i64_p, _c_i32_p]),
     "scvt_shard_plan": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, _vp, _c_i64_p]),
     "scvt_shard_rebuild": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int64, _vp]),

@@ -1856,15 +1856,25 @@ constexpr int FLIP_MAX_ROUNDS = 12;
 // touched cells after each), FLIP_ROUNDS_PER_SYNC rounds chained on the device between host
 // reads.  Leaves d_bad / d_nbad as the rebuild path expects them: the cells of orientation or
 // consistency failures, of rejected flips and of candidates still open after the last round.
-int flip_repair(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
+// detection pass of the flip repair over the sorted slots [lo, hi): candidates and bad marks
+int flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi) {
     cudaStream_t s = ctx->stream;
     int* cnt = ctx->d_fcnt;        // [0] candidates, [1] [2] list lengths, [3] flips
     CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
+    if (hi <= lo) return SCVT_OK;
     const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
-    k_verify<<<blocks_for(n * VERIFY_LANES, 128), 128, 0, s>>>(
-        z, ctx->d_ids, 0, (int)n, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
+    k_verify<<<blocks_for((hi - lo) * VERIFY_LANES, 128), 128, 0, s>>>(
+        z, ctx->d_ids, (int)lo, (int)hi, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
         ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad, fq);
     LAUNCHED();
+    return SCVT_OK;
+}
+
+// flip rounds on the queued candidates (cnt[0]) until none is left or the round limit
+int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
+    cudaStream_t s = ctx->stream;
+    int* cnt = ctx->d_fcnt;
+    const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
     int cur = 0, rounds = 0;
     for (;;) {
         CK(cudaMemcpyAsync(ctx->h_small, cnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1906,6 +1916,15 @@ int flip_repair(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
     ctx->flip_stats[2] += ctx->h_small[3];
     ctx->flip_stats[3] += open ? 1 : 0;
     return SCVT_OK;
+}
+
+// Certificate pass over every cell in flip mode, then Lawson flip rounds (detection of the
+// touched cells after each), FLIP_ROUNDS_PER_SYNC rounds chained on the device between host
+// reads.  Leaves d_bad / d_nbad as the rebuild path expects them: the cells of orientation or
+// consistency failures, of rejected flips and of candidates still open after the last round.
+int flip_repair(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
+    TRY(flip_detect(ctx, z, n, 0, n));
+    return flip_rounds(ctx, z, n, nbad_host);
 }
 
 // The bucket grid is only needed to rebuild cells: it is built on demand (*have_grid), so an
@@ -2605,6 +2624,57 @@ int scvt_shard_flip(scvt_ctx* ctx, const double* z, int64_t n, int32_t* nbad_hos
     CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), ctx->stream));
     int nbad = 0;
     TRY(flip_repair(ctx, z, n, &nbad));
+    if (nbad == 0) ctx->reuse_stats[2] += 1;   // certified: the evaluation reuses all cycles
+    *nbad_host = nbad;
+    return SCVT_OK;
+}
+
+int scvt_shard_flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                           int32_t* cand_send, int64_t cap, int32_t* counts_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (nshards < 1 || shard < 0 || shard >= nshards)
+        return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
+    counts_host[0] = -1;
+    counts_host[1] = 0;
+    if (ctx->cycles_n != n || !reuse_enabled() || !flips_enabled()) return SCVT_OK;
+    cudaStream_t s = ctx->stream;
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], s));
+    ctx->prof_n[3] = 0;
+    TRY(reset_status(ctx));
+    CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
+    CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
+    int64_t lo, hi;
+    shard_range(n, shard, nshards, &lo, &hi);
+    TRY(flip_detect(ctx, z, n, lo, hi));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_fcnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int nc = ctx->h_small[0];
+    if (nc > 0 && nc <= cap)
+        CK(cudaMemcpyAsync(cand_send, ctx->d_cand, (size_t)nc * sizeof(int4),
+                           cudaMemcpyDeviceToDevice, s));
+    counts_host[0] = nc;                       // > cap: the caller takes the rebuild rounds
+    counts_host[1] = ctx->h_small[4];
+    return SCVT_OK;
+}
+
+int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
+                           const int32_t* cand_all, int64_t cap, const int64_t* counts,
+                           int32_t* nbad_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    cudaStream_t s = ctx->stream;
+    int64_t total = 0;
+    for (int r = 0; r < nshards; ++r) {        // the shards' candidates, in rank order
+        if (counts[r] > 0)
+            CK(cudaMemcpyAsync(ctx->d_cand + total, cand_all + 4 * (int64_t)r * cap,
+                               (size_t)counts[r] * sizeof(int4), cudaMemcpyDeviceToDevice, s));
+        total += counts[r];
+    }
+    if (total > 3 * n) return fail(ctx, SCVT_ERR_CAPACITY, "%lld flip candidates", (long long)total);
+    ctx->h_small[8] = (int)total;
+    CK(cudaMemcpyAsync(ctx->d_fcnt, ctx->h_small + 8, sizeof(int), cudaMemcpyHostToDevice, s));
+    int nbad = 0;
+    TRY(flip_rounds(ctx, z, n, &nbad));
     if (nbad == 0) ctx->reuse_stats[2] += 1;   // certified: the evaluation reuses all cycles
     *nbad_host = nbad;
     return SCVT_OK;

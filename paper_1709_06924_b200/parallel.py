@@ -12,9 +12,10 @@ exchanges are two all-gathers per evaluation:
                 all-gathered, scattered to id order and reduced by the same fixed-shape kernel
                 on every rank.
 
-From the second evaluation on, the previous cycles are reused exactly as on one GPU: every
-rank runs the same flip repair on its replica of the cycles (deterministic, no exchange);
-cells it cannot repair go through the rounds: each rank certifies its owned cells at the new
+From the second evaluation on, the previous cycles are reused exactly as on one GPU: each
+rank runs the flip-mode certificate of its own cells, the non-Delaunay edges are all-gathered
+and every rank applies the same (deterministic) flip rounds to its replica of the cycles;
+cells the flips cannot repair go through the rounds: each rank certifies its owned cells at the new
 positions, the bad flags are all-reduced (max), every rank derives the same bad set and
 re-check list, rebuilds its own bad cells, and only those cycles are all-gathered; up to
 four rounds, then the full path above.
@@ -83,6 +84,27 @@ class CudaShardBackend:
         ctx.call("scvt_shard_recheck", _lib.dptr(z), z.shape[0], shard, nshards, rnd,
                  _lib.dptr(bad), ctypes.byref(ready), what="shard_recheck")
         return bool(ready.value)
+
+    def flip_detect(self, z, shard, nshards):
+        """Flip-mode certificate of the owned cells: ((cap, 4) int32 candidates, (count, bad))."""
+        import torch
+
+        n = z.shape[0]
+        ctx = self.ev._ensure_ctx(n)
+        cap = 4 * shard_rows(n, nshards) + 64
+        cand = torch.empty((cap, 4), dtype=torch.int32, device=z.device)
+        cnt = (ctypes.c_int32 * 2)()
+        ctx.call("scvt_shard_flip_detect", _lib.dptr(z), n, shard, nshards, _lib.dptr(cand), cap,
+                 cnt, what="shard_flip_detect")
+        return cand, (int(cnt[0]), int(cnt[1]))
+
+    def flip_rounds(self, z, nshards, cand_all, cap, counts) -> int:
+        ctx = self.ev._ensure_ctx(z.shape[0])
+        c = (ctypes.c_int64 * nshards)(*counts)
+        nb = ctypes.c_int32(0)
+        ctx.call("scvt_shard_flip_rounds", _lib.dptr(z), z.shape[0], nshards, _lib.dptr(cand_all),
+                 cap, c, ctypes.byref(nb), what="shard_flip_rounds")
+        return int(nb.value)
 
     def flip(self, z) -> int:
         """Flip repair of the held cycles, replicated on every rank (no exchange)."""
@@ -372,16 +394,43 @@ def _all_gather(out, inp, group):
 REUSE_ROUNDS = 4   # certificate passes before a full rebuild (same as the single-GPU loop)
 
 
-def _reuse_cycles(backend, z, shards, nshards, bad, cyc_send, cyc_all, reduce_bad, gather_rows):
+def _flip_sharded(backend, z, shards, nshards, gather_counts, gather_cand):
+    """Flip repair with the certificate pass sharded (include/scvt_b200.h
+    scvt_shard_flip_detect / _rounds): each shard queues the non-Delaunay edges of its cells,
+    the candidate lists are all-gathered, and every rank runs the same flip rounds on the
+    concatenation.  True: certified; False: take the rebuild rounds; None: no held cycles."""
+    import torch
+
+    cands, counts = [], []
+    for s in shards:
+        cand, cnt = backend.flip_detect(z, s, nshards)
+        cands.append(cand)
+        counts.append(torch.tensor(cnt, dtype=torch.int64, device=cand.device))
+    allc = gather_counts(counts).cpu().reshape(nshards, 2)
+    if bool((allc[:, 0] < 0).any()):
+        return None
+    if int(allc[:, 1].sum()) > 0 or int(allc[:, 0].max()) > cands[0].shape[0]:
+        return False                        # orientation/consistency failures or overflow
+    cap = int(allc[:, 0].max())
+    cand_all = gather_cand([c[:cap] for c in cands], cap) if cap else None
+    return backend.flip_rounds(z, nshards, cand_all, cap, allc[:, 0].tolist()) == 0
+
+
+def _reuse_cycles(backend, z, shards, nshards, bad, cyc_send, cyc_all, reduce_bad, gather_rows,
+                  gather_counts=None, gather_cand=None):
     """The single-GPU reuse loop split at its exchanges (include/scvt_b200.h).  `shards` are
     the shards this process runs (one under torch.distributed, all when emulating);
-    `reduce_bad(bad_of_each_shard) -> bad_all` and `gather_rows(rows_of_each_shard, cap)`
-    are the two collectives.  True when the held cycles were certified for z."""
+    `reduce_bad(bad_of_each_shard) -> bad_all`, `gather_rows(rows_of_each_shard, cap)`,
+    `gather_counts(counts_of_each_shard)` and `gather_cand(candidates_of_each_shard, cap)`
+    are the collectives.  True when the held cycles were certified for z."""
     n = z.shape[0]
     if not hasattr(backend, "recheck"):
         return False
-    if hasattr(backend, "flip") and backend.flip(z) == 0:
-        return True                                   # repaired by flips, identically everywhere
+    if hasattr(backend, "flip_detect") and gather_counts is not None:
+        if _flip_sharded(backend, z, shards, nshards, gather_counts, gather_cand):
+            return True                               # repaired by flips, identically everywhere
+    elif hasattr(backend, "flip") and backend.flip(z) == 0:
+        return True
     for rnd in range(REUSE_ROUNDS):
         local = []
         for s in shards:
@@ -433,8 +482,20 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
         def gather_rows(rows, cap):
             _all_gather(cyc_all[:world * cap], rows[0], group)
 
+        def gather_counts(local):
+            out = torch.empty(world * local[0].numel(), dtype=local[0].dtype,
+                              device=local[0].device)
+            _all_gather(out, local[0], group)
+            return out
+
+        def gather_cand(local, cap):
+            out = torch.empty((world * cap, 4), dtype=local[0].dtype, device=local[0].device)
+            _all_gather(out, local[0].contiguous(), group)
+            return out
+
         reused = _reuse_cycles(backend, z, [rank], world, bad, cyc_send, cyc_all,
-                               lambda local: _all_reduce_max(local[0], group), gather_rows)
+                               lambda local: _all_reduce_max(local[0], group), gather_rows,
+                               gather_counts, gather_cand)
     if reused:
         status = backend.moments(z, rank, world, None, res_send)
     else:
@@ -473,8 +534,11 @@ def emulate_shards(backend, z, nshards: int, q3=None, norms=None):
             for s, rw in enumerate(rows):
                 cyc_all[s * cap:(s + 1) * cap] = rw
 
+        import torch
+
         reused = _reuse_cycles(backend, z, list(range(nshards)), nshards, bad, cyc_send,
-                               cyc_all, reduce_bad, gather_rows)
+                               cyc_all, reduce_bad, gather_rows, lambda local: torch.cat(local),
+                               lambda local, cap: torch.cat(local))
     if not reused:
         for s in range(nshards):
             backend.cells(z, s, nshards, cyc_send)

@@ -44,8 +44,11 @@ class Timed(PL.CudaShardBackend):
     def rebuild(self, n_, s, ns, cap, rows):
         return timed("rebuild", s, super().rebuild, n_, s, ns, cap, rows)
 
-    def flip(self, z):
-        return timed("flip", -1, super().flip, z)
+    def flip_detect(self, z, s, ns):
+        return timed("flip_detect", s, super().flip_detect, z, s, ns)
+
+    def flip_rounds(self, z, ns, cand, cap, counts):
+        return timed("flip_rounds", -1, super().flip_rounds, z, ns, cand, cap, counts)
 
     def plan(self, n_, ns, bad):
         return timed("plan", -1, super().plan, n_, ns, bad)
