@@ -292,8 +292,10 @@ def run_b200(a):
                        "evals_per_iteration": evals / a.steps,
                        "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": "single GPU" if world == 1 else
-                       f"dp{world}: generators sharded in cube-map order, NCCL all-gather of "
-                       f"cycles and per-generator moments, optimizer replicated"},
+                       f"dp{world}: cells sharded in cube-map order (NCCL all-gathers of flip "
+                       f"candidates, rebuilt cycles and per-generator moments), optimizer "
+                       f"vectors in arithmetic layout (chunk partials all-reduced, positions "
+                       f"all-gathered)"},
             "roofline": roofline, "gpu_launches": launches,
             "clocks": clk.summary()}
     # e2e through the public API with host buffers
