@@ -686,3 +686,25 @@ def test_laplacian_trajectory_matches_reference(gold, pert):
     assert np.max(np.abs(e - g[f"{pert}_energy"]) / g[f"{pert}_energy"]) <= 1e-10
     assert [h.fevals for h in res.records] == g[f"{pert}_fevals"].tolist()
     assert rel(res.points, g[f"{pert}_final_z"]) <= (1e-10 if pert == "m2" else 1e-9)
+
+
+@pytest.mark.slow
+def test_flip_repair_full_size_c4(monkeypatch):
+    """BASELINE c4 size (N=655,362): five P-LBFGS iterations whose evaluations are certified by
+    the flip repair of the reused cycles (tens of thousands of flips each); the final
+    triangulation equals a fresh GPU build and Qhull's."""
+    n = 655362
+    z0 = P.sample_by_density(P.density_preset("c4"), n, 0)
+    monkeypatch.delenv("SCVT_NO_FLIPS", raising=False)
+    with _ev("c4", "7pt", 3) as ev, _ev("c4", "7pt", 3) as fresh:
+        st = P.Minimizer(torch.from_numpy(z0).cuda(), "lloyd-plbfgs", ev, 7)
+        for _ in range(5):
+            st.step()
+        fl = (ctypes.c_int64 * 4)()
+        ev.context.lib.scvt_profile_flips(ev.context.ptr, fl, 0)
+        t_reuse = ev.triangulation(st.z).triangles
+        monkeypatch.setenv("SCVT_NO_REUSE", "1")
+        t_fresh = fresh.triangulation(st.z).triangles
+    assert fl[2] > 10000
+    assert np.array_equal(t_reuse, t_fresh)
+    assert np.array_equal(t_fresh, O.convex_hull_delaunay(st.z.cpu().numpy()))
