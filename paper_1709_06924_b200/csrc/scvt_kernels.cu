@@ -1870,17 +1870,23 @@ int flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t h
     return SCVT_OK;
 }
 
-// flip rounds on the queued candidates (cnt[0]) until none is left or the round limit
-int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
+// flip rounds on the queued candidates (cnt[0]) until none is left or the round limit.
+// known_nonzero: the caller knows there are candidates (no host read before the first batch)
+int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
+                bool known_nonzero = false) {
     cudaStream_t s = ctx->stream;
     int* cnt = ctx->d_fcnt;
     const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
     int cur = 0, rounds = 0;
+    bool skip_read = known_nonzero;
     for (;;) {
-        CK(cudaMemcpyAsync(ctx->h_small, cnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (ctx->h_small[0] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
+        if (!skip_read) {
+            CK(cudaMemcpyAsync(ctx->h_small, cnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (ctx->h_small[0] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
+        }
+        skip_read = false;
         for (int r = 0; r < FLIP_ROUNDS_PER_SYNC && rounds < FLIP_MAX_ROUNDS; ++r, ++rounds) {
             const int nxt = 1 - cur;
             int* list = ctx->d_flist + (int64_t)nxt * n;
@@ -2674,7 +2680,7 @@ int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshard
     ctx->h_small[8] = (int)total;
     CK(cudaMemcpyAsync(ctx->d_fcnt, ctx->h_small + 8, sizeof(int), cudaMemcpyHostToDevice, s));
     int nbad = 0;
-    TRY(flip_rounds(ctx, z, n, &nbad));
+    TRY(flip_rounds(ctx, z, n, &nbad, total > 0));
     if (nbad == 0) ctx->reuse_stats[2] += 1;   // certified: the evaluation reuses all cycles
     *nbad_host = nbad;
     return SCVT_OK;
