@@ -313,6 +313,12 @@ int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* l
                                  double gamma, const double* z, int64_t n, double* q3_out,
                                  double* out_host);
 /* q3 = q - (q.z) z rowwise (optimizer.py:322-323); dphi0_host = sum g.q3 (333) */
+/* as scvt_lbfgs_direction_tangent without the host wait: the two scalars are copied to
+ * pinned memory behind the kernels; scvt_direction_result waits for that copy only (the
+ * caller may enqueue the first line-search trial in between) */
+int scvt_lbfgs_direction_tangent_async(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
+                                       double gamma, const double* z, int64_t n, double* q3);
+int scvt_direction_result(scvt_ctx* ctx, double* out_host);
 int scvt_tangent_project(scvt_ctx* ctx, const double* q, const double* z, const double* g,
                          int64_t n, double* q3_out, double* dphi0_host);
 /* v = z + alpha q3; norms = |v|; zt = v / norms (optimizer.py:325-328) */

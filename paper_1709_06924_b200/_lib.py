@@ -116,6 +116,9 @@ SIGNATURES = {
                                             _c_dbl_p]),
     "scvt_lbfgs_direction_tangent": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _vp,
                                                     ctypes.c_int64, _vp, _c_dbl_p]),
+    "scvt_lbfgs_direction_tangent_async": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _vp,
+                                                          ctypes.c_int64, _vp]),
+    "scvt_direction_result": (ctypes.c_int, [_vp, _c_dbl_p]),
     "scvt_tangent_project": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp, _c_dbl_p]),
     "scvt_trial_point": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int64, _vp,
                                         _vp]),

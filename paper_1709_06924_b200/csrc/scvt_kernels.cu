@@ -1501,6 +1501,8 @@ struct scvt_ctx {
     double* h_scal = nullptr;          // pinned [MAX_RED_VALS]
     int* h_status = nullptr;           // pinned [8]
     int* h_small = nullptr;            // pinned [16]: small readbacks (reuse counts)
+    double* h_dir = nullptr;           // pinned [2]: scalars of the asynchronous direction
+    cudaEvent_t dir_ev = nullptr;      // recorded after their copy
     int* d_rcount = nullptr;           // per-round bad counts of the chained reuse rounds
     int* d_queue = nullptr;            // work queue of the fixed-grid cell rebuilds
     int* d_mig = nullptr;              // covering migration class (scvt_migration)
@@ -2431,7 +2433,10 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
         cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 16 * sizeof(int));
         cudaError_t e4 = cudaMallocHost((void**)&ctx->h_counts, (MAX_SHARDS + 1) * sizeof(int));
-        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess)
+        cudaError_t e5 = cudaMallocHost((void**)&ctx->h_dir, 2 * sizeof(double));
+        cudaError_t e6 = cudaEventCreateWithFlags(&ctx->dir_ev, cudaEventDisableTiming);
+        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
+            e5 != cudaSuccess || e6 != cudaSuccess)
             return bail(fail(ctx, SCVT_ERR_CUDA, "cudaMallocHost failed"));
     }
     // CUB temp storage: max of radix sort (n) and scan (n+1)
@@ -2501,6 +2506,8 @@ int scvt_destroy(scvt_ctx* ctx) {
     if (ctx->h_status) cudaFreeHost(ctx->h_status);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
     if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+    if (ctx->h_dir) cudaFreeHost(ctx->h_dir);
+    if (ctx->dir_ev) cudaEventDestroy(ctx->dir_ev);
     delete ctx;
     return SCVT_OK;
 }
@@ -3177,6 +3184,29 @@ int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* l
     TRY(readback(ctx, 2));
     out_host[0] = ctx->h_scal[0];   // q . g
     out_host[1] = ctx->h_scal[1];   // dphi0 = g . q3
+    return SCVT_OK;
+}
+
+int scvt_lbfgs_direction_tangent_async(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
+                                       double gamma, const double* z, int64_t n, double* q3) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    Chunks ck;
+    TRY(make_chunks(ctx, n, 0, 1, &ck));
+    TRY(gram_phase(ctx, g, lloyd_diag, gamma, ck, ctx->d_partials));
+    TRY(combine_phase(ctx, g, lloyd_diag, gamma, z, ck, ctx->d_partials, q3, ctx->d_partials));
+    TRY(reduce_chunks(ctx, ctx->d_partials, 2, nullptr));
+    // the scalars go to their own pinned slots (later readbacks reuse h_scal)
+    CK(cudaMemcpyAsync(ctx->h_dir, ctx->d_scal, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaEventRecord(ctx->dir_ev, ctx->stream));
+    return SCVT_OK;
+}
+
+int scvt_direction_result(scvt_ctx* ctx, double* out_host) {
+    if (!ctx) return SCVT_ERR_CONFIG;
+    CK(cudaEventSynchronize(ctx->dir_ev));
+    out_host[0] = ctx->h_dir[0];
+    out_host[1] = ctx->h_dir[1];
     return SCVT_OK;
 }
 

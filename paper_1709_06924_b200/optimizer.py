@@ -78,8 +78,11 @@ class MinimizeResult:
 
 
 def wolfe_line_search(phi, f0: float, dphi0: float, c1: float = WOLFE_C1, c2: float = WOLFE_C2,
-                      max_evals: int = MAX_LINE_SEARCH_EVALS, initial_step: float = 1.0):
-    """Strong-Wolfe bracketing + quadratic zoom (optimizer.py:170-237), scalar logic only."""
+                      max_evals: int = MAX_LINE_SEARCH_EVALS, initial_step: float = 1.0,
+                      first=None):
+    """Strong-Wolfe bracketing + quadratic zoom (optimizer.py:170-237), scalar logic only.
+    ``first``: phi(initial_step) already evaluated (speculatively, while the direction's scalars
+    were in flight), used as the first trial."""
     if dphi0 >= 0.0:
         raise NonDescentError(f"line search needs a descent direction, dphi0={dphi0:.3e}")
     evals = 0
@@ -121,9 +124,13 @@ def wolfe_line_search(phi, f0: float, dphi0: float, c1: float = WOLFE_C1, c2: fl
 
     alpha_prev, f_prev, d_prev = 0.0, f0, dphi0
     alpha = initial_step
+    pre = first
     first = True
     while evals < max_evals:
-        f, d, payload = phi(alpha)
+        if pre is not None:
+            (f, d, payload), pre = pre, None
+        else:
+            f, d, payload = phi(alpha)
         evals += 1
         record(alpha, f, payload)
         if f > f0 + c1 * alpha * dphi0 or (not first and f >= f_prev):
@@ -176,6 +183,18 @@ class _DeviceOps:
         self.ctx.call("scvt_lbfgs_direction", _lib.dptr(g), _lib.dptr(diag), float(gamma), self.n,
                       _lib.dptr(q), ctypes.byref(qg))
         return qg.value
+
+    speculate = True     # the first line-search trial may be enqueued before the direction's
+                         # scalars are read (one host round trip less per iteration)
+
+    def direction_tangent_async(self, g, diag, gamma, z, q3):
+        self.ctx.call("scvt_lbfgs_direction_tangent_async", _lib.dptr(g), _lib.dptr(diag),
+                      float(gamma), _lib.dptr(z), self.n, _lib.dptr(q3))
+
+    def direction_result(self):
+        out = (ctypes.c_double * 2)()
+        self.ctx.call("scvt_direction_result", out)
+        return out[0], out[1]
 
     def direction_tangent(self, g, diag, gamma, z, q3):
         out = (ctypes.c_double * 2)()
@@ -313,7 +332,29 @@ class Minimizer:
                 def direction():   # two_loop_direction + projection, fused on the device
                     return ops.direction_tangent(res.grad, diag, gamma, z, q3)
             # optimizer.py:147-167, 312-333
-            qg, dphi0 = direction()
+            first = None
+            if getattr(ops, "speculate", False) and not self.method.startswith("laplacian"):
+                # the direction and the alpha = 1 trial (always the line search's first) are
+                # enqueued back to back; the direction's scalars are read after the trial's
+                # evaluation.  A non-descent direction discards the trial (and any error it
+                # raised), exactly as if it had never been evaluated.
+                ops.direction_tangent_async(res.grad, diag, gamma, z, q3)
+                zt, norms = ops.positions(z), ops.scalars(z)
+                ops.trial(z, q3, 1.0, zt, norms)
+                err = r1 = None
+                try:
+                    r1 = ev.evaluate_device(zt, q3, norms)
+                except Exception as exc:  # noqa: BLE001 - re-raised below unless discarded
+                    err = exc
+                qg, dphi0 = ops.direction_result()
+                if qg < 0.0:
+                    if err is not None:
+                        raise err
+                    first = (r1.energy, r1.dirderiv, (zt, r1))
+                elif r1 is not None:
+                    ev.evaluations -= 1
+            else:
+                qg, dphi0 = direction()
             if qg >= 0.0:
                 logger.warning("non-descent direction at iteration %d; history reset", n)
                 ops.history_clear()
@@ -331,12 +372,15 @@ class Minimizer:
                 return r.energy, r.dirderiv, (zt, r)
 
             try:
-                alpha, _, payload, evals, exhausted = wolfe_line_search(phi, res.energy, dphi0)
+                alpha, _, payload, evals, exhausted = wolfe_line_search(phi, res.energy, dphi0,
+                                                                        first=first)
                 z_new, res_new = payload
                 fevals_iter = evals
                 if exhausted:
                     logger.debug("line search exhausted at iteration %d", n)
             except (NonDescentError, LineSearchFailure) as exc:
+                if first is not None and isinstance(exc, NonDescentError):
+                    ev.evaluations -= 1                          # the speculative trial
                 logger.warning("line search failed at iteration %d (%s); Lloyd fallback", n, exc)
                 ops.history_clear()
                 self.resets += 1
