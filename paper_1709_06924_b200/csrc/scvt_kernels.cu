@@ -1517,6 +1517,7 @@ struct scvt_ctx {
     int* d_fflag = nullptr;            // [n]
     int* d_fcnt = nullptr;             // [8]
     int64_t flip_stats[4] = {0, 0, 0, 0};   // evaluations, rounds, flips, fell back
+    int64_t last_flips = 0;                  // flips of the previous repair
     int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
     int* h_counts = nullptr;           // pinned copy
     // LBFGS history
@@ -1932,7 +1933,12 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
 // consistency failures, of rejected flips and of candidates still open after the last round.
 int flip_repair(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
     TRY(flip_detect(ctx, z, n, 0, n));
-    return flip_rounds(ctx, z, n, nbad_host);
+    // the previous evaluation needed flips: so will this one, most likely — start the first
+    // batch of rounds without reading the candidate count (empty rounds are no-ops)
+    const int64_t flips0 = ctx->flip_stats[2];
+    TRY(flip_rounds(ctx, z, n, nbad_host, ctx->last_flips > 0));
+    ctx->last_flips = ctx->flip_stats[2] - flips0;
+    return SCVT_OK;
 }
 
 // The bucket grid is only needed to rebuild cells: it is built on demand (*have_grid), so an
