@@ -281,6 +281,12 @@ def run_b200(a):
                 "cells_ms_per_eval": ms[0] / max(cnt[0], 1),
                 "eval_ms": ms[2] / max(cnt[2], 1),
                 "traffic": _traffic_from_profiles()}
+    if dname == "c5":
+        roofline["note"] = ("algorithmic FLOPs charge both centres' density at every node, as the "
+                            "reference formulation (d = min over the centres) does; where one "
+                            "centre's fit dominates a whole patch k_quad evaluates that fit only "
+                            "(DESIGN.md §3 item 5), so the fraction can exceed 1; the FP64 pipe "
+                            "utilisation is in profiles/")
     line = {"metric": METRIC, "value": value, "unit": "generator-updates/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
             "higher_is_better": True, "scaling": "strong",
