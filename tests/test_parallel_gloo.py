@@ -320,3 +320,63 @@ def test_gloo_arithmetic_slices(world):
         assert np.array_equal(out[r]["red"], ref)
         assert np.array_equal(out[r]["full"], out[r]["z"])
     assert len(ref) == CHUNKS
+
+
+# ---- sharded flip repair protocol (parallel._flip_sharded): counts and candidates gathered
+class _FlipMock:
+    """Stand-in for the flip entry points: shard s queues s + 1 candidate rows {s, k, 0, 0};
+    the rounds record what they were given."""
+
+    def __init__(self, bad_on=None):
+        self.bad_on = bad_on
+        self.seen = None
+
+    def flip_detect(self, z, shard, nshards):
+        cap = 8
+        cand = torch.zeros((cap, 4), dtype=torch.int32)
+        for k in range(shard + 1):
+            cand[k] = torch.tensor([shard, k, 0, 0], dtype=torch.int32)
+        return cand, (shard + 1, 1 if shard == self.bad_on else 0)
+
+    def flip_rounds(self, z, nshards, cand_all, cap, counts):
+        self.seen = [cand_all[r * cap:r * cap + counts[r]].tolist() for r in range(nshards)]
+        return 0
+
+
+def _flip_worker(rank, world, port, bad_on, out):
+    from paper_1709_06924_b200.parallel import _all_gather, _flip_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        be = _FlipMock(bad_on)
+
+        def gather_counts(local):
+            o = torch.empty(world * local[0].numel(), dtype=local[0].dtype)
+            _all_gather(o, local[0], None)
+            return o
+
+        def gather_cand(local, cap):
+            o = torch.empty((world * cap, 4), dtype=local[0].dtype)
+            _all_gather(o, local[0].contiguous(), None)
+            return o
+
+        ok = _flip_sharded(be, torch.zeros((10, 3)), [rank], world, gather_counts, gather_cand)
+        out[rank] = {"ok": ok, "seen": be.seen}
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bad_on", [None, 1])
+def test_gloo_sharded_flip_protocol(bad_on):
+    """Every rank gets every shard's flip candidates in rank order (padded all-gather, counts
+    first); a bad cell on any rank sends all of them to the rebuild rounds."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_flip_worker, args=(2, _free_port(), bad_on, out), nprocs=2, join=True)
+    for r in (0, 1):
+        if bad_on is None:
+            assert out[r]["ok"] is True
+            assert out[r]["seen"] == [[[0, 0, 0, 0]], [[1, 0, 0, 0], [1, 1, 0, 0]]]
+        else:
+            assert out[r]["ok"] is False and out[r]["seen"] is None
