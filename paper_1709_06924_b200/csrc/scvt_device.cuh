@@ -997,21 +997,10 @@ SCVT_HD void fit_rho2(const FitEval& f, V3 x0, double inv0, V3 x1, double inv1, 
     const double t0 = fma(x0.z, f.m2c.z, fma(x0.y, f.m2c.y, x0.x * f.m2c.x));
     const double t1 = fma(x1.z, f.m2c.z, fma(x1.y, f.m2c.y, x1.x * f.m2c.x));
     const double s0 = fma(inv0, t0, f.k0), s1 = fma(inv1, t1, f.k0);
-#ifdef FIT_ESTRIN
-    // Estrin: depth 4 instead of Horner's 6 (one more FMA)
-    const double q0 = s0 * s0, q1 = s1 * s1;
-    const double l0 = fma(f.b[1], s0, f.b[0]), l1 = fma(f.b[1], s1, f.b[0]);
-    const double m0 = fma(f.b[3], s0, f.b[2]), m1 = fma(f.b[3], s1, f.b[2]);
-    double h0 = fma(f.b[5], s0, f.b[4]), h1 = fma(f.b[5], s1, f.b[4]);
-    h0 = fma(f.b[6], q0, h0); h1 = fma(f.b[6], q1, h1);
-    *r0 = fma(fma(h0, q0, m0), q0, l0);
-    *r1 = fma(fma(h1, q1, m1), q1, l1);
-#else
     double a0 = f.b[6], a1 = f.b[6];
 #pragma unroll
     for (int k = 5; k >= 0; --k) { a0 = fma(a0, s0, f.b[k]); a1 = fma(a1, s1, f.b[k]); }
     *r0 = a0; *r1 = a1;
-#endif
 }
 
 template <int KIND, int L, bool SERIES>
