@@ -494,7 +494,7 @@ def test_adversarial_triangulations_match_qhull(case):
     assert np.array_equal(t, O.convex_hull_delaunay(z))
 
 
-def _two_rank_worker(rank, world, port, z0, out):
+def _two_rank_worker(rank, world, port, z0, out, method="lloyd-plbfgs"):
     import os
 
     import torch.distributed as dist
@@ -505,15 +505,16 @@ def _two_rank_worker(rank, world, port, z0, out):
     try:
         crit = P.StoppingCriteria(max_iterations=6)
         with ShardedMeshEvaluator(P.density_preset("c4"), "7pt", subdivision=3) as ev:
-            r = P.minimize(z0, "lloyd-plbfgs", ev, crit, corrections=7)
+            r = P.minimize(z0, method, ev, crit, corrections=7)
         out[rank] = {"points": r.points, "energies": [h.energy for h in r.records],
                      "fevals": r.fevals, "grad": r.final.grad, "diag": r.final.lloyd_diag}
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_two_processes_sharded_run_matches_single_gpu(world):
+@pytest.mark.parametrize("world,method", [(2, "lloyd-plbfgs"), (4, "lloyd-plbfgs"),
+                                          (2, "lbfgs"), (2, "lloyd")])
+def test_two_processes_sharded_run_matches_single_gpu(world, method):
     """Real ranks (separate processes and contexts, gloo collectives staged through host
     memory, all on cuda:0 — host-mediated exchanges, no kernel waits on another rank) run
     the sharded P-LBFGS path: cells sharded with cycle reuse, the optimizer's vectors in
@@ -528,10 +529,9 @@ def test_two_processes_sharded_run_matches_single_gpu(world):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     out = mp.Manager().dict()
-    mp.spawn(_two_rank_worker, args=(world, port, z0, out), nprocs=world, join=True)
+    mp.spawn(_two_rank_worker, args=(world, port, z0, out, method), nprocs=world, join=True)
     with _ev("c4", "7pt", 3) as ev:
-        ref = P.minimize(z0, "lloyd-plbfgs", ev, P.StoppingCriteria(max_iterations=6),
-                         corrections=7)
+        ref = P.minimize(z0, method, ev, P.StoppingCriteria(max_iterations=6), corrections=7)
     for rank in range(world):
         assert np.array_equal(out[rank]["points"], ref.points)
         assert out[rank]["energies"] == [h.energy for h in ref.records]
