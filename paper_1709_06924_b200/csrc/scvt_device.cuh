@@ -1053,16 +1053,17 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
                         fit_rho2(f1, x0, inv0, x1, inv1, &r0b, &r1b);
                         rho0 = fmax(rho0, r0b); rho1 = fmax(rho1, r1b);
                     }
-                    const double ri0 = rho0 * inv0, ri1 = rho1 * inv1;
                     const double dx0 = fma(x0.x, inv0, -z.x), dx1 = fma(x1.x, inv1, -z.x);
                     const double dy0 = fma(x0.y, inv0, -z.y), dy1 = fma(x1.y, inv1, -z.y);
                     const double dz0 = fma(x0.z, inv0, -z.z), dz1 = fma(x1.z, inv1, -z.z);
                     const double e0 = fma(dz0, dz0, fma(dy0, dy0, dx0 * dx0));
                     const double e1 = fma(dz1, dz1, fma(dy1, dy1, dx1 * dx1));
                     mq += rho0 + rho1;
-                    xq = fma(ri1, x1.x, fma(ri0, x0.x, xq));
-                    yq = fma(ri1, x1.y, fma(ri0, x0.y, yq));
-                    zq = fma(ri1, x1.z, fma(ri0, x0.z, zq));
+                    // first moment relative to the generator: sum rho (y - z); z sum rho is
+                    // added once per rule node class (saves the rho/|x| product per node)
+                    xq = fma(rho1, dx1, fma(rho0, dx0, xq));
+                    yq = fma(rho1, dy1, fma(rho0, dy0, yq));
+                    zq = fma(rho1, dz1, fma(rho0, dz0, zq));
                     eq = fma(rho1, e1, fma(rho0, e0, eq));
                 }
                 if (b < nb) {
@@ -1077,15 +1078,15 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
                     }
                     double rho = fit_rho(f0, x, inv);
                     if (KIND == DEN_TANH4X2_TAB) rho = fmax(rho, fit_rho(f1, x, inv));
-                    const double ri = rho * inv;
                     mq += rho;
-                    xq = fma(ri, x.x, xq); yq = fma(ri, x.y, yq); zq = fma(ri, x.z, zq);
                     const double dx = fma(x.x, inv, -z.x), dy = fma(x.y, inv, -z.y),
                                  dz = fma(x.z, inv, -z.z);
+                    xq = fma(rho, dx, xq); yq = fma(rho, dy, yq); zq = fma(rho, dz, zq);
                     eq = fma(rho, dx * dx + dy * dy + dz * dz, eq);
                 }
             }
             const double wq = s.area * w[q == 0 ? 0 : (q < 4 ? 1 : 4)];
+            xq = fma(z.x, mq, xq); yq = fma(z.y, mq, yq); zq = fma(z.z, mq, zq);
             acc[0] = fma(wq, mq, acc[0]);
             acc[1] = fma(wq, xq, acc[1]); acc[2] = fma(wq, yq, acc[2]);
             acc[3] = fma(wq, zq, acc[3]);
