@@ -1011,6 +1011,7 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
     FitEval f1;
     if (KIND == DEN_TANH4X2_TAB) f1 = fit_eval(lf1);
     const double invL = 1.0 / (double)L;
+    const V3 de2 = mul(s.e2, invL);
     for (int pass = 0; pass < 2; ++pass) {          // 0: up-leaves, 1: down-leaves
         const double sg = pass ? -1.0 : 1.0;
         const int M = L - pass;
@@ -1026,15 +1027,14 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
                                    fma(fa, s.e1.z, r0.z));
                 const int nb = M - a;
                 int b = 0;
-                double fb = 0.0;
-                // two nodes per step, interleaved stage by stage in the source: ptxas keeps
-                // the order, and the two dependency chains hide the DFMA latency
-                for (; b + 1 < nb; b += 2, fb += 2.0 * invL) {
-                    const double fb1 = fb + invL;
-                    const V3 x0 = v3(fma(fb, s.e2.x, base.x), fma(fb, s.e2.y, base.y),
-                                     fma(fb, s.e2.z, base.z));
-                    const V3 x1 = v3(fma(fb1, s.e2.x, base.x), fma(fb1, s.e2.y, base.y),
-                                     fma(fb1, s.e2.z, base.z));
+                // two nodes per step, interleaved stage by stage in the source (ptxas keeps
+                // the order, the two dependency chains hide the DFMA latency); nodes advance
+                // along the row by de2 = e2 / L with one add per coordinate
+                V3 xn = base;                       // node b of the row
+                for (; b + 1 < nb; b += 2) {
+                    const V3 x0 = xn;
+                    const V3 x1 = add(x0, de2);
+                    xn = add(x1, de2);
                     double inv0, inv1;
                     if (SERIES) {
                         const double d0 = fma(-x0.z, x0.z, fma(-x0.y, x0.y, fma(-x0.x, x0.x, 1.0)));
@@ -1067,8 +1067,7 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
                     eq = fma(rho1, e1, fma(rho0, e0, eq));
                 }
                 if (b < nb) {
-                    const V3 x = v3(fma(fb, s.e2.x, base.x), fma(fb, s.e2.y, base.y),
-                                    fma(fb, s.e2.z, base.z));
+                    const V3 x = xn;
                     double inv;
                     if (SERIES) {
                         const double dl = fma(-x.z, x.z, fma(-x.y, x.y, fma(-x.x, x.x, 1.0)));
