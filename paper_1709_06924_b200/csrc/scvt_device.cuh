@@ -1003,6 +1003,24 @@ SCVT_HD void fit_rho2(const FitEval& f, V3 x0, double inv0, V3 x1, double inv1, 
     *r0 = a0; *r1 = a1;
 }
 
+// as fit_rho2 / fit_rho with t = x.(-2 sigma c) supplied by the caller
+SCVT_HD void fit_rho2_t(const FitEval& f, double t0, double inv0, double t1, double inv1,
+                        double* r0, double* r1) {
+    const double s0 = fma(inv0, t0, f.k0), s1 = fma(inv1, t1, f.k0);
+    double a0 = f.b[6], a1 = f.b[6];
+#pragma unroll
+    for (int k = 5; k >= 0; --k) { a0 = fma(a0, s0, f.b[k]); a1 = fma(a1, s1, f.b[k]); }
+    *r0 = a0; *r1 = a1;
+}
+
+SCVT_HD double fit_rho_t(const FitEval& f, double t, double inv) {
+    const double ds = fma(inv, t, f.k0);
+    double acc = f.b[6];
+#pragma unroll
+    for (int k = 5; k >= 0; --k) acc = fma(acc, ds, f.b[k]);
+    return acc;
+}
+
 template <int KIND, int L, bool SERIES>
 SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const double* l2,
                              const double* w, const LocalFit& lf0, const LocalFit& lf1,
@@ -1012,6 +1030,10 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
     if (KIND == DEN_TANH4X2_TAB) f1 = fit_eval(lf1);
     const double invL = 1.0 / (double)L;
     const V3 de2 = mul(s.e2, invL);
+    // single-centre fits: t = x.(-2 sigma c) is linear along a row, so it advances by
+    // dt = de2.(-2 sigma c) too (exact dot product at the start of every row)
+    constexpr bool TADD = KIND != DEN_TANH4X2_TAB;
+    const double dt = fma(de2.z, f0.m2c.z, fma(de2.y, f0.m2c.y, de2.x * f0.m2c.x));
     for (int pass = 0; pass < 2; ++pass) {          // 0: up-leaves, 1: down-leaves
         const double sg = pass ? -1.0 : 1.0;
         const int M = L - pass;
@@ -1031,10 +1053,14 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
                 // the order, the two dependency chains hide the DFMA latency); nodes advance
                 // along the row by de2 = e2 / L with one add per coordinate
                 V3 xn = base;                       // node b of the row
+                double tn = TADD ? fma(base.z, f0.m2c.z, fma(base.y, f0.m2c.y, base.x * f0.m2c.x))
+                                 : 0.0;
                 for (; b + 1 < nb; b += 2) {
                     const V3 x0 = xn;
                     const V3 x1 = add(x0, de2);
                     xn = add(x1, de2);
+                    const double t0 = tn, t1 = t0 + dt;
+                    tn = t1 + dt;
                     double inv0, inv1;
                     if (SERIES) {
                         const double d0 = fma(-x0.z, x0.z, fma(-x0.y, x0.y, fma(-x0.x, x0.x, 1.0)));
@@ -1047,6 +1073,8 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
                         inv1 = fast_rsqrt(x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
                     }
                     double rho0, rho1;
+                    if (TADD) fit_rho2_t(f0, t0, inv0, t1, inv1, &rho0, &rho1);
+                    else
                     fit_rho2(f0, x0, inv0, x1, inv1, &rho0, &rho1);
                     if (KIND == DEN_TANH4X2_TAB) {
                         double r0b, r1b;
@@ -1075,7 +1103,7 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
                     } else {
                         inv = fast_rsqrt(x.x * x.x + x.y * x.y + x.z * x.z);
                     }
-                    double rho = fit_rho(f0, x, inv);
+                    double rho = TADD ? fit_rho_t(f0, tn, inv) : fit_rho(f0, x, inv);
                     if (KIND == DEN_TANH4X2_TAB) rho = fmax(rho, fit_rho(f1, x, inv));
                     mq += rho;
                     const double dx = fma(x.x, inv, -z.x), dy = fma(x.y, inv, -z.y),
