@@ -209,12 +209,20 @@ def run_b200(a):
     import ctypes
 
     rank, world, local = dist_env()
+    # SCVT_BENCH_FUNCTIONAL=1: every rank on cuda:0 with gloo collectives — a functional check
+    # of the multi-rank path on a one-GPU box (the numbers it prints mean nothing)
+    functional = os.environ.get("SCVT_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     n, dname, m = CONFIGS[a.config]
     density = P.density_preset(dname)
     z0 = P.sample_by_density(density, n, SEED)               # host init (PCG64 parity)
@@ -262,16 +270,14 @@ def run_b200(a):
     lib.scvt_profile_enable(ctx.ptr, 0)
     total_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = _max_over_ranks(total_ms, dev)
     # strong scaling: the N generators are shared by all ranks; each iteration updates N
     value = a.steps * n / (total_ms * 1e-3)
     import oracle as O
 
     flops_eval = O.algorithmic_flops(n, 7, DEPTH, density.variant) / world   # this rank's share
     quad_ms = ms[1] / max(cnt[1], 1)
-    achieved = flops_eval / (quad_ms * 1e-3) / 1e12
+    achieved = flops_eval / (quad_ms * 1e-3) / 1e12 if quad_ms > 0 else float("nan")
     roofline = {"bound": "fp64", "kernel": "k_quad", "achieved": achieved, "peak": peak.value,
                 "unit": "TFLOP/s", "frac": achieved / peak.value,
                 "peak_source": "measured in this run: scvt_fp64_peak DFMA microbenchmark "
@@ -314,6 +320,16 @@ def run_b200(a):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _max_over_ranks(x: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
+    gloo = dist.get_backend() == "gloo"
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def _e2e(P, density, z0, m, steps, dev, world):
@@ -363,9 +379,7 @@ def _e2e(P, density, z0, m, steps, dev, world):
         wall = time.perf_counter() - t0
     n = len(z0)
     if world > 1:
-        t = torch.tensor([wall], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        wall = float(t.item())
+        wall = _max_over_ranks(wall, dev)
     return {"value": steps * n / wall, "unit": "generator-updates/s",
             "h2d_bytes_per_step": int(24 * n / steps), "d2h_bytes_per_step": int(24 * n),
             "note": f"minimize() from a pinned host array (H2D inside the timing), iterations "

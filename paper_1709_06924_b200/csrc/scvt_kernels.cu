@@ -2846,6 +2846,12 @@ int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
     CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     *status_host = ctx->h_status[0];
+    if (ctx->prof && tot[0] > 0) {   // this shard's k_quad launch (quad_range's event pair)
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+        ctx->prof_ms[1] += ms;
+        ++ctx->prof_n[1];
+    }
     return SCVT_OK;
 }
 
