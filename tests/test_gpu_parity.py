@@ -708,3 +708,31 @@ def test_flip_repair_full_size_c4(monkeypatch):
     assert fl[2] > 10000
     assert np.array_equal(t_reuse, t_fresh)
     assert np.array_equal(t_fresh, O.convex_hull_delaunay(st.z.cpu().numpy()))
+
+
+def test_bench_multi_rank_functional():
+    """The multi-rank bench path under torchrun (two ranks on this one GPU with gloo,
+    SCVT_BENCH_FUNCTIONAL=1): one JSON line from rank 0 with the contract keys; the numbers of
+    such a run mean nothing, the code path is what is checked."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, SCVT_BENCH_FUNCTIONAL="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                          str(port), "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3",
+                          "--config", "c2", "--no-cpu-baseline"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["roofline"]["avg_launch_ms"] > 0
