@@ -1880,7 +1880,7 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
     cudaStream_t s = ctx->stream;
     int* cnt = ctx->d_fcnt;
     const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
-    int cur = 0, rounds = 0;
+    int cur = 0, rounds = 0, flips_seen = -1;
     bool skip_read = known_nonzero;
     for (;;) {
         if (!skip_read) {
@@ -1888,6 +1888,10 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
             CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (ctx->h_small[0] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
+            // a whole batch without a flip: the open candidates are stuck (flips rejected at
+            // their vertices), so they go to the rebuild path now instead of after the limit
+            if (ctx->h_small[3] == flips_seen) break;
+            flips_seen = ctx->h_small[3];
         }
         skip_read = false;
         for (int r = 0; r < FLIP_ROUNDS_PER_SYNC && rounds < FLIP_MAX_ROUNDS; ++r, ++rounds) {
