@@ -287,7 +287,9 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
         namb += tier > 0;
         if (sgn > 0) {
             if (mode == 2) {
-                if (i < a) {
+                // edges at cells already bound for the rebuild path (a triangle there faces
+                // inward: the mesh folded, which no flip repairs) are not queued
+                if (i < a && !(bad[i] | bad[a] | bad[b] | bad[c])) {
                     const int k = atomicAdd(fq.ncand, 1);
                     if (k < fq.cap) fq.cand[k] = make_int4(i, a, b, c);
                 }
