@@ -286,7 +286,11 @@ def run_b200(a):
                 "share_of_step": ms[1] / total_ms if world == 1 else None,
                 "cells_ms_per_eval": ms[0] / max(cnt[0], 1),
                 "eval_ms": ms[2] / max(cnt[2], 1),
-                "traffic": _traffic_from_profiles()}
+                "traffic": _traffic_from_profiles(),
+                # the whole iteration against the same peak (all kernels, host
+                # round trips and idle time included)
+                "step_frac": (flops_eval * world * evals / a.steps) / (total_ms / a.steps * 1e-3)
+                             / 1e12 / peak.value}
     if dname == "c5":
         roofline["note"] = ("algorithmic FLOPs charge both centres' density at every node, as the "
                             "reference formulation (d = min over the centres) does; where one "
