@@ -108,6 +108,38 @@ def test_duplicate_points_raise():
         ev.evaluate(z)
 
 
+def _polyhedron(name):
+    u = lambda a: np.asarray(a, float) / np.linalg.norm(np.asarray(a, float), axis=1, keepdims=True)
+    if name == "tetra":
+        return u([[1, 1, 1], [1, -1, -1], [-1, 1, -1], [-1, -1, 1]])
+    if name == "octa":
+        return np.vstack([np.eye(3), -np.eye(3)])
+    if name == "cube":
+        return u([[a, b, c] for a in (1, -1) for b in (1, -1) for c in (1, -1)])
+    return P.icosahedron_vertices()
+
+
+@pytest.mark.parametrize("name", ["tetra", "octa", "ico", "cube"])
+def test_regular_polyhedra_vs_oracle(name):
+    """Smallest inputs the reference accepts: the tetrahedron (N=4), octahedron, icosahedron,
+    and the cube, whose faces are four cocircular points.  Delaunay is ambiguous there (Qhull
+    splits each square by its own rule) but both splits share the face's circumcentre, so the
+    triangle count and every moment still equal the oracle's (delaunay.py:181-202, 337-380)."""
+    z = _polyhedron(name)
+    o = O.Evaluator(O.density_for("const"), "7pt", 3).evaluate(z)
+    with _ev("const", "7pt", 3) as ev:
+        r = ev.evaluate(z)
+        t = ev.triangulation(z).triangles
+    ref = O.convex_hull_delaunay(z)
+    assert len(t) == len(ref) == 2 * len(z) - 4
+    if name != "cube":
+        assert np.array_equal(t, ref)
+    assert rel(r.mass, o.mass) <= TOL_M
+    assert rel(r.first, o.first) <= TOL_M
+    assert abs(r.energy - o.energy) <= TOL_M * o.energy
+    assert rel(r.lloyd_diag, o.lloyd_diag) <= TOL_M
+
+
 # ------------------------------------------------------------------------- moments
 @pytest.mark.parametrize("rule,depth", [("4pt", 0), ("9pt", 0), ("7pt", 0), ("7pt", 1),
                                         ("4pt", 3), ("7pt", 3)])
