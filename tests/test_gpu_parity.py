@@ -140,6 +140,47 @@ def test_regular_polyhedra_vs_oracle(name):
     assert rel(r.lloyd_diag, o.lloyd_diag) <= TOL_M
 
 
+def _latlon(nlat, nlon, poles):
+    th = (np.arange(nlat) + 0.5) / nlat * np.pi
+    ph = np.arange(nlon) / nlon * 2 * np.pi
+    t, f = np.meshgrid(th, ph, indexing="ij")
+    z = np.stack([np.sin(t) * np.cos(f), np.sin(t) * np.sin(f), np.cos(t)], -1).reshape(-1, 3)
+    return np.vstack([z, [[0.0, 0.0, 1.0], [0.0, 0.0, -1.0]]]) if poles else z
+
+
+@pytest.mark.parametrize("nlat,nlon,poles", [(48, 24, True), (48, 24, False)])
+def test_latlon_grid_cocircular_quads(nlat, nlon, poles):
+    """A latitude-longitude grid: every quad between two rings is an isosceles trapezoid, so
+    nlat x nlon four-point sets are exactly cocircular (and without the pole points each polar
+    cap is one nlon-gon of cocircular points).  The cell builder and its certificate must
+    terminate and give Qhull's triangle count with the oracle's moments; a short P-LBFGS run
+    from it (the flip repair sees the same ties) follows the oracle's energies."""
+    z = _latlon(nlat, nlon, poles)
+    o = O.Evaluator(O.density_for("x3"), "7pt", 1).evaluate(z)
+    with _ev("x3", "7pt", 1) as ev:
+        r = ev.evaluate(z)
+        assert len(ev.triangulation(z).triangles) == 2 * len(z) - 4
+        res = P.minimize(z, "lloyd-plbfgs", ev,
+                         P.StoppingCriteria(max_iterations=5, movement_tol=1e-300,
+                                            grad_tol=1e-300, stall_tol=1e-300), corrections=7)
+    assert rel(r.mass, o.mass) <= TOL_M
+    assert rel(r.first, o.first) <= TOL_M
+    assert abs(r.energy - o.energy) <= TOL_M * o.energy
+    ref = O.minimize(z, "lloyd-plbfgs", O.Evaluator(O.density_for("x3"), "7pt", 1),
+                     O.StoppingCriteria(5, 1e-300, 1e-300, 1e-300), corrections=7)
+    e = np.array([x.energy for x in res.records])
+    eo = np.array([x.energy for x in ref.records])
+    assert len(e) == len(eo)
+    assert np.max(np.abs(e - eo) / eo) <= 1e-10
+
+
+def test_valence_above_cap_raises():
+    """SCVT_MAX_DEGREE (32) caps the stored valence; a generator with more Delaunay neighbours
+    (the pole of a 96-longitude grid) raises CapacityError instead of truncating its cell."""
+    with _ev("x3", "7pt", 1) as ev, pytest.raises(P.CapacityError):
+        ev.evaluate(_latlon(48, 96, True))
+
+
 # ------------------------------------------------------------------------- moments
 @pytest.mark.parametrize("rule,depth", [("4pt", 0), ("9pt", 0), ("7pt", 0), ("7pt", 1),
                                         ("4pt", 3), ("7pt", 3)])
