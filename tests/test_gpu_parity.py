@@ -174,6 +174,40 @@ def test_latlon_grid_cocircular_quads(nlat, nlon, poles):
     assert np.max(np.abs(e - eo) / eo) <= 1e-10
 
 
+def test_minimize_normalizes_initial_points():
+    """minimize() projects its initial points onto the sphere first (optimizer.py:290), so
+    scaled and float32 starts follow the oracle's trajectory from the same input."""
+    z = P.random_sphere_points(10000, 5)
+    crit = P.StoppingCriteria(max_iterations=3, movement_tol=1e-300, grad_tol=1e-300,
+                              stall_tol=1e-300)
+    for start in (3.0 * z, (0.5 * z).astype(np.float32)):
+        with _ev("x3", "7pt", 1) as ev:
+            res = P.minimize(start, "lloyd-plbfgs", ev, crit, corrections=7)
+        ref = O.minimize(start, "lloyd-plbfgs", O.Evaluator(O.density_for("x3"), "7pt", 1),
+                         O.StoppingCriteria(3, 1e-300, 1e-300, 1e-300), corrections=7)
+        e = np.array([x.energy for x in res.records])
+        eo = np.array([x.energy for x in ref.records])
+        assert len(e) == len(eo) and np.max(np.abs(e - eo) / eo) <= 1e-10
+        assert np.max(np.abs(np.linalg.norm(res.points, axis=1) - 1.0)) <= 1e-15
+
+
+@pytest.mark.parametrize("sep", [1e-6, 1e-10, 1e-12])
+def test_near_duplicate_generators(sep):
+    """Two generators `sep` apart (exact duplicates raise, test_duplicate_points_raise): the
+    sliver cell between them is still built, Qhull's triangles are reproduced bitwise and the
+    moments match the oracle (tools/probe_edge.py)."""
+    z = P.random_sphere_points(10000, 5)
+    t = np.cross(z[3], [0.0, 0.0, 1.0])
+    z[7] = z[3] + sep * t / np.linalg.norm(t)
+    z[7] /= np.linalg.norm(z[7])
+    o = O.Evaluator(O.density_for("const"), "7pt", 1).evaluate(z)
+    with _ev("const", "7pt", 1) as ev:
+        r = ev.evaluate(z)
+        assert np.array_equal(ev.triangulation(z).triangles, O.convex_hull_delaunay(z))
+    assert rel(r.mass, o.mass) <= TOL_M
+    assert rel(r.first, o.first) <= TOL_M
+
+
 def test_valence_above_cap_raises():
     """SCVT_MAX_DEGREE (32) caps the stored valence; a generator with more Delaunay neighbours
     (the pole of a 96-longitude grid) raises CapacityError instead of truncating its cell."""
