@@ -17,6 +17,7 @@ from .errors import STATUS_ERRORS, DeviceError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libscvtb200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
+MAX_DEGREE = 32              # SCVT_MAX_DEGREE (include/scvt_b200.h): neighbour-row width
 
 _c_int_p = ctypes.POINTER(ctypes.c_int)
 _c_i32_p = ctypes.POINTER(ctypes.c_int32)

@@ -75,9 +75,9 @@ class DeviceLaplacian:
         if perturbation not in ("a6", "m2"):
             raise ValueError(f"unknown perturbation {perturbation!r}")
         self.ctx, self.n, self.perturbation = ctx, n, perturbation
-        self.wsym = torch.empty((n, 32), dtype=torch.float64, device=device)
+        self.wsym = torch.empty((n, _lib.MAX_DEGREE), dtype=torch.float64, device=device)
         self.diag = torch.empty(n, dtype=torch.float64, device=device)
-        self.nbr = torch.empty((n, 32), dtype=torch.int32, device=device)
+        self.nbr = torch.empty((n, _lib.MAX_DEGREE), dtype=torch.int32, device=device)
         self.deg = torch.empty(n, dtype=torch.int32, device=device)
         ctx.call("scvt_laplacian", n, _lib.dptr(self.wsym), _lib.dptr(self.diag),
                  _lib.dptr(self.nbr), _lib.dptr(self.deg), what="laplacian")

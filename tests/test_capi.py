@@ -90,6 +90,14 @@ def test_status_codes_map_to_reference_exceptions():
     assert errors.STATUS_ERRORS[codes["SCVT_ERR_POLE_AMBIGUITY"]] is errors.PoleAmbiguityError
 
 
+def test_row_width_matches_header():
+    """The host's neighbour-row width (Laplacian rows) is the header's SCVT_MAX_DEGREE."""
+    from paper_1709_06924_b200 import _lib
+
+    m = re.search(r"#define\s+SCVT_MAX_DEGREE\s+(\d+)", open(HEADER).read())
+    assert m and int(m.group(1)) == _lib.MAX_DEGREE
+
+
 def test_no_cpu_fallback_without_gpu():
     """The product path refuses to run without CUDA instead of computing on the host."""
     import torch
