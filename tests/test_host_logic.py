@@ -200,3 +200,21 @@ def test_covering_host_helpers_match_reference_golden():
     near = PointAssignment(arithmetic=a0.arithmetic, geometric=a0.arithmetic.copy())
     near.geometric[0] = one[near.arithmetic[0]][0]
     assert detect_migration(near, cov) == "neighbor-move"
+
+
+def test_neighbor_lists_reproduce_reference_covering():
+    """partition.neighbor_lists (partition.py:67-80) on the Delaunay triangles of the golden
+    covering's centres gives the reference's one-level lists exactly; every two-level list
+    holds its own cell and is closed over one more hop."""
+    from conftest import golden
+    from paper_1709_06924_b200.partition import neighbor_lists
+
+    g = golden("covering")
+    p = len(g["centers"])
+    one, two = neighbor_lists(O.convex_hull_delaunay(g["centers"]), p)
+    ref = tuple(tuple(int(x) for x in g["one_idx"][g["one_ptr"][k]:g["one_ptr"][k + 1]])
+                for k in range(p))
+    assert one == ref
+    for l in range(p):
+        assert l in two[l]
+        assert set(two[l]) == {l}.union(one[l], *(one[m] for m in one[l]))
