@@ -76,6 +76,7 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.at_end = False
         self.path = tempfile.mktemp(suffix=".csv")
 
     def __enter__(self):
@@ -94,8 +95,19 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            if not self._rows():
+                # timed region shorter than the sampler's start-up + 100 ms period (c1, c2):
+                # one query right at its end, while the clocks still reflect the load
+                self.at_end = True
+                try:
+                    with open(self.path, "a") as f:
+                        subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits"], stdout=f,
+                                       stderr=subprocess.DEVNULL, timeout=10)
+                except (OSError, subprocess.SubprocessError):
+                    pass
 
-    def summary(self):
+    def _rows(self):
         rows = []
         try:
             for line in open(self.path):
@@ -104,13 +116,20 @@ class ClockSampler:
                     rows.append(p)
         except OSError:
             pass
+        return rows
+
+    def summary(self):
+        rows = self._rows()
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(r[1]) for r in rows]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
-                "reasons": reasons, "samples": len(rows)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+               "reasons": reasons, "samples": len(rows)}
+        if self.at_end:
+            out["when"] = "end of the timed region (shorter than the 100 ms sampling period)"
+        return out
 
 
 # ----------------------------------------------------------------------------- CPU baseline
