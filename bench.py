@@ -422,12 +422,65 @@ def _traffic_from_profiles():
         return None
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(a) -> int:
+    """`--gpus N` without a torchrun environment: re-launch this command as N ranks (one
+    process per GPU) under torch.distributed.run on 127.0.0.1, as the driver would."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] spawning {a.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def run_functional_cpu(a):
+    """SCVT_BENCH_FUNCTIONAL=1 on a box without CUDA: exercises the launch path only (N ranks
+    spawned, gloo rendezvous, barriers, max over ranks, one line from rank 0); no number."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        dist.barrier()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "generator-updates/s",
+                          "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+                          "functional": "no CUDA device: launch path only",
+                          "max_over_ranks_probe": float(t.item())}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
+    if a.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(a))
+    _, world, _ = dist_env()
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}: one rank per GPU")
     if a.impl == "reference":
         run_reference(a)
-    else:
-        run_b200(a)
+        return
+    import torch
+
+    if os.environ.get("SCVT_BENCH_FUNCTIONAL") == "1" and not torch.cuda.is_available():
+        run_functional_cpu(a)
+        return
+    run_b200(a)
 
 
 if __name__ == "__main__":

@@ -291,7 +291,13 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
                 // inward: the mesh folded, which no flip repairs) are not queued
                 if (i < a && !(bad[i] | bad[a] | bad[b] | bad[c])) {
                     const int k = atomicAdd(fq.ncand, 1);
-                    if (k < fq.cap) fq.cand[k] = make_int4(i, a, b, c);
+                    if (k < fq.cap) {
+                        fq.cand[k] = make_int4(i, a, b, c);
+                    } else {       // queue overflow (cannot happen: <= 3n - 6 edges): rebuild
+                        const int v[4] = {i, a, b, c};
+                        for (int q = 0; q < 4; ++q)
+                            if (atomicExch(&bad[v[q]], 1) == 0) atomicAdd(nbad, 1);
+                    }
                 }
             } else {
                 mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, c);
@@ -314,9 +320,9 @@ __device__ __forceinline__ unsigned long long flip_key(const int4& c) {
     return ((unsigned long long)(unsigned)c.x << 32) | (unsigned)c.y;
 }
 
-__global__ void k_flip_lock(const int4* __restrict__ cand, const int* __restrict__ ncand,
+__global__ void k_flip_lock(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
                             unsigned long long* __restrict__ lock) {
-    const int nc = *ncand;
+    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
         const int4 c = cand[k];
         const unsigned long long key = flip_key(c);
@@ -339,13 +345,13 @@ __device__ __forceinline__ void cyc_store(int* __restrict__ row, const int* tmp,
     for (int k = 0; k < d; ++k) row[k] = tmp[(m + k) % d];
 }
 
-__global__ void k_flip_apply(const int4* __restrict__ cand, const int* __restrict__ ncand,
+__global__ void k_flip_apply(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
                              const unsigned long long* __restrict__ lock, int* __restrict__ nbr,
                              int* __restrict__ deg, int* __restrict__ dflag,
                              int* __restrict__ next, int* __restrict__ next_n,
                              int* __restrict__ bad, int* __restrict__ nbad,
                              int* __restrict__ nflips) {
-    const int nc = *ncand;
+    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
         const int4 c = cand[k];
         const int v[4] = {c.x, c.y, c.z, c.w};
@@ -394,9 +400,9 @@ __global__ void k_flip_apply(const int4* __restrict__ cand, const int* __restric
     }
 }
 
-__global__ void k_flip_unlock(const int4* __restrict__ cand, const int* __restrict__ ncand,
+__global__ void k_flip_unlock(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
                               unsigned long long* __restrict__ lock) {
-    const int nc = *ncand;
+    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
         const int4 c = cand[k];
         lock[c.x] = ~0ull; lock[c.y] = ~0ull; lock[c.z] = ~0ull; lock[c.w] = ~0ull;
@@ -411,9 +417,9 @@ __global__ void k_clear_flags(const int* __restrict__ list, const int* __restric
 }
 
 // the candidates left after the last round: their cells go to the rebuild path
-__global__ void k_cand_bad(const int4* __restrict__ cand, const int* __restrict__ ncand,
+__global__ void k_cand_bad(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
                            int* __restrict__ bad, int* __restrict__ nbad) {
-    const int nc = *ncand;
+    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
         const int4 c = cand[k];
         const int v[4] = {c.x, c.y, c.z, c.w};
@@ -1900,13 +1906,13 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
             const int nxt = 1 - cur;
             int* list = ctx->d_flist + (int64_t)nxt * n;
             CK(cudaMemsetAsync(cnt + 1 + nxt, 0, sizeof(int), s));
-            k_flip_lock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, ctx->d_lock);
+            k_flip_lock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
             LAUNCHED();
-            k_flip_apply<<<SPEC_BLOCKS, 128, 0, s>>>(ctx->d_cand, cnt, ctx->d_lock, ctx->d_nbr,
+            k_flip_apply<<<SPEC_BLOCKS, 128, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock, ctx->d_nbr,
                                                       ctx->d_deg, ctx->d_fflag, list, cnt + 1 + nxt,
                                                       ctx->d_bad, ctx->d_nbad, cnt + 3);
             LAUNCHED();
-            k_flip_unlock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, ctx->d_lock);
+            k_flip_unlock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
             LAUNCHED();
             k_clear_flags<<<SPEC_BLOCKS, 256, 0, s>>>(list, cnt + 1 + nxt, ctx->d_fflag);
             LAUNCHED();
@@ -1920,7 +1926,7 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
     }
     const bool open = ctx->h_small[0] > 0;
     if (open) {   // unconverged: those cells are rebuilt
-        k_cand_bad<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, ctx->d_bad, ctx->d_nbad);
+        k_cand_bad<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_bad, ctx->d_nbad);
         LAUNCHED();
         CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -2287,6 +2293,24 @@ int eval_scalars_phase(scvt_ctx* ctx, const Chunks& ck, const double* diag, cons
 
 }  // namespace
 
+// Every entry point runs on the context's device and restores the caller's current device
+// (a caller may have selected another GPU since scvt_create).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const scvt_ctx* ctx) {
+        if (!ctx) return;
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != ctx->device &&
+            cudaSetDevice(ctx->device) == cudaSuccess)
+            prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // ====================================================================== C ABI
 extern "C" {
 
@@ -2308,6 +2332,7 @@ const char* scvt_last_error(const scvt_ctx* ctx) { return ctx ? ctx->err.c_str()
 int64_t scvt_launch_count(const scvt_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int scvt_profile_enable(scvt_ctx* ctx, int on) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (on && !ctx->ev[0])
         for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
@@ -2316,6 +2341,7 @@ int scvt_profile_enable(scvt_ctx* ctx, int on) {
 }
 
 int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     CK(cudaMemcpy(out12, ctx->d_diag, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost));
     out12[8] = ctx->reuse_stats[2];   // evaluations whose cycles were certified by reuse
@@ -2332,6 +2358,7 @@ int scvt_profile_counters(scvt_ctx* ctx, int64_t* out12, int reset) {
 }
 
 int scvt_profile_flips(scvt_ctx* ctx, int64_t* out4, int reset) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     for (int k = 0; k < 4; ++k) {
         out4[k] = ctx->flip_stats[k];
@@ -2341,6 +2368,7 @@ int scvt_profile_flips(scvt_ctx* ctx, int64_t* out4, int reset) {
 }
 
 int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int reset) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     for (int k = 0; k < 3; ++k) {
         ms_out[k] = ctx->prof_ms[k];
@@ -2351,6 +2379,7 @@ int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int re
 }
 
 int scvt_set_stream(scvt_ctx* ctx, void* stream) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     ctx->stream = (cudaStream_t)stream;
     return SCVT_OK;
@@ -2359,6 +2388,13 @@ int scvt_set_stream(scvt_ctx* ctx, void* stream) {
 int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cfg) {
     if (!out || !cfg) return SCVT_ERR_CONFIG;
     *out = nullptr;
+    struct RestoreDevice {
+        int d = -1;
+        ~RestoreDevice() {
+            if (d >= 0) cudaSetDevice(d);
+        }
+    } restore_;
+    if (cudaGetDevice(&restore_.d) != cudaSuccess) restore_.d = -1;
     scvt_ctx* ctx = new scvt_ctx();
     ctx->device = device;
     ctx->n_max = n_max;
@@ -2501,6 +2537,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 }
 
 int scvt_destroy(scvt_ctx* ctx) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_OK;
     void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
                    ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_wdir, ctx->d_cgv, ctx->d_cg, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_fcnt, ctx->d_counts,
@@ -2526,6 +2563,7 @@ int scvt_destroy(scvt_ctx* ctx) {
 
 int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out,
                      uint8_t* flags_out, int64_t* stats_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     TRY(reset_status(ctx));
     ctx->cycles_n = -1;
@@ -2574,6 +2612,7 @@ int scvt_triangulate(scvt_ctx* ctx, const double* z, int64_t n, int64_t* tri_out
 
 int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
                   double* mass, double* lloyd_diag, double* scalars_host) {
+    DeviceGuard dg_(ctx);
     double sc[5];
     int rc = scvt_evaluate_ex(ctx, z, n, grad, first, mass, lloyd_diag, nullptr, nullptr, sc);
     if (rc == SCVT_OK)
@@ -2584,6 +2623,7 @@ int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, doubl
 int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
                      double* mass, double* lloyd_diag, const double* q3, const double* norms,
                      double* scalars_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
     ctx->prof_n[3] = 0;
@@ -2601,6 +2641,7 @@ int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, do
 int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const int64_t* tri,
                                int64_t t, double* grad, double* first, double* mass,
                                double* lloyd_diag, double* scalars_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n > n_max");
     if (t != 2 * n - 4) return fail(ctx, SCVT_ERR_COVERAGE, "T=%lld != 2n-4", (long long)t);
@@ -2619,6 +2660,7 @@ int64_t scvt_shard_rows(int64_t n, int nshards) {
 
 int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                      int32_t* cyc_send) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (nshards < 1 || shard < 0 || shard >= nshards)
         return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
@@ -2639,6 +2681,7 @@ int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int n
 
 // ---- sharded cycle reuse: the single-GPU reuse loop split at its two exchanges
 int scvt_shard_flip(scvt_ctx* ctx, const double* z, int64_t n, int32_t* nbad_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     *nbad_host = -1;
     if (ctx->cycles_n != n || !reuse_enabled() || !flips_enabled()) return SCVT_OK;
@@ -2656,6 +2699,7 @@ int scvt_shard_flip(scvt_ctx* ctx, const double* z, int64_t n, int32_t* nbad_hos
 
 int scvt_shard_flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                            int32_t* cand_send, int64_t cap, int32_t* counts_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (nshards < 1 || shard < 0 || shard >= nshards)
         return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
@@ -2686,16 +2730,24 @@ int scvt_shard_flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int shard,
 int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                            const int32_t* cand_all, int64_t cap, const int64_t* counts,
                            int32_t* nbad_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     cudaStream_t s = ctx->stream;
     int64_t total = 0;
+    for (int r = 0; r < nshards; ++r) {        // validate before any copy into d_cand
+        if (counts[r] < 0 || counts[r] > cap)
+            return fail(ctx, SCVT_ERR_CONFIG, "shard %d: %lld flip candidates > cap %lld", r,
+                        (long long)counts[r], (long long)cap);
+        total += counts[r];
+    }
+    if (total > 3 * n) return fail(ctx, SCVT_ERR_CAPACITY, "%lld flip candidates", (long long)total);
+    total = 0;
     for (int r = 0; r < nshards; ++r) {        // the shards' candidates, in rank order
         if (counts[r] > 0)
             CK(cudaMemcpyAsync(ctx->d_cand + total, cand_all + 4 * (int64_t)r * cap,
                                (size_t)counts[r] * sizeof(int4), cudaMemcpyDeviceToDevice, s));
         total += counts[r];
     }
-    if (total > 3 * n) return fail(ctx, SCVT_ERR_CAPACITY, "%lld flip candidates", (long long)total);
     ctx->h_small[8] = (int)total;
     CK(cudaMemcpyAsync(ctx->d_fcnt, ctx->h_small + 8, sizeof(int), cudaMemcpyHostToDevice, s));
     int nbad = 0;
@@ -2707,6 +2759,7 @@ int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshard
 
 int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                        int round, int32_t* bad_out, int32_t* ready_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (nshards < 1 || shard < 0 || shard >= nshards)
         return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
@@ -2740,6 +2793,7 @@ int scvt_shard_recheck(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
 
 int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_all,
                     int64_t* counts_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (nshards < 1 || nshards > MAX_SHARDS)
         return fail(ctx, SCVT_ERR_CONFIG, "bad shard count %d (max %d)", nshards, MAX_SHARDS);
@@ -2777,6 +2831,7 @@ int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_al
 
 int scvt_shard_rebuild(scvt_ctx* ctx, int64_t n, int shard, int nshards, int64_t cap,
                        int32_t* rows_send) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if ((int)ctx->plan_counts.size() != nshards || shard < 0 || shard >= nshards)
         return fail(ctx, SCVT_ERR_CONFIG, "scvt_shard_rebuild without a matching plan");
@@ -2808,6 +2863,7 @@ int scvt_shard_rebuild(scvt_ctx* ctx, int64_t n, int shard, int nshards, int64_t
 }
 
 int scvt_shard_install(scvt_ctx* ctx, int64_t n, const int32_t* rows, int64_t nrows) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (nrows <= 0) return SCVT_OK;
     k_unpack_cycles<<<blocks_for(nrows, 128), 128, 0, ctx->stream>>>(
@@ -2818,6 +2874,7 @@ int scvt_shard_install(scvt_ctx* ctx, int64_t n, const int32_t* rows, int64_t nr
 
 int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
                        const int32_t* cyc_all, double* res_send, int32_t* status_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     cudaStream_t s = ctx->stream;
     int64_t lo, hi, cap = scvt_shard_rows(n, nshards);
@@ -2862,6 +2919,7 @@ int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
 }
 
 int scvt_shard_status(scvt_ctx* ctx, int32_t status) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     return status_to_code(ctx, status);
 }
@@ -2869,6 +2927,7 @@ int scvt_shard_status(scvt_ctx* ctx, int32_t status) {
 int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                       const double* res_all, double* grad, double* first, double* mass,
                       double* lloyd_diag, double* scalars_host) {
+    DeviceGuard dg_(ctx);
     double sc[5];
     int rc = scvt_shard_finish_ex(ctx, z, n, nshards, res_all, grad, first, mass, lloyd_diag,
                                   nullptr, nullptr, sc);
@@ -2881,6 +2940,7 @@ int scvt_shard_finish_ex(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                          const double* res_all, double* grad, double* first, double* mass,
                          double* lloyd_diag, const double* q3, const double* norms,
                          double* scalars_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     cudaStream_t s = ctx->stream;
     int64_t cap = scvt_shard_rows(n, nshards);
@@ -2914,6 +2974,7 @@ int scvt_slice_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                       const double* res_all, int rank, int world, double* grad, double* first,
                       double* mass, double* lloyd_diag, const double* q3, const double* norms,
                       double* red) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, rank, world, &ck));
@@ -2931,6 +2992,7 @@ int scvt_slice_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
 }
 
 int scvt_slice_scalars(scvt_ctx* ctx, const double* red, double* scalars_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     static const unsigned char ops[5] = {0, 0, 0, 2, 0};
     TRY(reduce_chunks(ctx, red, 5, ops));
@@ -2948,6 +3010,7 @@ int scvt_slice_scalars(scvt_ctx* ctx, const double* red, double* scalars_host) {
 
 int scvt_slice_gram(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
                     int64_t n, int rank, int world, double* red, int32_t* nval_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, rank, world, &ck));
@@ -2958,6 +3021,7 @@ int scvt_slice_gram(scvt_ctx* ctx, const double* g, const double* lloyd_diag, do
 int scvt_slice_combine(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
                        const double* z, int64_t n, int rank, int world, const double* red_gram,
                        double* q3, double* red) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, rank, world, &ck));
@@ -2966,6 +3030,7 @@ int scvt_slice_combine(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
 
 int scvt_slice_tangent(scvt_ctx* ctx, const double* q, const double* z, const double* g,
                        int64_t n, int rank, int world, double* q3, double* red) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, rank, world, &ck));
@@ -2978,6 +3043,7 @@ int scvt_slice_tangent(scvt_ctx* ctx, const double* q, const double* z, const do
 int scvt_slice_history_pair(scvt_ctx* ctx, const double* z_old, const double* z_new,
                             const double* g_old, const double* g_new, int64_t n, int rank,
                             int world, double* red, int32_t* nval_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, rank, world, &ck));
@@ -2989,6 +3055,7 @@ int scvt_slice_history_pair(scvt_ctx* ctx, const double* z_old, const double* z_
 
 int scvt_slice_history_commit(scvt_ctx* ctx, const double* red, int64_t n, int rank, int world,
                               int32_t* pushed_host, double* movement_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, rank, world, &ck));
@@ -2997,6 +3064,7 @@ int scvt_slice_history_commit(scvt_ctx* ctx, const double* red, int64_t n, int r
 
 int scvt_reduce_chunks(scvt_ctx* ctx, const double* red, int32_t nval, const uint8_t* ops,
                        double* out_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     TRY(reduce_chunks(ctx, red, nval, ops));
     TRY(readback(ctx, nval));
@@ -3007,6 +3075,7 @@ int scvt_reduce_chunks(scvt_ctx* ctx, const double* red, int32_t nval, const uin
 int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* centers, int32_t p,
                    const uint32_t* adjacency, int32_t* arithmetic, int32_t fresh,
                    int32_t* class_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (p < 1) return fail(ctx, SCVT_ERR_CONFIG, "covering with %d cells", p);
     cudaStream_t s = ctx->stream;
@@ -3023,6 +3092,7 @@ int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* cent
 // ---------------------------------------------------------------------- graph Laplacian
 int scvt_laplacian(scvt_ctx* ctx, int64_t n, double* wsym, double* diag, int32_t* nbr_out,
                    int32_t* deg_out) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (ctx->cycles_n != n)
         return fail(ctx, SCVT_ERR_CONFIG, "scvt_laplacian needs the evaluation of these %lld points",
@@ -3050,6 +3120,7 @@ int scvt_laplacian(scvt_ctx* ctx, int64_t n, double* wsym, double* diag, int32_t
 int scvt_laplacian_solve(scvt_ctx* ctx, int64_t n, const int32_t* nbr, const int32_t* deg,
                          const double* wsym, const double* dpert, const double* b, double* x,
                          double tol, int32_t max_iter, int32_t* iters_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n > n_max");
     if (!ctx->d_cgv) TRY(dalloc(ctx, &ctx->d_cgv, (size_t)9 * ctx->n_max));
@@ -3115,6 +3186,7 @@ int scvt_laplacian_solve(scvt_ctx* ctx, int64_t n, const int32_t* nbr, const int
 }
 
 int scvt_twoloop_backward(scvt_ctx* ctx, const double* g, int64_t n, double* q) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     const int64_t len = 3 * n;
     cudaStream_t s = ctx->stream;
@@ -3133,6 +3205,7 @@ int scvt_twoloop_backward(scvt_ctx* ctx, const double* g, int64_t n, double* q) 
 }
 
 int scvt_twoloop_forward(scvt_ctx* ctx, double* q, const double* g, int64_t n, double* qg_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     const int64_t len = 3 * n;
     cudaStream_t s = ctx->stream;
@@ -3159,6 +3232,7 @@ int scvt_twoloop_forward(scvt_ctx* ctx, double* q, const double* g, int64_t n, d
 
 // ---------------------------------------------------------------------- optimizer algebra
 int scvt_history_clear(scvt_ctx* ctx) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     ctx->hist_head = 0;
     ctx->hist_count = 0;
@@ -3166,12 +3240,14 @@ int scvt_history_clear(scvt_ctx* ctx) {
 }
 
 int scvt_history_size(scvt_ctx* ctx, int32_t* size_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     *size_host = ctx->hist_count;
     return SCVT_OK;
 }
 
 int scvt_history_gamma(scvt_ctx* ctx, double* gamma_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (ctx->hist_count == 0) { *gamma_host = 1.0; return SCVT_OK; }
     int newest = (ctx->hist_head + ctx->hist_count - 1) % ctx->m;
@@ -3181,6 +3257,7 @@ int scvt_history_gamma(scvt_ctx* ctx, double* gamma_host) {
 
 int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new, const double* g_old,
                       const double* g_new, int64_t n, int32_t* pushed_host, double* movement_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
@@ -3193,6 +3270,7 @@ int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new, c
 int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
                                  double gamma, const double* z, int64_t n, double* q3,
                                  double* out_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
@@ -3207,6 +3285,7 @@ int scvt_lbfgs_direction_tangent(scvt_ctx* ctx, const double* g, const double* l
 
 int scvt_lbfgs_direction_tangent_async(scvt_ctx* ctx, const double* g, const double* lloyd_diag,
                                        double gamma, const double* z, int64_t n, double* q3) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
@@ -3221,6 +3300,7 @@ int scvt_lbfgs_direction_tangent_async(scvt_ctx* ctx, const double* g, const dou
 }
 
 int scvt_direction_result(scvt_ctx* ctx, double* out_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     CK(cudaEventSynchronize(ctx->dir_ev));
     out_host[0] = ctx->h_dir[0];
@@ -3230,6 +3310,7 @@ int scvt_direction_result(scvt_ctx* ctx, double* out_host) {
 
 int scvt_lbfgs_direction(scvt_ctx* ctx, const double* g, const double* lloyd_diag, double gamma,
                          int64_t n, double* q, double* qg_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     int64_t len = 3 * n;
     cudaStream_t s = ctx->stream;
@@ -3267,6 +3348,7 @@ int scvt_lbfgs_direction(scvt_ctx* ctx, const double* g, const double* lloyd_dia
 
 int scvt_tangent_project(scvt_ctx* ctx, const double* q, const double* z, const double* g,
                          int64_t n, double* q3, double* dphi0_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
@@ -3280,6 +3362,7 @@ int scvt_tangent_project(scvt_ctx* ctx, const double* q, const double* z, const 
 
 int scvt_trial_point(scvt_ctx* ctx, const double* z, const double* q3, double alpha, int64_t n,
                      double* zt, double* norms) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     k_trial<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(z, q3, alpha, n, zt, norms);
     LAUNCHED();
@@ -3288,6 +3371,7 @@ int scvt_trial_point(scvt_ctx* ctx, const double* z, const double* q3, double al
 
 int scvt_directional_derivative(scvt_ctx* ctx, const double* g, const double* q3,
                                 const double* norms, int64_t n, double* d_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
@@ -3300,6 +3384,7 @@ int scvt_directional_derivative(scvt_ctx* ctx, const double* g, const double* q3
 }
 
 int scvt_lloyd_step(scvt_ctx* ctx, const double* first, int64_t n, double* z_out) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     TRY(reset_status(ctx));
     k_lloyd<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(first, n, z_out, ctx->d_status);
@@ -3310,6 +3395,7 @@ int scvt_lloyd_step(scvt_ctx* ctx, const double* first, int64_t n, double* z_out
 }
 
 int scvt_min(scvt_ctx* ctx, const double* v, int64_t len, double* min_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     k_reduce_stage1<2><<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(v, len, ctx->d_partials);
     LAUNCHED();
@@ -3322,6 +3408,7 @@ int scvt_min(scvt_ctx* ctx, const double* v, int64_t len, double* min_host) {
 
 int scvt_max_abs_diff(scvt_ctx* ctx, const double* a, const double* b, int64_t len,
                       double* max_host) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     k_absdiff_stage1<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(a, b, len, ctx->d_partials);
     LAUNCHED();
@@ -3333,6 +3420,7 @@ int scvt_max_abs_diff(scvt_ctx* ctx, const double* a, const double* b, int64_t l
 }
 
 int scvt_scale(scvt_ctx* ctx, double a, const double* x, int64_t len, double* y) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     k_scale<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(a, x, len, y);
     LAUNCHED();
@@ -3340,6 +3428,7 @@ int scvt_scale(scvt_ctx* ctx, double a, const double* x, int64_t len, double* y)
 }
 
 int scvt_normalize_rows(scvt_ctx* ctx, double* z, int64_t n) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     k_normalize<<<RED_BLOCKS, VEC_THREADS, 0, ctx->stream>>>(z, n);
     LAUNCHED();

@@ -259,12 +259,104 @@ class _DeviceOps:
 
 def _to_host(res: EvalResult, z=None):
     """NumPy copy of a device result (and of the positions `z`), one pinned transfer."""
-    ts = [res.grad, res.lloyd_diag, res.first, res.mass] + ([z] if z is not None else [])
-    arr = to_numpy(*ts)
+    ts = [res.grad, res.lloyd_diag, res.first] + ([res.mass] if res.mass is not None else [])
+    arr = to_numpy(*ts, *([z] if z is not None else []))
+    mass = arr[3] if res.mass is not None else None
     out = EvalResult(energy=res.energy, grad=arr[0], grad_norm=res.grad_norm,
-                     lloyd_diag=arr[1], first=arr[2], migration=res.migration, mass=arr[3],
-                     obtuse_count=res.obtuse_count)
-    return (out, arr[4]) if z is not None else out
+                     lloyd_diag=arr[1], first=arr[2], migration=res.migration, mass=mass,
+                     obtuse_count=res.obtuse_count, laplacian=res.laplacian)
+    return (out, arr[-1]) if z is not None else out
+
+
+class _HostLaplacian:
+    """A reference-style preconditioner (``solve`` on NumPy (K, 3) arrays) seen from the
+    device optimizer (LaplacianInverse, optimizer.py:137-144)."""
+
+    def __init__(self, inner, device):
+        self.inner, self.device = inner, device
+
+    def solve(self, q):
+        import torch
+
+        x = np.asarray(self.inner.solve(to_numpy(q.reshape(-1, 3))[0]), dtype=np.float64)
+        return torch.as_tensor(x.reshape(q.shape), device=self.device)
+
+
+class HostEvaluatorAdapter:
+    """Any evaluator of the reference's duck-typed protocol (``evaluate(points) -> EvalResult``
+    with NumPy arrays, optional ``redecompose(points)``; optimizer.py:278-293) behind the
+    device interface `Minimizer` drives, so `minimize` accepts it exactly like the reference's
+    `minimize` does.  The optimizer algebra (two-loop, projection, trial points, history) still
+    runs on the GPU; every evaluation crosses to the host and back.  No speculative trial:
+    the wrapped evaluator sees exactly the reference's sequence of evaluations."""
+
+    def __init__(self, inner, device: int | None = None):
+        import torch
+
+        from .density import density_preset
+
+        if not callable(getattr(inner, "evaluate", None)):
+            raise TypeError("evaluator must provide evaluate(points) -> EvalResult")
+        self.inner = inner
+        dev = torch.cuda.current_device() if device is None else int(device)
+        # the algebra's context: any configuration works, the quadrature tables are unused
+        self._algebra = MeshEvaluator(density_preset("const"), "4pt", device=dev)
+        self.device = dev
+
+    @property
+    def evaluations(self):
+        return getattr(self.inner, "evaluations", 0)
+
+    @evaluations.setter
+    def evaluations(self, v):
+        if hasattr(self.inner, "evaluations"):
+            self.inner.evaluations = v
+
+    @property
+    def context(self):
+        return self._algebra.context
+
+    def _as_device(self, points):
+        return self._algebra._as_device(points)
+
+    def _ensure_ctx(self, n, m=None):
+        return self._algebra._ensure_ctx(n, m)
+
+    def optimizer_ops(self, ctx, n):
+        ops = _DeviceOps(ctx, n)
+        ops.speculate = False
+        return ops
+
+    def redecompose(self, points):
+        fn = getattr(self.inner, "redecompose", None)
+        if fn is not None:
+            fn(to_numpy(points)[0] if not isinstance(points, np.ndarray) else points)
+
+    def evaluate_device(self, z, q3=None, norms=None) -> EvalResult:
+        import torch
+
+        r = self.inner.evaluate(to_numpy(z)[0])
+        dev = z.device
+
+        def put(a):
+            return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+
+        grad, diag, first = put(r.grad), put(r.lloyd_diag), put(r.first)
+        mass = getattr(r, "mass", None)
+        dirderiv = float("nan")
+        if q3 is not None:                         # phi's derivative (optimizer.py:330)
+            qh, nh = to_numpy(q3, norms)
+            dirderiv = float(np.einsum("ij,ij->i", np.asarray(r.grad), qh / nh[:, None]).sum())
+        lap = getattr(r, "laplacian", None)
+        return EvalResult(energy=float(r.energy), grad=grad, grad_norm=float(r.grad_norm),
+                          lloyd_diag=diag, first=first,
+                          mass=put(mass) if mass is not None else None,
+                          migration=getattr(r, "migration", "in-place"),
+                          laplacian=_HostLaplacian(lap, dev) if lap is not None else None,
+                          min_diag=float(np.min(r.lloyd_diag)), dirderiv=dirderiv)
+
+    def close(self):
+        self._algebra.close()
 
 
 class Minimizer:
@@ -278,8 +370,8 @@ class Minimizer:
 
         if method not in METHODS:
             raise ValueError(f"unknown method {method!r}; expected one of {METHODS}")
-        if not isinstance(evaluator, MeshEvaluator):
-            raise TypeError("minimize drives the GPU MeshEvaluator of this package")
+        if not hasattr(evaluator, "optimizer_ops"):      # reference-protocol evaluator
+            evaluator = HostEvaluatorAdapter(evaluator)
         self.torch = torch
         self.method = method
         self.evaluator = evaluator
@@ -347,11 +439,13 @@ class Minimizer:
                 except Exception as exc:  # noqa: BLE001 - re-raised below unless discarded
                     err = exc
                 qg, dphi0 = ops.direction_result()
-                if qg < 0.0:
-                    if err is not None:
+                if qg < 0.0 and dphi0 < 0.0:
+                    if err is not None:     # the reference evaluates this very trial first
                         raise err
                     first = (r1.energy, r1.dirderiv, (zt, r1))
                 elif r1 is not None:
+                    # history reset (q.g >= 0) or Lloyd fallback (g.q3 >= 0, wolfe_line_search
+                    # raises before any evaluation): the trial never happened in the reference
                     ev.evaluations -= 1
             else:
                 qg, dphi0 = direction()
@@ -379,8 +473,6 @@ class Minimizer:
                 if exhausted:
                     logger.debug("line search exhausted at iteration %d", n)
             except (NonDescentError, LineSearchFailure) as exc:
-                if first is not None and isinstance(exc, NonDescentError):
-                    ev.evaluations -= 1                          # the speculative trial
                 logger.warning("line search failed at iteration %d (%s); Lloyd fallback", n, exc)
                 ops.history_clear()
                 self.resets += 1
@@ -401,13 +493,17 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
              corrections: int = 7, callback=None) -> MinimizeResult:
     """Drive one of the iteration methods to a stopping criterion (optimizer.py:278-391).
 
-    ``points``: (K, 3) NumPy array or CUDA tensor.  ``callback(n, z_new, res_new)`` receives
-    CUDA tensors (zero-copy; under a multi-GPU `ShardedMeshEvaluator` the vectors of res_new
-    hold the rank's arithmetic slice, `parallel.SliceOps`).  Returns NumPy ``points`` and
-    ``final`` (all rows)."""
+    ``points``: (K, 3) NumPy array or CUDA tensor.  ``evaluator``: this package's
+    `MeshEvaluator` / `ShardedMeshEvaluator`, or any object with the reference's duck-typed
+    ``evaluate``/``redecompose`` protocol (`HostEvaluatorAdapter`).  ``callback(n, z_new,
+    res_new)`` receives NumPy arrays with every row when ``points`` is NumPy (as in the
+    reference), and zero-copy CUDA tensors when ``points`` is a CUDA tensor (under a multi-GPU
+    `ShardedMeshEvaluator` the vectors of res_new then hold the rank's arithmetic slice,
+    `parallel.SliceOps`).  Returns NumPy ``points`` and ``final`` (all rows)."""
     criteria = criteria or StoppingCriteria()
     t0 = time.perf_counter()
     st = Minimizer(points, method, evaluator, corrections)
+    host_input = not (isinstance(points, st.torch.Tensor) and points.is_cuda)
     records: list[IterationRecord] = []
     reason = "max-iterations"
     for _ in range(criteria.max_iterations):
@@ -415,7 +511,11 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
         rec, movement, z_new, res_new = st.step()
         records.append(rec)
         if callback is not None:
-            callback(rec.n, z_new, res_new)
+            if host_input:       # the reference hands NumPy arrays to callbacks
+                res_h, z_h = _to_host(st.ops.full(res_new), z_new)
+                callback(rec.n, z_h, res_h)
+            else:
+                callback(rec.n, z_new, res_new)
         res = st.res
         if movement <= criteria.movement_tol:                   # optimizer.py:368-376
             reason = "movement"
@@ -432,7 +532,7 @@ def minimize(points, method: str, evaluator: MeshEvaluator, criteria: StoppingCr
             evaluator.redecompose(st.z)
             st.ops.history_clear()
             st.resets += 1
-    st.torch.cuda.current_stream().synchronize()
+    st.torch.cuda.current_stream(st.z.device).synchronize()
     wall = time.perf_counter() - t0
     final, points = _to_host(st.ops.full(st.res), st.z)
     return MinimizeResult(points=points, records=records, reason=reason,

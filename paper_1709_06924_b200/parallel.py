@@ -377,17 +377,19 @@ class SliceOps:
 def _all_gather(out, inp, group):
     import torch.distributed as dist
 
+    if out.numel() != dist.get_world_size(group) * inp.numel():
+        raise ValueError(f"all-gather of {tuple(inp.shape)} into {tuple(out.shape)} for "
+                         f"{dist.get_world_size(group)} ranks")
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, inp, group=group)
         return
-    # gloo (CPU tests; CUDA tensors staged through host memory): list form
+    # gloo (CPU tests; CUDA tensors staged through host memory): the same collective on the
+    # same shapes, so the CPU tests exercise exactly the NCCL call
     host = out.device.type != "cpu"
-    src = inp.cpu() if host else inp
-    dst = out.cpu() if host else out
-    r = src.shape[0]
-    parts = [dst[k * r:(k + 1) * r] for k in range(dst.shape[0] // r)]
-    dist.all_gather(parts, src, group=group)
-    if host:
+    src = (inp.cpu() if host else inp).contiguous()
+    dst = out.cpu() if host or not out.is_contiguous() else out
+    dist.all_gather_into_tensor(dst, src, group=group)
+    if dst is not out:
         out.copy_(dst)
 
 
@@ -503,9 +505,13 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
         _all_gather(cyc_all, cyc_send, group)
         status = backend.moments(z, rank, world, cyc_all, res_send)
     st = torch.tensor([status], dtype=torch.int32, device=cyc_send.device)
-    _all_reduce_max(st, group)                                # everyone raises, or no one
-    if int(st.item()):
-        backend.raise_status(int(st.item()))
+    st_all = torch.empty(world, dtype=torch.int32, device=cyc_send.device)
+    _all_gather(st_all, st, group)                            # everyone raises, or no one
+    status = 0
+    for w in st_all.tolist():      # status words are bit sets: OR them, as one GPU does
+        status |= int(w)
+    if status:
+        backend.raise_status(status)
     _all_gather(res_all, res_send, group)
     if finish is not None:
         return finish(res_all)
@@ -543,12 +549,12 @@ def emulate_shards(backend, z, nshards: int, q3=None, norms=None):
         for s in range(nshards):
             backend.cells(z, s, nshards, cyc_send)
             cyc_all[s * r:(s + 1) * r] = cyc_send
-    worst = 0
+    status = 0
     for s in range(nshards):
-        worst = max(worst, backend.moments(z, s, nshards, None if reused else cyc_all, res_send))
+        status |= backend.moments(z, s, nshards, None if reused else cyc_all, res_send)
         res_all[s * r:(s + 1) * r] = res_send
-    if worst:
-        backend.raise_status(worst)
+    if status:
+        backend.raise_status(status)
     if q3 is None:
         return backend.finish(z, nshards, res_all)
     return backend.finish(z, nshards, res_all, q3, norms)

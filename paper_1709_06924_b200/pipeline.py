@@ -37,9 +37,12 @@ def to_numpy(*tensors):
     array keeps its pinned tensor alive."""
     torch = _torch()
     outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in tensors]
+    devices = {t.device for t in tensors if t.is_cuda}
     for o, t in zip(outs, tensors):
-        o.copy_(t, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+        with torch.cuda.device(t.device):      # the copy is ordered on the tensor's stream
+            o.copy_(t, non_blocking=True)
+    for d in devices:                          # wait for every copy before handing out arrays
+        torch.cuda.current_stream(d).synchronize()
     return [o.numpy() for o in outs]
 
 

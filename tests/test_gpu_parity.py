@@ -291,7 +291,8 @@ def _run_traj(g, density, rule, depth, method, m, iters):
 
     def cb(n, z, res):
         if n in keep:
-            snaps[n] = z.cpu().numpy()
+            assert isinstance(z, np.ndarray)    # NumPy input -> NumPy callbacks (reference)
+            snaps[n] = z.copy()
 
     crit = P.StoppingCriteria(max_iterations=iters, movement_tol=1e-300, grad_tol=1e-300,
                               stall_tol=1e-300)
