@@ -131,6 +131,11 @@ int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n,
                                double* first, double* mass, double* lloyd_diag,
                                double* scalars_host);
 
+/* Per-cell energy E_i = sum over the cell's fan sub-triangles of int rho |y - z_i|^2 (the
+ * terms cvt_core.py:97-100 sums into the scalar energy) of the last single-GPU evaluation,
+ * copied into energy_out (n doubles, device memory).  Parity tests compare it per cell. */
+int scvt_cell_energy(scvt_ctx* ctx, int64_t n, double* energy_out);
+
 /* sharded evaluation (one process per GPU) -------------------------------------------------
  * The generators are split into `nshards` equal ranges of the cube-map bucket order; shard s
  * owns rows [s*R, (s+1)*R) with R = scvt_shard_rows(n, nshards).  Per evaluation:

@@ -393,13 +393,15 @@ def subdivide(f: Fans, depth: int) -> Fans:
     return Fans(verts, cells, edge_other, signed, f.obtuse_count)
 
 
-def cell_quadrature(points, f: Fans, density: Density, rule: Rule, k: int, measure="flat"):
-    """cvt_core.py:55-117 (with_pairs=False) — (mass (k,), first (k,3), energy)."""
+def cell_quadrature(points, f: Fans, density: Density, rule: Rule, k: int, measure="flat",
+                    cell_energy=False):
+    """cvt_core.py:55-117 (with_pairs=False) — (mass (k,), first (k,3), energy); with
+    ``cell_energy`` also the per-cell energies (k,) whose sum is the energy (test helper)."""
     pts = np.asarray(points, dtype=float)
     mass = np.zeros(k)
     first = np.zeros((k, 3))
     if len(f.cells) == 0:
-        return mass, first, 0.0
+        return (mass, first, 0.0, np.zeros(k)) if cell_energy else (mass, first, 0.0)
     nodes = np.einsum("qv,svj->sqj", rule.bary, f.verts)
     radii = np.linalg.norm(nodes, axis=-1)
     nodes = nodes / radii[..., None]
@@ -418,9 +420,14 @@ def cell_quadrature(points, f: Fans, density: Density, rule: Rule, k: int, measu
     z_cell = pts[f.cells]
     diff = nodes - z_cell[:, None, :]
     sq = np.einsum("sqj,sqj->sq", diff, diff)
-    energy = float(np.sum(((rho * sq) @ w) * f.signed_area))
+    sub_energy = ((rho * sq) @ w) * f.signed_area
+    energy = float(np.sum(sub_energy))
     np.add.at(mass, f.cells, sub_mass)
     np.add.at(first, f.cells, sub_first)
+    if cell_energy:
+        ecell = np.zeros(k)
+        np.add.at(ecell, f.cells, sub_energy)
+        return mass, first, energy, ecell
     return mass, first, energy
 
 

@@ -701,6 +701,40 @@ SCVT_HD FanPair fan_pair(V3 vi, V3 vj, V3 vk, int i, int j, int k) {
     return f;
 }
 
+// One fan sub-triangle of the incidence (half 0: (v_i, m_ij, oc), half 1: (m_ki, v_i, oc)),
+// without the other half's geometry; *obtuse (the triangle's six signed areas, as fan_pair)
+// is computed for half 0 only.  Same arithmetic as fan_pair, so the same bits.
+SCVT_HD SubTri fan_sub(V3 vi, V3 vj, V3 vk, int i, int j, int k, int half, int* obtuse,
+                       int* degenerate) {
+    V3 va, vb, vc;
+    if (i < j && i < k) { va = vi; vb = vj; vc = vk; }
+    else if (j < k) { va = vj; vb = vk; vc = vi; }
+    else { va = vk; vb = vi; vc = vj; }
+    const V3 oc = planar_circumcenter(va, vb, vc);
+    V3 n = cross(sub(vb, va), sub(vc, va));
+    const double nn = norm3(n);
+    *degenerate = !(nn > 0.0);
+    n = mul(n, 1.0 / nn);
+    if (dot(n, add(add(va, vb), vc)) < 0.0) n = mul(n, -1.0);
+    const V3 mij = mul(add(vi, vj), 0.5);
+    const V3 mki = mul(add(vk, vi), 0.5);
+    SubTri st;
+    if (half == 0) {
+        st.v0 = vi; st.e1 = sub(mij, vi); st.e2 = sub(oc, vi);
+        st.area = signed_area(vi, mij, oc, n);
+        const V3 mjk = mul(add(vj, vk), 0.5);
+        const double a1 = signed_area(mki, vi, oc, n);
+        const double a2 = signed_area(mij, vj, oc, n), a3 = signed_area(vj, mjk, oc, n);
+        const double a4 = signed_area(mjk, vk, oc, n), a5 = signed_area(vk, mki, oc, n);
+        *obtuse = (st.area < 0) | (a1 < 0) | (a2 < 0) | (a3 < 0) | (a4 < 0) | (a5 < 0);
+    } else {
+        st.v0 = mki; st.e1 = sub(vi, mki); st.e2 = sub(oc, mki);
+        st.area = signed_area(mki, vi, oc, n);
+        *obtuse = 0;
+    }
+    return st;
+}
+
 // Accumulate sum_q w_q rho(y_q) {1, y_q, |y_q - z|^2} over the composite nodes of one
 // sub-triangle (cvt_core.py:80-100 with the subdivision of delaunay.py:383-407 folded into
 // the node table).  acc = {m, cx, cy, cz, E}.
@@ -807,7 +841,7 @@ struct LocalFit {
 // 90 deg from c, comes too close to the sqrt singularity at s = 0, or the fit misses the table
 // by more than 4e-15 relative at any check point (the table itself is within 1.6e-15 of the
 // closed form; a degree-6 interpolant evaluated in FP64 has a ~1e-15 rounding floor).
-SCVT_COLD bool local_fit(const DensityParams& p, const SubTri& st, V3 c, LocalFit& f) {
+SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, LocalFit& f) {
     constexpr double CHEB_V[7] = {0.9749279121818236, 0.7818314824680298, 0.4338837391175582,
                               6.123233995736766e-17, -0.43388373911755806, -0.7818314824680295,
                               -0.9749279121818237};
@@ -892,6 +926,10 @@ SCVT_COLD bool local_fit(const DensityParams& p, const SubTri& st, V3 c, LocalFi
     f.rmin = fmin(rl, rh);
     f.rmax = fmax(rl, rh);
     return true;
+}
+
+SCVT_COLD bool local_fit(const DensityParams& p, const SubTri& st, V3 c, LocalFit& f) {
+    return local_fit_impl(p, st, c, f);
 }
 
 SCVT_HD double fit_u(const LocalFit& f, V3 x, double inv) {
@@ -1164,6 +1202,58 @@ SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const 
     const double w0 = w[0], w1 = w[1], w2 = w[4];
     double mo[5];
     sym7_leaves<KIND, L, false>(s, z, o, w0, w1, w2, dp, f0, f1, mo, pole);
+    acc[0] += s.area * mo[0];
+    acc[1] += s.area * mo[1]; acc[2] += s.area * mo[2]; acc[3] += s.area * mo[3];
+    acc[4] += s.area * mo[4];
+}
+
+// ---- two-phase form of subtri_moments_sym7 (k_quad): the prologue (fits, sweep choice) runs
+// inline and leaves its results in a per-thread shared-memory slot; the sweep reads them back.
+// Nothing but the slot crosses from one phase to the other, so the prologue's registers die
+// before the node loop and no out-of-line call (with its caller-saved stack frame) sits on the
+// per-sub-triangle path.
+enum : int { SWEEP_TABLE = 0, SWEEP_FIT0 = 1, SWEEP_FIT1 = 2, SWEEP_FIT2 = 3, SWEEP_SERIES = 4 };
+
+template <int KIND>
+SCVT_HD int sym7_prologue(const DensityParams& dp, const SubTri& s, LocalFit* f) {
+    const bool TAB = KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB;
+    if (!TAB) return SWEEP_TABLE;
+    if (!local_fit_impl(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f[0])) return SWEEP_TABLE;
+    int mode = SWEEP_FIT0;
+    if (KIND == DEN_TANH4X2_TAB) {
+        if (!local_fit_impl(dp, s, v3(dp.c1x, dp.c1y, dp.c1z), f[1])) return SWEEP_TABLE;
+        // one centre dominates the whole patch: its fit alone gives max(rho0, rho1)
+        mode = f[1].rmax < f[0].rmin * (1.0 - 1e-13) ? SWEEP_FIT0
+             : (f[0].rmax < f[1].rmin * (1.0 - 1e-13) ? SWEEP_FIT1 : SWEEP_FIT2);
+    }
+    const V3 nv = cross(s.e1, s.e2);
+    const double nn = dot(nv, nv), h = dot(nv, s.v0);
+    if (nn > 0.0 && nn - h * h <= 1e-4 * nn) mode |= SWEEP_SERIES;
+    return mode;
+}
+
+template <int KIND, int L>
+SCVT_HD void sym7_sweep(int mode, const SubTri& s, V3 z, const double* l1, const double* l2,
+                        const double* w, const DensityParams& dp, const LocalFit* f,
+                        double* acc, int* pole) {
+    const int fit = mode & 3;
+    const bool series = (mode & SWEEP_SERIES) != 0;
+    if (fit == SWEEP_FIT0 || fit == SWEEP_FIT1) {
+        const LocalFit& fd = f[fit - 1];
+        if (series) sym7_fit_leaves<DEN_TANH4_TAB, L, true>(s, z, l1, l2, w, fd, fd, acc);
+        else sym7_fit_leaves<DEN_TANH4_TAB, L, false>(s, z, l1, l2, w, fd, fd, acc);
+        return;
+    }
+    if (KIND == DEN_TANH4X2_TAB && fit == SWEEP_FIT2) {
+        if (series) sym7_fit_leaves<KIND, L, true>(s, z, l1, l2, w, f[0], f[1], acc);
+        else sym7_fit_leaves<KIND, L, false>(s, z, l1, l2, w, f[0], f[1], acc);
+        return;
+    }
+    V3 o[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) o[q] = add(mul(s.e1, l1[q]), mul(s.e2, l2[q]));
+    double mo[5];
+    sym7_leaves<KIND, L, false>(s, z, o, w[0], w[1], w[4], dp, f[0], f[0], mo, pole);
     acc[0] += s.area * mo[0];
     acc[1] += s.area * mo[1]; acc[2] += s.area * mo[2]; acc[3] += s.area * mo[3];
     acc[4] += s.area * mo[4];

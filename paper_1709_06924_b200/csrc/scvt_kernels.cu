@@ -45,10 +45,10 @@ constexpr int RED_THREADS = 256;
 constexpr int VEC_THREADS = 256;
 constexpr int QUAD_THREADS = 128;
 #ifndef QUAD_MINB
-#define QUAD_MINB 4      // k_quad fast path: CTAs per SM the register budget must allow
+#define QUAD_MINB 5      // k_quad fast path: CTAs per SM the register budget must allow
 #endif
 #ifndef QUAD_MINB2
-#define QUAD_MINB2 3     // two-centre fast path
+#define QUAD_MINB2 4     // two-centre fast path
 #endif
 constexpr int CELL_THREADS = 64;
 constexpr int PART_ROW = 10;         // per-incidence partials: [half][m, cx, cy, cz, E]
@@ -486,6 +486,7 @@ struct QuadArgs {
     int n;
     int cnt;                // owned sorted slots
     int n_inc;            // expected incidences 6n - 12
+    const DensityParams* dpg;   // device copy of dp (tab set): what out-of-line paths read
     const double* nodes;  // device [3][nq]: l1, l2, w
     const double* table;  // device rho^(1/4) table (tanh4 kinds) or null
     int nq;
@@ -502,10 +503,15 @@ template <int KIND, bool SPHERE, bool SYM7, bool SPLIT = false>
 __global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? (KIND == DEN_TANH4X2_TAB ? QUAD_MINB2 : QUAD_MINB) : 1)
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
-    for (int q = threadIdx.x; q < 3 * a.nq; q += blockDim.x) s_nodes[q] = a.nodes[q];
-    // the density table (28 KB) is read through the read-only cache, where it stays resident;
-    // staging it in shared memory per CTA cost 1.4-2.7 % of k_quad (c4, c3, c5)
-    if (KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB) a.dp.tab = a.table;
+    // the symmetric 7-node fast path reads only the first leaf's 7 nodes of each column: a
+    // compact [3][7] copy (keeps shared memory for more resident CTAs)
+    const int nq_s = (SYM7 && !SPHERE && SPLIT) ? 7 : a.nq;
+    for (int q = threadIdx.x; q < 3 * nq_s; q += blockDim.x)
+        s_nodes[q] = a.nodes[(q / nq_s) * a.nq + q % nq_s];
+    // the density table (28 KB) is read through the read-only cache, where it stays resident
+    // (staging it in shared memory per CTA cost 1.4-2.7 % of k_quad, c4, c3, c5); a.dp.tab
+    // points at it (set on the host: the kernel never takes the address of its parameters,
+    // which would copy them to the stack of every thread)
     __syncthreads();
     const int t_id = blockIdx.x * blockDim.x + threadIdx.x;
     const int u = SPLIT ? t_id >> 1 : t_id;
@@ -521,17 +527,41 @@ k_quad(QuadArgs a) {
     const int* row = a.nbr + (int64_t)i * MAXDEG;
     int j = row[t], k = row[t + 1 == d ? 0 : t + 1];
     V3 vi = load3(a.z, i), vj = load3(a.z, j), vk = load3(a.z, k);
-    FanPair f = fan_pair(vi, vj, vk, i, j, k);
-    if (f.degenerate) atomicOr(a.status, ST_DEGENERATE_TRI);
     double acc[5] = {0, 0, 0, 0, 0};
     int pole = 0;
     const double* l1 = s_nodes;
-    const double* l2 = s_nodes + a.nq;
-    const double* w = s_nodes + 2 * a.nq;
+    const double* l2 = s_nodes + nq_s;
+    const double* w = s_nodes + 2 * nq_s;
     if (SYM7 && !SPHERE && SPLIT) {
-        subtri_moments_sym7<KIND, 8>(f.s[half], vi, l1, l2, w, a.dp, acc, &pole);
-    } else {   // both halves in this thread, stored separately (per-sub-triangle masses feed
-               // the graph Laplacian; the gathers add the halves: the same sums as before)
+        // phase 1 -> shared slot -> phase 2 (scvt_device.cuh sym7_prologue / sym7_sweep):
+        // only this thread's half of the fan is built, and nothing but the slot (sub-triangle,
+        // generator, fits) is live across the node loop
+        constexpr int NF = KIND == DEN_TANH4X2_TAB ? 2 : 1;
+        __shared__ LocalFit s_fit[QUAD_THREADS][NF];
+        __shared__ SubTri s_sub[QUAD_THREADS];
+        __shared__ double s_z[QUAD_THREADS][3];
+        int obt, degen;
+        const SubTri st0 = fan_sub(vi, vj, vk, i, j, k, half, &obt, &degen);
+        if (degen) atomicOr(a.status, ST_DEGENERATE_TRI);
+        if (half == 0) a.obtuse[u] = (obt && i < j && i < k) ? 1 : 0;
+        const DensityParams& dp = *a.dpg;
+        const int mode = sym7_prologue<KIND>(dp, st0, s_fit[threadIdx.x]);
+        s_sub[threadIdx.x] = st0;
+        s_z[threadIdx.x][0] = vi.x; s_z[threadIdx.x][1] = vi.y; s_z[threadIdx.x][2] = vi.z;
+        asm volatile("" ::: "memory");    // the sweep reads its inputs back from the slot
+        const SubTri st = s_sub[threadIdx.x];
+        const V3 zc = v3(s_z[threadIdx.x][0], s_z[threadIdx.x][1], s_z[threadIdx.x][2]);
+        sym7_sweep<KIND, 8>(mode, st, zc, l1, l2, w, dp, s_fit[threadIdx.x], acc, &pole);
+        if (pole) atomicOr(a.status, ST_POLE);
+        double* out = a.part + (int64_t)u * PART_ROW + (half ? 5 : 0);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) out[c] = acc[c];
+        return;
+    }
+    FanPair f = fan_pair(vi, vj, vk, i, j, k);
+    if (f.degenerate) atomicOr(a.status, ST_DEGENERATE_TRI);
+    {   // both halves in this thread, stored separately (per-sub-triangle masses feed
+        // the graph Laplacian; the gathers add the halves: the same sums as before)
         subtri_moments<KIND, SPHERE>(f.s[0], vi, l1, l2, w, a.nq, a.dp, acc, &pole);
         double acc1[5] = {0, 0, 0, 0, 0};
         subtri_moments<KIND, SPHERE>(f.s[1], vi, l1, l2, w, a.nq, a.dp, acc1, &pole);
@@ -1488,6 +1518,7 @@ struct scvt_ctx {
     int m = 7;
     double* d_nodes = nullptr;   // [3][nq]
     double* d_table = nullptr;   // [2][tab_k][TAB_P+1] rho^(1/4) table (tanh4 kinds)
+    DensityParams* d_dp = nullptr;   // device copy of dp (tab = d_table)
     // grid
     int g_max = 1;
     uint32_t* d_keys = nullptr; uint32_t* d_skeys = nullptr;
@@ -2039,7 +2070,7 @@ int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t sme
         k_quad<KIND, true, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
     else if (ctx->sym7)         // the fast path always runs a thread per fan sub-triangle
         k_quad<KIND, false, true, true><<<blocks_for(2 * (int64_t)a.n_inc, QUAD_THREADS),
-                                           QUAD_THREADS, smem, ctx->stream>>>(a);
+                                           QUAD_THREADS, 21 * sizeof(double), ctx->stream>>>(a);
     else
         k_quad<KIND, false, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
     LAUNCHED();
@@ -2074,6 +2105,8 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
     a.nodes = ctx->d_nodes;
     a.nq = ctx->nq; a.dp = ctx->dp; a.part = ctx->d_part; a.obtuse = ctx->d_obt;
     a.table = ctx->d_table;
+    a.dp.tab = ctx->d_table;
+    a.dpg = ctx->d_dp;
     a.status = ctx->d_status;
     if (n_inc <= 0) return SCVT_OK;
     // split mode (thread per fan sub-triangle) on the 7-point fast path: twice the work units,
@@ -2454,6 +2487,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     if ((r = dalloc(ctx, &ctx->p, (size_t)(cnt)))) return bail(r)
     AL(d_nodes, 3 * ctx->nq);
     AL(d_table, 2 * (int64_t)dp.tab_k * (TAB_P + 1));
+    AL(d_dp, 1);
     AL(d_keys, n); AL(d_skeys, n); AL(d_vals, n); AL(d_ids, n);
     AL(d_start, nb + 1);
     AL(d_zs, 4 * n);
@@ -2519,6 +2553,21 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         if (e != cudaSuccess) return bail(fail(ctx, SCVT_ERR_CUDA, "table upload failed"));
     }
     size_t smem = 3 * (size_t)ctx->nq * sizeof(double);   // composite node table (quad_range)
+    {
+        // the split fast path adds its static per-thread fit slots (up to ~40 KB) to the
+        // node table: opt in so that static + dynamic may exceed 48 KB
+#define OPT7(K) \
+    cudaFuncSetAttribute(k_quad<K, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+        OPT7(DEN_CONST); OPT7(DEN_X3); OPT7(DEN_X16); OPT7(DEN_TANH); OPT7(DEN_TANH4);
+        OPT7(DEN_TANH4X2); OPT7(DEN_TANH4_TAB); OPT7(DEN_TANH4X2_TAB);
+#undef OPT7
+    }
+    DensityParams dpd = dp;          // device copy read by the out-of-line quadrature paths
+    dpd.tab = ctx->d_table;
+    {
+        cudaError_t e = cudaMemcpy(ctx->d_dp, &dpd, sizeof(dpd), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return bail(fail(ctx, SCVT_ERR_CUDA, "density upload failed"));
+    }
     if (smem > 48 * 1024) {
         // opt in to large dynamic shared memory for every instantiation
 #define OPT(K)                                                                             \
@@ -2539,7 +2588,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_OK;
-    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
+    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_dp, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
                    ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_wdir, ctx->d_cgv, ctx->d_cg, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_fcnt, ctx->d_counts,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
@@ -2656,6 +2705,16 @@ int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const 
 // ---------------------------------------------------------------------- sharded evaluation
 int64_t scvt_shard_rows(int64_t n, int nshards) {
     return nshards > 0 ? (n + nshards - 1) / nshards : 0;
+}
+
+int scvt_cell_energy(scvt_ctx* ctx, int64_t n, double* energy_out) {
+    DeviceGuard dg_(ctx);
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (n < 1 || n > ctx->n_max || !energy_out)
+        return fail(ctx, SCVT_ERR_CONFIG, "cell energy: n=%lld", (long long)n);
+    CK(cudaMemcpyAsync(energy_out, ctx->d_egen, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    return SCVT_OK;
 }
 
 int scvt_shard_cells(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,

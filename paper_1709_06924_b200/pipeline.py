@@ -336,6 +336,14 @@ class MeshEvaluator:
                                                              r.lloyd_diag)
         return r
 
+    def cell_energy(self, n: int):
+        """Per-cell energies of the last evaluation (device tensor, n doubles)."""
+        torch = _torch()
+        ctx = self._ensure_ctx(n)
+        out = torch.empty(n, dtype=torch.float64, device=f"cuda:{ctx.device}")
+        ctx.call("scvt_cell_energy", n, _lib.dptr(out), what="cell_energy")
+        return out
+
     def evaluate_on_triangles(self, points, triangles) -> EvalResult:
         """Moments over a caller-supplied canonical triangulation (parity tests)."""
         torch = _torch()

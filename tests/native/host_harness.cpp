@@ -185,11 +185,24 @@ extern "C" int harness_quad_sym7(const double* z, int n, const int* nbr, const i
         const int* row = nbr + (int64_t)i * MAXDEG;
         for (int t = 0; t < deg[i]; ++t) {
             int j = row[t], k = row[(t + 1) % deg[i]];
-            FanPair f = fan_pair(load3(z, i), load3(z, j), load3(z, k), i, j, k);
             for (int s = 0; s < 2; ++s) {
-                if (kind == 6) subtri_moments_sym7<6, 8>(f.s[s], load3(z, i), l1, l2, w, dp, acc, &pole);
-                else if (kind == 7) subtri_moments_sym7<7, 8>(f.s[s], load3(z, i), l1, l2, w, dp, acc, &pole);
-                else subtri_moments_sym7<0, 8>(f.s[s], load3(z, i), l1, l2, w, dp, acc, &pole);
+                // the k_quad fast path: this half's fan sub-triangle, prologue, sweep
+                int obt, degen;
+                const SubTri st = fan_sub(load3(z, i), load3(z, j), load3(z, k), i, j, k, s,
+                                          &obt, &degen);
+                LocalFit fit[2];
+                double h[5] = {0, 0, 0, 0, 0};
+                if (kind == 6) {
+                    int mode = sym7_prologue<6>(dp, st, fit);
+                    sym7_sweep<6, 8>(mode, st, load3(z, i), l1, l2, w, dp, fit, h, &pole);
+                } else if (kind == 7) {
+                    int mode = sym7_prologue<7>(dp, st, fit);
+                    sym7_sweep<7, 8>(mode, st, load3(z, i), l1, l2, w, dp, fit, h, &pole);
+                } else {
+                    int mode = sym7_prologue<0>(dp, st, fit);
+                    sym7_sweep<0, 8>(mode, st, load3(z, i), l1, l2, w, dp, fit, h, &pole);
+                }
+                for (int c = 0; c < 5; ++c) acc[c] += h[c];
             }
         }
         for (int c = 0; c < 5; ++c) out[5 * (int64_t)i + c] = acc[c];

@@ -514,30 +514,46 @@ def _oracle_cells(z, tri, density_name, rule, depth, gens):
     f = O.Fans(f.verts[sel], f.cells[sel], f.edge_other[sel], f.signed_area[sel], 0)
     mass = np.zeros(len(z))
     first = np.zeros((len(z), 3))
+    ecell = np.zeros(len(z))
     for s in range(0, len(f.cells), 8192):
         sub = O.subdivide(O.Fans(f.verts[s:s + 8192], f.cells[s:s + 8192],
                                  f.edge_other[s:s + 8192], f.signed_area[s:s + 8192], 0), depth)
-        m, c, _ = O.cell_quadrature(z, sub, dens, O.RULES[rule], len(z))
+        m, c, _, e = O.cell_quadrature(z, sub, dens, O.RULES[rule], len(z), cell_energy=True)
         mass += m
         first += c
-    return mass[gens], first[gens]
+        ecell += e
+    return mass[gens], first[gens], ecell[gens]
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg,n", [("c3", 163842), ("c4", 655362), ("c5", 2621442)])
+@pytest.mark.parametrize("cfg,n", [("const", 40962), ("c3", 163842), ("c4", 655362),
+                                   ("c5", 2621442)])
 def test_full_size_sampled_cell_parity(cfg, n):
-    """BASELINE sizes: GPU moments of 1500 random cells against the oracle's (Qhull hull +
-    reference fans + depth-3 subdivision + 7-pt rule), per generator at 1e-12."""
-    z = P.sample_by_density(P.density_preset(cfg), n, 0)
+    """BASELINE sizes: GPU moments AND per-cell energies of 1500 random cells against the
+    oracle's (Qhull hull + reference fans + depth-3 subdivision + 7-pt rule), per generator at
+    1e-12 (c2 = const density at N=40,962 on its own uniform generators)."""
+    if cfg == "const":
+        z = P.random_sphere_points(n, 0)
+    else:
+        z = P.sample_by_density(P.density_preset(cfg), n, 0)
     tri = O.convex_hull_delaunay(z)
     gens = np.sort(np.random.default_rng(5).choice(n, 1500, replace=False))
-    om, oc = _oracle_cells(z, tri, cfg, "7pt", 3, gens)
+    om, oc, oe = _oracle_cells(z, tri, cfg, "7pt", 3, gens)
     with _ev(cfg, "7pt", 3) as ev:
         r = ev.evaluate(z)
+        ecell = ev.cell_energy(n).cpu().numpy()
         t = ev.triangulation(z)
     assert np.array_equal(t.triangles, tri)
     assert np.max(np.abs(r.mass[gens] - om) / np.abs(om)) <= 1e-12
     assert np.max(np.linalg.norm(r.first[gens] - oc, axis=1) / np.linalg.norm(oc, axis=1)) <= 1e-12
+    # per-cell energies: the D7 norm-wise bound over the sample, and 1e-11 for the worst cell
+    # (|y - z|^2 is a difference of nearly equal unit vectors: at c5 the cells are ~1e-3
+    # across, so each node's rounding is ~1e-13 relative, and obtuse cells' signed
+    # sub-triangle areas partly cancel)
+    assert np.linalg.norm(ecell[gens] - oe) <= 1e-12 * np.linalg.norm(oe)
+    assert np.max(np.abs(ecell[gens] - oe) / np.abs(oe)) <= 1e-11
+    # the per-cell energies sum to the evaluation's energy (fixed-order reduction)
+    assert abs(ecell.sum() - r.energy) <= 1e-13 * r.energy
 
 
 @pytest.mark.slow
