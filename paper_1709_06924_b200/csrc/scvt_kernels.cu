@@ -1920,6 +1920,10 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
     int* cnt = ctx->d_fcnt;
     const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
     int cur = 0, rounds = 0, flips_seen = -1;
+    // grid-stride kernels over at most n items per round: small meshes get small grids
+    // (scheduling 1184 mostly idle blocks costs several microseconds per launch at c1)
+    const unsigned fb = (unsigned)std::min<int64_t>(SPEC_BLOCKS, blocks_for(n, 128));
+    const unsigned vb = (unsigned)std::min<int64_t>(SPEC_BLOCKS, blocks_for(VERIFY_LANES * n, 128));
     bool skip_read = known_nonzero;
     for (;;) {
         if (!skip_read) {
@@ -1937,18 +1941,18 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
             const int nxt = 1 - cur;
             int* list = ctx->d_flist + (int64_t)nxt * n;
             CK(cudaMemsetAsync(cnt + 1 + nxt, 0, sizeof(int), s));
-            k_flip_lock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
+            k_flip_lock<<<fb, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
             LAUNCHED();
-            k_flip_apply<<<SPEC_BLOCKS, 128, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock, ctx->d_nbr,
+            k_flip_apply<<<fb, 128, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock, ctx->d_nbr,
                                                       ctx->d_deg, ctx->d_fflag, list, cnt + 1 + nxt,
                                                       ctx->d_bad, ctx->d_nbad, cnt + 3);
             LAUNCHED();
-            k_flip_unlock<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
+            k_flip_unlock<<<fb, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
             LAUNCHED();
-            k_clear_flags<<<SPEC_BLOCKS, 256, 0, s>>>(list, cnt + 1 + nxt, ctx->d_fflag);
+            k_clear_flags<<<fb, 256, 0, s>>>(list, cnt + 1 + nxt, ctx->d_fflag);
             LAUNCHED();
             CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
-            k_verify<<<SPEC_BLOCKS, 128, 0, s>>>(
+            k_verify<<<vb, 128, 0, s>>>(
                 z, ctx->d_ids, 0, (int)n, list, cnt + 1 + nxt, ctx->d_nbr, ctx->d_deg,
                 ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad, fq, 1);
             LAUNCHED();
@@ -1957,7 +1961,7 @@ int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
     }
     const bool open = ctx->h_small[0] > 0;
     if (open) {   // unconverged: those cells are rebuilt
-        k_cand_bad<<<SPEC_BLOCKS, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_bad, ctx->d_nbad);
+        k_cand_bad<<<fb, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_bad, ctx->d_nbad);
         LAUNCHED();
         CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
