@@ -1206,12 +1206,14 @@ k_cg_spmv(const int* __restrict__ nbr, const int* __restrict__ deg,
     }
 }
 
-// x += alpha p, r -= alpha q (alpha = r.r / p.Ap per coordinate); partials of the new r.r
+// Jacobi-preconditioned CG (D = the perturbed diagonal): x += alpha p, r -= alpha q,
+// z = r / D (alpha = r.z / p.Ap per coordinate); partials of the new r.z and r.r
 __global__ void __launch_bounds__(RED_THREADS)
-k_cg_step(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-          const double* __restrict__ q, const double* __restrict__ cg, Chunks ck,
+k_cg_step(double* __restrict__ x, double* __restrict__ r, double* __restrict__ zv,
+          const double* __restrict__ p, const double* __restrict__ q,
+          const double* __restrict__ dpert, const double* __restrict__ cg, Chunks ck,
           double* __restrict__ red, int* __restrict__ status) {
-    double al[3], rr[3] = {0, 0, 0};
+    double al[3], rz[3] = {0, 0, 0}, rr[3] = {0, 0, 0};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         al[c] = cg[3 + c] != 0.0 ? cg[c] / cg[3 + c] : 0.0;
@@ -1221,47 +1223,67 @@ k_cg_step(double* __restrict__ x, double* __restrict__ r, const double* __restri
     int64_t i0, i1;
     chunk_span(ck, &i0, &i1);
     for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
+        const double inv_d = 1.0 / dpert[i];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const int64_t e = 3 * i + c;
             x[e] = fma(al[c], p[e], x[e]);
             const double rv = fma(-al[c], q[e], r[e]);
             r[e] = rv;
+            const double zz = rv * inv_d;
+            zv[e] = zz;
+            rz[c] += rv * zz;
             rr[c] += rv * rv;
         }
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double v = block_reduce<0>(rr[c]);
+        const double v = block_reduce<0>(rz[c]);
         if (threadIdx.x == 0) *chunk_slot(red, ck, c) = v;
+        const double w = block_reduce<0>(rr[c]);
+        if (threadIdx.x == 0) *chunk_slot(red, ck, 3 + c) = w;
     }
 }
 
-// chunk partials of b.b per coordinate
+// start of the preconditioned iteration: r = b, z = p = b / D; chunk partials of r.z and b.b
 __global__ void __launch_bounds__(RED_THREADS)
-k_cg_norms(const double* __restrict__ b, Chunks ck, double* __restrict__ red) {
-    double bb[3] = {0, 0, 0};
+k_cg_start(const double* __restrict__ b, const double* __restrict__ dpert,
+           double* __restrict__ r, double* __restrict__ zv, double* __restrict__ p, Chunks ck,
+           double* __restrict__ red) {
+    double rz[3] = {0, 0, 0}, bb[3] = {0, 0, 0};
     int64_t i0, i1;
     chunk_span(ck, &i0, &i1);
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS)
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += RED_THREADS) {
+        const double inv_d = 1.0 / dpert[i];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) bb[c] += b[3 * i + c] * b[3 * i + c];
+        for (int c = 0; c < 3; ++c) {
+            const int64_t e = 3 * i + c;
+            const double bv = b[e], zz = bv * inv_d;
+            r[e] = bv;
+            zv[e] = zz;
+            p[e] = zz;
+            rz[c] += bv * zz;
+            bb[c] += bv * bv;
+        }
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double v = block_reduce<0>(bb[c]);
+        const double v = block_reduce<0>(rz[c]);
         if (threadIdx.x == 0) *chunk_slot(red, ck, c) = v;
+        const double w = block_reduce<0>(bb[c]);
+        if (threadIdx.x == 0) *chunk_slot(red, ck, 3 + c) = w;
     }
 }
 
-// p = r + beta p (beta = new r.r / r.r), then r.r <- new r.r (one thread, after the pass)
-__global__ void k_cg_dir(double* __restrict__ p, const double* __restrict__ r,
+// p = z + beta p (beta = new r.z / r.z), then r.z <- new r.z (one thread, after the pass)
+__global__ void k_cg_dir(double* __restrict__ p, const double* __restrict__ zv,
                          double* __restrict__ cg, int64_t len) {
     double be[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) be[c] = cg[c] != 0.0 ? cg[6 + c] / cg[c] : 0.0;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
          e += (int64_t)gridDim.x * blockDim.x)
-        p[e] = fma(be[e % 3], p[e], r[e]);
+        p[e] = fma(be[e % 3], p[e], zv[e]);
 }
 
 __global__ void k_cg_roll(double* __restrict__ cg) {
@@ -3186,29 +3208,31 @@ int scvt_laplacian_solve(scvt_ctx* ctx, int64_t n, const int32_t* nbr, const int
     DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
     if (n > ctx->n_max) return fail(ctx, SCVT_ERR_CAPACITY, "n > n_max");
-    if (!ctx->d_cgv) TRY(dalloc(ctx, &ctx->d_cgv, (size_t)9 * ctx->n_max));
+    if (!ctx->d_cgv) TRY(dalloc(ctx, &ctx->d_cgv, (size_t)12 * ctx->n_max));
     if (!ctx->d_cg) TRY(dalloc(ctx, &ctx->d_cg, (size_t)16));
     cudaStream_t s = ctx->stream;
     const int64_t len = 3 * n;
     double* r = ctx->d_cgv;
     double* pv = r + 3 * ctx->n_max;
     double* qv = pv + 3 * ctx->n_max;
+    double* zv = qv + 3 * ctx->n_max;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
     TRY(reset_status(ctx));
     CK(cudaMemsetAsync(x, 0, len * sizeof(double), s));
-    CK(cudaMemcpyAsync(r, b, len * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(pv, b, len * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    ctx->launches += 3;
+    ctx->launches += 1;
+    // Jacobi-preconditioned CG: the x64 / x16 Laplacians have diagonals spanning ~1e7, which
+    // unpreconditioned CG cannot resolve to 1e-14.  cg: [0..2] r.z, [3..5] p.Ap,
+    // [6..8] new r.z, [9..11] new r.r, [12..14] b.b (per coordinate)
     RedOps ro;
-    for (int v = 0; v < 3; ++v) ro.op[v] = 0;
+    for (int v = 0; v < 6; ++v) ro.op[v] = 0;
     CK(cudaMemsetAsync(ctx->d_cg, 0, 16 * sizeof(double), s));
-    k_cg_norms<<<ck.nc, RED_THREADS, 0, s>>>(b, ck, ctx->d_partials);              // b.b
+    k_cg_start<<<ck.nc, RED_THREADS, 0, s>>>(b, dpert, r, zv, pv, ck, ctx->d_partials);
     LAUNCHED();
-    k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg);         // r.r = b.b
+    k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 6, ro, ctx->d_cg + 9);   // r.z, b.b
     LAUNCHED();
-    k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg + 9);
-    LAUNCHED();
+    CK(cudaMemcpyAsync(ctx->d_cg, ctx->d_cg + 9, 3 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    ctx->launches += 1;
     int it = 0;
     constexpr int CHECK = 8;
     for (;;) {
@@ -3218,23 +3242,23 @@ int scvt_laplacian_solve(scvt_ctx* ctx, int64_t n, const int32_t* nbr, const int
             LAUNCHED();
             k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg + 3);   // p.Ap
             LAUNCHED();
-            k_cg_step<<<ck.nc, RED_THREADS, 0, s>>>(x, r, pv, qv, ctx->d_cg, ck, ctx->d_partials,
-                                                     ctx->d_status);
+            k_cg_step<<<ck.nc, RED_THREADS, 0, s>>>(x, r, zv, pv, qv, dpert, ctx->d_cg, ck,
+                                                     ctx->d_partials, ctx->d_status);
             LAUNCHED();
-            k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 3, ro, ctx->d_cg + 6);   // new r.r
+            k_reduce_chunks<<<1, 1024, 0, s>>>(ctx->d_partials, 6, ro, ctx->d_cg + 6);   // r.z, r.r
             LAUNCHED();
-            k_cg_dir<<<RED_BLOCKS, VEC_THREADS, 0, s>>>(pv, r, ctx->d_cg, len);
+            k_cg_dir<<<RED_BLOCKS, VEC_THREADS, 0, s>>>(pv, zv, ctx->d_cg, len);
             LAUNCHED();
             k_cg_roll<<<1, 32, 0, s>>>(ctx->d_cg);
             LAUNCHED();
         }
-        CK(cudaMemcpyAsync(ctx->h_scal, ctx->d_cg, 12 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_scal, ctx->d_cg, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (ctx->h_status[0]) return status_to_code(ctx, ctx->h_status[0]);
         bool done = true;
         for (int c = 0; c < 3; ++c) {
-            const double rr = ctx->h_scal[c], bb = ctx->h_scal[9 + c];
+            const double rr = ctx->h_scal[9 + c], bb = ctx->h_scal[12 + c];
             if (!std::isfinite(rr))
                 return fail(ctx, SCVT_ERR_FACTORIZATION, "Laplacian solve produced non-finite values");
             if (rr > tol * tol * bb) done = false;
