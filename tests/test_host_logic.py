@@ -218,3 +218,105 @@ def test_neighbor_lists_reproduce_reference_covering():
     for l in range(p):
         assert l in two[l]
         assert set(two[l]) == {l}.union(one[l], *(one[m] for m in one[l]))
+
+
+class _FakeOps:
+    """Host stand-in for the device optimizer algebra (Minimizer control-flow tests)."""
+
+    speculate = True
+
+    def __init__(self, qg, dphi0):
+        self.qg, self.dphi0 = qg, dphi0
+        self.cleared = 0
+
+    def vec3(self, z):
+        return z.new_zeros(z.shape)
+
+    positions = vec3
+
+    def scalars(self, z):
+        return z.new_ones(z.shape[0])
+
+    def normalize(self, z):
+        z /= z.norm(dim=1, keepdim=True)
+
+    def history_clear(self):
+        self.cleared += 1
+
+    def gamma(self):
+        return 1.0
+
+    def direction_tangent_async(self, g, diag, gamma, z, q3):
+        q3.copy_(-g)
+
+    def direction_result(self):
+        return self.qg, self.dphi0
+
+    def trial(self, z, q3, alpha, zt, norms):
+        zt.copy_(z + alpha * q3)
+
+    def lloyd(self, first, z_out):
+        z_out.copy_(first / first.norm(dim=1, keepdim=True))
+
+    def push(self, z_old, z_new, g_old, g_new):
+        return True, float((z_new - z_old).abs().max())
+
+
+class _FakeEvaluator:
+    """Evaluations succeed except at the speculative alpha = 1 trial point."""
+
+    def __init__(self, ops):
+        self.ops = ops
+        self.evaluations = 0
+        self.trial_calls = 0
+
+    def _as_device(self, points):
+        import torch
+
+        return torch.as_tensor(np.asarray(points, dtype=float)), True
+
+    def _ensure_ctx(self, n, m=None):
+        return None
+
+    def optimizer_ops(self, ctx, n):
+        return self.ops
+
+    def redecompose(self, points):
+        return None
+
+    def evaluate_device(self, z, q3=None, norms=None):
+        from paper_1709_06924_b200.errors import CapacityError
+        from paper_1709_06924_b200.pipeline import EvalResult
+
+        if q3 is not None:
+            self.trial_calls += 1
+            raise CapacityError("trial point out of capacity")
+        self.evaluations += 1
+        return EvalResult(energy=1.0, grad=0.1 * z, grad_norm=1.0, lloyd_diag=z.new_ones(len(z)),
+                          first=z.clone(), min_diag=1.0)
+
+
+def test_failed_speculative_trial_discarded_on_lloyd_fallback():
+    """q.g < 0 but g.q3 >= 0 -- the reference's line search raises NonDescentError
+    before evaluating anything and takes the Lloyd fallback (optimizer.py:333-349), so an
+    error raised by the speculative alpha = 1 trial must be discarded, not re-raised."""
+    from paper_1709_06924_b200.optimizer import Minimizer
+
+    ops = _FakeOps(qg=-1.0, dphi0=0.5)
+    ev = _FakeEvaluator(ops)
+    st = Minimizer(P.random_sphere_points(12, 0), "lloyd-plbfgs", ev, 5)
+    rec, _, _, _ = st.step()
+    assert ev.trial_calls == 1 and rec.step == 0.0 and rec.fevals == 1
+    assert st.resets == 1 and ev.evaluations == 2       # initial + Lloyd step, trial uncounted
+
+
+def test_failed_speculative_trial_reraised_when_the_reference_evaluates_it():
+    """q.g < 0 and g.q3 < 0: the reference evaluates the alpha = 1 trial first, so its error
+    propagates."""
+    from paper_1709_06924_b200.errors import CapacityError
+    from paper_1709_06924_b200.optimizer import Minimizer
+
+    ev = _FakeEvaluator(_FakeOps(qg=-1.0, dphi0=-0.5))
+    st = Minimizer(P.random_sphere_points(12, 0), "lloyd-plbfgs", ev, 5)
+    with pytest.raises(CapacityError):
+        st.step()
