@@ -166,13 +166,21 @@ SCVT_HD bool cap_face_range(const CapBox& cb, int face, int G, int* iu0, int* iu
 
 // ------------------------------------------------------------------ predicates
 // insphere on the unit sphere == orient3d: for CCW-outward (o, a, b), point c lies inside
-// the circumcircle of (o, a, b) iff det[a-o, b-o, c-o] > 0.  Three tiers:
-//   1. FP64 static filter (decides almost always);
-//   2. double-double evaluation (error ~1e-30 of the permanent);
-//   3. exact ties -> Simulation of Simplicity: the lowest-index point of the four is
-//      pushed radially outward by an infinitesimal, i.e. treated as inside the circle of the
-//      other three.  Every cell that meets the same four points therefore takes the same
-//      decision, which keeps the cycles of a cocircular quad mutually consistent.
+// the circumcircle of (o, a, b) iff D = det[a-o, b-o, c-o] > 0.  Three tiers:
+//   0. FP64 static filter (decides almost always: seeded inputs never leave it);
+//   1. exact sign of D by floating-point expansion arithmetic (Shewchuk's two-sum /
+//      two-product / zero-eliminating expansion sums; every product of three input doubles is
+//      a 4-term expansion, D a sum of at most 96 of them, nothing rounded);
+//   2. D == 0 exactly (cocircular quad) -> Simulation of Simplicity: every point is pushed
+//      radially outward by an infinitesimal, larger for lower indices (eps_0 >> eps_1 >> ...).
+//      D is affine in each point, so the perturbed sign is the sign of the first non-zero
+//      first-order term E_p = dD/d(eps_p) in index order, each evaluated exactly; when all
+//      vanish (four points on a great circle) the tie is +1.  The perturbed set is in general
+//      position, so all decisions are consistent: every cell that meets the same four points
+//      takes the same decision.
+// With T1 = [a,b,c], T2 = [o,b,c], T3 = [a,o,c], T4 = [a,b,o] ([p,q,r] = p.(q x r)):
+//   D = T1 - T2 - T3 - T4,  E_a = T1 - T3 - T4,  E_b = T1 - T2 - T4,  E_c = T1 - T2 - T3,
+//   E_o = -(T2 + T3 + T4)   (o = the origin, index < 0, is never perturbed).
 struct DD { double hi, lo; };
 
 SCVT_HD DD dd_two_sum(double a, double b) {
@@ -186,38 +194,146 @@ SCVT_HD DD dd_two_prod(double a, double b) {
     DD r; r.hi = p; r.lo = fma(a, b, -p);
     return r;
 }
-SCVT_HD DD dd_norm(double hi, double lo) {
-    double s = hi + lo;
-    DD r; r.hi = s; r.lo = lo - (s - hi);
-    return r;
-}
-SCVT_HD DD dd_add(DD a, DD b) {
-    DD s = dd_two_sum(a.hi, b.hi);
-    DD t = dd_two_sum(a.lo, b.lo);
-    double lo = s.lo + t.hi;
-    DD u = dd_norm(s.hi, lo);
-    return dd_norm(u.hi, u.lo + t.lo);
-}
-SCVT_HD DD dd_neg(DD a) { a.hi = -a.hi; a.lo = -a.lo; return a; }
-SCVT_HD DD dd_mul(DD a, DD b) {
-    DD p = dd_two_prod(a.hi, b.hi);
-    double lo = p.lo + (a.hi * b.lo + a.lo * b.hi);
-    return dd_norm(p.hi, lo);
-}
-SCVT_HD DD dd_diff(double a, double b) { return dd_two_sum(a, -b); }
 
-// det[a-o, b-o, c-o] in double-double; *perm gets the permanent (magnitude scale)
-SCVT_HD DD orient_dd(V3 o, V3 a, V3 b, V3 c, double* perm) {
-    DD ax = dd_diff(a.x, o.x), ay = dd_diff(a.y, o.y), az = dd_diff(a.z, o.z);
-    DD bx = dd_diff(b.x, o.x), by = dd_diff(b.y, o.y), bz = dd_diff(b.z, o.z);
-    DD cx = dd_diff(c.x, o.x), cy = dd_diff(c.y, o.y), cz = dd_diff(c.z, o.z);
-    DD m1 = dd_add(dd_mul(by, cz), dd_neg(dd_mul(bz, cy)));
-    DD m2 = dd_add(dd_mul(bz, cx), dd_neg(dd_mul(bx, cz)));
-    DD m3 = dd_add(dd_mul(bx, cy), dd_neg(dd_mul(by, cx)));
-    *perm = fabs(ax.hi) * (fabs(by.hi * cz.hi) + fabs(bz.hi * cy.hi)) +
-            fabs(ay.hi) * (fabs(bz.hi * cx.hi) + fabs(bx.hi * cz.hi)) +
-            fabs(az.hi) * (fabs(bx.hi * cy.hi) + fabs(by.hi * cx.hi));
-    return dd_add(dd_add(dd_mul(ax, m1), dd_mul(ay, m2)), dd_mul(az, m3));
+// h = e + f for nonoverlapping expansions in increasing magnitude (fast_expansion_sum with
+// zero elimination); returns the length of h (<= elen + flen)
+SCVT_HD int exp_sum(int elen, const double* e, int flen, const double* f, double* h) {
+    double q, qn, hh;
+    int ei = 0, fi = 0, hi = 0;
+    double en = e[0], fn = f[0];
+    if ((fn > en) == (fn > -en)) { q = en; ++ei; }
+    else { q = fn; ++fi; }
+    if (ei < elen && fi < flen) {
+        en = e[ei]; fn = f[fi];
+        if ((fn > en) == (fn > -en)) {          // fast two-sum of en and q
+            qn = en + q; hh = q - (qn - en); ++ei;
+        } else {
+            qn = fn + q; hh = q - (qn - fn); ++fi;
+        }
+        q = qn;
+        if (hh != 0.0) h[hi++] = hh;
+        while (ei < elen && fi < flen) {
+            en = e[ei]; fn = f[fi];
+            DD t;
+            if ((fn > en) == (fn > -en)) { t = dd_two_sum(q, en); ++ei; }
+            else { t = dd_two_sum(q, fn); ++fi; }
+            q = t.hi;
+            if (t.lo != 0.0) h[hi++] = t.lo;
+        }
+    }
+    while (ei < elen) {
+        DD t = dd_two_sum(q, e[ei++]);
+        q = t.hi;
+        if (t.lo != 0.0) h[hi++] = t.lo;
+    }
+    while (fi < flen) {
+        DD t = dd_two_sum(q, f[fi++]);
+        q = t.hi;
+        if (t.lo != 0.0) h[hi++] = t.lo;
+    }
+    if (q != 0.0 || hi == 0) h[hi++] = q;
+    return hi;
+}
+
+// h = b * e (scale_expansion with zero elimination); returns the length (<= 2 elen)
+SCVT_HD int exp_scale(int elen, const double* e, double b, double* h) {
+    DD p = dd_two_prod(e[0], b);
+    double q = p.hi;
+    int hi = 0;
+    if (p.lo != 0.0) h[hi++] = p.lo;
+    for (int k = 1; k < elen; ++k) {
+        DD pk = dd_two_prod(e[k], b);
+        DD s = dd_two_sum(q, pk.lo);
+        if (s.lo != 0.0) h[hi++] = s.lo;
+        DD t = dd_two_sum(pk.hi, s.hi);       // |pk.hi| >= |s.hi|: exact either way
+        if (t.lo != 0.0) h[hi++] = t.lo;
+        q = t.hi;
+    }
+    if (q != 0.0 || hi == 0) h[hi++] = q;
+    return hi;
+}
+
+SCVT_HD double exp_sign(int len, const double* e) {
+    for (int k = len - 1; k >= 0; --k)
+        if (e[k] != 0.0) return e[k];
+    return 0.0;
+}
+
+// exact [p, q, r] = p.(q x r) as an expansion (<= 24 terms)
+SCVT_HD int exp_det3(V3 p, V3 q, V3 r, double* out) {
+    const double px[3] = {p.x, p.y, p.z}, qx[3] = {q.x, q.y, q.z}, rx[3] = {r.x, r.y, r.z};
+    const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 2, 0}, {1, 0, 2}, {2, 0, 1}, {2, 1, 0}};
+    const double sg[6] = {1, -1, 1, -1, 1, -1};
+    double acc[24], tmp[24];
+    int n = 0;
+    for (int t = 0; t < 6; ++t) {
+        DD qr = dd_two_prod(qx[perm[t][1]], rx[perm[t][2]]);
+        const double e2[2] = {qr.lo, qr.hi};
+        double term[4];
+        int tl = e2[0] != 0.0 ? exp_scale(2, e2, sg[t] * px[perm[t][0]], term)
+                              : exp_scale(1, e2 + 1, sg[t] * px[perm[t][0]], term);
+        if (n == 0) {
+            for (int k = 0; k < tl; ++k) acc[k] = term[k];
+            n = tl;
+        } else {
+            n = exp_sum(n, acc, tl, term, tmp);
+            for (int k = 0; k < n; ++k) acc[k] = tmp[k];
+        }
+    }
+    for (int k = 0; k < n; ++k) out[k] = acc[k];
+    return n;
+}
+
+// sign of s1 * A + s2 * B + s3 * C + s4 * D over exact expansions (signs +-1 or 0)
+SCVT_HD int exp_combine_sign(const double* const* x, const int* len, const double* sg) {
+    double acc[96], tmp[96], neg[24];
+    int n = 0;
+    for (int t = 0; t < 4; ++t) {
+        if (sg[t] == 0.0) continue;
+        for (int k = 0; k < len[t]; ++k) neg[k] = sg[t] * x[t][k];
+        if (n == 0) {
+            for (int k = 0; k < len[t]; ++k) acc[k] = neg[k];
+            n = len[t];
+        } else {
+            n = exp_sum(n, acc, len[t], neg, tmp);
+            for (int k = 0; k < n; ++k) acc[k] = tmp[k];
+        }
+    }
+    const double v = n ? exp_sign(n, acc) : 0.0;
+    return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0);
+}
+
+// tiers 1-2.  io < 0 marks o as the (unperturbed) origin.
+// inline: a call site in the certificate / cell kernels costs them ~15 % through the call
+// ABI's register constraints (k_verify 282 vs 211 us per c4 iteration); the expansion
+// buffers live in local memory and are touched only on this path
+SCVT_HD int orient_exact_sos(V3 o, V3 a, V3 b, V3 c, int io, int ia, int ib, int ic, int* tier) {
+    double t1[24], t2[24], t3[24], t4[24];
+    const int l1 = exp_det3(a, b, c, t1), l2 = exp_det3(o, b, c, t2);
+    const int l3 = exp_det3(a, o, c, t3), l4 = exp_det3(a, b, o, t4);
+    const double* x[4] = {t1, t2, t3, t4};
+    const int len[4] = {l1, l2, l3, l4};
+    const double sd[4] = {1, -1, -1, -1};
+    const int s = exp_combine_sign(x, len, sd);
+    if (s) { *tier = 1; return s; }
+    *tier = 2;
+    // E_p for the points in increasing index order (the origin is never perturbed)
+    const int idx[4] = {io, ia, ib, ic};
+    const double se[4][4] = {{0, -1, -1, -1},    // E_o
+                             {1, 0, -1, -1},     // E_a
+                             {1, -1, 0, -1},     // E_b
+                             {1, -1, -1, 0}};    // E_c
+    bool used[4] = {false, false, false, false};
+    for (int step = 0; step < 4; ++step) {
+        int w = -1;
+        for (int k = 0; k < 4; ++k)
+            if (!used[k] && idx[k] >= 0 && (w < 0 || idx[k] < idx[w])) w = k;
+        if (w < 0) break;
+        used[w] = true;
+        const int e = exp_combine_sign(x, len, se[w]);
+        if (e) return e;
+    }
+    return 1;
 }
 
 // FP64 value + static filter; returns sign or 0 when undecided
@@ -236,40 +352,21 @@ SCVT_HD int orient_filter(V3 o, V3 a, V3 b, V3 c) {
     return 0;
 }
 
-// Robust sign of det[a-o, b-o, c-o] with SoS tie-breaking; *tier = 0/1/2 (filter/dd/sos)
+// Robust sign of det[a-o, b-o, c-o] with SoS tie-breaking; *tier = 0/1/2 (filter/exact/sos)
 SCVT_HD int orient_robust(V3 o, V3 a, V3 b, V3 c, int io, int ia, int ib, int ic, int* tier) {
     int s = orient_filter(o, a, b, c);
     if (s) { *tier = 0; return s; }
-    double perm;
-    DD d = orient_dd(o, a, b, c, &perm);
-    double v = d.hi + d.lo;
-    if (fabs(v) > 1e-28 * perm) { *tier = 1; return v > 0 ? 1 : -1; }
-    *tier = 2;
-    // push the lowest-index point radially outward (D is affine in each point)
-    const double f = 1.0 + 9.5367431640625e-07;   // 1 + 2^-20
-    int lo = io, which = 0;
-    if (ia < lo) { lo = ia; which = 1; }
-    if (ib < lo) { lo = ib; which = 2; }
-    if (ic < lo) { lo = ic; which = 3; }
-    if (which == 0) o = mul(o, f);
-    else if (which == 1) a = mul(a, f);
-    else if (which == 2) b = mul(b, f);
-    else c = mul(c, f);
-    d = orient_dd(o, a, b, c, &perm);
-    v = d.hi + d.lo;
-    return v > 0 ? 1 : (v < 0 ? -1 : 1);
+    return orient_exact_sos(o, a, b, c, io, ia, ib, ic, tier);
 }
 
-// Legacy interface for the verification pass: sign with an "ambiguous" flag when the FP64
-// filter cannot decide (such edges are reported as flagged cocircular candidates).
+// Sign without tie-breaking (0 for an exact tie) and whether the FP64 filter was undecided.
 SCVT_HD int insphere_sign(V3 o, V3 a, V3 b, V3 c, bool* ambiguous) {
     int s = orient_filter(o, a, b, c);
     *ambiguous = s == 0;
     if (s) return s;
-    double perm;
-    DD d = orient_dd(o, a, b, c, &perm);
-    double v = d.hi + d.lo;
-    return v > 0 ? 1 : (v < 0 ? -1 : 0);
+    int tier;
+    s = orient_exact_sos(o, a, b, c, 0, 1, 2, 3, &tier);
+    return tier == 2 ? 0 : s;
 }
 
 // ------------------------------------------------------------------ Voronoi cell clipping

@@ -2473,6 +2473,15 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
             return bail(fail(ctx, SCVT_ERR_CUDA, "cudaSetDevice(%d): %s", device,
                              cudaGetErrorString(e)));
     }
+    {
+        // the exact predicate's expansion buffers give the triangulation kernels a ~3 KB
+        // stack frame; reserve it once (otherwise the driver grows and shrinks the local
+        // memory pool around every launch that needs it)
+        size_t stack = 0;
+        if (cudaDeviceGetLimit(&stack, cudaLimitStackSize) == cudaSuccess && stack < 4096)
+            cudaDeviceSetLimit(cudaLimitStackSize, 4096);
+        cudaGetLastError();
+    }
     DensityParams& dp = ctx->dp;
     dp.kind = cfg->density_kind;
     dp.gamma = cfg->gamma; dp.beta = cfg->beta; dp.alpha = cfg->alpha;

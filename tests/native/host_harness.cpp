@@ -56,6 +56,19 @@ extern "C" int harness_insphere(const double* o, const double* a, const double* 
     return s;
 }
 
+// exact orient3d with symbolic perturbation (orient_robust): sign, *tier = 0/1/2
+extern "C" int harness_orient(const double* o, const double* a, const double* b, const double* c,
+                              int io, int ia, int ib, int ic, int* tier) {
+    return orient_robust(load3(o, 0), load3(a, 0), load3(b, 0), load3(c, 0), io, ia, ib, ic, tier);
+}
+
+// the exact tiers alone (skipping the FP64 filter)
+extern "C" int harness_orient_exact(const double* o, const double* a, const double* b,
+                                    const double* c, int io, int ia, int ib, int ic, int* tier) {
+    return orient_exact_sos(load3(o, 0), load3(a, 0), load3(b, 0), load3(c, 0), io, ia, ib, ic,
+                            tier);
+}
+
 template <int K>
 static void quad_all(const double* z, int n, const int* nbr, const int* deg, const double* l1,
                      const double* l2, const double* w, int nq, const DensityParams& dp, int sphere,

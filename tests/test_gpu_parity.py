@@ -860,3 +860,50 @@ def test_bench_multi_rank_functional():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["roofline"]["avg_launch_ms"] > 0
+
+
+def _exact_local_delaunay_violations(z, tri):
+    """Brute-force certificate in exact rational arithmetic (delaunay.py:117-130, 305-313
+    without the floating-point margin): for every interior edge (a, b) with opposite vertices
+    c (in triangle a, b, c) and d, the sign of det[b-a, c-a, d-a] must not say "d inside the
+    circumcircle of (a, b, c)" (ties, D = 0, are allowed: any triangulation of a cocircular
+    quad is Delaunay).  Returns the number of violating edges."""
+    from fractions import Fraction as F
+
+    zf = [[F(float(v)) for v in p] for p in z]
+    opp = {}
+    for t in tri:
+        for k in range(3):
+            a, b, c = int(t[k]), int(t[(k + 1) % 3]), int(t[(k + 2) % 3])
+            opp[(a, b)] = c
+    bad = 0
+    for (a, b), c in opp.items():
+        d = opp.get((b, a))
+        if d is None or a > b:
+            continue
+        pa, pb, pc, pd = zf[a], zf[b], zf[c], zf[d]
+        u = [pb[k] - pa[k] for k in range(3)]
+        v = [pc[k] - pa[k] for k in range(3)]
+        w = [pd[k] - pa[k] for k in range(3)]
+        det = (u[0] * (v[1] * w[2] - v[2] * w[1]) + u[1] * (v[2] * w[0] - v[0] * w[2])
+               + u[2] * (v[0] * w[1] - v[1] * w[0]))
+        bad += det > 0
+    return bad
+
+
+@pytest.mark.parametrize("scale", [0.0, 1.0, 2.0 ** -20, 2.0 ** -40])
+def test_near_cocircular_grid_exact_delaunay(scale):
+    """Lat-lon grids whose trapezoid quads are cocircular exactly (scale 0) or up to relative
+    margins of ~1e-16 ... 1e-28 (every z coordinate moved by scale x a few ulp): the GPU
+    triangulation must be exactly (SoS-)Delaunay, certified in rational arithmetic, with the
+    Euler counts of a closed triangulation."""
+    rng = np.random.default_rng(int(scale * 1e6) + 1)
+    z = _latlon(24, 20, False)
+    if scale:
+        dz = rng.integers(-3, 4, len(z)) * np.spacing(np.abs(z[:, 2])) * scale
+        z = z.copy()
+        z[:, 2] = z[:, 2] + dz
+    with _ev("const", "4pt", 0) as ev:
+        t = ev.triangulation(z).triangles
+    assert len(t) == 2 * len(z) - 4
+    assert _exact_local_delaunay_violations(z, t) == 0

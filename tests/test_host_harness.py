@@ -206,3 +206,102 @@ def test_sym7_fit_path_vs_golden(h, gold, cfg, which):
     assert rel(out[:, 0], g[pref + "mass"]) <= 1e-13
     assert rel(out[:, 1:4], g[pref + "first"]) <= 1e-13
     assert abs(out[:, 4].sum() - g[pref + "energy"]) <= 1e-13 * g[pref + "energy"]
+
+
+# ------------------------------------------------------------ exact predicate
+def _frac_det(o, a, b, c):
+    from fractions import Fraction as F
+
+    o, a, b, c = ([F(float(v)) for v in p] for p in (o, a, b, c))
+    u = [a[k] - o[k] for k in range(3)]
+    v = [b[k] - o[k] for k in range(3)]
+    w = [c[k] - o[k] for k in range(3)]
+    return (u[0] * (v[1] * w[2] - v[2] * w[1]) + u[1] * (v[2] * w[0] - v[0] * w[2])
+            + u[2] * (v[0] * w[1] - v[1] * w[0]))
+
+
+def _frac_sign(x):
+    return (x > 0) - (x < 0)
+
+
+def _sos_truth(pts, idx):
+    """Sign under the radial symbolic perturbation, in exact rationals: D, then the
+    first-order terms of the points in increasing index order (origin: index < 0, fixed)."""
+    from fractions import Fraction as F
+
+    o, a, b, c = pts
+    d = _frac_det(o, a, b, c)
+    if d != 0:
+        return _frac_sign(d), 1
+
+    def det3(p, q, r):
+        p, q, r = ([F(float(v)) for v in x] for x in (p, q, r))
+        return (p[0] * (q[1] * r[2] - q[2] * r[1]) + p[1] * (q[2] * r[0] - q[0] * r[2])
+                + p[2] * (q[0] * r[1] - q[1] * r[0]))
+
+    t1, t2, t3, t4 = det3(a, b, c), det3(o, b, c), det3(a, o, c), det3(a, b, o)
+    e = [-(t2 + t3 + t4), t1 - t3 - t4, t1 - t2 - t4, t1 - t2 - t3]
+    for k in sorted((k for k in range(4) if idx[k] >= 0), key=lambda k: idx[k]):
+        if e[k] != 0:
+            return _frac_sign(e[k]), 2
+    return 1, 2
+
+
+def _orient(h, pts, idx, exact_only=False):
+    tier = ctypes.c_int(-1)
+    fn = h.harness_orient_exact if exact_only else h.harness_orient
+    s = fn(*(dp(np.ascontiguousarray(p, dtype=float)) for p in pts), *idx, ctypes.byref(tier))
+    return s, tier.value
+
+
+def test_exact_orient_on_near_coplanar_quads(h):
+    """Relative margins 1e-20 ... 1e-30 (a point lifted off the plane of three others by a few
+    ulp of its coordinate, or less): the FP64 filter cannot decide; the exact tier must agree
+    with rational arithmetic, sign for sign."""
+    rng = np.random.default_rng(7)
+    checked = 0
+    for trial in range(400):
+        zh = rng.uniform(-0.9, 0.9)
+        r = np.sqrt(1 - zh * zh)
+        ang = rng.uniform(0, 2 * np.pi, 4)
+        pts = [np.array([r * np.cos(t), r * np.sin(t), zh]) for t in ang]
+        k = rng.integers(0, 4)
+        pts[k] = pts[k].copy()
+        pts[k][2] = zh + rng.choice([-1, 1]) * rng.integers(0, 4) * np.spacing(zh) * 2.0 ** -rng.integers(0, 40)
+        idx = [int(x) for x in rng.permutation(4)]
+        truth, ttier = _sos_truth(pts, idx)
+        s, tier = _orient(h, pts, idx)
+        assert s == truth, (trial, pts, idx, s, truth)
+        se, te = _orient(h, pts, idx, exact_only=True)
+        assert se == truth and te == ttier
+        checked += tier > 0
+    assert checked > 300       # most cases reached the exact tiers
+
+
+def test_sos_consistency_on_exactly_coplanar_quads(h):
+    """Exact ties (four points on one circle of latitude: coplanar, D = 0 exactly): the
+    symbolic perturbation decides, consistently with the rational first-order terms, and a
+    quad seen from any rotation of its triangle gives the same answer."""
+    rng = np.random.default_rng(11)
+    for trial in range(200):
+        zh = float(rng.choice([0.25, -0.5, 0.125, 0.75]))
+        r = np.sqrt(1 - zh * zh)
+        ang = np.sort(rng.uniform(0, 2 * np.pi, 4))
+        pts = [np.array([r * np.cos(t), r * np.sin(t), zh]) for t in ang]
+        assert _frac_det(*pts) == 0
+        idx = [int(x) for x in rng.choice(1000, 4, replace=False)]
+        truth, ttier = _sos_truth(pts, idx)
+        s, tier = _orient(h, pts, idx)
+        assert tier == 2 and s == truth and ttier == 2
+        # cyclic relabelling of the triangle (o, a, b) -> (a, b, o) leaves D and the decision
+        p2 = [pts[1], pts[2], pts[0], pts[3]]
+        i2 = [idx[1], idx[2], idx[0], idx[3]]
+        assert _orient(h, p2, i2)[0] == s
+
+
+def test_orientation_against_the_origin_great_circle_tie(h):
+    """o = the origin (index -1, never perturbed): three points on a great circle give
+    D = 0 and every first-order term vanishes -> the documented +1."""
+    pts = [np.zeros(3), np.array([1.0, 0, 0]), np.array([0, 1.0, 0]), np.array([-1.0, 0, 0])]
+    s, tier = _orient(h, pts, [-1, 5, 6, 7])
+    assert s == 1 and tier == 2
