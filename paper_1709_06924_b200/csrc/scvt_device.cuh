@@ -993,6 +993,26 @@ SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, Loca
         for (int j = 0; j < 7; ++j) acc = fma(CHEB_A[m][j], u[j], acc);
         a[m] = acc;
     }
+    // a-posteriori truncation estimate from the Chebyshev tail: the coefficients of a
+    // function analytic on the interval decay geometrically, so with the decay ratio r of
+    // the last coefficients above the rounding floor of the table values (~4e-15 relative)
+    // the omitted a7, a8, ... sum to ~|a_last| r^k / (1 - r).  A patch is accepted only when
+    // that estimate is below the fit tolerance -- in addition to the check points below.
+    {
+        double umin = u[0];
+#pragma unroll
+        for (int j = 1; j < 7; ++j) umin = fmin(umin, u[j]);
+        const double a4 = fabs(a[4]), a5 = fabs(a[5]), a6 = fabs(a[6]);
+        const double noise = 4e-15 * umin, tol = 1.6e-14 * umin;
+        // division-free: with r <= 1/2, 1 / (1 - r) <= 2
+        bool ok = true;
+        if (a6 > noise)                         // a7 ~ a6 r, r = max(a6/a5, a5/a4)
+            ok = a6 <= 0.5 * a5 && a5 <= 0.5 * a4 && 2.0 * a6 * a6 <= tol * a5 &&
+                 2.0 * a6 * a5 <= tol * a4;
+        else if (a5 > noise)                    // a7 ~ a5 r^2, r = a5/a4
+            ok = a5 <= 0.5 * a4 && 2.0 * a5 * a5 * a5 <= tol * a4 * a4;
+        if (!ok) return false;
+    }
     double b[7];   // monomials in v = (s - sc) / hw
     b[0] = a[0] - a[2] + a[4] - a[6];
     b[1] = a[1] - 3.0 * a[3] + 5.0 * a[5];
