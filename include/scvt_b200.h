@@ -269,6 +269,20 @@ int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* cent
                    const uint32_t* adjacency, int32_t* arithmetic, int32_t fresh,
                    int32_t* class_host);
 
+/* region-path fallback decision (MeshEvaluator.fallbacks, pipeline.py:127-128, 244-259),
+ * right after the evaluation of these n points: *fail_host = 0 when the reference's region
+ * path would succeed for the covering (centers (p,3), one-level `adjacency` bitmap as above,
+ * eps_proj of the stereographic projection), else a bit set: 1 a Delaunay triangle at an
+ * owned generator is not kept by select_region_triangles (CoverageError, truncated fan),
+ * 2 a member near its region's projection antipode (AntipodeError), 4 a region with owned
+ * points has < 3 members (InsufficientPointsError); region_fail_host (p host ints, may be
+ * NULL) gets the bits of every region (0 for regions without owned points, which the
+ * reference does not triangulate).  p <= 128.  Moments do not depend on it (the
+ * reference falls back to the global path, which this library always evaluates). */
+int scvt_region_cover(scvt_ctx* ctx, const double* z, int64_t n, const double* centers,
+                      int32_t p, const uint32_t* adjacency, double eps_proj, int32_t* fail_host,
+                      int32_t* region_fail_host);   /* optional: the bits per region (p) */
+
 /* graph Laplacian preconditioner (methods laplacian-a6 / laplacian-m2) ---------------------
  * LaplacianPreconditioner (cvt_core.py:192-240): a_ij = -int_{T_ij u T_ji} rho over the fan
  * sub-triangles next to edge ij, zero row sums.  scvt_laplacian, right after the evaluation of

@@ -104,6 +104,8 @@ SIGNATURES = {
     "scvt_reduce_chunks": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _c_dbl_p]),
     "scvt_migration": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int32, _vp, _vp,
                                       ctypes.c_int32, _c_i32_p]),
+    "scvt_region_cover": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int32, _vp,
+                                         ctypes.c_double, _c_i32_p, _c_i32_p]),
     "scvt_laplacian": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
     "scvt_laplacian_solve": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp,
                                             ctypes.c_double, ctypes.c_int32, _c_i32_p]),

@@ -1435,6 +1435,115 @@ __global__ void k_migration(const double* __restrict__ z, int64_t n,
     atomicMax(cls, near ? 1 : 2);
 }
 
+// ------------------------------------------------------------------ region-path fallback
+// The reference's region path (pipeline.py:62-98, 171-242, 244-259) triangulates every
+// Voronoi-sort region of a covering separately and falls back to the global path -- counting
+// the evaluation in MeshEvaluator.fallbacks -- when a region fails.  Its moments equal the
+// global path's, so only that decision is reproduced here, from the global cycles: a region
+// fails when it holds an owned point but < 3 members (InsufficientPointsError,
+// pipeline.py:188-191), when a member sits within eps of the antipode of its contact point
+// (AntipodeError, geometry.py:76-79), or when a Delaunay triangle at an owned generator is not
+// kept by select_region_triangles (delaunay.py:252-273: a vertex outside the region, or
+// d_out - d_in < 2 r), which truncates that generator's fan (CoverageError, validate_fans
+// delaunay.py:410-426).  Arithmetic as the reference's NumPy: no FMA contraction, canonical
+// vertex order for the circumcircle (delaunay.py:150-169 with the cap's `avoid`).
+__device__ __forceinline__ bool cov_adj(const uint32_t* adj, int words, int a, int b) {
+    return (adj[(int64_t)a * words + (b >> 5)] >> (b & 31)) & 1u;
+}
+
+__global__ void k_geo_cells(const double* __restrict__ z, int64_t n,
+                            const double* __restrict__ centers, int p, int* __restrict__ geo,
+                            int* __restrict__ hist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x = z[3 * i], y = z[3 * i + 1], w = z[3 * i + 2];
+    double best = -INFINITY;
+    int arg = 0;
+    for (int c = 0; c < p; ++c) {
+        const double sc = x * __ldg(centers + 3 * c) + y * __ldg(centers + 3 * c + 1) +
+                          w * __ldg(centers + 3 * c + 2);
+        if (sc > best) { best = sc; arg = c; }
+    }
+    geo[i] = arg;
+    atomicAdd(&hist[arg], 1);
+}
+
+__device__ __forceinline__ double np_dot3(V3 a, V3 b) {     // ((ax bx + ay by) + az bz)
+    return __dadd_rn(__dadd_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dmul_rn(a.z, b.z));
+}
+
+__device__ __forceinline__ V3 np_cross(V3 a, V3 b) {
+    return v3(__dsub_rn(__dmul_rn(a.y, b.z), __dmul_rn(a.z, b.y)),
+              __dsub_rn(__dmul_rn(a.z, b.x), __dmul_rn(a.x, b.z)),
+              __dsub_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+
+__device__ __forceinline__ double np_geodesic(V3 a, V3 b) {   // geometry.py:29-40
+    const V3 c = np_cross(a, b);
+    return atan2(sqrt(np_dot3(c, c)), np_dot3(a, b));
+}
+
+// fail[l] bits of region l: 1 coverage (truncated fan), 2 antipode (4, too few members, is
+// added on the host)
+__global__ void k_region_cover(const double* __restrict__ z, int64_t n, const int* __restrict__ nbr,
+                               const int* __restrict__ deg, const double* __restrict__ centers,
+                               int p, const uint32_t* __restrict__ adj,
+                               const int* __restrict__ geo, const int* __restrict__ hist,
+                               double eps_proj, int* __restrict__ fail) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int words = (p + 31) / 32;
+    const int g = geo[i];
+    const V3 zi = load3(z, i);
+    // antipode of the contact point of every region that has i as a member and owns points
+    for (int l = 0; l < p; ++l) {
+        if (hist[l] == 0 || !(l == g || cov_adj(adj, words, l, g))) continue;
+        const V3 t = load3(centers, l);
+        const double den = __dadd_rn(__dadd_rn(__dmul_rn(t.x, __dadd_rn(zi.x, t.x)),
+                                               __dmul_rn(t.y, __dadd_rn(zi.y, t.y))),
+                                     __dmul_rn(t.z, __dadd_rn(zi.z, t.z)));
+        if (den <= eps_proj) atomicOr(&fail[l], 2);
+    }
+    // the triangles at the owned generator i (region g) must all be kept
+    const int d = deg[i];
+    const int* row = nbr + i * MAXDEG;
+    const V3 tc = load3(centers, g);
+    for (int k = 0; k < d; ++k) {
+        const int a = row[k], b = row[k + 1 == d ? 0 : k + 1];
+        const int ga = geo[a], gb = geo[b];
+        if (!(ga == g || cov_adj(adj, words, g, ga)) || !(gb == g || cov_adj(adj, words, g, gb))) {
+            atomicOr(&fail[g], 1);
+            return;
+        }
+        // canonical rotation (min id first, orientation kept)
+        int v0 = (int)i, v1 = a, v2 = b;
+        if (a < v0 && a < b) { v0 = a; v1 = b; v2 = (int)i; }
+        else if (b < v0 && b < a) { v0 = b; v1 = (int)i; v2 = a; }
+        const V3 p0 = load3(z, v0), p1 = load3(z, v1), p2 = load3(z, v2);
+        const V3 e1 = v3(__dsub_rn(p1.x, p0.x), __dsub_rn(p1.y, p0.y), __dsub_rn(p1.z, p0.z));
+        const V3 e2 = v3(__dsub_rn(p2.x, p0.x), __dsub_rn(p2.y, p0.y), __dsub_rn(p2.z, p0.z));
+        const V3 nv = np_cross(e1, e2);
+        const double nn = sqrt(np_dot3(nv, nv));
+        V3 c = v3(__ddiv_rn(nv.x, nn), __ddiv_rn(nv.y, nn), __ddiv_rn(nv.z, nn));
+        double r = np_geodesic(c, p0);
+        if (np_geodesic(c, v3(-tc.x, -tc.y, -tc.z)) < r) {    // the cap's `avoid`
+            c = v3(-c.x, -c.y, -c.z);
+            r = M_PI - r;
+        }
+        double din = INFINITY, dout = INFINITY;
+        for (int l = 0; l < p; ++l) {
+            const double cs = fmin(fmax(np_dot3(c, load3(centers, l)), -1.0), 1.0);
+            const double dl = acos(cs);
+            if (l == g || cov_adj(adj, words, g, l)) din = fmin(din, dl);
+            else dout = fmin(dout, dl);
+        }
+        if (dout != INFINITY && !(__dsub_rn(dout, din) >= __dmul_rn(2.0, r))) {
+            atomicOr(&fail[g], 1);
+            return;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ canonical triangles
 __global__ void k_tri_count(int n, const int* __restrict__ nbr, const int* __restrict__ deg,
                             int* __restrict__ cnt) {
@@ -3180,6 +3289,51 @@ int scvt_migration(scvt_ctx* ctx, const double* z, int64_t n, const double* cent
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_mig, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     *class_host = ctx->h_small[0];
+    return SCVT_OK;
+}
+
+int scvt_region_cover(scvt_ctx* ctx, const double* z, int64_t n, const double* centers,
+                      int32_t p, const uint32_t* adjacency, double eps_proj, int32_t* fail_host,
+                      int32_t* region_fail_host) {
+    DeviceGuard dg_(ctx);
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (p < 1 || p > MAX_SHARDS / 2)
+        return fail(ctx, SCVT_ERR_CONFIG, "covering with %d cells (1..%d)", p, MAX_SHARDS / 2);
+    if (ctx->cycles_n != n)
+        return fail(ctx, SCVT_ERR_CONFIG, "scvt_region_cover needs the evaluation of these %lld points",
+                    (long long)n);
+    cudaStream_t s = ctx->stream;
+    // geo cells in d_list (n ints); per-cell counts and per-region flags in d_counts
+    int* geo = ctx->d_list;
+    int* hist = ctx->d_counts;
+    int* rfail = ctx->d_counts + p;
+    CK(cudaMemsetAsync(hist, 0, 2 * (size_t)p * sizeof(int), s));
+    k_geo_cells<<<blocks_for(n, 256), 256, 0, s>>>(z, n, centers, p, geo, hist);
+    LAUNCHED();
+    k_region_cover<<<blocks_for(n, 128), 128, 0, s>>>(z, n, ctx->d_nbr, ctx->d_deg, centers, p,
+                                                     adjacency, geo, hist, eps_proj, rfail);
+    LAUNCHED();
+    CK(cudaMemcpyAsync(ctx->h_counts, hist, 2 * (size_t)p * sizeof(int), cudaMemcpyDeviceToHost, s));
+    std::vector<uint32_t> adj((size_t)p * ((p + 31) / 32));
+    CK(cudaMemcpyAsync(adj.data(), adjacency, adj.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int words = (p + 31) / 32;
+    int f = 0;
+    for (int l = 0; l < p; ++l) {
+        int rf = ctx->h_counts[p + l];
+        if (ctx->h_counts[l] > 0) {           // regions holding owned points: >= 3 members
+            int64_t members = ctx->h_counts[l];
+            for (int k = 0; k < p; ++k)
+                if (k != l && ((adj[(size_t)l * words + (k >> 5)] >> (k & 31)) & 1u))
+                    members += ctx->h_counts[k];
+            if (members < 3) rf |= 4;
+        } else {
+            rf = 0;                            // no payload: the reference skips the region
+        }
+        if (region_fail_host) region_fail_host[l] = rf;
+        f |= rf;
+    }
+    *fail_host = f;
     return SCVT_OK;
 }
 

@@ -446,7 +446,7 @@ class Minimizer:
                 elif r1 is not None:
                     # history reset (q.g >= 0) or Lloyd fallback (g.q3 >= 0, wolfe_line_search
                     # raises before any evaluation): the trial never happened in the reference
-                    ev.evaluations -= 1
+                    ev.discard_evaluation()
             else:
                 qg, dphi0 = direction()
             if qg >= 0.0:

@@ -610,6 +610,7 @@ class ShardedMeshEvaluator(MeshEvaluator):
                     z, self.world, res_all, self.rank, self.world, self._red, self._sum, q3,
                     norms))
         r.migration = self._migration(z)
+        self._region_fallback(z)      # replicated: every rank holds every certified cycle
         self.evaluations += 1
         return r
 

@@ -284,6 +284,43 @@ class MeshEvaluator:
                                  ctypes.byref(cls), what="migration")
         return MIGRATION_CLASSES[cls.value]
 
+    _FALLBACK_REASONS = {1: "truncated Voronoi fans (CoverageError)",
+                         2: "point near the projection antipode (AntipodeError)",
+                         4: "region with fewer than 3 members (InsufficientPointsError)"}
+
+    def region_failures(self, z) -> np.ndarray:
+        """Per covering cell, the reason bits (1 CoverageError, 2 AntipodeError,
+        4 InsufficientPointsError) for which the reference's region task of that cell would
+        fail at these (just evaluated) points; 0 where it succeeds or has no owned point."""
+        centers, adj, p = self._cov_dev
+        f = ctypes.c_int32()
+        per = (ctypes.c_int32 * p)()
+        self._ctx.call("scvt_region_cover", _lib.dptr(z), z.shape[0], _lib.dptr(centers), p,
+                       _lib.dptr(adj), float(self.eps_proj), ctypes.byref(f), per,
+                       what="region_cover")
+        return np.frombuffer(per, dtype=np.int32).copy()
+
+    def _region_fallback(self, z):
+        """With a covering: whether the reference's region path would have failed for these
+        points and fallen back to the global path (pipeline.py:244-259), which counts the
+        evaluation in `fallbacks`; the moments are the global path's either way."""
+        self._last_fallback = 0
+        if self.covering is None:
+            return
+        f = ctypes.c_int32(int(np.bitwise_or.reduce(self.region_failures(z))))
+        if f.value:
+            self.fallbacks += 1
+            self._last_fallback = 1
+            why = "; ".join(v for k, v in self._FALLBACK_REASONS.items() if f.value & k)
+            logger.warning("region path failed (%s); global fallback", why)
+
+    def discard_evaluation(self):
+        """Forget the last evaluation (a speculative line-search trial the reference never
+        evaluates): its evaluation and fallback counts."""
+        self.evaluations -= 1
+        self.fallbacks -= getattr(self, "_last_fallback", 0)
+        self._last_fallback = 0
+
     def optimizer_ops(self, ctx, n: int):
         """The optimizer's vector algebra for this evaluator's layout (one GPU: all rows)."""
         from .optimizer import _DeviceOps
@@ -319,11 +356,13 @@ class MeshEvaluator:
                  _lib.dptr(mass), _lib.dptr(diag), _lib.dptr(q3), _lib.dptr(norms), sc,
                  what="evaluate")
         self.evaluations += 1
+        migration = self._migration(z)
+        self._region_fallback(z)
         return EvalResult(energy=float(sc[0]), grad=grad, grad_norm=float(sc[1]),
                           lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]),
                           min_diag=float(sc[3]),
                           dirderiv=float(sc[4]) if q3 is not None else float("nan"),
-                          migration=self._migration(z),
+                          migration=migration,
                           laplacian=(DeviceLaplacian(ctx, n, self.laplacian, z.device)
                                      if self.laplacian is not None else None))
 

@@ -367,6 +367,17 @@ def case_covering():
     cov = partition.bootstrap_partition_cvt(64, seed=0, density=field_for("const"))
     ev = pipeline.MeshEvaluator(field_for("const"), geometry.QUADRATURE_RULES["4pt"], cov,
                                 workers=1, backend="thread")
+    # per evaluation (line-search trials included): did the region path fall back?
+    fb_seq = []
+    orig_eval = ev.evaluate
+
+    def evaluate(points):
+        before = ev.fallbacks
+        r = orig_eval(points)
+        fb_seq.append(ev.fallbacks - before)
+        return r
+
+    ev.evaluate = evaluate
     crit = optimizer.StoppingCriteria(max_iterations=40, movement_tol=1e-300, grad_tol=1e-300,
                                       stall_tol=1e-300)
     mig = []
@@ -381,7 +392,51 @@ def case_covering():
          energy=np.array([r.energy for r in res.records]),
          fevals=np.array([-1 if r.fevals is None else r.fevals for r in res.records]),
          migration=np.array(mig), resets=np.int64(res.resets), final_z=res.points,
-         reason=np.array(res.reason))
+         reason=np.array(res.reason), fallbacks=np.int64(ev.fallbacks),
+         fallback_seq=np.array(fb_seq, dtype=np.int64))
+
+
+def case_region_cover():
+    """Region path (pipeline.py:62-98, 171-242): which Voronoi-sort regions of a covering the
+    reference's `_region_task` fails for (CoverageError 1, AntipodeError 2,
+    InsufficientPointsError 4, CollinearInputError 8), uniform points over bootstrap
+    coverings; the GPU predicts the same per-region outcome from the global cycles."""
+    import warnings
+
+    from scvtmesh import errors, partition
+
+    warnings.simplefilter("ignore")
+    _DEPTH["d"] = 0
+    codes = {errors.CoverageError: 1, errors.AntipodeError: 2,
+             errors.InsufficientPointsError: 4, errors.CollinearInputError: 8}
+    out = {}
+    for ci, (k, p, seed) in enumerate([(2562, 64, 5), (1282, 32, 5), (5122, 64, 5),
+                                        (10242, 64, 5), (642, 64, 2)]):
+        z0 = geometry.random_sphere_points(k, seed)
+        cov = partition.bootstrap_partition_cvt(p, seed=0, density=field_for("const"))
+        ev = pipeline.MeshEvaluator(field_for("const"), geometry.QUADRATURE_RULES["4pt"], cov,
+                                    workers=1, backend="thread")
+        assign = ev._assign(z0)
+        res = np.zeros(p, dtype=np.int64)
+        for l in range(p):
+            owned = np.flatnonzero(assign.geometric == l)
+            if len(owned) == 0:
+                continue
+            try:
+                pl = next(x for x in ev._payloads(z0, assign, False)
+                          if np.array_equal(x["contact"], cov.centers[l]))
+                pipeline._region_task(pl)
+            except tuple(codes) as exc:
+                res[l] = codes[type(exc)]
+        ev.close()
+        one_ptr = np.cumsum([0] + [len(t) for t in cov.one_level])
+        one_idx = np.concatenate([np.asarray(t, dtype=np.int64) for t in cov.one_level])
+        out.update({f"case{ci}_k": np.int64(k), f"case{ci}_seed": np.int64(seed),
+                    f"case{ci}_centers": cov.centers, f"case{ci}_one_ptr": one_ptr,
+                    f"case{ci}_one_idx": one_idx, f"case{ci}_fail": res})
+        print(f"  region cover k={k} p={p}: failing regions {np.flatnonzero(res).tolist()} "
+              f"codes {res[res > 0].tolist()}", flush=True)
+    save("region_cover", **out)
 
 
 def case_laplacian():
@@ -419,6 +474,7 @@ CASES = {
     "traj_fast": case_traj_fast, "traj_slow": case_traj_slow,
     "traj_fallback": case_traj_fallback, "medium_slim": case_medium_slim,
     "run_ladder": case_run_ladder, "covering": case_covering, "laplacian": case_laplacian,
+    "region_cover": case_region_cover,
 }
 
 if __name__ == "__main__":

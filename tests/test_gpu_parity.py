@@ -714,10 +714,33 @@ def test_covering_migration_resets_match_reference(gold):
                          callback=lambda n, z, r: mig.append(r.migration))
     assert mig == [str(m) for m in g["migration"]]
     assert res.resets == int(g["resets"]) > 0
+    assert ev.fallbacks == int(g["fallbacks"])        # every evaluation of this run falls back
     e = np.array([r.energy for r in res.records])
     assert np.max(np.abs(e - g["energy"]) / g["energy"]) <= 1e-10
     assert [r.fevals if r.fevals is not None else -1 for r in res.records] == g["fevals"].tolist()
     assert rel(res.points, g["final_z"]) <= 1e-10
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_region_failures_match_reference_region_tasks(gold, case):
+    """Region-path semantics (delaunay.py:252-292, pipeline.py:62-98):
+    per covering cell, the reference's `_region_task` fails (CoverageError: the interior
+    selection truncates an owned fan) for exactly the regions the GPU predicts from the global
+    cycles, over uniform points and bootstrap coverings."""
+    from paper_1709_06924_b200.partition import Covering
+
+    g = gold("region_cover")
+    c = f"case{case}_"
+    one = tuple(tuple(int(x) for x in g[c + "one_idx"][g[c + "one_ptr"][k]:g[c + "one_ptr"][k + 1]])
+                for k in range(len(g[c + "centers"])))
+    cov = Covering(centers=g[c + "centers"], one_level=one, two_level=())
+    z = P.random_sphere_points(int(g[c + "k"]), int(g[c + "seed"]))
+    with P.MeshEvaluator(P.density_preset("const"), "4pt", cov) as ev:
+        zt = torch.from_numpy(z).cuda()
+        ev.evaluate_device(zt)
+        pred = ev.region_failures(zt)
+        assert ev.fallbacks == int(np.any(g[c + "fail"]))
+    assert pred.tolist() == g[c + "fail"].tolist()
 
 
 def test_bootstrap_partition_cvt_matches_reference(gold):
