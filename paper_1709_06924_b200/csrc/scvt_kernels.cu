@@ -224,54 +224,71 @@ struct FlipQueue {
     int cap;
 };
 
-__global__ void k_verify(const double* __restrict__ z, const int* __restrict__ ids, int p_lo,
-                         int p_hi, const int* __restrict__ list, const int* __restrict__ list_n,
-                         const int* __restrict__ nbr, const int* __restrict__ deg,
-                         uint8_t* __restrict__ amb, int* __restrict__ status,
-                         int* __restrict__ stats, int mode, int* __restrict__ bad,
-                         int* __restrict__ nbad, FlipQueue fq = FlipQueue{nullptr, nullptr, 0},
-                         int list_ids = 0) {
-    // VERIFY_LANES threads per cell, each taking every VERIFY_LANES-th edge of its cycle: the
-    // dependent neighbour-row lookups of different edges run in parallel instead of in one
-    // thread's loop (the pass is memory-latency bound)
-    for (int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;;
-         gidx += (int64_t)gridDim.x * blockDim.x) {
+// Arguments of one certificate pass (k_verify, and the fused flip-round kernel).
+struct VerifyArgs {
+    const double* z;
+    const int* ids;
+    int p_lo, p_hi;
+    const int* list;
+    const int* list_n;
+    const int* nbr;
+    const int* deg;
+    uint8_t* amb;
+    int* status;
+    int* stats;
+    int mode;
+    int* bad;
+    int* nbad;
+    FlipQueue fq;
+    int list_ids;
+};
+
+// one (cell, lane) work item of the certificate; true once past the end of the work.  The
+// cycles, lists and positions were written by earlier launches: read-only-path loads.
+__device__ __forceinline__ bool verify_item(const VerifyArgs& v, int64_t gidx) {
     const int idx = (int)(gidx / VERIFY_LANES), lane = (int)(gidx % VERIFY_LANES);
     int p, i;
-    if (list) {                 // re-certification of a compacted list of sorted slots
-        if (idx >= *list_n) return;
-        if (list_ids) {
-            i = list[idx];
+    if (v.list) {               // re-certification of a compacted list of sorted slots
+        if (idx >= __ldg(v.list_n)) return true;
+        if (v.list_ids) {
+            i = __ldg(v.list + idx);
         } else {
-            p = list[idx];
-            if (p < p_lo || p >= p_hi) continue;   // sharded re-check: owned slots only
-            i = ids[p];
+            p = __ldg(v.list + idx);
+            if (p < v.p_lo || p >= v.p_hi) return false;   // sharded re-check: owned slots only
+            i = __ldg(v.ids + p);
         }
     } else {
-        p = p_lo + idx;
-        if (p >= p_hi) return;
-        i = ids[p];
+        p = v.p_lo + idx;
+        if (p >= v.p_hi) return true;
+        i = __ldg(v.ids + p);
     }
-    int d = deg[i];
-    const int* row = nbr + (int64_t)i * MAXDEG;
+    const int mode = v.mode;
+    const int d = __ldg(v.deg + i);
+    const int* row = v.nbr + (int64_t)i * MAXDEG;
     if (d < 3 || d > MAXDEG) {
-        if (lane == 0) mark_bad(mode > 1 ? 1 : mode, status, ST_INCONSISTENT, bad, nbad, i, -1, -1, -1);
-        continue;
+        if (lane == 0)
+            mark_bad(mode > 1 ? 1 : mode, v.status, ST_INCONSISTENT, v.bad, v.nbad, i, -1, -1, -1);
+        return false;
     }
+    const double* z = v.z;
     V3 zi = load3(z, i);
     int namb = 0;
     for (int t = lane; t < d; t += VERIFY_LANES) {
-        int a = row[t], b = row[t + 1 == d ? 0 : t + 1], c = row[t == 0 ? d - 1 : t - 1];
-        int da = deg[a];
-        const int* ra = nbr + (int64_t)a * MAXDEG;
-        int q = da >= 3 && da <= MAXDEG ? find_in_cycle(ra, da, i) : -1;
-        bool ok = q >= 0 && ra[q == 0 ? da - 1 : q - 1] == b;
-        if (!ok) mark_bad(mode, status, ST_INCONSISTENT, bad, nbad, i, a, b, -1);
+        int a = __ldg(row + t), b = __ldg(row + (t + 1 == d ? 0 : t + 1)),
+            c = __ldg(row + (t == 0 ? d - 1 : t - 1));
+        int da = __ldg(v.deg + a);
+        const int* ra = v.nbr + (int64_t)a * MAXDEG;
+        int q = -1;
+        if (da >= 3 && da <= MAXDEG)
+            for (int k = 0; k < da; ++k)
+                if (__ldg(ra + k) == i) { q = k; break; }
+        bool ok = q >= 0 && __ldg(ra + (q == 0 ? da - 1 : q - 1)) == b;
+        if (!ok) mark_bad(mode, v.status, ST_INCONSISTENT, v.bad, v.nbad, i, a, b, -1);
         V3 za = load3(z, a), zb = load3(z, b), zc = load3(z, c);
         if (mode >= 1) {   // reused cycles: the triangle must still face outward
             int tier;
             if (orient_robust(v3(0, 0, 0), zi, za, zb, -1, i, a, b, &tier) <= 0) {
-                mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, -1);
+                mark_bad(mode, v.status, ST_NOT_DELAUNAY, v.bad, v.nbad, i, a, b, -1);
 #ifdef SCVT_PROBE_FLIPS
                 atomicAdd(&g_probe[1], 1);
 #endif
@@ -283,29 +300,47 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
         if (mode >= 1 && sgn > 0) atomicAdd(&g_probe[0], 1);
         if (mode >= 1 && !ok) atomicAdd(&g_probe[2], 1);
 #endif
-        amb[(int64_t)i * MAXDEG + t] = tier > 0 ? 1 : 0;
+        v.amb[(int64_t)i * MAXDEG + t] = tier > 0 ? 1 : 0;
         namb += tier > 0;
         if (sgn > 0) {
             if (mode == 2) {
                 // edges at cells already bound for the rebuild path (a triangle there faces
                 // inward: the mesh folded, which no flip repairs) are not queued
+                int* bad = v.bad;
                 if (i < a && !(bad[i] | bad[a] | bad[b] | bad[c])) {
-                    const int k = atomicAdd(fq.ncand, 1);
-                    if (k < fq.cap) {
-                        fq.cand[k] = make_int4(i, a, b, c);
+                    const int k = atomicAdd(v.fq.ncand, 1);
+                    if (k < v.fq.cap) {
+                        v.fq.cand[k] = make_int4(i, a, b, c);
                     } else {       // queue overflow (cannot happen: <= 3n - 6 edges): rebuild
-                        const int v[4] = {i, a, b, c};
-                        for (int q = 0; q < 4; ++q)
-                            if (atomicExch(&bad[v[q]], 1) == 0) atomicAdd(nbad, 1);
+                        const int vv[4] = {i, a, b, c};
+                        for (int qq = 0; qq < 4; ++qq)
+                            if (atomicExch(&bad[vv[qq]], 1) == 0) atomicAdd(v.nbad, 1);
                     }
                 }
             } else {
-                mark_bad(mode, status, ST_NOT_DELAUNAY, bad, nbad, i, a, b, c);
+                mark_bad(mode, v.status, ST_NOT_DELAUNAY, v.bad, v.nbad, i, a, b, c);
             }
         }
     }
-    if (namb) atomicAdd(&stats[3], namb);
-    }
+    if (namb) atomicAdd(&v.stats[3], namb);
+    return false;
+}
+
+__global__ void k_verify(const double* __restrict__ z, const int* __restrict__ ids, int p_lo,
+                         int p_hi, const int* __restrict__ list, const int* __restrict__ list_n,
+                         const int* __restrict__ nbr, const int* __restrict__ deg,
+                         uint8_t* __restrict__ amb, int* __restrict__ status,
+                         int* __restrict__ stats, int mode, int* __restrict__ bad,
+                         int* __restrict__ nbad, FlipQueue fq = FlipQueue{nullptr, nullptr, 0},
+                         int list_ids = 0) {
+    // VERIFY_LANES threads per cell, each taking every VERIFY_LANES-th edge of its cycle: the
+    // dependent neighbour-row lookups of different edges run in parallel instead of in one
+    // thread's loop (the pass is memory-latency bound)
+    const VerifyArgs v{z, ids, p_lo, p_hi, list, list_n, nbr, deg, amb, status, stats, mode,
+                       bad, nbad, fq, list_ids};
+    for (int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;;
+         gidx += (int64_t)gridDim.x * blockDim.x)
+        if (verify_item(v, gidx)) return;
 }
 
 // ------------------------------------------------------------------ flip repair
@@ -406,6 +441,43 @@ __global__ void k_flip_unlock(const int4* __restrict__ cand, const int* __restri
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
         const int4 c = cand[k];
         lock[c.x] = ~0ull; lock[c.y] = ~0ull; lock[c.z] = ~0ull; lock[c.w] = ~0ull;
+    }
+}
+
+// Fused flip round, launch 1 of 3: tickets of the current queue; resets the counters the
+// round fills next (the touched-cell list of launch 2, the next queue of launch 3).
+__global__ void k_round_lock(const int4* __restrict__ cand, const int* __restrict__ ncand,
+                             int cap, unsigned long long* __restrict__ lock,
+                             int* __restrict__ list_n, int* __restrict__ next_n) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) { *list_n = 0; *next_n = 0; }
+    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+        const int4 c = cand[k];
+        const unsigned long long key = flip_key(c);
+        atomicMin(&lock[c.x], key); atomicMin(&lock[c.y], key);
+        atomicMin(&lock[c.z], key); atomicMin(&lock[c.w], key);
+    }
+}
+
+// launch 3 of 3 (launch 2 is k_flip_apply): release the tickets of the current queue, clear
+// the touched-cell flags, and re-certify the touched cells (flip mode) into the next queue --
+// three independent index ranges of one grid-stride loop.
+__global__ void k_round_finish(const int4* __restrict__ cand, const int* __restrict__ ncand,
+                               int cap, unsigned long long* __restrict__ lock,
+                               int* __restrict__ flag, VerifyArgs v) {
+    const int nc = min(*ncand, cap);
+    const int nl = *v.list_n;
+    const int64_t total = (int64_t)nc + nl + (int64_t)VERIFY_LANES * nl;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        if (g < nc) {
+            const int4 c = cand[g];
+            lock[c.x] = ~0ull; lock[c.y] = ~0ull; lock[c.z] = ~0ull; lock[c.w] = ~0ull;
+        } else if (g < nc + nl) {
+            flag[v.list[g - nc]] = 0;
+        } else {
+            verify_item(v, g - nc - nl);
+        }
     }
 }
 
@@ -1670,7 +1742,7 @@ struct scvt_ctx {
     int* d_status = nullptr;           // [1 + 4 stats]
     double* h_scal = nullptr;          // pinned [MAX_RED_VALS]
     int* h_status = nullptr;           // pinned [8]
-    int* h_small = nullptr;            // pinned [16]: small readbacks (reuse counts)
+    int* h_small = nullptr;            // pinned [32]: small readbacks (reuse counts, flip rounds)
     double* h_dir = nullptr;           // pinned [2]: scalars of the asynchronous direction
     cudaEvent_t dir_ev = nullptr;      // recorded after their copy
     int* d_rcount = nullptr;           // per-round bad counts of the chained reuse rounds
@@ -1685,7 +1757,7 @@ struct scvt_ctx {
     unsigned long long* d_lock = nullptr;
     int* d_flist = nullptr;            // [2][n]
     int* d_fflag = nullptr;            // [n]
-    int* d_fcnt = nullptr;             // [8]
+    int* d_fcnt = nullptr;             // [8] flip_rounds counters (queues, lists, flips)
     int64_t flip_stats[4] = {0, 0, 0, 0};   // evaluations, rounds, flips, fell back
     int64_t last_flips = 0;                  // flips of the previous repair
     int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
@@ -2032,7 +2104,7 @@ constexpr int FLIP_MAX_ROUNDS = 12;
 // detection pass of the flip repair over the sorted slots [lo, hi): candidates and bad marks
 int flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi) {
     cudaStream_t s = ctx->stream;
-    int* cnt = ctx->d_fcnt;        // [0] candidates, [1] [2] list lengths, [3] flips
+    int* cnt = ctx->d_fcnt;        // [0] candidates (queue 0); flip_rounds uses the rest
     CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
     if (hi <= lo) return SCVT_OK;
     const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
@@ -2043,64 +2115,65 @@ int flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t h
     return SCVT_OK;
 }
 
-// flip rounds on the queued candidates (cnt[0]) until none is left or the round limit.
-// known_nonzero: the caller knows there are candidates (no host read before the first batch)
+// flip rounds on the queued candidates (queue 0, cnt[0]) until none is left or the round
+// limit.  Double-buffered queues (d_cand, d_cand + 3n) and touched-cell lists; each round is
+// three launches (k_round_lock, k_flip_apply, k_round_finish) and no memset; cnt: [0] [1]
+// queue lengths, [2] [3] list lengths, [4] flips.  known_nonzero: the caller knows there are
+// candidates (no host read before the first batch).
 int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
                 bool known_nonzero = false) {
     cudaStream_t s = ctx->stream;
     int* cnt = ctx->d_fcnt;
-    const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
+    const int cap = (int)(3 * n);
+    int4* cand[2] = {ctx->d_cand, ctx->d_cand + 3 * n};
+    int* list[2] = {ctx->d_flist, ctx->d_flist + n};
     int cur = 0, rounds = 0, flips_seen = -1;
+    bool skip_read = known_nonzero;
     // grid-stride kernels over at most n items per round: small meshes get small grids
     // (scheduling 1184 mostly idle blocks costs several microseconds per launch at c1)
     const unsigned fb = (unsigned)std::min<int64_t>(SPEC_BLOCKS, blocks_for(n, 128));
     const unsigned vb = (unsigned)std::min<int64_t>(SPEC_BLOCKS, blocks_for(VERIFY_LANES * n, 128));
-    bool skip_read = known_nonzero;
     for (;;) {
         if (!skip_read) {
-            CK(cudaMemcpyAsync(ctx->h_small, cnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(ctx->h_small, cnt, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(ctx->h_small + 8, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            if (ctx->h_small[0] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
+            if (ctx->h_small[cur] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
             // a whole batch without a flip: the open candidates are stuck (flips rejected at
             // their vertices), so they go to the rebuild path now instead of after the limit
-            if (ctx->h_small[3] == flips_seen) break;
-            flips_seen = ctx->h_small[3];
+            if (ctx->h_small[4] == flips_seen) break;
+            flips_seen = ctx->h_small[4];
         }
         skip_read = false;
         for (int r = 0; r < FLIP_ROUNDS_PER_SYNC && rounds < FLIP_MAX_ROUNDS; ++r, ++rounds) {
             const int nxt = 1 - cur;
-            int* list = ctx->d_flist + (int64_t)nxt * n;
-            CK(cudaMemsetAsync(cnt + 1 + nxt, 0, sizeof(int), s));
-            k_flip_lock<<<fb, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
+            k_round_lock<<<fb, 256, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock,
+                                            cnt + 2 + nxt, cnt + nxt);
             LAUNCHED();
-            k_flip_apply<<<fb, 128, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock, ctx->d_nbr,
-                                                      ctx->d_deg, ctx->d_fflag, list, cnt + 1 + nxt,
-                                                      ctx->d_bad, ctx->d_nbad, cnt + 3);
+            k_flip_apply<<<fb, 128, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock, ctx->d_nbr,
+                                            ctx->d_deg, ctx->d_fflag, list[nxt], cnt + 2 + nxt,
+                                            ctx->d_bad, ctx->d_nbad, cnt + 4);
             LAUNCHED();
-            k_flip_unlock<<<fb, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_lock);
-            LAUNCHED();
-            k_clear_flags<<<fb, 256, 0, s>>>(list, cnt + 1 + nxt, ctx->d_fflag);
-            LAUNCHED();
-            CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
-            k_verify<<<vb, 128, 0, s>>>(
-                z, ctx->d_ids, 0, (int)n, list, cnt + 1 + nxt, ctx->d_nbr, ctx->d_deg,
-                ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad, fq, 1);
+            const VerifyArgs v{z, ctx->d_ids, 0, (int)n, list[nxt], cnt + 2 + nxt, ctx->d_nbr,
+                               ctx->d_deg, ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2,
+                               ctx->d_bad, ctx->d_nbad, FlipQueue{cand[nxt], cnt + nxt, cap}, 1};
+            k_round_finish<<<vb, 128, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock,
+                                              ctx->d_fflag, v);
             LAUNCHED();
             cur = nxt;
         }
     }
-    const bool open = ctx->h_small[0] > 0;
+    const bool open = ctx->h_small[cur] > 0;
     if (open) {   // unconverged: those cells are rebuilt
-        k_cand_bad<<<fb, 256, 0, s>>>(ctx->d_cand, cnt, fq.cap, ctx->d_bad, ctx->d_nbad);
+        k_cand_bad<<<fb, 256, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_bad, ctx->d_nbad);
         LAUNCHED();
-        CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_small + 8, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
-    *nbad_host = ctx->h_small[4];
+    *nbad_host = ctx->h_small[8];
     ctx->flip_stats[0] += 1;
     ctx->flip_stats[1] += rounds;
-    ctx->flip_stats[2] += ctx->h_small[3];
+    ctx->flip_stats[2] += ctx->h_small[4];
     ctx->flip_stats[3] += open ? 1 : 0;
     return SCVT_OK;
 }
@@ -2645,7 +2718,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_status, 16);
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
-    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_cand, 3 * n); AL(d_lock, n); AL(d_flist, 2 * n); AL(d_fflag, n); AL(d_fcnt, 8); AL(d_counts, MAX_SHARDS + 1);
+    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_cand, 6 * n); AL(d_lock, n); AL(d_flist, 2 * n); AL(d_fflag, n); AL(d_fcnt, 8); AL(d_counts, MAX_SHARDS + 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
@@ -2657,7 +2730,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     {
         cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_RED_VALS * sizeof(double));
         cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
-        cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 16 * sizeof(int));
+        cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 32 * sizeof(int));
         cudaError_t e4 = cudaMallocHost((void**)&ctx->h_counts, (MAX_SHARDS + 1) * sizeof(int));
         cudaError_t e5 = cudaMallocHost((void**)&ctx->h_dir, 2 * sizeof(double));
         cudaError_t e6 = cudaEventCreateWithFlags(&ctx->dir_ev, cudaEventDisableTiming);
@@ -2952,6 +3025,7 @@ int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshard
         total += counts[r];
     }
     ctx->h_small[8] = (int)total;
+    CK(cudaMemsetAsync(ctx->d_fcnt, 0, 8 * sizeof(int), s));
     CK(cudaMemcpyAsync(ctx->d_fcnt, ctx->h_small + 8, sizeof(int), cudaMemcpyHostToDevice, s));
     int nbad = 0;
     TRY(flip_rounds(ctx, z, n, &nbad, total > 0));
