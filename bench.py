@@ -165,13 +165,13 @@ class CpuRegionSample:
         self.R = R
 
     def step(self):
+        t0 = time.perf_counter()          # payload assembly (pipeline.py:171-197) is timed too
         jobs = []
         for _ in range(self.per_step):
             l = self.next % self.p
             self.next += 1
             jobs.append((self.R.region_payload(self.z, self.geo, self.centers, self.one, l),
                          self.density))
-        t0 = time.perf_counter()
         owned = sum(self.pool.map(_region_worker, jobs))
         return owned, time.perf_counter() - t0
 
@@ -180,7 +180,14 @@ class CpuRegionSample:
         self.pool.join()
 
 
-def cpu_measure(cfg, steps, warmup, regions=0):
+def workload(cfg: str) -> str:
+    """The workload string both arms report (the same configuration)."""
+    n, dname, m = CONFIGS[cfg]
+    return (f"{cfg}: N={n}, {dname} density, {RULE} rule on depth-{DEPTH} subdivided fans, "
+            f"Lloyd-P-LBFGS m={m}")
+
+
+def cpu_measure(cfg, steps, warmup, regions=0, evals_per_iteration=1.0):
     s = CpuRegionSample(cfg, regions)
     try:
         for _ in range(warmup):
@@ -190,13 +197,18 @@ def cpu_measure(cfg, steps, warmup, regions=0):
             o, t = s.step()
             tot_owned += o
             tot_t += t
-        return {"value": tot_owned / tot_t, "unit": "generator-updates/s", "cores": s.cores,
+        return {"value": tot_owned / tot_t / evals_per_iteration,
+                "unit": "generator-updates/s", "cores": s.cores,
                 "kind": "port",
                 "sample": (f"oracle restatement of the reference region path (covering p={s.p}, "
                            f"Voronoi-sort regions, cap Delaunay via SciPy/Qhull, 7pt on depth-3 "
                            f"fans); {steps} steps x {s.per_step} regions on a {s.cores}-process "
-                           f"pool, {tot_owned} owned generators integrated in {tot_t:.2f} s; "
-                           f"assumes 1 evaluation per iteration")}
+                           f"pool, {tot_owned} owned generators integrated in {tot_t:.2f} s "
+                           f"(payload assembly included); generator-updates = generator "
+                           f"evaluations / {evals_per_iteration:.2f} evaluations per iteration "
+                           f"(the GPU arm's measured rate; the reference's own default covering "
+                           f"p = default_partitions(N) = 64 regions would take ~40 s per region "
+                           f"task, so a step samples a finer covering of the same path)")}
     finally:
         s.close()
 
@@ -211,8 +223,9 @@ def run_reference(a):
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded rho-sampling, seed 0)",
-            "config": {"workload": f"{a.config}: N={n}, {CONFIGS[a.config][1]} density, "
-                                   f"{RULE} rule on depth-{DEPTH} fans, CPU region path"},
+            "config": {"workload": workload(a.config), "N": n,
+                       "implementation": "reference algorithm on the host CPU cores "
+                                         "(region path, fork pool)"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -321,8 +334,7 @@ def run_b200(a):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (rho-sampled generators, default_rng seed 0)",
-            "config": {"workload": f"{a.config}: N={n}, tanh^4 density ({dname}), {RULE} rule on "
-                                   f"depth-{DEPTH} subdivided fans, Lloyd-P-LBFGS m={m}",
+            "config": {"workload": workload(a.config),
                        "N": n, "iteration_window": f"{a.warmup + 1}..{a.warmup + a.steps}",
                        "evals_per_iteration": evals / a.steps,
                        "l2": "flushed (256 MB write) before every timed step",
@@ -337,7 +349,8 @@ def run_b200(a):
     if not a.no_e2e:
         line["e2e"] = _e2e(P, density, z0, m, a.steps, dev, world)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_measure(a.config, 2, 1)
+        line["cpu_baseline"] = cpu_measure(a.config, 2, 1,
+                                           evals_per_iteration=max(evals / a.steps, 1.0))
     ev.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
