@@ -1277,6 +1277,113 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
     }
 }
 
+// Two nodes of the fitted sweep (independent chains): positions x0, x1, fit arguments t0, t1
+// (t = x.(-2 sigma c), single-centre fits) accumulated into the rule node's sums.
+template <int KIND, bool SERIES, bool TADD>
+SCVT_HD void fit_pair(const FitEval& f0, const FitEval& f1, V3 z, V3 x0, V3 x1, double t0,
+                      double t1, double& mq, double& xq, double& yq, double& zq, double& eq) {
+    double inv0, inv1;
+    if (SERIES) {
+        const double d0 = fma(-x0.z, x0.z, fma(-x0.y, x0.y, fma(-x0.x, x0.x, 1.0)));
+        const double d1 = fma(-x1.z, x1.z, fma(-x1.y, x1.y, fma(-x1.x, x1.x, 1.0)));
+        const double p0 = fma(d0, 0.3125, 0.375), p1 = fma(d1, 0.3125, 0.375);
+        const double q0 = fma(d0, p0, 0.5), q1 = fma(d1, p1, 0.5);
+        inv0 = fma(d0, q0, 1.0); inv1 = fma(d1, q1, 1.0);
+    } else {
+        inv0 = fast_rsqrt(x0.x * x0.x + x0.y * x0.y + x0.z * x0.z);
+        inv1 = fast_rsqrt(x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+    }
+    double rho0, rho1;
+    if (TADD) fit_rho2_t(f0, t0, inv0, t1, inv1, &rho0, &rho1);
+    else fit_rho2(f0, x0, inv0, x1, inv1, &rho0, &rho1);
+    if (KIND == DEN_TANH4X2_TAB) {
+        double r0b, r1b;
+        fit_rho2(f1, x0, inv0, x1, inv1, &r0b, &r1b);
+        rho0 = fmax(rho0, r0b); rho1 = fmax(rho1, r1b);
+    }
+    const double dx0 = fma(x0.x, inv0, -z.x), dx1 = fma(x1.x, inv1, -z.x);
+    const double dy0 = fma(x0.y, inv0, -z.y), dy1 = fma(x1.y, inv1, -z.y);
+    const double dz0 = fma(x0.z, inv0, -z.z), dz1 = fma(x1.z, inv1, -z.z);
+    const double e0 = fma(dz0, dz0, fma(dy0, dy0, dx0 * dx0));
+    const double e1 = fma(dz1, dz1, fma(dy1, dy1, dx1 * dx1));
+    mq += rho0 + rho1;
+    xq = fma(rho1, dx1, fma(rho0, dx0, xq));
+    yq = fma(rho1, dy1, fma(rho0, dy0, yq));
+    zq = fma(rho1, dz1, fma(rho0, dz0, zq));
+    eq = fma(rho1, e1, fma(rho0, e0, eq));
+}
+
+// The fitted sweep with the up- and down-leaf rows merged (same result up to the summation
+// order).  For rule node q the down-leaf node of leaf row a is the up-leaf node of the same
+// row shifted by D_q = (1/L - 2 l1_q) e1 + (1/L - 2 l2_q) e2 (l1_q, l2_q: the node's
+// coordinates in the first leaf), so one row carries both as
+// two chains (L - 1 - a pairs), and the L up-leaf nodes left over -- the row ends, on the
+// leaf-grid diagonal -- are swept as L / 2 pairs along the diagonal: per rule node L + 1 row
+// setups instead of 2 L - 1, and no single-node tails.
+template <int KIND, int L, bool SERIES>
+SCVT_HD void sym7_fit_leaves_merged(const SubTri& s, V3 z, const double* l1, const double* l2,
+                                    const double* w, const LocalFit& lf0, const LocalFit& lf1,
+                                    double* acc) {
+    static_assert(L % 2 == 0, "diagonal pairs");
+    const FitEval f0 = fit_eval(lf0);
+    FitEval f1;
+    if (KIND == DEN_TANH4X2_TAB) f1 = fit_eval(lf1);
+    constexpr bool TADD = KIND != DEN_TANH4X2_TAB;
+    const double invL = 1.0 / (double)L;
+    const V3 de2 = mul(s.e2, invL);
+    const V3 dd = mul(sub(s.e1, s.e2), invL);           // along the diagonal
+    const double dt = TADD ? fma(de2.z, f0.m2c.z, fma(de2.y, f0.m2c.y, de2.x * f0.m2c.x)) : 0.0;
+    const double ddt = TADD ? fma(dd.z, f0.m2c.z, fma(dd.y, f0.m2c.y, dd.x * f0.m2c.x)) : 0.0;
+#pragma unroll 1
+    for (int q = 0; q < 7; ++q) {
+        // l1, l2: node coordinates in the first leaf (already scaled by 1/L)
+        const double ga = l1[q], gb = l2[q];
+        const double ka = fma(-2.0, ga, invL), kb = fma(-2.0, gb, invL);
+        const V3 D = v3(fma(ka, s.e1.x, kb * s.e2.x), fma(ka, s.e1.y, kb * s.e2.y),
+                        fma(ka, s.e1.z, kb * s.e2.z));
+        const double tD = TADD ? fma(D.z, f0.m2c.z, fma(D.y, f0.m2c.y, D.x * f0.m2c.x)) : 0.0;
+        const V3 r0 = v3(fma(gb, s.e2.x, s.v0.x), fma(gb, s.e2.y, s.v0.y),
+                         fma(gb, s.e2.z, s.v0.z));
+        double mq = 0.0, xq = 0.0, yq = 0.0, zq = 0.0, eq = 0.0;
+        for (int a = 0; a < L - 1; ++a) {
+            const double fa = fma((double)a, invL, ga);
+            V3 xn = v3(fma(fa, s.e1.x, r0.x), fma(fa, s.e1.y, r0.y), fma(fa, s.e1.z, r0.z));
+            double tn = TADD ? fma(xn.z, f0.m2c.z, fma(xn.y, f0.m2c.y, xn.x * f0.m2c.x)) : 0.0;
+            for (int b = 0; b < L - 1 - a; ++b) {
+                const V3 x1 = add(xn, D);
+                fit_pair<KIND, SERIES, TADD>(f0, f1, z, xn, x1, tn, tn + tD, mq, xq, yq, zq, eq);
+                xn = add(xn, de2);
+                tn += dt;
+            }
+        }
+        {   // the row ends: up-leaf (a, L-1-a), a = 0..L-1, in pairs along the diagonal
+            const double fb = fma((double)(L - 1), invL, gb);
+            V3 xn = v3(fma(ga, s.e1.x, fma(fb, s.e2.x, s.v0.x)),
+                       fma(ga, s.e1.y, fma(fb, s.e2.y, s.v0.y)),
+                       fma(ga, s.e1.z, fma(fb, s.e2.z, s.v0.z)));
+            double tn = TADD ? fma(xn.z, f0.m2c.z, fma(xn.y, f0.m2c.y, xn.x * f0.m2c.x)) : 0.0;
+            for (int k = 0; k < L / 2; ++k) {
+                const V3 x1 = add(xn, dd);
+                fit_pair<KIND, SERIES, TADD>(f0, f1, z, xn, x1, tn, tn + ddt, mq, xq, yq, zq, eq);
+                xn = add(x1, dd);
+                tn += 2.0 * ddt;
+            }
+        }
+        const double wq = s.area * w[q == 0 ? 0 : (q < 4 ? 1 : 4)];
+        xq = fma(z.x, mq, xq); yq = fma(z.y, mq, yq); zq = fma(z.z, mq, zq);
+        acc[0] = fma(wq, mq, acc[0]);
+        acc[1] = fma(wq, xq, acc[1]); acc[2] = fma(wq, yq, acc[2]);
+        acc[3] = fma(wq, zq, acc[3]);
+        acc[4] = fma(wq, eq, acc[4]);
+    }
+}
+
+#ifdef SCVT_SWEEP_ROWS
+#define SCVT_FIT_SWEEP sym7_fit_leaves
+#else
+#define SCVT_FIT_SWEEP sym7_fit_leaves_merged
+#endif
+
 template <int KIND, int L>
 SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const double* l2,
                                  const double* w, const DensityParams& dp, double* acc,
@@ -1357,13 +1464,13 @@ SCVT_HD void sym7_sweep(int mode, const SubTri& s, V3 z, const double* l1, const
     const bool series = (mode & SWEEP_SERIES) != 0;
     if (fit == SWEEP_FIT0 || fit == SWEEP_FIT1) {
         const LocalFit& fd = f[fit - 1];
-        if (series) sym7_fit_leaves<DEN_TANH4_TAB, L, true>(s, z, l1, l2, w, fd, fd, acc);
-        else sym7_fit_leaves<DEN_TANH4_TAB, L, false>(s, z, l1, l2, w, fd, fd, acc);
+        if (series) SCVT_FIT_SWEEP<DEN_TANH4_TAB, L, true>(s, z, l1, l2, w, fd, fd, acc);
+        else SCVT_FIT_SWEEP<DEN_TANH4_TAB, L, false>(s, z, l1, l2, w, fd, fd, acc);
         return;
     }
     if (KIND == DEN_TANH4X2_TAB && fit == SWEEP_FIT2) {
-        if (series) sym7_fit_leaves<KIND, L, true>(s, z, l1, l2, w, f[0], f[1], acc);
-        else sym7_fit_leaves<KIND, L, false>(s, z, l1, l2, w, f[0], f[1], acc);
+        if (series) SCVT_FIT_SWEEP<KIND, L, true>(s, z, l1, l2, w, f[0], f[1], acc);
+        else SCVT_FIT_SWEEP<KIND, L, false>(s, z, l1, l2, w, f[0], f[1], acc);
         return;
     }
     V3 o[7];
