@@ -224,6 +224,49 @@ struct FlipQueue {
     int cap;
 };
 
+// Block-local staging of detected flip candidates: same-address global atomics serialise at
+// ~4 ns each (20k candidates queued one atomicAdd at a time were most of the detection pass),
+// so a block collects its candidates in shared memory and reserves their slots in the global
+// queue with ONE atomicAdd when it flushes.
+constexpr int SINK_CAP = 512;
+struct CandSink {
+    int4* q;      // shared [SINK_CAP]
+    int* n;       // shared counter
+};
+
+__device__ __forceinline__ void queue_overflow(const int4 c, int* bad, int* nbad) {
+    const int vv[4] = {c.x, c.y, c.z, c.w};     // cannot hold it: those cells are rebuilt
+    for (int q = 0; q < 4; ++q)
+        if (atomicExch(&bad[vv[q]], 1) == 0) atomicAdd(nbad, 1);
+}
+
+__device__ __forceinline__ void sink_push(const CandSink& sk, const FlipQueue& fq, const int4 c,
+                                          int* bad, int* nbad) {
+    const int k = atomicAdd(sk.n, 1);
+    if (k < SINK_CAP) { sk.q[k] = c; return; }
+    const int g = atomicAdd(fq.ncand, 1);       // staging full: straight to the global queue
+    if (g < fq.cap) fq.cand[g] = c;
+    else queue_overflow(c, bad, nbad);
+}
+
+// all threads of the block: move the staged candidates to the global queue (one atomicAdd)
+__device__ __forceinline__ void sink_flush(const CandSink& sk, const FlipQueue& fq, int* bad,
+                                           int* nbad) {
+    __shared__ int s_base;
+    __syncthreads();
+    const int m = min(*sk.n, SINK_CAP);
+    if (threadIdx.x == 0 && m > 0) s_base = atomicAdd(fq.ncand, m);
+    __syncthreads();
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+        const int g = s_base + k;
+        if (g < fq.cap) fq.cand[g] = sk.q[k];
+        else queue_overflow(sk.q[k], bad, nbad);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *sk.n = 0;
+    __syncthreads();
+}
+
 // Arguments of one certificate pass (k_verify, and the fused flip-round kernel).
 struct VerifyArgs {
     const double* z;
@@ -241,19 +284,35 @@ struct VerifyArgs {
     int* nbad;
     FlipQueue fq;
     int list_ids;
+    int list_len;       // >= 0: the list's length (entries < 0 are holes); < 0: read *list_n
 };
 
-// one (cell, lane) work item of the certificate; true once past the end of the work.  The
-// cycles, lists and positions were written by earlier launches: read-only-path loads.
-__device__ __forceinline__ bool verify_item(const VerifyArgs& v, int64_t gidx) {
+// loads of the cycles: through the read-only path when an earlier launch wrote them (RO), plain
+// L2 loads inside the kernel that rewrites them between its own rounds (k_flip_tail)
+template <bool RO>
+__device__ __forceinline__ int ldc(const int* p) {
+    if (RO) return __ldg(p);
+    return __ldcg(p);
+}
+
+// one (cell, lane) work item of the certificate; true once past the end of the work.
+// Mode 2 runs on cycles that were certified at the previous positions and since then changed
+// only by flips, which keep them combinatorially consistent (k_flip_apply checks the quad
+// before it rewrites the four rows): the consistency lookup in the neighbour's row is skipped,
+// every edge is tested once (from its lower-id end, which also queues the candidate) and every
+// triangle's orientation once (from its minimum vertex).  The ambiguity flags feed only
+// scvt_triangulate, which always runs a fresh mode-0 pass: modes 1-2 do not write them.
+template <bool RO>
+__device__ __forceinline__ bool verify_item(const VerifyArgs& v, int64_t gidx, const CandSink& sk) {
     const int idx = (int)(gidx / VERIFY_LANES), lane = (int)(gidx % VERIFY_LANES);
     int p, i;
     if (v.list) {               // re-certification of a compacted list of sorted slots
-        if (idx >= __ldg(v.list_n)) return true;
+        if (idx >= (v.list_len >= 0 ? v.list_len : ldc<RO>(v.list_n))) return true;
         if (v.list_ids) {
-            i = __ldg(v.list + idx);
+            i = ldc<RO>(v.list + idx);
+            if (i < 0) return false;                       // hole of a touched-cell list
         } else {
-            p = __ldg(v.list + idx);
+            p = ldc<RO>(v.list + idx);
             if (p < v.p_lo || p >= v.p_hi) return false;   // sharded re-check: owned slots only
             i = __ldg(v.ids + p);
         }
@@ -263,7 +322,7 @@ __device__ __forceinline__ bool verify_item(const VerifyArgs& v, int64_t gidx) {
         i = __ldg(v.ids + p);
     }
     const int mode = v.mode;
-    const int d = __ldg(v.deg + i);
+    const int d = ldc<RO>(v.deg + i);
     const int* row = v.nbr + (int64_t)i * MAXDEG;
     if (d < 3 || d > MAXDEG) {
         if (lane == 0)
@@ -272,55 +331,58 @@ __device__ __forceinline__ bool verify_item(const VerifyArgs& v, int64_t gidx) {
     }
     const double* z = v.z;
     V3 zi = load3(z, i);
-    int namb = 0;
-    for (int t = lane; t < d; t += VERIFY_LANES) {
-        int a = __ldg(row + t), b = __ldg(row + (t + 1 == d ? 0 : t + 1)),
-            c = __ldg(row + (t == 0 ? d - 1 : t - 1));
-        int da = __ldg(v.deg + a);
-        const int* ra = v.nbr + (int64_t)a * MAXDEG;
-        int q = -1;
-        if (da >= 3 && da <= MAXDEG)
-            for (int k = 0; k < da; ++k)
-                if (__ldg(ra + k) == i) { q = k; break; }
-        bool ok = q >= 0 && __ldg(ra + (q == 0 ? da - 1 : q - 1)) == b;
-        if (!ok) mark_bad(mode, v.status, ST_INCONSISTENT, v.bad, v.nbad, i, a, b, -1);
-        V3 za = load3(z, a), zb = load3(z, b), zc = load3(z, c);
-        if (mode >= 1) {   // reused cycles: the triangle must still face outward
+    if (mode == 2) {
+        for (int t = lane; t < d; t += VERIFY_LANES) {
+            const int a = ldc<RO>(row + t);
+            if (a < i) continue;            // the edge and its triangles belong to lower ids
+            const int b = ldc<RO>(row + (t + 1 == d ? 0 : t + 1)),
+                      c = ldc<RO>(row + (t == 0 ? d - 1 : t - 1));
+            const V3 za = load3(z, a), zb = load3(z, b), zc = load3(z, c);
             int tier;
-            if (orient_robust(v3(0, 0, 0), zi, za, zb, -1, i, a, b, &tier) <= 0) {
-                mark_bad(mode, v.status, ST_NOT_DELAUNAY, v.bad, v.nbad, i, a, b, -1);
+            if (i < b && orient_robust(v3(0, 0, 0), zi, za, zb, -1, i, a, b, &tier) <= 0) {
+                mark_bad(1, v.status, ST_NOT_DELAUNAY, v.bad, v.nbad, i, a, b, -1);
 #ifdef SCVT_PROBE_FLIPS
                 atomicAdd(&g_probe[1], 1);
 #endif
             }
-        }
-        int tier;
-        int sgn = orient_robust(zi, za, zb, zc, i, a, b, c, &tier);
+            if (orient_robust(zi, za, zb, zc, i, a, b, c, &tier) > 0) {
 #ifdef SCVT_PROBE_FLIPS
-        if (mode >= 1 && sgn > 0) atomicAdd(&g_probe[0], 1);
-        if (mode >= 1 && !ok) atomicAdd(&g_probe[2], 1);
+                atomicAdd(&g_probe[0], 1);
 #endif
-        v.amb[(int64_t)i * MAXDEG + t] = tier > 0 ? 1 : 0;
-        namb += tier > 0;
-        if (sgn > 0) {
-            if (mode == 2) {
                 // edges at cells already bound for the rebuild path (a triangle there faces
                 // inward: the mesh folded, which no flip repairs) are not queued
                 int* bad = v.bad;
-                if (i < a && !(bad[i] | bad[a] | bad[b] | bad[c])) {
-                    const int k = atomicAdd(v.fq.ncand, 1);
-                    if (k < v.fq.cap) {
-                        v.fq.cand[k] = make_int4(i, a, b, c);
-                    } else {       // queue overflow (cannot happen: <= 3n - 6 edges): rebuild
-                        const int vv[4] = {i, a, b, c};
-                        for (int qq = 0; qq < 4; ++qq)
-                            if (atomicExch(&bad[vv[qq]], 1) == 0) atomicAdd(v.nbad, 1);
-                    }
-                }
-            } else {
-                mark_bad(mode, v.status, ST_NOT_DELAUNAY, v.bad, v.nbad, i, a, b, c);
+                if (!(__ldcg(bad + i) | __ldcg(bad + a) | __ldcg(bad + b) | __ldcg(bad + c)))
+                    sink_push(sk, v.fq, make_int4(i, a, b, c), bad, v.nbad);
             }
         }
+        return false;
+    }
+    int namb = 0;
+    for (int t = lane; t < d; t += VERIFY_LANES) {
+        int a = ldc<RO>(row + t), b = ldc<RO>(row + (t + 1 == d ? 0 : t + 1)),
+            c = ldc<RO>(row + (t == 0 ? d - 1 : t - 1));
+        int da = ldc<RO>(v.deg + a);
+        const int* ra = v.nbr + (int64_t)a * MAXDEG;
+        int q = -1;
+        if (da >= 3 && da <= MAXDEG)
+            for (int k = 0; k < da; ++k)
+                if (ldc<RO>(ra + k) == i) { q = k; break; }
+        bool ok = q >= 0 && ldc<RO>(ra + (q == 0 ? da - 1 : q - 1)) == b;
+        if (!ok) mark_bad(mode, v.status, ST_INCONSISTENT, v.bad, v.nbad, i, a, b, -1);
+        V3 za = load3(z, a), zb = load3(z, b), zc = load3(z, c);
+        if (mode >= 1) {   // reused cycles: the triangle must still face outward
+            int tier;
+            if (orient_robust(v3(0, 0, 0), zi, za, zb, -1, i, a, b, &tier) <= 0)
+                mark_bad(mode, v.status, ST_NOT_DELAUNAY, v.bad, v.nbad, i, a, b, -1);
+        }
+        int tier;
+        int sgn = orient_robust(zi, za, zb, zc, i, a, b, c, &tier);
+        if (mode == 0) {
+            v.amb[(int64_t)i * MAXDEG + t] = tier > 0 ? 1 : 0;
+            namb += tier > 0;
+        }
+        if (sgn > 0) mark_bad(mode, v.status, ST_NOT_DELAUNAY, v.bad, v.nbad, i, a, b, c);
     }
     if (namb) atomicAdd(&v.stats[3], namb);
     return false;
@@ -337,10 +399,16 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
     // dependent neighbour-row lookups of different edges run in parallel instead of in one
     // thread's loop (the pass is memory-latency bound)
     const VerifyArgs v{z, ids, p_lo, p_hi, list, list_n, nbr, deg, amb, status, stats, mode,
-                       bad, nbad, fq, list_ids};
+                       bad, nbad, fq, list_ids, -1};
+    __shared__ int4 s_q[SINK_CAP];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const CandSink sk{s_q, &s_n};
     for (int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;;
          gidx += (int64_t)gridDim.x * blockDim.x)
-        if (verify_item(v, gidx)) return;
+        if (verify_item<true>(v, gidx, sk)) break;
+    if (mode == 2) sink_flush(sk, fq, bad, nbad);
 }
 
 // ------------------------------------------------------------------ flip repair
@@ -351,153 +419,241 @@ __global__ void k_verify(const double* __restrict__ z, const int* __restrict__ i
 // candidate, flipped or not, are re-certified by the next detection pass (the only edges whose
 // status a flip changes are the quad's, whose ends are all among them).  Anything unexpected
 // (degree limits, inconsistent neighbourhoods) marks the four cells bad for the rebuild path.
+//
+// A round is lock -> apply -> finish.  The first rounds (tens of thousands of candidates) run
+// as three grid-wide launches each; once the queue is short the remaining rounds run inside
+// ONE thread block (k_flip_tail: block barriers between the phases, no launches, no host
+// reads), which also turns whatever is left after its round limit into bad cells.  The host
+// never reads a counter between rounds: it sizes the number of grid-wide rounds from the queue
+// lengths the previous evaluation reported (read back with that evaluation's scalars).
 __device__ __forceinline__ unsigned long long flip_key(const int4& c) {
     return ((unsigned long long)(unsigned)c.x << 32) | (unsigned)c.y;
 }
 
-__global__ void k_flip_lock(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
-                            unsigned long long* __restrict__ lock) {
-    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-        const int4 c = cand[k];
-        const unsigned long long key = flip_key(c);
-        atomicMin(&lock[c.x], key); atomicMin(&lock[c.y], key);
-        atomicMin(&lock[c.z], key); atomicMin(&lock[c.w], key);
-    }
+constexpr unsigned FULL_MASK = 0xffffffffu;
+
+__device__ __forceinline__ void lock_item(const int4 c, unsigned long long* __restrict__ lock) {
+    const unsigned long long key = flip_key(c);
+    atomicMin(&lock[c.x], key); atomicMin(&lock[c.y], key);
+    atomicMin(&lock[c.z], key); atomicMin(&lock[c.w], key);
 }
 
-__device__ __forceinline__ int cyc_pos(const int* __restrict__ row, int d, int x) {
-    for (int k = 0; k < d; ++k)
-        if (row[k] == x) return k;
-    return -1;
+// store the cyclic sequence y (one entry per lane, d entries) rotated so its minimum comes first
+__device__ __forceinline__ void cyc_store_warp(int* __restrict__ row, int* __restrict__ degp,
+                                               int y, int d, int lane) {
+    const int mn = __reduce_min_sync(FULL_MASK, lane < d ? y : 0x7fffffff);
+    const int pos = __ffs(__ballot_sync(FULL_MASK, lane < d && y == mn)) - 1;
+    int src = lane + pos;
+    if (src >= d) src -= d;
+    const int out = __shfl_sync(FULL_MASK, y, src & 31);
+    if (lane < d) row[lane] = out;
+    if (lane == 0) *degp = d;
 }
 
-// write `tmp` (d entries, cyclic) into `row` rotated so that its minimum comes first
-__device__ __forceinline__ void cyc_store(int* __restrict__ row, const int* tmp, int d) {
-    int m = 0;
-    for (int k = 1; k < d; ++k)
-        if (tmp[k] < tmp[m]) m = k;
-    for (int k = 0; k < d; ++k) row[k] = tmp[(m + k) % d];
-}
-
-__global__ void k_flip_apply(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
-                             const unsigned long long* __restrict__ lock, int* __restrict__ nbr,
-                             int* __restrict__ deg, int* __restrict__ dflag,
-                             int* __restrict__ next, int* __restrict__ next_n,
-                             int* __restrict__ bad, int* __restrict__ nbad,
-                             int* __restrict__ nflips) {
-    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-        const int4 c = cand[k];
-        const int v[4] = {c.x, c.y, c.z, c.w};
-        for (int q = 0; q < 4; ++q)
-            if (atomicExch(&dflag[v[q]], 1) == 0) next[atomicAdd(next_n, 1)] = v[q];
-        const unsigned long long key = flip_key(c);
-        if (lock[c.x] != key || lock[c.y] != key || lock[c.z] != key || lock[c.w] != key)
-            continue;                                   // a conflicting flip won this round
-        const int i = c.x, a = c.y, b = c.z, cc = c.w;
-        const int di = deg[i], da = deg[a], db = deg[b], dc = deg[cc];
-        int* ri = nbr + (int64_t)i * MAXDEG;
-        int* ra = nbr + (int64_t)a * MAXDEG;
-        int* rb = nbr + (int64_t)b * MAXDEG;
-        int* rc = nbr + (int64_t)cc * MAXDEG;
-        bool ok = di > 3 && da > 3 && db < MAXDEG && dc < MAXDEG && b != cc;
-        int ti = -1, ta = -1, tb = -1, tc = -1;
+// One candidate (queue slot k) handled by one warp: lane k holds entry k of each of the four
+// cycles, so the four rows are four coalesced loads issued together, positions are ballots and
+// the rewritten rows are shuffles (one thread walking the rows serially took ~20 dependent
+// loads per flip).  The cycles are read through L2 (__ldcg): k_flip_tail rewrites them between
+// its rounds.  The touched-cell list has four fixed slots per candidate, next[4k .. 4k+3]: a
+// vertex this candidate is the first to touch, or -1 (a hole) -- no list counter to contend
+// for.  Returns 1 when the flip was made.
+__device__ __forceinline__ int flip_warp(const int4 c, int k, int lane,
+                                         const unsigned long long* __restrict__ lock,
+                                         int* __restrict__ nbr, int* __restrict__ deg,
+                                         int* __restrict__ dflag, int* __restrict__ next,
+                                         int* __restrict__ bad, int* __restrict__ nbad) {
+    const int vq = lane == 0 ? c.x : lane == 1 ? c.y : lane == 2 ? c.z : c.w;
+    if (lane < 4) next[4 * (int64_t)k + lane] = atomicExch(&dflag[vq], 1) == 0 ? vq : -1;
+    const unsigned long long key = flip_key(c);
+    const bool mine = lane >= 4 || __ldcg(lock + vq) == key;
+    if (!__all_sync(FULL_MASK, mine)) return 0;        // a conflicting flip won this round
+    const int i = c.x, a = c.y, b = c.z, cc = c.w;
+    const int dq = lane < 4 ? __ldcg(deg + vq) : 0;
+    const int di = __shfl_sync(FULL_MASK, dq, 0), da = __shfl_sync(FULL_MASK, dq, 1),
+              db = __shfl_sync(FULL_MASK, dq, 2), dc = __shfl_sync(FULL_MASK, dq, 3);
+    int* ri = nbr + (int64_t)i * MAXDEG;
+    int* ra = nbr + (int64_t)a * MAXDEG;
+    int* rb = nbr + (int64_t)b * MAXDEG;
+    int* rc = nbr + (int64_t)cc * MAXDEG;
+    bool ok = di > 3 && di <= MAXDEG && da > 3 && da <= MAXDEG && db >= 3 && db < MAXDEG &&
+              dc >= 3 && dc < MAXDEG && b != cc;
+    if (ok) {
+        const int xi = lane < di ? __ldcg(ri + lane) : -1;
+        const int xa = lane < da ? __ldcg(ra + lane) : -1;
+        const int xb = lane < db ? __ldcg(rb + lane) : -1;
+        const int xc = lane < dc ? __ldcg(rc + lane) : -1;
+        const int ti = __ffs(__ballot_sync(FULL_MASK, xi == a)) - 1;
+        const int ta = __ffs(__ballot_sync(FULL_MASK, xa == i)) - 1;
+        const int tb = __ffs(__ballot_sync(FULL_MASK, xb == i)) - 1;
+        const int tc = __ffs(__ballot_sync(FULL_MASK, xc == a)) - 1;
+        const unsigned bc_edge = __ballot_sync(FULL_MASK, xb == cc) | __ballot_sync(FULL_MASK, xc == b);
+        ok = ti >= 0 && ta >= 0 && tb >= 0 && tc >= 0 && bc_edge == 0;     // b-c not an edge
         if (ok) {
-            ti = cyc_pos(ri, di, a); ta = cyc_pos(ra, da, i);
-            tb = cyc_pos(rb, db, i); tc = cyc_pos(rc, dc, a);
-            ok = ti >= 0 && ta >= 0 && tb >= 0 && tc >= 0 &&
-                 ri[(ti + 1) % di] == b && ri[(ti + di - 1) % di] == cc &&    // i: c, a, b
-                 ra[(ta + da - 1) % da] == b && ra[(ta + 1) % da] == cc &&    // a: b, i, c
-                 rb[(tb + 1) % db] == a &&                                  // b: i, a
-                 rc[(tc + 1) % dc] == i &&                                  // c: a, i
-                 cyc_pos(rb, db, cc) < 0 && cyc_pos(rc, dc, b) < 0;          // b-c not an edge
+            const int i_nx = __shfl_sync(FULL_MASK, xi, (ti + 1) % di);
+            const int i_pv = __shfl_sync(FULL_MASK, xi, (ti + di - 1) % di);
+            const int a_pv = __shfl_sync(FULL_MASK, xa, (ta + da - 1) % da);
+            const int a_nx = __shfl_sync(FULL_MASK, xa, (ta + 1) % da);
+            const int b_nx = __shfl_sync(FULL_MASK, xb, (tb + 1) % db);
+            const int c_nx = __shfl_sync(FULL_MASK, xc, (tc + 1) % dc);
+            ok = i_nx == b && i_pv == cc &&       // i: c, a, b
+                 a_pv == b && a_nx == cc &&       // a: b, i, c
+                 b_nx == a &&                     // b: i, a
+                 c_nx == i;                       // c: a, i
         }
-        if (!ok) {
-            for (int q = 0; q < 4; ++q)
-                if (atomicExch(&bad[v[q]], 1) == 0) atomicAdd(nbad, 1);
-            continue;
+        if (ok) {
+            // i: drop a;  a: drop i
+            const int yi = __shfl_sync(FULL_MASK, xi, (lane + (lane >= ti ? 1 : 0)) & 31);
+            const int ya = __shfl_sync(FULL_MASK, xa, (lane + (lane >= ta ? 1 : 0)) & 31);
+            // b: i, c, a;  c: a, b, i
+            const int sb = __shfl_sync(FULL_MASK, xb, (lane + 31) & 31);
+            const int sc = __shfl_sync(FULL_MASK, xc, (lane + 31) & 31);
+            const int yb = lane <= tb ? xb : (lane == tb + 1 ? cc : sb);
+            const int yc = lane <= tc ? xc : (lane == tc + 1 ? b : sc);
+            cyc_store_warp(ri, deg + i, yi, di - 1, lane);
+            cyc_store_warp(ra, deg + a, ya, da - 1, lane);
+            cyc_store_warp(rb, deg + b, yb, db + 1, lane);
+            cyc_store_warp(rc, deg + cc, yc, dc + 1, lane);
+            return 1;
         }
-        int tmp[MAXDEG];
-        int m = 0;                                       // i: drop a
-        for (int t = 0; t < di; ++t) if (t != ti) tmp[m++] = ri[t];
-        cyc_store(ri, tmp, di - 1); deg[i] = di - 1;
-        m = 0;                                           // a: drop i
-        for (int t = 0; t < da; ++t) if (t != ta) tmp[m++] = ra[t];
-        cyc_store(ra, tmp, da - 1); deg[a] = da - 1;
-        m = 0;                                           // b: i, c, a
-        for (int t = 0; t < db; ++t) { tmp[m++] = rb[t]; if (t == tb) tmp[m++] = cc; }
-        cyc_store(rb, tmp, db + 1); deg[b] = db + 1;
-        m = 0;                                           // c: a, b, i
-        for (int t = 0; t < dc; ++t) { tmp[m++] = rc[t]; if (t == tc) tmp[m++] = b; }
-        cyc_store(rc, tmp, dc + 1); deg[cc] = dc + 1;
-        atomicAdd(nflips, 1);
     }
+    if (lane < 4 && atomicExch(&bad[vq], 1) == 0) atomicAdd(nbad, 1);
+    return 0;
 }
 
-__global__ void k_flip_unlock(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
-                              unsigned long long* __restrict__ lock) {
-    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-        const int4 c = cand[k];
-        lock[c.x] = ~0ull; lock[c.y] = ~0ull; lock[c.z] = ~0ull; lock[c.w] = ~0ull;
-    }
-}
-
-// Fused flip round, launch 1 of 3: tickets of the current queue; resets the counters the
-// round fills next (the touched-cell list of launch 2, the next queue of launch 3).
+// Flip round, launch 1 of 3: tickets of the current queue; resets the counter the round
+// fills next (the next queue of launch 3) and records the queue length for the host's sizing
+// of the next evaluation's rounds.
 __global__ void k_round_lock(const int4* __restrict__ cand, const int* __restrict__ ncand,
                              int cap, unsigned long long* __restrict__ lock,
-                             int* __restrict__ list_n, int* __restrict__ next_n) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) { *list_n = 0; *next_n = 0; }
+                             int* __restrict__ next_n, int* __restrict__ hist) {
     const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-        const int4 c = cand[k];
-        const unsigned long long key = flip_key(c);
-        atomicMin(&lock[c.x], key); atomicMin(&lock[c.y], key);
-        atomicMin(&lock[c.z], key); atomicMin(&lock[c.w], key);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { *next_n = 0; *hist = nc; }
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x)
+        lock_item(cand[k], lock);
+}
+
+// launch 2 of 3: a warp per candidate; the flips are counted per block (one atomicAdd each)
+constexpr int APPLY_THREADS = 256;
+__global__ void __launch_bounds__(APPLY_THREADS)
+k_flip_apply(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
+             const unsigned long long* __restrict__ lock, int* __restrict__ nbr,
+             int* __restrict__ deg, int* __restrict__ dflag, int* __restrict__ next,
+             int* __restrict__ bad, int* __restrict__ nbad, int* __restrict__ nflips) {
+    __shared__ int s_flips;
+    if (threadIdx.x == 0) s_flips = 0;
+    __syncthreads();
+    const int nc = min(*ncand, cap);
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    int mine = 0;
+    for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nc; k += nwarps)
+        mine += flip_warp(cand[k], k, lane, lock, nbr, deg, dflag, next, bad, nbad);
+    if (lane == 0 && mine) atomicAdd(&s_flips, mine);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_flips) atomicAdd(nflips, s_flips);
+}
+
+// one item of a round's last phase: release the tickets of the current queue, clear the
+// touched-cell flags, and re-certify the touched cells (flip mode) into the next queue --
+// three independent index ranges (the touched list has 4 nc slots, holes included)
+template <bool RO>
+__device__ __forceinline__ void finish_item(int64_t g, const int4* __restrict__ cand, int nc,
+                                            unsigned long long* __restrict__ lock,
+                                            int* __restrict__ flag, const VerifyArgs& v,
+                                            const CandSink& sk) {
+    if (g < nc) {
+        const int4 c = RO ? cand[g] : __ldcg(cand + g);
+        lock[c.x] = ~0ull; lock[c.y] = ~0ull; lock[c.z] = ~0ull; lock[c.w] = ~0ull;
+    } else if (g < 5 * (int64_t)nc) {
+        const int i = ldc<RO>(v.list + (g - nc));
+        if (i >= 0) flag[i] = 0;
+    } else {
+        verify_item<RO>(v, g - 5 * (int64_t)nc, sk);
     }
 }
 
-// launch 3 of 3 (launch 2 is k_flip_apply): release the tickets of the current queue, clear
-// the touched-cell flags, and re-certify the touched cells (flip mode) into the next queue --
-// three independent index ranges of one grid-stride loop.
+// launch 3 of 3
 __global__ void k_round_finish(const int4* __restrict__ cand, const int* __restrict__ ncand,
                                int cap, unsigned long long* __restrict__ lock,
                                int* __restrict__ flag, VerifyArgs v) {
+    __shared__ int4 s_q[SINK_CAP];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const CandSink sk{s_q, &s_n};
     const int nc = min(*ncand, cap);
-    const int nl = *v.list_n;
-    const int64_t total = (int64_t)nc + nl + (int64_t)VERIFY_LANES * nl;
+    v.list_len = 4 * nc;
+    const int64_t total = (5 + 4 * VERIFY_LANES) * (int64_t)nc;
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        if (g < nc) {
-            const int4 c = cand[g];
-            lock[c.x] = ~0ull; lock[c.y] = ~0ull; lock[c.z] = ~0ull; lock[c.w] = ~0ull;
-        } else if (g < nc + nl) {
-            flag[v.list[g - nc]] = 0;
-        } else {
-            verify_item(v, g - nc - nl);
-        }
-    }
+         g += (int64_t)gridDim.x * blockDim.x)
+        finish_item<true>(g, cand, nc, lock, flag, v, sk);
+    sink_flush(sk, v.fq, v.bad, v.nbad);
 }
 
-__global__ void k_clear_flags(const int* __restrict__ list, const int* __restrict__ list_n,
-                              int* __restrict__ flag) {
-    const int nl = *list_n;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nl; k += gridDim.x * blockDim.x)
-        flag[list[k]] = 0;
+// The remaining rounds in one thread-block cluster (TAIL_CTAS SMs, hardware cluster barrier
+// between the phases; all mutable data is read through L2 and fenced before each barrier).
+// cnt: [0] [1] queue lengths, [4] flips, [5] rounds run here, [6] queue length on entry,
+// [7] candidates given up.  Stops when the queue is empty, after TAIL_MAX_ROUNDS, or after
+// TAIL_STUCK rounds in a row without a flip (the open candidates keep losing their tickets
+// to rejected ones: rebuild path).
+constexpr int TAIL_THREADS = 512;
+constexpr int TAIL_CTAS = 8;
+constexpr int TAIL_MAX_ROUNDS = 40;
+constexpr int TAIL_STUCK = 3;
+
+__device__ __forceinline__ void cluster_barrier() {
+    __threadfence();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-// the candidates left after the last round: their cells go to the rebuild path
-__global__ void k_cand_bad(const int4* __restrict__ cand, const int* __restrict__ ncand, int cap,
-                           int* __restrict__ bad, int* __restrict__ nbad) {
-    const int nc = min(*ncand, cap);   // entries past the queue capacity were never stored
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-        const int4 c = cand[k];
-        const int v[4] = {c.x, c.y, c.z, c.w};
-        for (int q = 0; q < 4; ++q)
-            if (atomicExch(&bad[v[q]], 1) == 0) atomicAdd(nbad, 1);
+__global__ void __cluster_dims__(TAIL_CTAS, 1, 1) __launch_bounds__(TAIL_THREADS)
+k_flip_tail(int4* __restrict__ cand0, int4* __restrict__ cand1, int* __restrict__ cnt, int cur,
+            int cap, unsigned long long* __restrict__ lock, int* __restrict__ nbr,
+            int* __restrict__ deg, int* __restrict__ fflag, int* __restrict__ list0,
+            int* __restrict__ list1, VerifyArgs v) {
+    __shared__ int4 s_q[SINK_CAP];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const CandSink sk{s_q, &s_n};
+    const int nthreads = TAIL_CTAS * TAIL_THREADS;
+    const int tid = blockIdx.x * TAIL_THREADS + threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int rounds = 0, stuck = 0;
+    const int entry = min(__ldcg(cnt + cur), cap);
+    for (;;) {
+        const int nc = min(__ldcg(cnt + cur), cap);
+        if (nc == 0 || rounds >= TAIL_MAX_ROUNDS || stuck >= TAIL_STUCK) break;
+        const int nxt = 1 - cur;
+        const int4* cq = cur ? cand1 : cand0;
+        int4* nq = cur ? cand0 : cand1;
+        int* nlist = nxt ? list1 : list0;
+        const int flips0 = __ldcg(cnt + 4);
+        cluster_barrier();                // everyone has read the counters of this round
+        if (tid == 0) atomicExch(cnt + nxt, 0);
+        for (int k = tid; k < nc; k += nthreads) lock_item(__ldcg(cq + k), lock);
+        cluster_barrier();
+        int mine = 0;
+        for (int k = warp; k < nc; k += nthreads / 32)
+            mine += flip_warp(__ldcg(cq + k), k, lane, lock, nbr, deg, fflag, nlist, v.bad, v.nbad);
+        if (lane == 0 && mine) atomicAdd(cnt + 4, mine);
+        cluster_barrier();
+        VerifyArgs w = v;
+        w.list = nlist; w.list_len = 4 * nc; w.fq = FlipQueue{nq, cnt + nxt, cap};
+        const int64_t total = (5 + 4 * VERIFY_LANES) * (int64_t)nc;
+        for (int64_t g = tid; g < total; g += nthreads)
+            finish_item<false>(g, cq, nc, lock, fflag, w, sk);
+        sink_flush(sk, w.fq, v.bad, v.nbad);
+        cluster_barrier();
+        stuck = __ldcg(cnt + 4) == flips0 ? stuck + 1 : 0;
+        ++rounds;
+        cur = nxt;
     }
+    // whatever is still queued goes to the rebuild path
+    const int nc = min(__ldcg(cnt + cur), cap);
+    const int4* cq = cur ? cand1 : cand0;
+    for (int k = tid; k < nc; k += nthreads) queue_overflow(__ldcg(cq + k), v.bad, v.nbad);
+    if (tid == 0) { cnt[5] = rounds; cnt[6] = entry; cnt[7] = nc; }
 }
 
 __global__ void k_flag_slots(int n, const int* __restrict__ ids, const int* __restrict__ bad,
@@ -531,9 +687,14 @@ __global__ void k_deg_sorted(int p_lo, int cnt, const int* __restrict__ ids,
 }
 
 __global__ void k_fill_incidences(int p_lo, int cnt, const int* __restrict__ ids,
-                                  const int* __restrict__ deg, const int* __restrict__ inc_start,
-                                  int* __restrict__ inc_base, int* __restrict__ inc_gen, int cap) {
+                                  const int* __restrict__ deg, const int* inc_start,
+                                  int* __restrict__ inc_base, int* __restrict__ inc_gen, int cap,
+                                  const int* __restrict__ skip, int* __restrict__ total) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
+    // skip (the bad count of a flip repair still in flight) != 0: the cycles are not certified,
+    // so the incidence total is poisoned and k_quad / k_gather integrate nothing (their Euler
+    // check); the host sees the count with the evaluation's scalars and resumes the rebuild
+    if (q == 0 && skip && *skip) *total = -1;
     if (q >= cnt) return;
     int i = ids[p_lo + q];
     int s = inc_start[q], d = deg[i];
@@ -1739,9 +1900,9 @@ struct scvt_ctx {
     // reductions and status
     double* d_partials = nullptr;      // [MAX_SLOTS][RED_BLOCKS] and [MAX_RED_VALS][CHUNKS]
     double* d_scal = nullptr;          // [MAX_RED_VALS]
-    int* d_status = nullptr;           // [1 + 4 stats]
+    int* d_status = nullptr;           // [64]: status + stats [0,16), d_nbad [16], d_fcnt [24,32), d_fhist [32,48)
     double* h_scal = nullptr;          // pinned [MAX_RED_VALS]
-    int* h_status = nullptr;           // pinned [8]
+    int* h_status = nullptr;           // pinned [64]: one copy of the whole d_status block
     int* h_small = nullptr;            // pinned [32]: small readbacks (reuse counts, flip rounds)
     double* h_dir = nullptr;           // pinned [2]: scalars of the asynchronous direction
     cudaEvent_t dir_ev = nullptr;      // recorded after their copy
@@ -1755,9 +1916,12 @@ struct scvt_ctx {
     double* d_cgv = nullptr;           // CG work vectors r, p, q: [3][3 n] (lazy)
     double* d_cg = nullptr;            // CG scalars [16] (lazy)
     unsigned long long* d_lock = nullptr;
-    int* d_flist = nullptr;            // [2][n]
+    int* d_flist = nullptr;            // [2][4 n]: touched cells, four slots per candidate
     int* d_fflag = nullptr;            // [n]
-    int* d_fcnt = nullptr;             // [8] flip_rounds counters (queues, lists, flips)
+    int* d_fcnt = nullptr;             // [8] flip counters (queues, lists, flips, tail): d_status + 24
+    int* d_fhist = nullptr;            // [16] queue length per grid-wide round: d_status + 32
+    int flip_grid_rounds = 3;          // grid-wide rounds before k_flip_tail (adapted per evaluation)
+    int flip_rounds_enqueued = 0;      // grid-wide rounds of the repair in flight
     int64_t flip_stats[4] = {0, 0, 0, 0};   // evaluations, rounds, flips, fell back
     int64_t last_flips = 0;                  // flips of the previous repair
     int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
@@ -1914,7 +2078,7 @@ int dalloc(scvt_ctx* ctx, T** p, size_t count) {
 int readback(scvt_ctx* ctx, int nd) {
     if (nd) CK(cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, nd * sizeof(double),
                                cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 64 * sizeof(int), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return SCVT_OK;
@@ -2094,122 +2258,116 @@ int reuse_round_device(scvt_ctx* ctx, const double* z, int64_t n, const GridView
 // host (certified evaluations stop there); passes 1-2 with their rebuild rounds are chained
 // on the device and read back once.
 bool flips_enabled() { return getenv("SCVT_NO_FLIPS") == nullptr; }
-constexpr int FLIP_ROUNDS_PER_SYNC = 4;
-constexpr int FLIP_MAX_ROUNDS = 12;
+constexpr int FLIP_GRID_ROUNDS_MAX = 10;   // grid-wide rounds before the single-block tail
+constexpr int FLIP_TAIL_ENTER = 512;       // queue length the tail handles well (32 warps)
+constexpr int FLIP_HIST = 16;              // d_fhist: queue length at the start of each grid round
 
-// Certificate pass over every cell in flip mode, then Lawson flip rounds (detection of the
-// touched cells after each), FLIP_ROUNDS_PER_SYNC rounds chained on the device between host
-// reads.  Leaves d_bad / d_nbad as the rebuild path expects them: the cells of orientation or
-// consistency failures, of rejected flips and of candidates still open after the last round.
 // detection pass of the flip repair over the sorted slots [lo, hi): candidates and bad marks
 int flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi) {
     cudaStream_t s = ctx->stream;
-    int* cnt = ctx->d_fcnt;        // [0] candidates (queue 0); flip_rounds uses the rest
-    CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
+    int* cnt = ctx->d_fcnt;        // [0] candidates (queue 0); the rounds use the rest
+    CK(cudaMemsetAsync(cnt, 0, (8 + FLIP_HIST) * sizeof(int), s));   // d_fcnt and d_fhist
     if (hi <= lo) return SCVT_OK;
-    const FlipQueue fq{ctx->d_cand, cnt, (int)(3 * n)};
-    k_verify<<<blocks_for((hi - lo) * VERIFY_LANES, 128), 128, 0, s>>>(
+    const FlipQueue fq{ctx->d_cand, cnt, (int)n};
+    // a bounded grid: every block certifies many cells and stages its candidates in shared
+    // memory (one global atomicAdd per block instead of one per candidate)
+    const unsigned vb = (unsigned)std::min<int64_t>(2 * SPEC_BLOCKS,
+                                                    blocks_for((hi - lo) * VERIFY_LANES, 128));
+    k_verify<<<vb, 128, 0, s>>>(
         z, ctx->d_ids, (int)lo, (int)hi, nullptr, nullptr, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
         ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad, fq);
     LAUNCHED();
     return SCVT_OK;
 }
 
-// flip rounds on the queued candidates (queue 0, cnt[0]) until none is left or the round
-// limit.  Double-buffered queues (d_cand, d_cand + 3n) and touched-cell lists; each round is
-// three launches (k_round_lock, k_flip_apply, k_round_finish) and no memset; cnt: [0] [1]
-// queue lengths, [2] [3] list lengths, [4] flips.  known_nonzero: the caller knows there are
-// candidates (no host read before the first batch).
-int flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host,
-                bool known_nonzero = false) {
+// Flip rounds on the queued candidates (queue 0, cnt[0]), enqueued without any host read:
+// ctx->flip_grid_rounds grid-wide rounds (three launches each: k_round_lock, k_flip_apply,
+// k_round_finish; double-buffered queues d_cand / d_cand + 3n and touched-cell lists, no
+// memsets), then k_flip_tail runs the remaining rounds in one block and marks what it gives
+// up on as bad.  Leaves d_bad / d_nbad as the rebuild path expects them: the cells of
+// orientation or consistency failures, of rejected flips and of candidates still open.
+int flip_rounds_enqueue(scvt_ctx* ctx, const double* z, int64_t n) {
     cudaStream_t s = ctx->stream;
     int* cnt = ctx->d_fcnt;
-    const int cap = (int)(3 * n);
-    int4* cand[2] = {ctx->d_cand, ctx->d_cand + 3 * n};
-    int* list[2] = {ctx->d_flist, ctx->d_flist + n};
-    int cur = 0, rounds = 0, flips_seen = -1;
-    bool skip_read = known_nonzero;
+    const int cap = (int)n;          // queue capacity (more candidates: rebuild path)
+    int4* cand[2] = {ctx->d_cand, ctx->d_cand + n};
+    int* list[2] = {ctx->d_flist, ctx->d_flist + 4 * n};   // four slots per candidate
+    int cur = 0;
     // grid-stride kernels over at most n items per round: small meshes get small grids
     // (scheduling 1184 mostly idle blocks costs several microseconds per launch at c1)
     const unsigned fb = (unsigned)std::min<int64_t>(SPEC_BLOCKS, blocks_for(n, 128));
+    const unsigned ab = (unsigned)std::min<int64_t>(SPEC_BLOCKS, blocks_for(2 * n, APPLY_THREADS));
     const unsigned vb = (unsigned)std::min<int64_t>(SPEC_BLOCKS, blocks_for(VERIFY_LANES * n, 128));
-    for (;;) {
-        if (!skip_read) {
-            CK(cudaMemcpyAsync(ctx->h_small, cnt, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(ctx->h_small + 8, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            if (ctx->h_small[cur] == 0 || rounds >= FLIP_MAX_ROUNDS) break;
-            // a whole batch without a flip: the open candidates are stuck (flips rejected at
-            // their vertices), so they go to the rebuild path now instead of after the limit
-            if (ctx->h_small[4] == flips_seen) break;
-            flips_seen = ctx->h_small[4];
-        }
-        skip_read = false;
-        for (int r = 0; r < FLIP_ROUNDS_PER_SYNC && rounds < FLIP_MAX_ROUNDS; ++r, ++rounds) {
-            const int nxt = 1 - cur;
-            k_round_lock<<<fb, 256, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock,
-                                            cnt + 2 + nxt, cnt + nxt);
-            LAUNCHED();
-            k_flip_apply<<<fb, 128, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock, ctx->d_nbr,
-                                            ctx->d_deg, ctx->d_fflag, list[nxt], cnt + 2 + nxt,
-                                            ctx->d_bad, ctx->d_nbad, cnt + 4);
-            LAUNCHED();
-            const VerifyArgs v{z, ctx->d_ids, 0, (int)n, list[nxt], cnt + 2 + nxt, ctx->d_nbr,
-                               ctx->d_deg, ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2,
-                               ctx->d_bad, ctx->d_nbad, FlipQueue{cand[nxt], cnt + nxt, cap}, 1};
-            k_round_finish<<<vb, 128, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock,
-                                              ctx->d_fflag, v);
-            LAUNCHED();
-            cur = nxt;
-        }
-    }
-    const bool open = ctx->h_small[cur] > 0;
-    if (open) {   // unconverged: those cells are rebuilt
-        k_cand_bad<<<fb, 256, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_bad, ctx->d_nbad);
+    const int G = std::max(0, std::min(ctx->flip_grid_rounds, FLIP_GRID_ROUNDS_MAX));
+    for (int r = 0; r < G; ++r) {
+        const int nxt = 1 - cur;
+        k_round_lock<<<fb, 256, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock, cnt + nxt,
+                                        ctx->d_fhist + r);
         LAUNCHED();
-        CK(cudaMemcpyAsync(ctx->h_small + 8, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        k_flip_apply<<<ab, APPLY_THREADS, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock,
+                                                  ctx->d_nbr, ctx->d_deg, ctx->d_fflag, list[nxt],
+                                                  ctx->d_bad, ctx->d_nbad, cnt + 4);
+        LAUNCHED();
+        const VerifyArgs v{z, ctx->d_ids, 0, (int)n, list[nxt], nullptr, ctx->d_nbr,
+                           ctx->d_deg, ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2,
+                           ctx->d_bad, ctx->d_nbad, FlipQueue{cand[nxt], cnt + nxt, cap}, 1, 0};
+        k_round_finish<<<vb, 128, 0, s>>>(cand[cur], cnt + cur, cap, ctx->d_lock, ctx->d_fflag, v);
+        LAUNCHED();
+        cur = nxt;
     }
-    *nbad_host = ctx->h_small[8];
-    ctx->flip_stats[0] += 1;
-    ctx->flip_stats[1] += rounds;
-    ctx->flip_stats[2] += ctx->h_small[4];
-    ctx->flip_stats[3] += open ? 1 : 0;
+    const VerifyArgs v{z, ctx->d_ids, 0, (int)n, nullptr, nullptr, ctx->d_nbr, ctx->d_deg,
+                       ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad,
+                       FlipQueue{nullptr, nullptr, cap}, 1, 0};
+    k_flip_tail<<<TAIL_CTAS, TAIL_THREADS, 0, s>>>(cand[0], cand[1], cnt, cur, cap, ctx->d_lock,
+                                           ctx->d_nbr, ctx->d_deg, ctx->d_fflag, list[0], list[1], v);
+    LAUNCHED();
+    ctx->flip_rounds_enqueued = G;
     return SCVT_OK;
 }
 
-// Certificate pass over every cell in flip mode, then Lawson flip rounds (detection of the
-// touched cells after each), FLIP_ROUNDS_PER_SYNC rounds chained on the device between host
-// reads.  Leaves d_bad / d_nbad as the rebuild path expects them: the cells of orientation or
-// consistency failures, of rejected flips and of candidates still open after the last round.
+// After a readback of the status block (h_status holds d_nbad, d_fcnt and d_fhist): the
+// repair's statistics, the number of grid-wide rounds for the next evaluation (as many as
+// started with more than FLIP_TAIL_ENTER candidates this time, one more when the tail was
+// entered with more), and the bad count.
+int flip_account(scvt_ctx* ctx) {
+    const int* fc = ctx->h_status + 24;
+    const int* hist = ctx->h_status + 32;
+    const int G = ctx->flip_rounds_enqueued;
+    int big = 0, used = 0;
+    for (int r = 0; r < G; ++r) {
+        used += hist[r] > 0;
+        big += hist[r] > FLIP_TAIL_ENTER;
+    }
+    int next = big;
+    if (big == G && fc[6] > FLIP_TAIL_ENTER) next = G + 1 + (fc[6] > 8 * FLIP_TAIL_ENTER);
+    ctx->flip_grid_rounds = std::min(next, FLIP_GRID_ROUNDS_MAX);
+    ctx->flip_stats[0] += 1;
+    ctx->flip_stats[1] += used + fc[5];
+    ctx->flip_stats[2] += fc[4];
+    ctx->flip_stats[3] += fc[7] > 0 ? 1 : 0;
+    ctx->last_flips = fc[4];
+    return ctx->h_status[16];
+}
+
+// synchronous flip repair (sharded entry points): detection, rounds, one readback
 int flip_repair(scvt_ctx* ctx, const double* z, int64_t n, int* nbad_host) {
     TRY(flip_detect(ctx, z, n, 0, n));
-    // the previous evaluation needed flips: so will this one, most likely — start the first
-    // batch of rounds without reading the candidate count (empty rounds are no-ops)
-    const int64_t flips0 = ctx->flip_stats[2];
-    TRY(flip_rounds(ctx, z, n, nbad_host, ctx->last_flips > 0));
-    ctx->last_flips = ctx->flip_stats[2] - flips0;
+    TRY(flip_rounds_enqueue(ctx, z, n));
+    TRY(readback(ctx, 0));
+    *nbad_host = flip_account(ctx);
     return SCVT_OK;
 }
 
+// The reuse path once the certificate's bad count is known on the host (nbad > 0): rebuild
+// (grid method) only the cells of failing triangles, re-certify those cells and their previous
+// neighbours; the first two rebuild rounds are chained on the device and read back once.
 // The bucket grid is only needed to rebuild cells: it is built on demand (*have_grid), so an
 // evaluation certified by the flip pass keeps the previous slot order (any permutation is
 // valid; outputs do not depend on it).
-int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, GridView& g, bool* have_grid,
-                      bool* done) {
+int rebuild_bad_cells(scvt_ctx* ctx, const double* z, int64_t n, int nbad, GridView& g,
+                      bool* have_grid, bool* done) {
     cudaStream_t s = ctx->stream;
     *done = false;
-    CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
-    CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
-    int nbad = 0;
-    if (flips_enabled()) {
-        TRY(flip_repair(ctx, z, n, &nbad));
-    } else {
-        TRY(verify_range(ctx, z, 0, n, 1));
-        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        nbad = ctx->h_small[0];
-    }
     ctx->reuse_stats[0] += 1;                       // certificate passes run
     ctx->reuse_stats[1] += nbad;
     if (nbad == 0) { *done = true; return SCVT_OK; }
@@ -2238,23 +2396,69 @@ int build_cells_reuse(scvt_ctx* ctx, const double* z, int64_t n, GridView& g, bo
     return SCVT_OK;
 }
 
-int build_cells(scvt_ctx* ctx, const double* z, int64_t n) {
+int build_cells_full(scvt_ctx* ctx, const double* z, int64_t n, GridView& g, bool have_grid) {
+    if (!have_grid) TRY(build_grid(ctx, z, n, &g));
+    TRY(build_cells_range(ctx, g, 0, n));
+    return verify_range(ctx, z, 0, n, 0);
+}
+
+// Cells for an evaluation at z.  With certified cycles of the previous evaluation at hand they
+// are reused: flip-mode certificate + flip rounds.  deferred != null: the repair is only
+// ENQUEUED and *deferred set -- the caller runs the moments behind it (they skip themselves on
+// the device when d_nbad != 0), reads d_nbad back with the evaluation's scalars and calls
+// build_cells_resume if it is not zero: a certified evaluation costs one host round trip.
+int build_cells(scvt_ctx* ctx, const double* z, int64_t n, bool* deferred = nullptr) {
     GridView g;
     bool have_grid = false;
+    cudaStream_t s = ctx->stream;
+    if (deferred) *deferred = false;
     if (ctx->cycles_n == n && reuse_enabled()) {
-        if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], s));
+        CK(cudaMemsetAsync(ctx->d_bad, 0, n * sizeof(int), s));
+        CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
+        int nbad = 0;
+        if (flips_enabled()) {
+            if (deferred) {
+                TRY(flip_detect(ctx, z, n, 0, n));
+                TRY(flip_rounds_enqueue(ctx, z, n));
+                if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
+                *deferred = true;
+                return SCVT_OK;
+            }
+            TRY(flip_repair(ctx, z, n, &nbad));
+        } else {
+            TRY(verify_range(ctx, z, 0, n, 1));
+            CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            nbad = ctx->h_small[0];
+        }
         bool done = false;
-        TRY(build_cells_reuse(ctx, z, n, g, &have_grid, &done));
-        if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        TRY(rebuild_bad_cells(ctx, z, n, nbad, g, &have_grid, &done));
+        if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
         if (done) {
             ctx->reuse_stats[2] += 1;
             return SCVT_OK;
         }
-        CK(cudaMemsetAsync(ctx->d_status + 8, 0, 8 * sizeof(int), ctx->stream));
+        CK(cudaMemsetAsync(ctx->d_status + 8, 0, 8 * sizeof(int), s));
     }
-    if (!have_grid) TRY(build_grid(ctx, z, n, &g));
-    TRY(build_cells_range(ctx, g, 0, n));
-    return verify_range(ctx, z, 0, n, 0);
+    return build_cells_full(ctx, z, n, g, have_grid);
+}
+
+// a deferred flip repair reported nbad > 0 bad cells: the rebuild path, then (if the churn is
+// too large or the rounds do not converge) everything from scratch
+int build_cells_resume(scvt_ctx* ctx, const double* z, int64_t n, int nbad) {
+    GridView g;
+    bool have_grid = false, done = false;
+    cudaStream_t s = ctx->stream;
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], s));
+    TRY(rebuild_bad_cells(ctx, z, n, nbad, g, &have_grid, &done));
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
+    if (done) {
+        ctx->reuse_stats[2] += 1;
+        return SCVT_OK;
+    }
+    CK(cudaMemsetAsync(ctx->d_status + 8, 0, 8 * sizeof(int), s));
+    return build_cells_full(ctx, z, n, g, have_grid);
 }
 
 int cells_from_triangles(scvt_ctx* ctx, const int64_t* tri, int64_t t, int64_t n) {
@@ -2286,7 +2490,8 @@ int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t sme
 }
 
 // incidence CSR over the sorted slots [lo, hi) (spatially coherent warps)
-int incidences_range(scvt_ctx* ctx, int64_t lo, int64_t hi, int64_t cap) {
+int incidences_range(scvt_ctx* ctx, int64_t lo, int64_t hi, int64_t cap,
+                     const int* skip = nullptr) {
     cudaStream_t s = ctx->stream;
     int64_t cnt = hi - lo;
     k_deg_sorted<<<blocks_for(cnt + 1, 256), 256, 0, s>>>((int)lo, (int)cnt, ctx->d_ids,
@@ -2298,7 +2503,7 @@ int incidences_range(scvt_ctx* ctx, int64_t lo, int64_t hi, int64_t cap) {
     k_fill_incidences<<<blocks_for(cnt, 256), 256, 0, s>>>((int)lo, (int)cnt, ctx->d_ids,
                                                            ctx->d_deg, ctx->d_inc_start,
                                                            ctx->d_inc_base, ctx->d_inc_gen,
-                                                           (int)cap);
+                                                           (int)cap, skip, ctx->d_inc_start + cnt);
     LAUNCHED();
     return SCVT_OK;
 }
@@ -2341,7 +2546,8 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
 // fixed-chunk reductions of E_i, |g_i|^2, obtuse_i over ALL n generators (id order), so the
 // scalars are bitwise identical whatever the shard count; reads back and checks status
 int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* diag,
-                  const double* grad, const double* q3, const double* norms, int nsc) {
+                  const double* grad, const double* q3, const double* norms, int nsc,
+                  int* deferred_nbad = nullptr) {
     cudaStream_t s = ctx->stream;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
@@ -2352,6 +2558,20 @@ int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* 
     TRY(reduce_chunks(ctx, ctx->d_partials, 5, ops));
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[5], s));
     TRY(readback(ctx, 5));
+    if (deferred_nbad) {
+        // the flip repair enqueued ahead of these moments: its statistics and bad count
+        *deferred_nbad = flip_account(ctx);
+        if (*deferred_nbad != 0) {     // not certified: the moments skipped themselves
+            if (ctx->prof) {
+                float a = 0.f;
+                CK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+                ctx->prof_ms[0] += a;   // the resumed rebuild adds its share and the count
+            }
+            return SCVT_OK;
+        }
+        ctx->reuse_stats[0] += 1;
+        ctx->reuse_stats[2] += 1;
+    }
     if (ctx->prof) {
         float a = 0.f, b = 0.f, c = 0.f;
         CK(cudaEventElapsedTime(&b, ctx->ev[2], ctx->ev[3]));
@@ -2375,16 +2595,16 @@ int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* 
 
 int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
             double* mass, double* diag, double* scalars_host, const double* q3 = nullptr,
-            const double* norms = nullptr, int nsc = 3) {
+            const double* norms = nullptr, int nsc = 3, int* deferred_nbad = nullptr) {
     int64_t n_inc = 6 * n - 12;   // Euler: a closed triangulation has exactly 6n-12 incidences
-    TRY(incidences_range(ctx, 0, n, n_inc));
+    TRY(incidences_range(ctx, 0, n, n_inc, deferred_nbad ? ctx->d_nbad : nullptr));
     TRY(quad_range(ctx, z, n, 0, n, n_inc));
     k_gather<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
         z, (int)n, (int)n, ctx->d_inc_start, ctx->d_inc_base, ctx->d_deg, ctx->d_part,
         ctx->d_obt, n_inc, grad, first, mass, diag, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen,
         ctx->split);
     LAUNCHED();
-    return reduce_finish(ctx, n, scalars_host, diag, grad, q3, norms, nsc);
+    return reduce_finish(ctx, n, scalars_host, diag, grad, q3, norms, nsc, deferred_nbad);
 }
 
 inline void shard_range(int64_t n, int shard, int nshards, int64_t* lo, int64_t* hi) {
@@ -2715,21 +2935,25 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_egen, n); AL(d_g2gen, n); AL(d_obgen, n);
     AL(d_partials, std::max<int64_t>((int64_t)MAX_SLOTS * RED_BLOCKS, (int64_t)MAX_RED_VALS * CHUNKS));
     AL(d_scal, MAX_RED_VALS);
-    AL(d_status, 16);
+    AL(d_status, 64);
+    ctx->d_nbad = ctx->d_status + 16;
+    ctx->d_fcnt = ctx->d_status + 24;
+    ctx->d_fhist = ctx->d_status + 32;
     AL(d_diag, 10);
-    AL(d_bad, n); AL(d_nbad, 1); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
-    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_cand, 6 * n); AL(d_lock, n); AL(d_flist, 2 * n); AL(d_fflag, n); AL(d_fcnt, 8); AL(d_counts, MAX_SHARDS + 1);
+    AL(d_bad, n); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
+    AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_cand, 2 * n); AL(d_lock, n); AL(d_flist, 8 * n); AL(d_fflag, n); AL(d_counts, MAX_SHARDS + 1);
     AL(d_S, (int64_t)ctx->m * 3 * n); AL(d_Y, (int64_t)ctx->m * 3 * n);
     AL(d_alpha, ctx->m);
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
     AL(d_coef, 2 * MAXM);
 #undef AL
-    if (cudaMemset(ctx->d_lock, 0xFF, (size_t)n * sizeof(unsigned long long)) != cudaSuccess ||
+    if (cudaMemset(ctx->d_status, 0, 64 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(ctx->d_lock, 0xFF, (size_t)n * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(ctx->d_fflag, 0, (size_t)n * sizeof(int)) != cudaSuccess)
         return bail(fail(ctx, SCVT_ERR_CUDA, "flip buffers init failed"));
     {
         cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_RED_VALS * sizeof(double));
-        cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 16 * sizeof(int));
+        cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 64 * sizeof(int));
         cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 32 * sizeof(int));
         cudaError_t e4 = cudaMallocHost((void**)&ctx->h_counts, (MAX_SHARDS + 1) * sizeof(int));
         cudaError_t e5 = cudaMallocHost((void**)&ctx->h_dir, 2 * sizeof(double));
@@ -2805,8 +3029,8 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_OK;
-    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_dp, ctx->d_diag, ctx->d_bad, ctx->d_nbad,
-                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_wdir, ctx->d_cgv, ctx->d_cg, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_fcnt, ctx->d_counts,
+    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_dp, ctx->d_diag, ctx->d_bad,
+                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_wdir, ctx->d_cgv, ctx->d_cg, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_counts,
                    ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
                    ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
                    ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
@@ -2895,10 +3119,20 @@ int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, do
     ctx->prof_n[3] = 0;
     TRY(reset_status(ctx));
     const int nsc = q3 ? 5 : (norms ? 4 : 3);
-    int rc = build_cells(ctx, z, n);
+    bool deferred = false;
+    int nbad = 0;
+    int rc = build_cells(ctx, z, n, &deferred);
     if (rc == SCVT_OK)
         rc = moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host, q3, norms,
-                     q3 ? 5 : 4);
+                     q3 ? 5 : 4, deferred ? &nbad : nullptr);
+    if (rc == SCVT_OK && deferred && nbad != 0) {
+        // the flips left bad cells: rebuild them (host-driven rounds), then the moments again
+        rc = reset_status(ctx);
+        if (rc == SCVT_OK) rc = build_cells_resume(ctx, z, n, nbad);
+        if (rc == SCVT_OK)
+            rc = moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host, q3, norms,
+                         q3 ? 5 : 4);
+    }
     (void)nsc;
     ctx->cycles_n = rc == SCVT_OK ? n : -1;   // certified cycles may seed the next evaluation
     return rc;
@@ -3016,7 +3250,10 @@ int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshard
                         (long long)counts[r], (long long)cap);
         total += counts[r];
     }
-    if (total > 3 * n) return fail(ctx, SCVT_ERR_CAPACITY, "%lld flip candidates", (long long)total);
+    if (total > n) {               // more than the queue holds: the caller takes the rebuild rounds
+        *nbad_host = (int32_t)std::min<int64_t>(total, INT32_MAX);
+        return SCVT_OK;
+    }
     total = 0;
     for (int r = 0; r < nshards; ++r) {        // the shards' candidates, in rank order
         if (counts[r] > 0)
@@ -3025,10 +3262,12 @@ int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshard
         total += counts[r];
     }
     ctx->h_small[8] = (int)total;
-    CK(cudaMemsetAsync(ctx->d_fcnt, 0, 8 * sizeof(int), s));
+    CK(cudaMemsetAsync(ctx->d_fcnt, 0, (8 + FLIP_HIST) * sizeof(int), s));
     CK(cudaMemcpyAsync(ctx->d_fcnt, ctx->h_small + 8, sizeof(int), cudaMemcpyHostToDevice, s));
     int nbad = 0;
-    TRY(flip_rounds(ctx, z, n, &nbad, total > 0));
+    TRY(flip_rounds_enqueue(ctx, z, n));
+    TRY(readback(ctx, 0));
+    nbad = flip_account(ctx);
     if (nbad == 0) ctx->reuse_stats[2] += 1;   // certified: the evaluation reuses all cycles
     *nbad_host = nbad;
     return SCVT_OK;
