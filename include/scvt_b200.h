@@ -124,6 +124,16 @@ int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, do
                      double* mass, double* lloyd_diag, const double* q3, const double* norms,
                      double* scalars_host);
 
+/* scvt_evaluate_ex for a line-search trial that also STAGES the correction pair the optimizer
+ * would push if it accepts this point (s = z - z_old, y = grad - g_old; optimizer.py:351-353):
+ * the pair's scalars (y.s, s.s, y.y, max|s| and the products with the stored pairs) are reduced
+ * with the evaluation's and come back in the same host read, so that
+ * scvt_history_commit_staged needs no kernel pass and no host round trip.  A later evaluation,
+ * scvt_history_push or scvt_history_clear drops the staged pair. */
+int scvt_evaluate_staged(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                         double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                         const double* z_old, const double* g_old, double* scalars_host);
+
 /* Moments only over an externally supplied canonical triangulation (T,3) int64 — used by
  * parity tests to isolate the quadrature from the triangulation. Same outputs as above. */
 int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n,
@@ -317,6 +327,11 @@ int scvt_history_gamma(scvt_ctx* ctx, double* gamma_host);
 int scvt_history_push(scvt_ctx* ctx, const double* z_old, const double* z_new,
                       const double* g_old, const double* g_new, int64_t n,
                       int32_t* pushed_host, double* movement_host);
+/* scvt_history_push of the pair staged by scvt_evaluate_staged(z_new -> g_new): same outputs,
+ * same curvature test; SCVT_ERR_CONFIG when no pair is staged for exactly these buffers and
+ * this history state (the caller then uses scvt_history_push). */
+int scvt_history_commit_staged(scvt_ctx* ctx, const double* z_new, const double* g_new,
+                               int64_t n, int32_t* pushed_host, double* movement_host);
 /* two_loop_direction (optimizer.py:147-167): q = -H g with h0 = diag(1/lloyd_diag) blockwise
  * when inv_diag_src != NULL (LloydDiagonal, optimizer.py:127-134; the ARRAY passed is
  * lloyd_diag itself, inverted on the fly), else gamma*I (GammaIdentity, 117-124).

@@ -62,6 +62,8 @@ SIGNATURES = {
     "scvt_evaluate": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _c_dbl_p]),
     "scvt_evaluate_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp,
                                         _c_dbl_p]),
+    "scvt_evaluate_staged": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                            _vp, _vp, _c_dbl_p]),
     "scvt_evaluate_on_triangles": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
                                                   _vp, _vp, _vp, _vp, _c_dbl_p]),
     "scvt_cell_energy": (ctypes.c_int, [_vp, ctypes.c_int64, _vp]),
@@ -116,6 +118,8 @@ SIGNATURES = {
     "scvt_history_gamma": (ctypes.c_int, [_vp, _c_dbl_p]),
     "scvt_history_push": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _c_i32_p,
                                          _c_dbl_p]),
+    "scvt_history_commit_staged": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _c_i32_p,
+                                                  _c_dbl_p]),
     "scvt_lbfgs_direction": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int64, _vp,
                                             _c_dbl_p]),
     "scvt_lbfgs_direction_tangent": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _vp,

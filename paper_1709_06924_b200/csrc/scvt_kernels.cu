@@ -1934,6 +1934,12 @@ struct scvt_ctx {
     double* d_coef = nullptr;          // two-loop coefficients a[MAXM], c[MAXM] (device)
     int hist_head = 0, hist_count = 0;
     double* d_tmp_s = nullptr; double* d_tmp_y = nullptr;   // staging for push
+    // history pair staged by an evaluation (scvt_evaluate_staged): its scalars came back with
+    // the evaluation's, so committing it needs no kernel pass and no host round trip
+    bool staged_valid = false;
+    const double* staged_z = nullptr; const double* staged_g = nullptr;
+    int staged_head = 0, staged_count = 0;
+    double staged_sc[4 + 2 * 16] = {};
     // live per-kernel timing (bench roofline): pairs {cells, quad, evaluate}
     bool prof = false;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -2543,21 +2549,26 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
     return SCVT_OK;
 }
 
+int pair_phase(scvt_ctx* ctx, const double* zo, const double* zn, const double* go,
+               const double* gn, const Chunks& ck, double* red, int* nval);
+
 // fixed-chunk reductions of E_i, |g_i|^2, obtuse_i over ALL n generators (id order), so the
 // scalars are bitwise identical whatever the shard count; reads back and checks status
 int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* diag,
                   const double* grad, const double* q3, const double* norms, int nsc,
-                  int* deferred_nbad = nullptr) {
+                  int* deferred_nbad = nullptr, int pair_vals = 0) {
     cudaStream_t s = ctx->stream;
     Chunks ck;
     TRY(make_chunks(ctx, n, 0, 1, &ck));
     k_eval_reduce<<<ck.nc, RED_THREADS, 0, s>>>(ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, diag,
                                                  grad, q3, norms, ck, ctx->d_partials);
     LAUNCHED();
-    static const unsigned char ops[5] = {0, 0, 0, 2, 0};
-    TRY(reduce_chunks(ctx, ctx->d_partials, 5, ops));
+    // values 0-4: the evaluation's scalars; 5 ..: the staged history pair's (max at 5 + 3)
+    unsigned char ops[5 + 4 + 2 * MAXM] = {0, 0, 0, 2, 0};
+    for (int v = 0; v < pair_vals; ++v) ops[5 + v] = v == 3 ? 1 : 0;
+    TRY(reduce_chunks(ctx, ctx->d_partials, 5 + pair_vals, ops));
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[5], s));
-    TRY(readback(ctx, 5));
+    TRY(readback(ctx, 5 + pair_vals));
     if (deferred_nbad) {
         // the flip repair enqueued ahead of these moments: its statistics and bad count
         *deferred_nbad = flip_account(ctx);
@@ -2595,7 +2606,8 @@ int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* 
 
 int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
             double* mass, double* diag, double* scalars_host, const double* q3 = nullptr,
-            const double* norms = nullptr, int nsc = 3, int* deferred_nbad = nullptr) {
+            const double* norms = nullptr, int nsc = 3, int* deferred_nbad = nullptr,
+            const double* pair_z_old = nullptr, const double* pair_g_old = nullptr) {
     int64_t n_inc = 6 * n - 12;   // Euler: a closed triangulation has exactly 6n-12 incidences
     TRY(incidences_range(ctx, 0, n, n_inc, deferred_nbad ? ctx->d_nbad : nullptr));
     TRY(quad_range(ctx, z, n, 0, n, n_inc));
@@ -2604,7 +2616,24 @@ int moments(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* fir
         ctx->d_obt, n_inc, grad, first, mass, diag, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen,
         ctx->split);
     LAUNCHED();
-    return reduce_finish(ctx, n, scalars_host, diag, grad, q3, norms, nsc, deferred_nbad);
+    int pair_vals = 0;
+    ctx->staged_valid = false;
+    if (pair_z_old && pair_g_old) {
+        // the history pair this point would make if the line search accepts it (it usually
+        // does): staged now so that its scalars ride on this evaluation's readback
+        Chunks ck;
+        TRY(make_chunks(ctx, n, 0, 1, &ck));
+        TRY(pair_phase(ctx, pair_z_old, z, pair_g_old, grad, ck, ctx->d_partials + 5 * CHUNKS,
+                       &pair_vals));
+    }
+    TRY(reduce_finish(ctx, n, scalars_host, diag, grad, q3, norms, nsc, deferred_nbad, pair_vals));
+    if (pair_vals && !(deferred_nbad && *deferred_nbad != 0)) {
+        for (int v = 0; v < pair_vals; ++v) ctx->staged_sc[v] = ctx->h_scal[5 + v];
+        ctx->staged_valid = true;
+        ctx->staged_z = z; ctx->staged_g = grad;
+        ctx->staged_head = ctx->hist_head; ctx->staged_count = ctx->hist_count;
+    }
+    return SCVT_OK;
 }
 
 inline void shard_range(int64_t n, int shard, int nshards, int64_t* lo, int64_t* hi) {
@@ -2706,6 +2735,9 @@ int pair_phase(scvt_ctx* ctx, const double* zo, const double* zn, const double* 
 
 // history push, phase 2: fixed-order scalars, curvature test (optimizer.py:98-104), commit of
 // the staged slice into the ring slot and of the cross products into the host y.s matrix
+int commit_scalars(scvt_ctx* ctx, const double* sc, int64_t len, int32_t* pushed_host,
+                   double* movement_host);
+
 int commit_phase(scvt_ctx* ctx, const double* red, int64_t len, int32_t* pushed_host,
                  double* movement_host) {
     const int K = ctx->hist_count;
@@ -2713,8 +2745,17 @@ int commit_phase(scvt_ctx* ctx, const double* red, int64_t len, int32_t* pushed_
     for (int v = 0; v < 4 + 2 * K; ++v) ops[v] = v == 3 ? 1 : 0;
     TRY(reduce_chunks(ctx, red, 4 + 2 * K, ops));
     TRY(readback(ctx, 4 + 2 * K));
-    double ys = ctx->h_scal[0], ss = ctx->h_scal[1], yy = ctx->h_scal[2];
-    *movement_host = ctx->h_scal[3];
+    return commit_scalars(ctx, ctx->h_scal, len, pushed_host, movement_host);
+}
+
+// the host half of a push: sc = {y.s, s.s, y.y, max|s|, y_new.s_k (K), y_k.s_new (K)} of the
+// pair staged in d_tmp_s / d_tmp_y
+int commit_scalars(scvt_ctx* ctx, const double* sc, int64_t len, int32_t* pushed_host,
+                   double* movement_host) {
+    const int K = ctx->hist_count;
+    ctx->staged_valid = false;
+    double ys = sc[0], ss = sc[1], yy = sc[2];
+    *movement_host = sc[3];
     if (ys <= 1e-14 * sqrt(ss) * sqrt(yy)) {
         *pushed_host = 0;
         return SCVT_OK;
@@ -2731,8 +2772,8 @@ int commit_phase(scvt_ctx* ctx, const double* red, int64_t len, int32_t* pushed_
     for (int k = 0; k < K; ++k) {                 // cross products with the kept pairs
         const int sk = (ctx->hist_head + k) % ctx->m;
         if (sk == slot) continue;                 // the pair being overwritten
-        ctx->YS[slot][sk] = ctx->h_scal[4 + k];       // y_new . s_k
-        ctx->YS[sk][slot] = ctx->h_scal[4 + K + k];   // y_k . s_new
+        ctx->YS[slot][sk] = sc[4 + k];       // y_new . s_k
+        ctx->YS[sk][slot] = sc[4 + K + k];   // y_k . s_new
     }
     ctx->YS[slot][slot] = ys;
     if (ctx->hist_count < ctx->m) ++ctx->hist_count;
@@ -3110,11 +3151,9 @@ int scvt_evaluate(scvt_ctx* ctx, const double* z, int64_t n, double* grad, doubl
     return rc;
 }
 
-int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
-                     double* mass, double* lloyd_diag, const double* q3, const double* norms,
-                     double* scalars_host) {
-    DeviceGuard dg_(ctx);
-    if (!ctx) return SCVT_ERR_CONFIG;
+static int evaluate_impl(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                         double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                         const double* z_old, const double* g_old, double* scalars_host) {
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[4], ctx->stream));
     ctx->prof_n[3] = 0;
     TRY(reset_status(ctx));
@@ -3124,18 +3163,49 @@ int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, do
     int rc = build_cells(ctx, z, n, &deferred);
     if (rc == SCVT_OK)
         rc = moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host, q3, norms,
-                     q3 ? 5 : 4, deferred ? &nbad : nullptr);
+                     q3 ? 5 : 4, deferred ? &nbad : nullptr, z_old, g_old);
     if (rc == SCVT_OK && deferred && nbad != 0) {
         // the flips left bad cells: rebuild them (host-driven rounds), then the moments again
         rc = reset_status(ctx);
         if (rc == SCVT_OK) rc = build_cells_resume(ctx, z, n, nbad);
         if (rc == SCVT_OK)
             rc = moments(ctx, z, n, grad, first, mass, lloyd_diag, scalars_host, q3, norms,
-                         q3 ? 5 : 4);
+                         q3 ? 5 : 4, nullptr, z_old, g_old);
     }
     (void)nsc;
     ctx->cycles_n = rc == SCVT_OK ? n : -1;   // certified cycles may seed the next evaluation
     return rc;
+}
+
+int scvt_evaluate_ex(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                     double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                     double* scalars_host) {
+    DeviceGuard dg_(ctx);
+    if (!ctx) return SCVT_ERR_CONFIG;
+    return evaluate_impl(ctx, z, n, grad, first, mass, lloyd_diag, q3, norms, nullptr, nullptr,
+                         scalars_host);
+}
+
+// scvt_evaluate_ex that also stages the LBFGS pair (z - z_old, grad - g_old) this point would
+// push if the line search accepts it; scvt_history_commit_staged then commits it without a
+// kernel pass or a host round trip (the pair's scalars came back with the evaluation's).
+int scvt_evaluate_staged(scvt_ctx* ctx, const double* z, int64_t n, double* grad, double* first,
+                         double* mass, double* lloyd_diag, const double* q3, const double* norms,
+                         const double* z_old, const double* g_old, double* scalars_host) {
+    DeviceGuard dg_(ctx);
+    if (!ctx) return SCVT_ERR_CONFIG;
+    return evaluate_impl(ctx, z, n, grad, first, mass, lloyd_diag, q3, norms, z_old, g_old,
+                         scalars_host);
+}
+
+int scvt_history_commit_staged(scvt_ctx* ctx, const double* z_new, const double* g_new,
+                               int64_t n, int32_t* pushed_host, double* movement_host) {
+    DeviceGuard dg_(ctx);
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (!ctx->staged_valid || ctx->staged_z != z_new || ctx->staged_g != g_new ||
+        ctx->staged_head != ctx->hist_head || ctx->staged_count != ctx->hist_count)
+        return fail(ctx, SCVT_ERR_CONFIG, "no staged history pair for this point");
+    return commit_scalars(ctx, ctx->staged_sc, n, pushed_host, movement_host);
 }
 
 int scvt_evaluate_on_triangles(scvt_ctx* ctx, const double* z, int64_t n, const int64_t* tri,
@@ -3799,6 +3869,7 @@ int scvt_history_clear(scvt_ctx* ctx) {
     if (!ctx) return SCVT_ERR_CONFIG;
     ctx->hist_head = 0;
     ctx->hist_count = 0;
+    ctx->staged_valid = false;
     return SCVT_OK;
 }
 

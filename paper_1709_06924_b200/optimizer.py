@@ -241,11 +241,19 @@ class _DeviceOps:
     def scale(self, a, x, y):
         self.ctx.call("scvt_scale", float(a), _lib.dptr(x), x.numel(), _lib.dptr(y))
 
-    def push(self, z_old, z_new, g_old, g_new):
+    stage_pairs = True   # line-search trials stage their correction pair (one host round trip
+                         # per iteration instead of two)
+
+    def push(self, z_old, z_new, g_old, g_new, staged=False):
         pushed = ctypes.c_int32()
         mv = ctypes.c_double()
-        self.ctx.call("scvt_history_push", _lib.dptr(z_old), _lib.dptr(z_new), _lib.dptr(g_old),
-                      _lib.dptr(g_new), self.n, ctypes.byref(pushed), ctypes.byref(mv))
+        if staged:    # the pair was reduced with z_new's evaluation (scvt_evaluate_staged)
+            self.ctx.call("scvt_history_commit_staged", _lib.dptr(z_new), _lib.dptr(g_new),
+                          self.n, ctypes.byref(pushed), ctypes.byref(mv))
+        else:
+            self.ctx.call("scvt_history_push", _lib.dptr(z_old), _lib.dptr(z_new),
+                          _lib.dptr(g_old), _lib.dptr(g_new), self.n, ctypes.byref(pushed),
+                          ctypes.byref(mv))
         return bool(pushed.value), mv.value
 
     def max_abs_diff(self, a, b) -> float:
@@ -325,6 +333,7 @@ class HostEvaluatorAdapter:
     def optimizer_ops(self, ctx, n):
         ops = _DeviceOps(ctx, n)
         ops.speculate = False
+        ops.stage_pairs = False
         return ops
 
     def redecompose(self, points):
@@ -388,6 +397,7 @@ class Minimizer:
         self.n = 0
         self.q = self.ops.vec3(self.z)
         self.q3 = self.ops.vec3(self.z)
+        self._last_eval = None
 
     def step(self):
         """One iteration (optimizer.py:300-366).  Returns (record, movement, z_new, res_new)
@@ -425,6 +435,15 @@ class Minimizer:
                     return ops.direction_tangent(res.grad, diag, gamma, z, q3)
             # optimizer.py:147-167, 312-333
             first = None
+            # trials stage the correction pair they would push (z, g are this iteration's)
+            stage = getattr(ops, "stage_pairs", False)
+
+            def trial_eval(zt, q3, norms):
+                r = (ev.evaluate_device(zt, q3, norms, pair=(z, res.grad)) if stage
+                     else ev.evaluate_device(zt, q3, norms))
+                self._last_eval = r
+                return r
+
             if getattr(ops, "speculate", False) and not self.method.startswith("laplacian"):
                 # the direction and the alpha = 1 trial (always the line search's first) are
                 # enqueued back to back; the direction's scalars are read after the trial's
@@ -435,7 +454,7 @@ class Minimizer:
                 ops.trial(z, q3, 1.0, zt, norms)
                 err = r1 = None
                 try:
-                    r1 = ev.evaluate_device(zt, q3, norms)
+                    r1 = trial_eval(zt, q3, norms)
                 except Exception as exc:  # noqa: BLE001 - re-raised below unless discarded
                     err = exc
                 qg, dphi0 = ops.direction_result()
@@ -462,7 +481,7 @@ class Minimizer:
                 zt = ops.positions(z)
                 norms = ops.scalars(z)
                 ops.trial(z, q3, alpha, zt, norms)
-                r = ev.evaluate_device(zt, q3, norms)            # derivative fused in
+                r = trial_eval(zt, q3, norms)                    # derivative fused in
                 return r.energy, r.dirderiv, (zt, r)
 
             try:
@@ -479,10 +498,17 @@ class Minimizer:
                 z_new = ops.positions(z)
                 ops.lloyd(res.first, z_new)
                 res_new = ev.evaluate_device(z_new)
+                self._last_eval = res_new
                 fevals_iter = 1
                 alpha = 0.0
             self.fevals += fevals_iter
-            _, movement = ops.push(z, z_new, res.grad, res_new.grad)   # optimizer.py:351-355
+            # optimizer.py:351-355; the pair staged by res_new's own evaluation is still the
+            # context's staged one only if that evaluation was the last (a zoom may end on an
+            # earlier trial): the commit checks the buffers and the general push is the fallback
+            if getattr(res_new, "staged", False) and self._last_eval is res_new:
+                _, movement = ops.push(z, z_new, res.grad, res_new.grad, staged=True)
+            else:
+                _, movement = ops.push(z, z_new, res.grad, res_new.grad)
         rec = IterationRecord(n=n, energy=res_new.energy, grad_norm=res_new.grad_norm, step=alpha,
                               fevals=fevals_iter, time_ms=(time.perf_counter() - t_iter) * 1e3)
         self.z, self.res = z_new, res_new

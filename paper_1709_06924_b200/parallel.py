@@ -587,7 +587,9 @@ class ShardedMeshEvaluator(MeshEvaluator):
     def optimizer_ops(self, ctx, n: int):
         """One GPU: the all-rows algebra; several: this rank's arithmetic slice."""
         if self.world == 1:
-            return super().optimizer_ops(ctx, n)
+            ops = super().optimizer_ops(ctx, n)
+            ops.stage_pairs = False      # the sharded evaluation has no staged-pair variant
+            return ops
         return SliceOps(ctx, n, self.rank, self.world, self.group)
 
     def _sum(self, t):

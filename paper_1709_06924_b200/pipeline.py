@@ -61,6 +61,7 @@ class EvalResult:
     obtuse_count: int = 0
     min_diag: float = float("nan")      # min lloyd_diag (cvt_core.py:184 test), device path
     dirderiv: float = float("nan")      # sum g.(q3/|v|) when evaluated as a line-search trial
+    staged: bool = False                # the evaluation staged its LBFGS pair (evaluate_device)
 
 
 class DeviceLaplacian:
@@ -340,10 +341,12 @@ class MeshEvaluator:
             raise ValueError("points must be (K, 3)")
         return torch.from_numpy(arr).to(f"cuda:{self._device_index()}"), True
 
-    def evaluate_device(self, z, q3=None, norms=None) -> EvalResult:
+    def evaluate_device(self, z, q3=None, norms=None, pair=None) -> EvalResult:
         """Device-resident evaluation: ``z`` is a contiguous float64 CUDA tensor (K, 3).
         With ``q3``/``norms`` (a line-search trial z = v/|v|, v = z0 + alpha q3) the result also
-        carries the directional derivative sum g.(q3/|v|) (optimizer.py:330)."""
+        carries the directional derivative sum g.(q3/|v|) (optimizer.py:330).  ``pair`` =
+        (z_old, g_old): also stage the LBFGS correction pair this point would push
+        (`scvt_evaluate_staged`), so the optimizer's push costs no further host round trip."""
         torch = _torch()
         n = z.shape[0]
         ctx = self._ensure_ctx(n)
@@ -352,9 +355,14 @@ class MeshEvaluator:
         mass = torch.empty(n, dtype=torch.float64, device=z.device)
         diag = torch.empty(n, dtype=torch.float64, device=z.device)
         sc = (ctypes.c_double * 5)()
-        ctx.call("scvt_evaluate_ex", _lib.dptr(z), n, _lib.dptr(grad), _lib.dptr(first),
-                 _lib.dptr(mass), _lib.dptr(diag), _lib.dptr(q3), _lib.dptr(norms), sc,
-                 what="evaluate")
+        if pair is not None:
+            ctx.call("scvt_evaluate_staged", _lib.dptr(z), n, _lib.dptr(grad), _lib.dptr(first),
+                     _lib.dptr(mass), _lib.dptr(diag), _lib.dptr(q3), _lib.dptr(norms),
+                     _lib.dptr(pair[0]), _lib.dptr(pair[1]), sc, what="evaluate")
+        else:
+            ctx.call("scvt_evaluate_ex", _lib.dptr(z), n, _lib.dptr(grad), _lib.dptr(first),
+                     _lib.dptr(mass), _lib.dptr(diag), _lib.dptr(q3), _lib.dptr(norms), sc,
+                     what="evaluate")
         self.evaluations += 1
         migration = self._migration(z)
         self._region_fallback(z)
@@ -362,7 +370,7 @@ class MeshEvaluator:
                           lloyd_diag=diag, first=first, mass=mass, obtuse_count=int(sc[2]),
                           min_diag=float(sc[3]),
                           dirderiv=float(sc[4]) if q3 is not None else float("nan"),
-                          migration=migration,
+                          migration=migration, staged=pair is not None,
                           laplacian=(DeviceLaplacian(ctx, n, self.laplacian, z.device)
                                      if self.laplacian is not None else None))
 

@@ -284,6 +284,29 @@ def test_determinism_bitwise():
     assert np.array_equal(a.grad, b.grad)
 
 
+@pytest.mark.parametrize("density,n,iters", [("c4", 40962, 12), ("x64", 2562, 25)])
+def test_staged_history_pair_is_bitwise_the_push(density, n, iters):
+    """Line-search trials stage their LBFGS pair (scvt_evaluate_staged) and the push commits
+    it from the evaluation's own readback: the run is bitwise the one that makes every pair
+    with scvt_history_push, including iterations that zoom, reset or fall back to Lloyd."""
+    import torch
+
+    den = P.density_preset(density)
+    z0 = P.random_sphere_points(n, 0) if density == "x64" else P.sample_by_density(den, n, 0)
+    runs = []
+    for stage in (True, False):
+        with P.MeshEvaluator(den, "7pt" if density == "c4" else "4pt",
+                             subdivision=3 if density == "c4" else 0) as ev:
+            st = P.Minimizer(torch.from_numpy(z0).cuda(), "lloyd-plbfgs", ev, 5)
+            st.ops.stage_pairs = stage
+            recs = [st.step()[0] for _ in range(iters)]
+            runs.append((st.z.cpu().numpy(), [(r.energy, r.grad_norm, r.step, r.fevals)
+                                              for r in recs], st.resets))
+    assert runs[0][1] == runs[1][1]
+    assert runs[0][2] == runs[1][2]
+    assert np.array_equal(runs[0][0], runs[1][0])
+
+
 # ------------------------------------------------------------------------- trajectories
 def _run_traj(g, density, rule, depth, method, m, iters):
     snaps = {}
