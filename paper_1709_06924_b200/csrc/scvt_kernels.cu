@@ -2265,7 +2265,14 @@ int reuse_round_device(scvt_ctx* ctx, const double* z, int64_t n, const GridView
 // on the device and read back once.
 bool flips_enabled() { return getenv("SCVT_NO_FLIPS") == nullptr; }
 constexpr int FLIP_GRID_ROUNDS_MAX = 10;   // grid-wide rounds before the single-block tail
-constexpr int FLIP_TAIL_ENTER = 512;       // queue length the tail handles well (32 warps)
+// queue length below which the remaining rounds go to the cluster tail (128 warps)
+int flip_tail_enter() {
+    static const int v = [] {
+        const char* e = getenv("SCVT_TAIL_ENTER");
+        return e ? atoi(e) : 128;
+    }();
+    return v;
+}
 constexpr int FLIP_HIST = 16;              // d_fhist: queue length at the start of each grid round
 
 // detection pass of the flip repair over the sorted slots [lo, hi): candidates and bad marks
@@ -2333,7 +2340,7 @@ int flip_rounds_enqueue(scvt_ctx* ctx, const double* z, int64_t n) {
 
 // After a readback of the status block (h_status holds d_nbad, d_fcnt and d_fhist): the
 // repair's statistics, the number of grid-wide rounds for the next evaluation (as many as
-// started with more than FLIP_TAIL_ENTER candidates this time, one more when the tail was
+// started with more than flip_tail_enter() candidates this time, one more when the tail was
 // entered with more), and the bad count.
 int flip_account(scvt_ctx* ctx) {
     const int* fc = ctx->h_status + 24;
@@ -2342,10 +2349,10 @@ int flip_account(scvt_ctx* ctx) {
     int big = 0, used = 0;
     for (int r = 0; r < G; ++r) {
         used += hist[r] > 0;
-        big += hist[r] > FLIP_TAIL_ENTER;
+        big += hist[r] > flip_tail_enter();
     }
     int next = big;
-    if (big == G && fc[6] > FLIP_TAIL_ENTER) next = G + 1 + (fc[6] > 8 * FLIP_TAIL_ENTER);
+    if (big == G && fc[6] > flip_tail_enter()) next = G + 1 + (fc[6] > 8 * flip_tail_enter());
     ctx->flip_grid_rounds = std::min(next, FLIP_GRID_ROUNDS_MAX);
     ctx->flip_stats[0] += 1;
     ctx->flip_stats[1] += used + fc[5];

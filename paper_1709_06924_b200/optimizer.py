@@ -398,6 +398,12 @@ class Minimizer:
         self.q = self.ops.vec3(self.z)
         self.q3 = self.ops.vec3(self.z)
         self._last_eval = None
+        import inspect
+
+        try:    # an evaluator (or subclass) whose evaluate_device takes no `pair` never stages
+            self._ev_stages = "pair" in inspect.signature(evaluator.evaluate_device).parameters
+        except (TypeError, ValueError):
+            self._ev_stages = False
 
     def step(self):
         """One iteration (optimizer.py:300-366).  Returns (record, movement, z_new, res_new)
@@ -436,7 +442,7 @@ class Minimizer:
             # optimizer.py:147-167, 312-333
             first = None
             # trials stage the correction pair they would push (z, g are this iteration's)
-            stage = getattr(ops, "stage_pairs", False)
+            stage = getattr(ops, "stage_pairs", False) and self._ev_stages
 
             def trial_eval(zt, q3, norms):
                 r = (ev.evaluate_device(zt, q3, norms, pair=(z, res.grad)) if stage

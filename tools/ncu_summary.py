@@ -38,6 +38,17 @@ def summary(rep, kernel_filter=None):
             if key in hdr:
                 k = hdr.index(key)
                 res[key] = f"{vals[k]} {units[k]}".strip()
+        # warp stall reasons (cycles stalled per issued instruction), largest first
+        stalls = []
+        for k, name in enumerate(hdr):
+            if "issue_stalled" in name and name.endswith("_per_warp_active.pct"):
+                try:
+                    stalls.append((float(vals[k].replace(",", "")), name))
+                except ValueError:
+                    pass
+        for v, name in sorted(stalls, reverse=True)[:6]:
+            short = name.split("issue_stalled_")[1].replace("_per_warp_active.pct", "")
+            res[f"stall {short}"] = f"{v:.1f} % of warp-active cycles"
     return res
 
 
