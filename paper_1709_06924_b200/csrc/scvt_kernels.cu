@@ -43,7 +43,10 @@ constexpr int CHUNKS = SCVT_CHUNKS;
 constexpr int MAX_RED_VALS = 176;    // >= 2K + K(K+1)/2 + 1 for K <= 16
 constexpr int RED_THREADS = 256;
 constexpr int VEC_THREADS = 256;
-constexpr int QUAD_THREADS = 128;
+#ifndef QUAD_THREADS_DEF
+#define QUAD_THREADS_DEF 128
+#endif
+constexpr int QUAD_THREADS = QUAD_THREADS_DEF;   // k_quad block size
 #ifndef QUAD_MINB
 #define QUAD_MINB 5      // k_quad fast path: CTAs per SM the register budget must allow
 #endif
@@ -1920,8 +1923,9 @@ struct scvt_ctx {
     int* d_fflag = nullptr;            // [n]
     int* d_fcnt = nullptr;             // [8] flip counters (queues, lists, flips, tail): d_status + 24
     int* d_fhist = nullptr;            // [16] queue length per grid-wide round: d_status + 32
-    int flip_grid_rounds = 3;          // grid-wide rounds before k_flip_tail (adapted per evaluation)
+    int flip_grid_rounds = 6;          // grid-wide rounds before k_flip_tail (adapted per evaluation)
     int flip_rounds_enqueued = 0;      // grid-wide rounds of the repair in flight
+    int last_nbad = 0;                 // bad cells the previous flip repair left (rebuild path taken)
     int64_t flip_stats[4] = {0, 0, 0, 0};   // evaluations, rounds, flips, fell back
     int64_t last_flips = 0;                  // flips of the previous repair
     int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
@@ -2359,6 +2363,7 @@ int flip_account(scvt_ctx* ctx) {
     ctx->flip_stats[2] += fc[4];
     ctx->flip_stats[3] += fc[7] > 0 ? 1 : 0;
     ctx->last_flips = fc[4];
+    ctx->last_nbad = ctx->h_status[16];
     return ctx->h_status[16];
 }
 
@@ -2431,7 +2436,11 @@ int build_cells(scvt_ctx* ctx, const double* z, int64_t n, bool* deferred = null
         CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
         int nbad = 0;
         if (flips_enabled()) {
-            if (deferred) {
+            // deferring pays when the repair certifies everything (the usual case while the
+            // mesh still moves a lot); late in a run a few folded cells need the rebuild path
+            // at almost every evaluation, and then reading the count right away is cheaper
+            // than moments that skip themselves (predicted from the previous evaluation)
+            if (deferred && ctx->last_nbad == 0) {
                 TRY(flip_detect(ctx, z, n, 0, n));
                 TRY(flip_rounds_enqueue(ctx, z, n));
                 if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
