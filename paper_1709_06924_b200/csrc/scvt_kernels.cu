@@ -614,7 +614,7 @@ __global__ void __cluster_dims__(TAIL_CTAS, 1, 1) __launch_bounds__(TAIL_THREADS
 k_flip_tail(int4* __restrict__ cand0, int4* __restrict__ cand1, int* __restrict__ cnt, int cur,
             int cap, unsigned long long* __restrict__ lock, int* __restrict__ nbr,
             int* __restrict__ deg, int* __restrict__ fflag, int* __restrict__ list0,
-            int* __restrict__ list1, VerifyArgs v) {
+            int* __restrict__ list1, VerifyArgs v, int max_rounds) {
     __shared__ int4 s_q[SINK_CAP];
     __shared__ int s_n;
     if (threadIdx.x == 0) s_n = 0;
@@ -626,7 +626,7 @@ k_flip_tail(int4* __restrict__ cand0, int4* __restrict__ cand1, int* __restrict_
     const int entry = min(__ldcg(cnt + cur), cap);
     for (;;) {
         const int nc = min(__ldcg(cnt + cur), cap);
-        if (nc == 0 || rounds >= TAIL_MAX_ROUNDS || stuck >= TAIL_STUCK) break;
+        if (nc == 0 || rounds >= max_rounds || stuck >= TAIL_STUCK) break;
         const int nxt = 1 - cur;
         const int4* cq = cur ? cand1 : cand0;
         int4* nq = cur ? cand0 : cand1;
@@ -1926,6 +1926,9 @@ struct scvt_ctx {
     int flip_grid_rounds = 6;          // grid-wide rounds before k_flip_tail (adapted per evaluation)
     int flip_rounds_enqueued = 0;      // grid-wide rounds of the repair in flight
     int last_nbad = 0;                 // bad cells the previous flip repair left (rebuild path taken)
+    int tail_enter = 128;              // see flip_account (SCVT_TAIL_ENTER)
+    int tail_rounds = TAIL_MAX_ROUNDS; // k_flip_tail round limit (SCVT_TAIL_ROUNDS: tests force give-ups)
+    int64_t flip_cap = 0;              // flip queue capacity, 0 = n (SCVT_FLIP_CAP: tests force overflows)
     int64_t flip_stats[4] = {0, 0, 0, 0};   // evaluations, rounds, flips, fell back
     int64_t last_flips = 0;                  // flips of the previous repair
     int* d_counts = nullptr;           // sharded reuse: per-shard bad counts [MAX_SHARDS+1]
@@ -2269,14 +2272,8 @@ int reuse_round_device(scvt_ctx* ctx, const double* z, int64_t n, const GridView
 // on the device and read back once.
 bool flips_enabled() { return getenv("SCVT_NO_FLIPS") == nullptr; }
 constexpr int FLIP_GRID_ROUNDS_MAX = 10;   // grid-wide rounds before the single-block tail
-// queue length below which the remaining rounds go to the cluster tail (128 warps)
-int flip_tail_enter() {
-    static const int v = [] {
-        const char* e = getenv("SCVT_TAIL_ENTER");
-        return e ? atoi(e) : 128;
-    }();
-    return v;
-}
+// ctx->tail_enter: queue length below which the remaining rounds go to the cluster tail
+// (128 warps); SCVT_TAIL_ENTER at context creation
 constexpr int FLIP_HIST = 16;              // d_fhist: queue length at the start of each grid round
 
 // detection pass of the flip repair over the sorted slots [lo, hi): candidates and bad marks
@@ -2285,7 +2282,7 @@ int flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t h
     int* cnt = ctx->d_fcnt;        // [0] candidates (queue 0); the rounds use the rest
     CK(cudaMemsetAsync(cnt, 0, (8 + FLIP_HIST) * sizeof(int), s));   // d_fcnt and d_fhist
     if (hi <= lo) return SCVT_OK;
-    const FlipQueue fq{ctx->d_cand, cnt, (int)n};
+    const FlipQueue fq{ctx->d_cand, cnt, (int)(ctx->flip_cap > 0 ? std::min(ctx->flip_cap, n) : n)};
     // a bounded grid: every block certifies many cells and stages its candidates in shared
     // memory (one global atomicAdd per block instead of one per candidate)
     const unsigned vb = (unsigned)std::min<int64_t>(2 * SPEC_BLOCKS,
@@ -2306,7 +2303,8 @@ int flip_detect(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t h
 int flip_rounds_enqueue(scvt_ctx* ctx, const double* z, int64_t n) {
     cudaStream_t s = ctx->stream;
     int* cnt = ctx->d_fcnt;
-    const int cap = (int)n;          // queue capacity (more candidates: rebuild path)
+    // queue capacity (more candidates: rebuild path)
+    const int cap = (int)(ctx->flip_cap > 0 ? std::min(ctx->flip_cap, n) : n);
     int4* cand[2] = {ctx->d_cand, ctx->d_cand + n};
     int* list[2] = {ctx->d_flist, ctx->d_flist + 4 * n};   // four slots per candidate
     int cur = 0;
@@ -2336,7 +2334,8 @@ int flip_rounds_enqueue(scvt_ctx* ctx, const double* z, int64_t n) {
                        ctx->d_amb, ctx->d_status, ctx->d_status + 8, 2, ctx->d_bad, ctx->d_nbad,
                        FlipQueue{nullptr, nullptr, cap}, 1, 0};
     k_flip_tail<<<TAIL_CTAS, TAIL_THREADS, 0, s>>>(cand[0], cand[1], cnt, cur, cap, ctx->d_lock,
-                                           ctx->d_nbr, ctx->d_deg, ctx->d_fflag, list[0], list[1], v);
+                                           ctx->d_nbr, ctx->d_deg, ctx->d_fflag, list[0], list[1], v,
+                                           ctx->tail_rounds);
     LAUNCHED();
     ctx->flip_rounds_enqueued = G;
     return SCVT_OK;
@@ -2344,7 +2343,7 @@ int flip_rounds_enqueue(scvt_ctx* ctx, const double* z, int64_t n) {
 
 // After a readback of the status block (h_status holds d_nbad, d_fcnt and d_fhist): the
 // repair's statistics, the number of grid-wide rounds for the next evaluation (as many as
-// started with more than flip_tail_enter() candidates this time, one more when the tail was
+// started with more than ctx->tail_enter candidates this time, one more when the tail was
 // entered with more), and the bad count.
 int flip_account(scvt_ctx* ctx) {
     const int* fc = ctx->h_status + 24;
@@ -2353,10 +2352,10 @@ int flip_account(scvt_ctx* ctx) {
     int big = 0, used = 0;
     for (int r = 0; r < G; ++r) {
         used += hist[r] > 0;
-        big += hist[r] > flip_tail_enter();
+        big += hist[r] > ctx->tail_enter;
     }
     int next = big;
-    if (big == G && fc[6] > flip_tail_enter()) next = G + 1 + (fc[6] > 8 * flip_tail_enter());
+    if (big == G && fc[6] > ctx->tail_enter) next = G + 1 + (fc[6] > 8 * ctx->tail_enter);
     ctx->flip_grid_rounds = std::min(next, FLIP_GRID_ROUNDS_MAX);
     ctx->flip_stats[0] += 1;
     ctx->flip_stats[1] += used + fc[5];
@@ -3076,6 +3075,9 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         OPT(DEN_TANH4_TAB); OPT(DEN_TANH4X2_TAB);
 #undef OPT
     }
+    if (const char* e = getenv("SCVT_TAIL_ENTER")) ctx->tail_enter = std::max(0, atoi(e));
+    if (const char* e = getenv("SCVT_TAIL_ROUNDS")) ctx->tail_rounds = std::max(0, atoi(e));
+    if (const char* e = getenv("SCVT_FLIP_CAP")) ctx->flip_cap = std::max(0, atoi(e));
     ctx->rho.assign(ctx->m, 0.0);
     ctx->ys.assign(ctx->m, 0.0);
     ctx->yy.assign(ctx->m, 0.0);
@@ -3336,7 +3338,8 @@ int scvt_shard_flip_rounds(scvt_ctx* ctx, const double* z, int64_t n, int nshard
                         (long long)counts[r], (long long)cap);
         total += counts[r];
     }
-    if (total > n) {               // more than the queue holds: the caller takes the rebuild rounds
+    if (total > (ctx->flip_cap > 0 ? std::min<int64_t>(ctx->flip_cap, n) : n)) {
+        // more than the queue holds: the caller takes the rebuild rounds
         *nbad_host = (int32_t)std::min<int64_t>(total, INT32_MAX);
         return SCVT_OK;
     }

@@ -307,6 +307,35 @@ def test_staged_history_pair_is_bitwise_the_push(density, n, iters):
     assert np.array_equal(runs[0][0], runs[1][0])
 
 
+@pytest.mark.parametrize("env", [{"SCVT_TAIL_ROUNDS": "0"}, {"SCVT_TAIL_ROUNDS": "1"},
+                                 {"SCVT_FLIP_CAP": "96"}, {"SCVT_TAIL_ENTER": "1000000"},
+                                 {"SCVT_TAIL_ENTER": "0"}])
+def test_flip_repair_give_up_and_overflow_paths(monkeypatch, env):
+    """What the flip repair cannot finish -- candidates the cluster tail gives up on (round
+    limit 0 / 1), candidates beyond the queue capacity -- becomes bad cells for the rebuild
+    path, and every split between grid-wide rounds and the tail repairs the same cycles: the
+    run is bitwise the default one (the certified triangulation is unique)."""
+    import torch
+
+    den = P.density_preset("c4")
+    z0 = P.sample_by_density(den, 40962, 0)
+
+    def run():
+        with P.MeshEvaluator(den, "7pt", subdivision=3) as ev:
+            st = P.Minimizer(torch.from_numpy(z0).cuda(), "lloyd-plbfgs", ev, 7)
+            e = [st.step()[0].energy for _ in range(8)]
+            tri, _, _ = ev.triangulate_device(st.z)
+            return e, st.z.cpu().numpy(), tri.cpu().numpy()
+
+    ref = run()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)          # read at context creation
+    got = run()
+    assert got[0] == ref[0]
+    assert np.array_equal(got[1], ref[1])
+    assert np.array_equal(got[2], ref[2])
+
+
 # ------------------------------------------------------------------------- trajectories
 def _run_traj(g, density, rule, depth, method, m, iters):
     snaps = {}
