@@ -212,6 +212,11 @@ int scvt_shard_plan(scvt_ctx* ctx, int64_t n, int nshards, const int32_t* bad_al
 int scvt_shard_rebuild(scvt_ctx* ctx, int64_t n, int shard, int nshards, int64_t cap,
                        int32_t* rows_send);
 int scvt_shard_install(scvt_ctx* ctx, int64_t n, const int32_t* rows, int64_t nrows);
+/* scvt_shard_moments for certified held cycles (cyc_all == NULL) without a host read: k_quad
+ * takes the shard's incidence count from the device and the status word is copied to
+ * status_dev (device, 1 int32) for the caller's all-gather of the ranks' status words. */
+int scvt_shard_moments_async(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                             double* res_send, int32_t* status_dev);
 int scvt_shard_status(scvt_ctx* ctx, int32_t status);
 int scvt_shard_finish(scvt_ctx* ctx, const double* z, int64_t n, int nshards,
                       const double* res_all, double* grad, double* first, double* mass,

@@ -82,6 +82,8 @@ SIGNATURES = {
     "scvt_shard_rebuild": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int64, _vp]),
     "scvt_shard_install": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64]),
+    "scvt_shard_moments_async": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int,
+                                                ctypes.c_int, _vp, _vp]),
     "scvt_shard_status": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "scvt_shard_finish": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp,
                                          _vp, _vp, _c_dbl_p]),

@@ -721,7 +721,8 @@ struct QuadArgs {
     const int* inc_gen;
     int n;
     int cnt;                // owned sorted slots
-    int n_inc;            // expected incidences 6n - 12
+    int n_inc;            // expected incidences 6n - 12 (n_inc_dev: an upper bound, see k_quad)
+    int n_inc_dev;        // 1: the incidence count is inc_start[cnt] on the device (shards, fast path)
     const DensityParams* dpg;   // device copy of dp (tab set): what out-of-line paths read
     const double* nodes;  // device [3][nq]: l1, l2, w
     const double* table;  // device rho^(1/4) table (tanh4 kinds) or null
@@ -735,7 +736,7 @@ struct QuadArgs {
 // SPLIT: one thread per fan sub-triangle instead of per incidence (twice the work units, a
 // finer last wave, shorter per-thread chains); the two halves land in part[0..5) and
 // part[5..10) and the gathers add them in a fixed order.
-template <int KIND, bool SPHERE, bool SYM7, bool SPLIT = false>
+template <int KIND, bool SPHERE, bool SYM7, bool SPLIT = false, bool DEVCOUNT = false>
 __global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? (KIND == DEN_TANH4X2_TAB ? QUAD_MINB2 : QUAD_MINB) : 1)
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
@@ -753,7 +754,17 @@ k_quad(QuadArgs a) {
     const int u = SPLIT ? t_id >> 1 : t_id;
     const int half = SPLIT ? t_id & 1 : 0;
     if (u >= a.n_inc) return;
-    if (a.inc_start[a.cnt] != a.n_inc) {   // not a closed triangulation: nothing to integrate
+    if (DEVCOUNT) {
+        // shards: only the device knows the shard's incidence count; n_inc bounds it (the
+        // grid's size).  A separate instantiation: this handful of instructions changes the
+        // register allocation of the whole kernel (240 B of spills instead of 20)
+        const int total = a.inc_start[a.cnt];
+        if (total > a.n_inc) {
+            if (u == 0) atomicOr(a.status, ST_EULER);
+            return;
+        }
+        if (u >= total) return;
+    } else if (a.inc_start[a.cnt] != a.n_inc) {   // not a closed triangulation: nothing to integrate
         if (u == 0) atomicOr(a.status, ST_EULER);
         return;
     }
@@ -1926,6 +1937,7 @@ struct scvt_ctx {
     int flip_grid_rounds = 6;          // grid-wide rounds before k_flip_tail (adapted per evaluation)
     int flip_rounds_enqueued = 0;      // grid-wide rounds of the repair in flight
     int last_nbad = 0;                 // bad cells the previous flip repair left (rebuild path taken)
+    bool shard_quad_pending = false;   // a sharded k_quad event pair not yet added to prof_ms
     int tail_enter = 128;              // see flip_account (SCVT_TAIL_ENTER)
     int tail_rounds = TAIL_MAX_ROUNDS; // k_flip_tail round limit (SCVT_TAIL_ROUNDS: tests force give-ups)
     int64_t flip_cap = 0;              // flip queue capacity, 0 = n (SCVT_FLIP_CAP: tests force overflows)
@@ -2501,6 +2513,9 @@ template <int KIND>
 int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t smem) {
     if (ctx->measure)
         k_quad<KIND, true, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
+    else if (ctx->sym7 && a.n_inc_dev)   // shards: incidence count on the device
+        k_quad<KIND, false, true, true, true><<<blocks_for(2 * (int64_t)a.n_inc, QUAD_THREADS),
+                                                 QUAD_THREADS, 21 * sizeof(double), ctx->stream>>>(a);
     else if (ctx->sym7)         // the fast path always runs a thread per fan sub-triangle
         k_quad<KIND, false, true, true><<<blocks_for(2 * (int64_t)a.n_inc, QUAD_THREADS),
                                            QUAD_THREADS, 21 * sizeof(double), ctx->stream>>>(a);
@@ -2531,11 +2546,12 @@ int incidences_range(scvt_ctx* ctx, int64_t lo, int64_t hi, int64_t cap,
 
 // fan quadrature over n_inc incidences of the slots [lo, hi)
 int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi,
-               int64_t n_inc) {
+               int64_t n_inc, bool count_on_device = false) {
     QuadArgs a;
     a.z = z; a.nbr = ctx->d_nbr; a.deg = ctx->d_deg; a.inc_start = ctx->d_inc_start;
     a.inc_base = ctx->d_inc_base;
     a.inc_gen = ctx->d_inc_gen; a.n = (int)n; a.cnt = (int)(hi - lo); a.n_inc = (int)n_inc;
+    a.n_inc_dev = count_on_device ? 1 : 0;
     a.nodes = ctx->d_nodes;
     a.nq = ctx->nq; a.dp = ctx->dp; a.part = ctx->d_part; a.obtuse = ctx->d_obt;
     a.table = ctx->d_table;
@@ -2884,9 +2900,24 @@ int scvt_profile_flips(scvt_ctx* ctx, int64_t* out4, int reset) {
     return SCVT_OK;
 }
 
+// the event pair of an asynchronous sharded k_quad launch (scvt_shard_moments_async), added
+// to the profile once it has completed
+static int flush_shard_quad(scvt_ctx* ctx) {
+    if (!ctx->shard_quad_pending) return SCVT_OK;
+    ctx->shard_quad_pending = false;
+    if (!ctx->prof) return SCVT_OK;
+    float ms = 0.f;
+    CK(cudaEventSynchronize(ctx->ev[3]));
+    CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+    ctx->prof_ms[1] += ms;
+    ++ctx->prof_n[1];
+    return SCVT_OK;
+}
+
 int scvt_profile_read(scvt_ctx* ctx, double* ms_out, int64_t* counts_out, int reset) {
     DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_ERR_CONFIG;
+    TRY(flush_shard_quad(ctx));
     for (int k = 0; k < 3; ++k) {
         ms_out[k] = ctx->prof_ms[k];
         counts_out[k] = ctx->prof_n[k];
@@ -3054,7 +3085,8 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
         // the split fast path adds its static per-thread fit slots (up to ~40 KB) to the
         // node table: opt in so that static + dynamic may exceed 48 KB
 #define OPT7(K) \
-    cudaFuncSetAttribute(k_quad<K, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+    cudaFuncSetAttribute(k_quad<K, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(k_quad<K, false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
         OPT7(DEN_CONST); OPT7(DEN_X3); OPT7(DEN_X16); OPT7(DEN_TANH); OPT7(DEN_TANH4);
         OPT7(DEN_TANH4X2); OPT7(DEN_TANH4_TAB); OPT7(DEN_TANH4X2_TAB);
 #undef OPT7
@@ -3520,6 +3552,43 @@ int scvt_shard_moments(scvt_ctx* ctx, const double* z, int64_t n, int shard, int
         ctx->prof_ms[1] += ms;
         ++ctx->prof_n[1];
     }
+    return SCVT_OK;
+}
+
+// scvt_shard_moments for cycles the sharded reuse rounds certified (cyc_all == NULL), without
+// a host read: k_quad takes the shard's incidence count from the device (its grid is sized
+// for an upper bound) and the status word is copied to status_dev (device, 1 int32), which
+// the caller all-gathers with the other ranks' anyway.
+int scvt_shard_moments_async(scvt_ctx* ctx, const double* z, int64_t n, int shard, int nshards,
+                             double* res_send, int32_t* status_dev) {
+    DeviceGuard dg_(ctx);
+    if (!ctx) return SCVT_ERR_CONFIG;
+    if (nshards < 1 || shard < 0 || shard >= nshards || !status_dev)
+        return fail(ctx, SCVT_ERR_CONFIG, "bad shard %d of %d", shard, nshards);
+    cudaStream_t s = ctx->stream;
+    TRY(flush_shard_quad(ctx));
+    int64_t lo, hi, cap = scvt_shard_rows(n, nshards);
+    shard_range(n, shard, nshards, &lo, &hi);
+    TRY(incidences_range(ctx, lo, hi, 6 * n));
+    int64_t bound;
+    if (ctx->sym7 && !ctx->measure) {
+        // valence averages < 6 over any large range; a shard that exceeded the bound would set
+        // ST_EULER (coverage error), never integrate a truncated range silently
+        bound = std::min<int64_t>(6 * n, 8 * (hi - lo) + 4096);
+        TRY(quad_range(ctx, z, n, lo, hi, bound, true));
+    } else {        // generic quadrature kernels take the exact count: one host read
+        int tot = 0;
+        CK(cudaMemcpyAsync(&tot, ctx->d_inc_start + (hi - lo), sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        bound = tot;
+        TRY(quad_range(ctx, z, n, lo, hi, bound));
+    }
+    k_gather_pack<<<blocks_for(cap, 128), 128, 0, s>>>(
+        (int)lo, (int)(hi - lo), (int)cap, ctx->d_ids, ctx->d_inc_base, ctx->d_deg, ctx->d_part,
+        ctx->d_obt, bound, res_send, ctx->split);
+    LAUNCHED();
+    CK(cudaMemcpyAsync(status_dev, ctx->d_status, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    ctx->shard_quad_pending = ctx->prof;   // its event pair is read once it has completed
     return SCVT_OK;
 }
 

@@ -69,8 +69,17 @@ class CudaShardBackend:
         ctx.call("scvt_shard_cells", _lib.dptr(z), z.shape[0], shard, nshards,
                  _lib.dptr(cyc_send), what="shard_cells")
 
-    def moments(self, z, shard, nshards, cyc_all, res_send) -> int:
+    def moments(self, z, shard, nshards, cyc_all, res_send):
+        """The shard's moments into res_send; returns its status word: an int, or (certified
+        held cycles, no host read) a 1-element int32 device tensor."""
         ctx = self.ev._ensure_ctx(z.shape[0])
+        if cyc_all is None:
+            import torch
+
+            st_dev = torch.empty(1, dtype=torch.int32, device=z.device)
+            ctx.call("scvt_shard_moments_async", _lib.dptr(z), z.shape[0], shard, nshards,
+                     _lib.dptr(res_send), _lib.dptr(st_dev), what="shard_moments")
+            return st_dev
         st = ctypes.c_int32(0)
         ctx.call("scvt_shard_moments", _lib.dptr(z), z.shape[0], shard, nshards,
                  _lib.dptr(cyc_all) if cyc_all is not None else None, _lib.dptr(res_send),
@@ -504,7 +513,8 @@ def sharded_evaluate(backend, z, rank: int, world: int, group=None, comm_device=
         backend.cells(z, rank, world, cyc_send)
         _all_gather(cyc_all, cyc_send, group)
         status = backend.moments(z, rank, world, cyc_all, res_send)
-    st = torch.tensor([status], dtype=torch.int32, device=cyc_send.device)
+    st = (status.to(cyc_send.device) if isinstance(status, torch.Tensor) else
+          torch.tensor([status], dtype=torch.int32, device=cyc_send.device))
     st_all = torch.empty(world, dtype=torch.int32, device=cyc_send.device)
     _all_gather(st_all, st, group)                            # everyone raises, or no one
     status = 0
@@ -550,9 +560,12 @@ def emulate_shards(backend, z, nshards: int, q3=None, norms=None):
             backend.cells(z, s, nshards, cyc_send)
             cyc_all[s * r:(s + 1) * r] = cyc_send
     status = 0
+    words = []
     for s in range(nshards):
-        status |= backend.moments(z, s, nshards, None if reused else cyc_all, res_send)
+        words.append(backend.moments(z, s, nshards, None if reused else cyc_all, res_send))
         res_all[s * r:(s + 1) * r] = res_send
+    for w in words:                 # device status words are read after every shard ran
+        status |= int(w.item()) if hasattr(w, "item") else int(w)
     if status:
         backend.raise_status(status)
     if q3 is None:
