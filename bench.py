@@ -198,6 +198,7 @@ def cpu_measure(cfg, steps, warmup, regions=0, evals_per_iteration=1.0):
             tot_owned += o
             tot_t += t
         return {"value": tot_owned / tot_t / evals_per_iteration,
+                "ms_per_step": tot_t / max(steps, 1) * 1e3,
                 "unit": "generator-updates/s", "cores": s.cores,
                 "kind": "port",
                 "sample": (f"oracle restatement of the reference region path (covering p={s.p}, "
@@ -221,7 +222,8 @@ def run_reference(a):
     cb = cpu_measure(a.config, a.steps, a.warmup, a.cpu_sample_regions)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"],
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            # wall time of one step = one bounded sample (cores regions) of the workload
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded rho-sampling, seed 0)",
             "config": {"workload": workload(a.config), "N": n,
                        "implementation": "reference algorithm on the host CPU cores "
