@@ -1938,6 +1938,7 @@ struct scvt_ctx {
     int flip_rounds_enqueued = 0;      // grid-wide rounds of the repair in flight
     int last_nbad = 0;                 // bad cells the previous flip repair left (rebuild path taken)
     bool shard_quad_pending = false;   // a sharded k_quad event pair not yet added to prof_ms
+    int deferred_rounds = 0;           // rebuild rounds chained behind the deferred flip repair
     int tail_enter = 128;              // see flip_account (SCVT_TAIL_ENTER)
     int tail_rounds = TAIL_MAX_ROUNDS; // k_flip_tail round limit (SCVT_TAIL_ROUNDS: tests force give-ups)
     int64_t flip_cap = 0;              // flip queue capacity, 0 = n (SCVT_FLIP_CAP: tests force overflows)
@@ -2357,7 +2358,7 @@ int flip_rounds_enqueue(scvt_ctx* ctx, const double* z, int64_t n) {
 // repair's statistics, the number of grid-wide rounds for the next evaluation (as many as
 // started with more than ctx->tail_enter candidates this time, one more when the tail was
 // entered with more), and the bad count.
-int flip_account(scvt_ctx* ctx) {
+int flip_account(scvt_ctx* ctx, bool deferred = false) {
     const int* fc = ctx->h_status + 24;
     const int* hist = ctx->h_status + 32;
     const int G = ctx->flip_rounds_enqueued;
@@ -2374,7 +2375,13 @@ int flip_account(scvt_ctx* ctx) {
     ctx->flip_stats[2] += fc[4];
     ctx->flip_stats[3] += fc[7] > 0 ? 1 : 0;
     ctx->last_flips = fc[4];
-    ctx->last_nbad = ctx->h_status[16];
+    // the bad count right after the flips (a deferred repair copies it to d_status[17] before
+    // any chained rebuild round changes d_nbad): the next evaluation's prediction
+    ctx->last_nbad = deferred ? ctx->h_status[17] : ctx->h_status[16];
+    if (deferred && ctx->deferred_rounds) {      // the chained rounds' certificate passes
+        ctx->reuse_stats[0] += ctx->deferred_rounds;
+        ctx->reuse_stats[1] += ctx->h_status[17] + ctx->h_status[18];
+    }
     return ctx->h_status[16];
 }
 
@@ -2447,13 +2454,31 @@ int build_cells(scvt_ctx* ctx, const double* z, int64_t n, bool* deferred = null
         CK(cudaMemsetAsync(ctx->d_nbad, 0, sizeof(int), s));
         int nbad = 0;
         if (flips_enabled()) {
-            // deferring pays when the repair certifies everything (the usual case while the
-            // mesh still moves a lot); late in a run a few folded cells need the rebuild path
-            // at almost every evaluation, and then reading the count right away is cheaper
-            // than moments that skip themselves (predicted from the previous evaluation)
-            if (deferred && ctx->last_nbad == 0) {
+            if (deferred) {
+                // Late in a run a few folded cells (no flip repairs those) need the rebuild
+                // path at almost every evaluation.  Predicted from the previous evaluation:
+                // the bucket grid is built up front and two rebuild rounds are chained on the
+                // device behind the flips (device-side counts, no-ops when nothing is bad), so
+                // this case, too, costs one host round trip.
+                const bool predicted = ctx->last_nbad > 0;
+                if (predicted) {
+                    TRY(build_grid(ctx, z, n, &g));
+                    have_grid = true;
+                }
                 TRY(flip_detect(ctx, z, n, 0, n));
                 TRY(flip_rounds_enqueue(ctx, z, n));
+                CK(cudaMemcpyAsync(ctx->d_status + 17, ctx->d_nbad, sizeof(int),
+                                   cudaMemcpyDeviceToDevice, s));
+                ctx->deferred_rounds = 0;
+                if (predicted) {
+                    for (int r = 0; r < 2; ++r) {
+                        TRY(reuse_round_device(ctx, z, n, g, -1));
+                        if (r == 0)
+                            CK(cudaMemcpyAsync(ctx->d_status + 18, ctx->d_nbad, sizeof(int),
+                                               cudaMemcpyDeviceToDevice, s));
+                    }
+                    ctx->deferred_rounds = 2;
+                }
                 if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
                 *deferred = true;
                 return SCVT_OK;
@@ -2480,11 +2505,21 @@ int build_cells(scvt_ctx* ctx, const double* z, int64_t n, bool* deferred = null
 // a deferred flip repair reported nbad > 0 bad cells: the rebuild path, then (if the churn is
 // too large or the rounds do not converge) everything from scratch
 int build_cells_resume(scvt_ctx* ctx, const double* z, int64_t n, int nbad) {
-    GridView g;
-    bool have_grid = false, done = false;
+    GridView g = ctx->gv;
+    bool have_grid = ctx->deferred_rounds > 0, done = false;
     cudaStream_t s = ctx->stream;
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], s));
-    TRY(rebuild_bad_cells(ctx, z, n, nbad, g, &have_grid, &done));
+    if (ctx->deferred_rounds == 0) {
+        TRY(rebuild_bad_cells(ctx, z, n, nbad, g, &have_grid, &done));
+    } else if (nbad <= (3 * n) / 4) {
+        // two rounds already ran behind the flips: the fourth and last pass
+        TRY(reuse_round_device(ctx, z, n, g, nbad));
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ctx->reuse_stats[0] += 1;
+        ctx->reuse_stats[1] += nbad;
+        done = ctx->h_small[0] == 0;
+    }
     if (ctx->prof) CK(cudaEventRecord(ctx->ev[1], s));
     if (done) {
         ctx->reuse_stats[2] += 1;
@@ -2602,7 +2637,7 @@ int reduce_finish(scvt_ctx* ctx, int64_t n, double* scalars_host, const double* 
     TRY(readback(ctx, 5 + pair_vals));
     if (deferred_nbad) {
         // the flip repair enqueued ahead of these moments: its statistics and bad count
-        *deferred_nbad = flip_account(ctx);
+        *deferred_nbad = flip_account(ctx, true);
         if (*deferred_nbad != 0) {     // not certified: the moments skipped themselves
             if (ctx->prof) {
                 float a = 0.f;
