@@ -21,6 +21,7 @@ import numpy as np
 from . import _lib
 from .errors import (
     CentroidAtOriginError,
+    ConfigError,
     LineSearchFailure,
     NonDescentError,
 )
@@ -511,9 +512,14 @@ class Minimizer:
             # optimizer.py:351-355; the pair staged by res_new's own evaluation is still the
             # context's staged one only if that evaluation was the last (a zoom may end on an
             # earlier trial): the commit checks the buffers and the general push is the fallback
+            done = False
             if getattr(res_new, "staged", False) and self._last_eval is res_new:
-                _, movement = ops.push(z, z_new, res.grad, res_new.grad, staged=True)
-            else:
+                try:
+                    _, movement = ops.push(z, z_new, res.grad, res_new.grad, staged=True)
+                    done = True
+                except ConfigError:     # the library holds no pair for these buffers
+                    logger.debug("staged pair unavailable at iteration %d; regular push", n)
+            if not done:
                 _, movement = ops.push(z, z_new, res.grad, res_new.grad)
         rec = IterationRecord(n=n, energy=res_new.energy, grad_norm=res_new.grad_norm, step=alpha,
                               fevals=fevals_iter, time_ms=(time.perf_counter() - t_iter) * 1e3)
