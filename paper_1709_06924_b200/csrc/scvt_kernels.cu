@@ -1904,6 +1904,8 @@ struct scvt_ctx {
     int* d_start = nullptr;
     double* d_zs = nullptr;
     void* d_cub = nullptr; size_t cub_bytes = 0;
+    char* arena = nullptr;       // the one device allocation every d_* buffer below lives in
+    void* h_arena = nullptr;     // the one pinned allocation of the h_* readback words
     // cells
     int* d_nbr = nullptr; int* d_deg = nullptr; uint8_t* d_amb = nullptr;
     int* d_inc_start = nullptr; int* d_inc_gen = nullptr; int* d_inc_base = nullptr;
@@ -3042,8 +3044,18 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     int64_t nb = 6LL * G * G;
     int64_t n_inc = 6 * n;
     int r = SCVT_OK;
+    // every per-context buffer is a 256-byte aligned range of ONE device allocation (and the
+    // pinned readback words of one host allocation): the ~50 cudaMalloc + 5 cudaMallocHost
+    // calls they replace cost 20 ms per context at N = 655,362
+    struct Slot { void** p; size_t off; };
+    std::vector<Slot> slots;
+    size_t arena_bytes = 0;
+    auto reserve = [&](void** p, size_t bytes) {
+        slots.push_back({p, arena_bytes});
+        arena_bytes += (std::max<size_t>(bytes, 1) + 255) & ~(size_t)255;
+    };
 #define AL(p, cnt) \
-    if ((r = dalloc(ctx, &ctx->p, (size_t)(cnt)))) return bail(r)
+    reserve((void**)&ctx->p, (size_t)(cnt) * sizeof(*ctx->p))
     AL(d_nodes, 3 * ctx->nq);
     AL(d_table, 2 * (int64_t)dp.tab_k * (TAB_P + 1));
     AL(d_dp, 1);
@@ -3058,9 +3070,6 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_partials, std::max<int64_t>((int64_t)MAX_SLOTS * RED_BLOCKS, (int64_t)MAX_RED_VALS * CHUNKS));
     AL(d_scal, MAX_RED_VALS);
     AL(d_status, 64);
-    ctx->d_nbad = ctx->d_status + 16;
-    ctx->d_fcnt = ctx->d_status + 24;
-    ctx->d_fhist = ctx->d_status + 32;
     AL(d_diag, 10);
     AL(d_bad, n); AL(d_slotflag, n); AL(d_list, n); AL(d_recheck, n); AL(d_nlist, 1);
     AL(d_list2, n); AL(d_nlist2, 1); AL(d_cnt, 1); AL(d_rcount, 4); AL(d_queue, 1); AL(d_mig, 1); AL(d_cand, 2 * n); AL(d_lock, n); AL(d_flist, 8 * n); AL(d_fflag, n); AL(d_counts, MAX_SHARDS + 1);
@@ -3069,33 +3078,42 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_tmp_s, 3 * n); AL(d_tmp_y, 3 * n);
     AL(d_coef, 2 * MAXM);
 #undef AL
+    // CUB temp storage: max of radix sort (n), scan (n+1) and flagged select (the size queries
+    // look at the argument types only)
+    {
+        size_t b1 = 0, b2 = 0, b3 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, b1, ctx->d_keys, ctx->d_skeys, ctx->d_vals,
+                                        ctx->d_ids, (int)n, 0, 32);
+        cub::DeviceScan::ExclusiveSum(nullptr, b2, ctx->d_deg, ctx->d_inc_start, (int)n + 1);
+        thrust::counting_iterator<int> it(0);
+        cub::DeviceSelect::Flagged(nullptr, b3, it, ctx->d_slotflag, ctx->d_list, ctx->d_nbad,
+                                   (int)n);
+        ctx->cub_bytes = std::max(std::max(b1, b2), b3);
+        reserve(&ctx->d_cub, ctx->cub_bytes);
+    }
+    if ((r = dalloc(ctx, &ctx->arena, arena_bytes))) return bail(r);
+    for (const Slot& sl : slots) *sl.p = ctx->arena + sl.off;
+    ctx->d_nbad = ctx->d_status + 16;
+    ctx->d_fcnt = ctx->d_status + 24;
+    ctx->d_fhist = ctx->d_status + 32;
     if (cudaMemset(ctx->d_status, 0, 64 * sizeof(int)) != cudaSuccess ||
         cudaMemset(ctx->d_lock, 0xFF, (size_t)n * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(ctx->d_fflag, 0, (size_t)n * sizeof(int)) != cudaSuccess)
         return bail(fail(ctx, SCVT_ERR_CUDA, "flip buffers init failed"));
     {
-        cudaError_t e1 = cudaMallocHost((void**)&ctx->h_scal, MAX_RED_VALS * sizeof(double));
-        cudaError_t e2 = cudaMallocHost((void**)&ctx->h_status, 64 * sizeof(int));
-        cudaError_t e3 = cudaMallocHost((void**)&ctx->h_small, 32 * sizeof(int));
-        cudaError_t e4 = cudaMallocHost((void**)&ctx->h_counts, (MAX_SHARDS + 1) * sizeof(int));
-        cudaError_t e5 = cudaMallocHost((void**)&ctx->h_dir, 2 * sizeof(double));
-        cudaError_t e6 = cudaEventCreateWithFlags(&ctx->dir_ev, cudaEventDisableTiming);
-        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
-            e5 != cudaSuccess || e6 != cudaSuccess)
+        // pinned readback words: h_scal [MAX_RED_VALS] doubles, h_dir [2] doubles, h_status
+        // [64], h_small [32], h_counts [MAX_SHARDS + 1] ints
+        size_t nd = MAX_RED_VALS + 2, ni = 64 + 32 + MAX_SHARDS + 1;
+        cudaError_t e1 = cudaMallocHost((void**)&ctx->h_arena, nd * sizeof(double) + ni * sizeof(int));
+        cudaError_t e2 = cudaEventCreateWithFlags(&ctx->dir_ev, cudaEventDisableTiming);
+        if (e1 != cudaSuccess || e2 != cudaSuccess)
             return bail(fail(ctx, SCVT_ERR_CUDA, "cudaMallocHost failed"));
+        ctx->h_scal = (double*)ctx->h_arena;
+        ctx->h_dir = ctx->h_scal + MAX_RED_VALS;
+        ctx->h_status = (int*)(ctx->h_dir + 2);
+        ctx->h_small = ctx->h_status + 64;
+        ctx->h_counts = ctx->h_small + 32;
     }
-    // CUB temp storage: max of radix sort (n) and scan (n+1)
-    size_t b1 = 0, b2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b1, ctx->d_keys, ctx->d_skeys, ctx->d_vals,
-                                    ctx->d_ids, (int)n, 0, 32);
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, ctx->d_deg, ctx->d_inc_start, (int)n + 1);
-    size_t b3 = 0;
-    {
-        thrust::counting_iterator<int> it(0);
-        cub::DeviceSelect::Flagged(nullptr, b3, it, ctx->d_slotflag, ctx->d_list, ctx->d_nbad, (int)n);
-    }
-    ctx->cub_bytes = std::max(std::max(b1, b2), b3);
-    if ((r = dalloc(ctx, (char**)&ctx->d_cub, ctx->cub_bytes))) return bail(r);
     // node table
     std::vector<double> tbl(3 * (size_t)ctx->nq);
     for (int q = 0; q < ctx->nq; ++q) {
@@ -3155,23 +3173,12 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
 int scvt_destroy(scvt_ctx* ctx) {
     DeviceGuard dg_(ctx);
     if (!ctx) return SCVT_OK;
-    void* dev[] = {ctx->d_nodes, ctx->d_table, ctx->d_dp, ctx->d_diag, ctx->d_bad,
-                   ctx->d_recheck, ctx->d_nlist, ctx->d_list2, ctx->d_nlist2, ctx->d_cnt, ctx->d_rcount, ctx->d_queue, ctx->d_mig, ctx->d_wdir, ctx->d_cgv, ctx->d_cg, ctx->d_cand, ctx->d_lock, ctx->d_flist, ctx->d_fflag, ctx->d_counts,
-                   ctx->d_slotflag, ctx->d_list, ctx->d_keys, ctx->d_skeys, ctx->d_vals, ctx->d_ids,
-                   ctx->d_start, ctx->d_zs, ctx->d_cub, ctx->d_nbr, ctx->d_deg, ctx->d_amb,
-                   ctx->d_inc_start, ctx->d_inc_gen, ctx->d_inc_base, ctx->d_pairs, ctx->d_cursor, ctx->d_part,
-                   ctx->d_obt, ctx->d_egen, ctx->d_g2gen, ctx->d_obgen, ctx->d_partials,
-                   ctx->d_scal, ctx->d_status, ctx->d_S, ctx->d_Y, ctx->d_alpha,
-                   ctx->d_tmp_s, ctx->d_tmp_y, ctx->d_coef};
+    void* dev[] = {ctx->arena, ctx->d_wdir, ctx->d_cgv, ctx->d_cg};   // arena + the lazy ones
     for (void* p : dev)
         if (p) cudaFree(p);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
-    if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
-    if (ctx->h_status) cudaFreeHost(ctx->h_status);
-    if (ctx->h_small) cudaFreeHost(ctx->h_small);
-    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
-    if (ctx->h_dir) cudaFreeHost(ctx->h_dir);
+    if (ctx->h_arena) cudaFreeHost(ctx->h_arena);
     if (ctx->dir_ev) cudaEventDestroy(ctx->dir_ev);
     delete ctx;
     return SCVT_OK;

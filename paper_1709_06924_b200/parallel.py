@@ -578,7 +578,7 @@ class ShardedMeshEvaluator(MeshEvaluator):
     (one GPU per rank, backend NCCL).  With world size 1 it runs the same sharded code path
     with no communication."""
 
-    def __init__(self, *args, group=None, backend=None, **kwargs):
+    def __init__(self, *args, group=None, backend=None, force_collectives=False, **kwargs):
         super().__init__(*args, **kwargs)
         import torch.distributed as dist
 
@@ -594,12 +594,14 @@ class ShardedMeshEvaluator(MeshEvaluator):
         else:
             self.rank, self.world = 0, 1
         self.backend = backend or CudaShardBackend(self)
-
+        # force_collectives: a one-rank group still goes through every collective call (the
+        # NCCL code path on a one-GPU box: tests/test_gpu_parity.py)
+        self.collective = self.world > 1 or (force_collectives and dist.is_initialized())
         self._red = None
 
     def optimizer_ops(self, ctx, n: int):
         """One GPU: the all-rows algebra; several: this rank's arithmetic slice."""
-        if self.world == 1:
+        if not self.collective:
             ops = super().optimizer_ops(ctx, n)
             ops.stage_pairs = False      # the sharded evaluation has no staged-pair variant
             return ops
@@ -611,7 +613,7 @@ class ShardedMeshEvaluator(MeshEvaluator):
     def evaluate_device(self, z, q3=None, norms=None) -> EvalResult:
         """World size 1: all rows.  Several ranks: the vectors of the result hold this rank's
         arithmetic slice (`slice_range`); the scalars are global."""
-        if self.world == 1:
+        if not self.collective:
             r = emulate_shards(self.backend, z, 1, q3, norms)
         else:
             import torch
@@ -635,7 +637,7 @@ class ShardedMeshEvaluator(MeshEvaluator):
 
         z, host = self._as_device(points)
         r = self.evaluate_device(z)
-        if self.world > 1:
+        if self.collective:
             r = SliceOps(self._ensure_ctx(z.shape[0]), z.shape[0], self.rank, self.world,
                          self.group).full(r)
         if host:

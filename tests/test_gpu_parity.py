@@ -716,6 +716,59 @@ def test_two_processes_sharded_run_matches_single_gpu(world, method):
         assert np.array_equal(out[rank]["diag"], ref.final.lloyd_diag)
 
 
+def _nccl_one_rank_worker(rank, port, z0, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    from paper_1709_06924_b200.parallel import ShardedMeshEvaluator
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        crit = P.StoppingCriteria(max_iterations=6)
+        with ShardedMeshEvaluator(P.density_preset("c4"), "7pt", subdivision=3,
+                                  force_collectives=True) as ev:
+            assert ev.collective
+            r = P.minimize(z0, "lloyd-plbfgs", ev, crit, corrections=7)
+            e = ev.evaluate(r.points)
+        dist.barrier()
+        out[0] = {"points": r.points, "energies": [h.energy for h in r.records],
+                  "fevals": r.fevals, "grad": r.final.grad, "diag": r.final.lloyd_diag,
+                  "e": e.energy}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_backend_one_rank_group_matches_single_gpu():
+    """The NCCL branch of every collective (all_gather_into_tensor on the padded device
+    buffers, all-reduce SUM / MAX of device tensors, the status all-gather) on a one-rank NCCL
+    group — what a one-GPU box can run of the real backend: the sharded evaluation and the
+    arithmetic-layout optimizer with `force_collectives`, bitwise equal to the single-GPU
+    run."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    z0 = P.sample_by_density(P.density_preset("c4"), 40962, 0)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = mp.Manager().dict()
+    mp.spawn(_nccl_one_rank_worker, args=(port, z0, out), nprocs=1, join=True)
+    with _ev("c4", "7pt", 3) as ev:
+        ref = P.minimize(z0, "lloyd-plbfgs", ev, P.StoppingCriteria(max_iterations=6),
+                         corrections=7)
+        e = ev.evaluate(ref.points)
+    assert np.array_equal(out[0]["points"], ref.points)
+    assert out[0]["energies"] == [h.energy for h in ref.records]
+    assert out[0]["fevals"] == ref.fevals
+    assert np.array_equal(out[0]["grad"], ref.final.grad)
+    assert np.array_equal(out[0]["diag"], ref.final.lloyd_diag)
+    assert out[0]["e"] == e.energy
+
+
 @pytest.mark.parametrize("sharded", [False, True])
 def test_reuse_escalates_to_full_rebuild_under_large_moves(sharded):
     """Positions moved by about a cell spacing between evaluations (most certificates fail):
