@@ -925,6 +925,8 @@ SCVT_HD double tab_u_chord(const DensityParams& p, double x, int br) {
     return acc;
 }
 
+constexpr double FIT_NOISE = 4e-15;   // rounding floor of rho = (table u)^4, relative
+
 struct LocalFit {
     double sc;          // centre of the s interval
     double b[7];        // rho(s) = sum_k b[k] (s - sc)^k
@@ -938,7 +940,8 @@ struct LocalFit {
 // 90 deg from c, comes too close to the sqrt singularity at s = 0, or the fit misses the table
 // by more than 4e-15 relative at any check point (the table itself is within 1.6e-15 of the
 // closed form; a degree-6 interpolant evaluated in FP64 has a ~1e-15 rounding floor).
-SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, LocalFit& f) {
+SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, LocalFit& f,
+                            int* drop = nullptr, double* tail_stats = nullptr) {
     constexpr double CHEB_V[7] = {0.9749279121818236, 0.7818314824680298, 0.4338837391175582,
                               6.123233995736766e-17, -0.43388373911755806, -0.7818314824680295,
                               -0.9749279121818237};
@@ -1003,7 +1006,7 @@ SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, Loca
 #pragma unroll
         for (int j = 1; j < 7; ++j) umin = fmin(umin, u[j]);
         const double a4 = fabs(a[4]), a5 = fabs(a[5]), a6 = fabs(a[6]);
-        const double noise = 4e-15 * umin, tol = 1.6e-14 * umin;
+        const double noise = FIT_NOISE * umin, tol = 1.6e-14 * umin;
         // division-free: with r <= 1/2, 1 / (1 - r) <= 2
         bool ok = true;
         if (a6 > noise)                         // a7 ~ a6 r, r = max(a6/a5, a5/a4)
@@ -1012,6 +1015,37 @@ SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, Loca
         else if (a5 > noise)                    // a7 ~ a5 r^2, r = a5/a4
             ok = a5 <= 0.5 * a4 && 2.0 * a5 * a5 * a5 <= tol * a4 * a4;
         if (!ok) return false;
+    }
+    // degree selection: |T_k| <= 1 on the interval, so dropping the last Chebyshev terms
+    // moves the polynomial by at most the sum of their magnitudes anywhere on the patch.  At
+    // the rounding floor of the table values (FIT_NOISE relative: the same floor the tail
+    // estimate above uses) a6, or a5 and a6, carry no information about rho -- they follow the
+    // table's rounding noise -- and are set to zero EXACTLY (b6 = 0, or b5 = b6 = 0 below); a
+    // warp whose patches all qualify evaluates the fit from b5 or b4 down: one or two steps
+    // less on every node's dependent chain.  A degree-6 Horner evaluation of such a fit gives
+    // the same bits (0 * s + b5 = b5), so the result of a patch does not depend on which
+    // sweep its warp takes (sharded and single-GPU runs group the patches differently).
+    {
+        double umin = u[0];
+#pragma unroll
+        for (int j = 1; j < 7; ++j) umin = fmin(umin, u[j]);
+        if (tail_stats) {
+            tail_stats[0] = fabs(a[6]) / umin;
+            tail_stats[1] = (fabs(a[6]) + fabs(a[5])) / umin;
+            tail_stats[2] = (fabs(a[6]) + fabs(a[5]) + fabs(a[4])) / umin;
+            tail_stats[3] = (fabs(a[6]) + fabs(a[5]) + fabs(a[4]) + fabs(a[3])) / umin;
+        }
+        const double a5 = fabs(a[5]), a6 = fabs(a[6]);
+        int d = 0;
+        if (a6 <= FIT_NOISE * umin) {
+            d = 1;
+            a[6] = 0.0;
+            if (a5 + a6 <= FIT_NOISE * umin) {
+                d = 2;
+                a[5] = 0.0;
+            }
+        }
+        if (drop) *drop = d;
     }
     double b[7];   // monomials in v = (s - sc) / hw
     b[0] = a[0] - a[2] + a[4] - a[6];
@@ -1147,24 +1181,27 @@ SCVT_HD double fit_rho(const FitEval& f, V3 x, double inv) {
     return acc;
 }
 
+// DEG: the fit's degree (6, or 5 / 4 when its last coefficients are exact zeros)
+template <int DEG = 6>
 SCVT_HD void fit_rho2(const FitEval& f, V3 x0, double inv0, V3 x1, double inv1, double* r0,
                       double* r1) {
     const double t0 = fma(x0.z, f.m2c.z, fma(x0.y, f.m2c.y, x0.x * f.m2c.x));
     const double t1 = fma(x1.z, f.m2c.z, fma(x1.y, f.m2c.y, x1.x * f.m2c.x));
     const double s0 = fma(inv0, t0, f.k0), s1 = fma(inv1, t1, f.k0);
-    double a0 = f.b[6], a1 = f.b[6];
+    double a0 = f.b[DEG], a1 = f.b[DEG];
 #pragma unroll
-    for (int k = 5; k >= 0; --k) { a0 = fma(a0, s0, f.b[k]); a1 = fma(a1, s1, f.b[k]); }
+    for (int k = DEG - 1; k >= 0; --k) { a0 = fma(a0, s0, f.b[k]); a1 = fma(a1, s1, f.b[k]); }
     *r0 = a0; *r1 = a1;
 }
 
 // as fit_rho2 / fit_rho with t = x.(-2 sigma c) supplied by the caller
+template <int DEG = 6>
 SCVT_HD void fit_rho2_t(const FitEval& f, double t0, double inv0, double t1, double inv1,
                         double* r0, double* r1) {
     const double s0 = fma(inv0, t0, f.k0), s1 = fma(inv1, t1, f.k0);
-    double a0 = f.b[6], a1 = f.b[6];
+    double a0 = f.b[DEG], a1 = f.b[DEG];
 #pragma unroll
-    for (int k = 5; k >= 0; --k) { a0 = fma(a0, s0, f.b[k]); a1 = fma(a1, s1, f.b[k]); }
+    for (int k = DEG - 1; k >= 0; --k) { a0 = fma(a0, s0, f.b[k]); a1 = fma(a1, s1, f.b[k]); }
     *r0 = a0; *r1 = a1;
 }
 
@@ -1279,7 +1316,7 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
 
 // Two nodes of the fitted sweep (independent chains): positions x0, x1, fit arguments t0, t1
 // (t = x.(-2 sigma c), single-centre fits) accumulated into the rule node's sums.
-template <int KIND, bool SERIES, bool TADD>
+template <int KIND, bool SERIES, bool TADD, int DEG = 6>
 SCVT_HD void fit_pair(const FitEval& f0, const FitEval& f1, V3 z, V3 x0, V3 x1, double t0,
                       double t1, double& mq, double& xq, double& yq, double& zq, double& eq) {
     double inv0, inv1;
@@ -1294,8 +1331,8 @@ SCVT_HD void fit_pair(const FitEval& f0, const FitEval& f1, V3 z, V3 x0, V3 x1, 
         inv1 = fast_rsqrt(x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
     }
     double rho0, rho1;
-    if (TADD) fit_rho2_t(f0, t0, inv0, t1, inv1, &rho0, &rho1);
-    else fit_rho2(f0, x0, inv0, x1, inv1, &rho0, &rho1);
+    if (TADD) fit_rho2_t<DEG>(f0, t0, inv0, t1, inv1, &rho0, &rho1);
+    else fit_rho2<DEG>(f0, x0, inv0, x1, inv1, &rho0, &rho1);
     if (KIND == DEN_TANH4X2_TAB) {
         double r0b, r1b;
         fit_rho2(f1, x0, inv0, x1, inv1, &r0b, &r1b);
@@ -1320,7 +1357,7 @@ SCVT_HD void fit_pair(const FitEval& f0, const FitEval& f1, V3 z, V3 x0, V3 x1, 
 // two chains (L - 1 - a pairs), and the L up-leaf nodes left over -- the row ends, on the
 // leaf-grid diagonal -- are swept as L / 2 pairs along the diagonal: per rule node L + 1 row
 // setups instead of 2 L - 1, and no single-node tails.
-template <int KIND, int L, bool SERIES>
+template <int KIND, int L, bool SERIES, int DEG = 6>
 SCVT_HD void sym7_fit_leaves_merged(const SubTri& s, V3 z, const double* l1, const double* l2,
                                     const double* w, const LocalFit& lf0, const LocalFit& lf1,
                                     double* acc) {
@@ -1351,7 +1388,7 @@ SCVT_HD void sym7_fit_leaves_merged(const SubTri& s, V3 z, const double* l1, con
             double tn = TADD ? fma(xn.z, f0.m2c.z, fma(xn.y, f0.m2c.y, xn.x * f0.m2c.x)) : 0.0;
             for (int b = 0; b < L - 1 - a; ++b) {
                 const V3 x1 = add(xn, D);
-                fit_pair<KIND, SERIES, TADD>(f0, f1, z, xn, x1, tn, tn + tD, mq, xq, yq, zq, eq);
+                fit_pair<KIND, SERIES, TADD, DEG>(f0, f1, z, xn, x1, tn, tn + tD, mq, xq, yq, zq, eq);
                 xn = add(xn, de2);
                 tn += dt;
             }
@@ -1364,7 +1401,7 @@ SCVT_HD void sym7_fit_leaves_merged(const SubTri& s, V3 z, const double* l1, con
             double tn = TADD ? fma(xn.z, f0.m2c.z, fma(xn.y, f0.m2c.y, xn.x * f0.m2c.x)) : 0.0;
             for (int k = 0; k < L / 2; ++k) {
                 const V3 x1 = add(xn, dd);
-                fit_pair<KIND, SERIES, TADD>(f0, f1, z, xn, x1, tn, tn + ddt, mq, xq, yq, zq, eq);
+                fit_pair<KIND, SERIES, TADD, DEG>(f0, f1, z, xn, x1, tn, tn + ddt, mq, xq, yq, zq, eq);
                 xn = add(x1, dd);
                 tn += 2.0 * ddt;
             }
@@ -1436,20 +1473,24 @@ SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const 
 // Nothing but the slot crosses from one phase to the other, so the prologue's registers die
 // before the node loop and no out-of-line call (with its caller-saved stack frame) sits on the
 // per-sub-triangle path.
-enum : int { SWEEP_TABLE = 0, SWEEP_FIT0 = 1, SWEEP_FIT1 = 2, SWEEP_FIT2 = 3, SWEEP_SERIES = 4 };
+// bits 3-4: how many of the fit's last coefficients are exact zeros (0, 1, 2: local_fit_impl)
+enum : int { SWEEP_TABLE = 0, SWEEP_FIT0 = 1, SWEEP_FIT1 = 2, SWEEP_FIT2 = 3, SWEEP_SERIES = 4,
+             SWEEP_DROP_SHIFT = 3 };
 
 template <int KIND>
 SCVT_HD int sym7_prologue(const DensityParams& dp, const SubTri& s, LocalFit* f) {
     const bool TAB = KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB;
     if (!TAB) return SWEEP_TABLE;
-    if (!local_fit_impl(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f[0])) return SWEEP_TABLE;
+    int drop0 = 0, drop1 = 0;
+    if (!local_fit_impl(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f[0], &drop0)) return SWEEP_TABLE;
     int mode = SWEEP_FIT0;
     if (KIND == DEN_TANH4X2_TAB) {
-        if (!local_fit_impl(dp, s, v3(dp.c1x, dp.c1y, dp.c1z), f[1])) return SWEEP_TABLE;
+        if (!local_fit_impl(dp, s, v3(dp.c1x, dp.c1y, dp.c1z), f[1], &drop1)) return SWEEP_TABLE;
         // one centre dominates the whole patch: its fit alone gives max(rho0, rho1)
         mode = f[1].rmax < f[0].rmin * (1.0 - 1e-13) ? SWEEP_FIT0
              : (f[0].rmax < f[1].rmin * (1.0 - 1e-13) ? SWEEP_FIT1 : SWEEP_FIT2);
     }
+    mode |= (mode == SWEEP_FIT0 ? drop0 : (mode == SWEEP_FIT1 ? drop1 : 0)) << SWEEP_DROP_SHIFT;
     const V3 nv = cross(s.e1, s.e2);
     const double nn = dot(nv, nv), h = dot(nv, s.v0);
     if (nn > 0.0 && nn - h * h <= 1e-4 * nn) mode |= SWEEP_SERIES;
@@ -1464,6 +1505,20 @@ SCVT_HD void sym7_sweep(int mode, const SubTri& s, V3 z, const double* l1, const
     const bool series = (mode & SWEEP_SERIES) != 0;
     if (fit == SWEEP_FIT0 || fit == SWEEP_FIT1) {
         const LocalFit& fd = f[fit - 1];
+#ifndef SCVT_SWEEP_ROWS
+        if (series) {
+            // the lowest degree every patch of the warp on this path allows (same bits as the
+            // degree-6 sweep: the dropped coefficients are exact zeros)
+            int drop = (mode >> SWEEP_DROP_SHIFT) & 3;
+#ifdef __CUDA_ARCH__
+            drop = __reduce_min_sync(__activemask(), drop);
+#endif
+            if (drop == 2) sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, 4>(s, z, l1, l2, w, fd, fd, acc);
+            else if (drop == 1) sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, 5>(s, z, l1, l2, w, fd, fd, acc);
+            else sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, 6>(s, z, l1, l2, w, fd, fd, acc);
+            return;
+        }
+#endif
         if (series) SCVT_FIT_SWEEP<DEN_TANH4_TAB, L, true>(s, z, l1, l2, w, fd, fd, acc);
         else SCVT_FIT_SWEEP<DEN_TANH4_TAB, L, false>(s, z, l1, l2, w, fd, fd, acc);
         return;

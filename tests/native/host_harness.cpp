@@ -222,3 +222,39 @@ extern "C" int harness_quad_sym7(const double* z, int n, const int* nbr, const i
     }
     return pole;
 }
+
+
+// distribution of the Chebyshev tail of the accepted single-centre fits, in the order given by
+// `order` (generator ids; the kernel's incidence order is by cube-map bucket): per
+// sub-triangle the tail sums |a6|, |a5|+|a6|, ... relative to min rho (tail[4 * idx ...]) and
+// the accepted flag; returns the number of sub-triangles
+extern "C" long long harness_fit_tails(const double* z, int n, const int* order, const int* nbr,
+                                       const int* deg, const double* table, int tab_k,
+                                       double tab_w, const double* prm, int kind, double* tail,
+                                       int* accepted) {
+    DensityParams dp{};
+    dp.kind = kind;
+    dp.gamma = prm[0]; dp.beta = prm[1]; dp.alpha = prm[2];
+    dp.c0x = prm[3]; dp.c0y = prm[4]; dp.c0z = prm[5];
+    dp.c1x = prm[6]; dp.c1y = prm[7]; dp.c1z = prm[8];
+    dp.tab = table; dp.tab_k = tab_k; dp.tab_invw = 1.0 / tab_w;
+    long long idx = 0;
+    for (int p = 0; p < n; ++p) {
+        const int i = order[p];
+        const int* row = nbr + (int64_t)i * MAXDEG;
+        for (int t = 0; t < deg[i]; ++t) {
+            int j = row[t], k = row[(t + 1) % deg[i]];
+            FanPair f = fan_pair(load3(z, i), load3(z, j), load3(z, k), i, j, k);
+            for (int s = 0; s < 2; ++s) {
+                LocalFit lf;
+                int low = 0;
+                double ts[4] = {1, 1, 1, 1};
+                bool a = local_fit_impl(dp, f.s[s], v3(dp.c0x, dp.c0y, dp.c0z), lf, &low, ts);
+                accepted[idx] = a ? 1 + low : 0;
+                for (int q = 0; q < 4; ++q) tail[4 * idx + q] = ts[q];
+                ++idx;
+            }
+        }
+    }
+    return idx;
+}
