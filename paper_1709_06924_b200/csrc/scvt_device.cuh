@@ -940,6 +940,9 @@ struct LocalFit {
 // 90 deg from c, comes too close to the sqrt singularity at s = 0, or the fit misses the table
 // by more than 4e-15 relative at any check point (the table itself is within 1.6e-15 of the
 // closed form; a degree-6 interpolant evaluated in FP64 has a ~1e-15 rounding floor).
+// BOUNDS: also record rho at the ends of the s interval (f.rmin, f.rmax: read only by the
+// two-centre dominance test; two table evaluations the single-centre kernels skip).
+template <bool BOUNDS = true>
 SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, LocalFit& f,
                             int* drop = nullptr, double* tail_stats = nullptr) {
     constexpr double CHEB_V[7] = {0.9749279121818236, 0.7818314824680298, 0.4338837391175582,
@@ -1072,10 +1075,12 @@ SCVT_HD bool local_fit_impl(const DensityParams& p, const SubTri& st, V3 c, Loca
 #pragma unroll
     for (int k = 0; k < 7; ++k) { f.b[k] = b[k] * sc_k; sc_k *= ih; }
     f.sc = sc;
-    const double ul = tab_u_chord(p, lo * fast_rsqrt(lo), br), uh = tab_u_chord(p, hi * fast_rsqrt(hi), br);
-    const double rl = (ul * ul) * (ul * ul), rh = (uh * uh) * (uh * uh);
-    f.rmin = fmin(rl, rh);
-    f.rmax = fmax(rl, rh);
+    if (BOUNDS) {
+        const double ul = tab_u_chord(p, lo * fast_rsqrt(lo), br), uh = tab_u_chord(p, hi * fast_rsqrt(hi), br);
+        const double rl = (ul * ul) * (ul * ul), rh = (uh * uh) * (uh * uh);
+        f.rmin = fmin(rl, rh);
+        f.rmax = fmax(rl, rh);
+    }
     return true;
 }
 
@@ -1482,7 +1487,8 @@ SCVT_HD int sym7_prologue(const DensityParams& dp, const SubTri& s, LocalFit* f)
     const bool TAB = KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB;
     if (!TAB) return SWEEP_TABLE;
     int drop0 = 0, drop1 = 0;
-    if (!local_fit_impl(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f[0], &drop0)) return SWEEP_TABLE;
+    if (!local_fit_impl<KIND == DEN_TANH4X2_TAB>(dp, s, v3(dp.c0x, dp.c0y, dp.c0z), f[0], &drop0))
+        return SWEEP_TABLE;
     int mode = SWEEP_FIT0;
     if (KIND == DEN_TANH4X2_TAB) {
         if (!local_fit_impl(dp, s, v3(dp.c1x, dp.c1y, dp.c1z), f[1], &drop1)) return SWEEP_TABLE;
