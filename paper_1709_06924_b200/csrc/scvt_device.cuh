@@ -1321,14 +1321,18 @@ SCVT_HD void sym7_fit_leaves(const SubTri& s, V3 z, const double* l1, const doub
 
 // Two nodes of the fitted sweep (independent chains): positions x0, x1, fit arguments t0, t1
 // (t = x.(-2 sigma c), single-centre fits) accumulated into the rule node's sums.
-template <int KIND, bool SERIES, bool TADD, int DEG = 6>
+// SER2: every patch of the warp has 1 - |x|^2 <= SER2_MAX, where the cubic term of the 1/|x|
+// series is below the truncation the three-term series is admitted with; such a patch carries
+// c3 = 0 (otherwise 5/16), so the three-term form gives it the same bits (d * 0 + 3/8 = 3/8).
+template <int KIND, bool SERIES, bool TADD, int DEG = 6, bool SER2 = false>
 SCVT_HD void fit_pair(const FitEval& f0, const FitEval& f1, V3 z, V3 x0, V3 x1, double t0,
-                      double t1, double& mq, double& xq, double& yq, double& zq, double& eq) {
+                      double t1, double c3, double& mq, double& xq, double& yq, double& zq,
+                      double& eq) {
     double inv0, inv1;
     if (SERIES) {
         const double d0 = fma(-x0.z, x0.z, fma(-x0.y, x0.y, fma(-x0.x, x0.x, 1.0)));
         const double d1 = fma(-x1.z, x1.z, fma(-x1.y, x1.y, fma(-x1.x, x1.x, 1.0)));
-        const double p0 = fma(d0, 0.3125, 0.375), p1 = fma(d1, 0.3125, 0.375);
+        const double p0 = SER2 ? 0.375 : fma(d0, c3, 0.375), p1 = SER2 ? 0.375 : fma(d1, c3, 0.375);
         const double q0 = fma(d0, p0, 0.5), q1 = fma(d1, p1, 0.5);
         inv0 = fma(d0, q0, 1.0); inv1 = fma(d1, q1, 1.0);
     } else {
@@ -1362,10 +1366,10 @@ SCVT_HD void fit_pair(const FitEval& f0, const FitEval& f1, V3 z, V3 x0, V3 x1, 
 // two chains (L - 1 - a pairs), and the L up-leaf nodes left over -- the row ends, on the
 // leaf-grid diagonal -- are swept as L / 2 pairs along the diagonal: per rule node L + 1 row
 // setups instead of 2 L - 1, and no single-node tails.
-template <int KIND, int L, bool SERIES, int DEG = 6>
+template <int KIND, int L, bool SERIES, int DEG = 6, bool SER2 = false>
 SCVT_HD void sym7_fit_leaves_merged(const SubTri& s, V3 z, const double* l1, const double* l2,
                                     const double* w, const LocalFit& lf0, const LocalFit& lf1,
-                                    double* acc) {
+                                    double* acc, double c3 = 0.3125) {
     static_assert(L % 2 == 0, "diagonal pairs");
     const FitEval f0 = fit_eval(lf0);
     FitEval f1;
@@ -1393,7 +1397,7 @@ SCVT_HD void sym7_fit_leaves_merged(const SubTri& s, V3 z, const double* l1, con
             double tn = TADD ? fma(xn.z, f0.m2c.z, fma(xn.y, f0.m2c.y, xn.x * f0.m2c.x)) : 0.0;
             for (int b = 0; b < L - 1 - a; ++b) {
                 const V3 x1 = add(xn, D);
-                fit_pair<KIND, SERIES, TADD, DEG>(f0, f1, z, xn, x1, tn, tn + tD, mq, xq, yq, zq, eq);
+                fit_pair<KIND, SERIES, TADD, DEG, SER2>(f0, f1, z, xn, x1, tn, tn + tD, c3, mq, xq, yq, zq, eq);
                 xn = add(xn, de2);
                 tn += dt;
             }
@@ -1406,7 +1410,7 @@ SCVT_HD void sym7_fit_leaves_merged(const SubTri& s, V3 z, const double* l1, con
             double tn = TADD ? fma(xn.z, f0.m2c.z, fma(xn.y, f0.m2c.y, xn.x * f0.m2c.x)) : 0.0;
             for (int k = 0; k < L / 2; ++k) {
                 const V3 x1 = add(xn, dd);
-                fit_pair<KIND, SERIES, TADD, DEG>(f0, f1, z, xn, x1, tn, tn + ddt, mq, xq, yq, zq, eq);
+                fit_pair<KIND, SERIES, TADD, DEG, SER2>(f0, f1, z, xn, x1, tn, tn + ddt, c3, mq, xq, yq, zq, eq);
                 xn = add(x1, dd);
                 tn += 2.0 * ddt;
             }
@@ -1479,8 +1483,12 @@ SCVT_HD void subtri_moments_sym7(const SubTri& s, V3 z, const double* l1, const 
 // before the node loop and no out-of-line call (with its caller-saved stack frame) sits on the
 // per-sub-triangle path.
 // bits 3-4: how many of the fit's last coefficients are exact zeros (0, 1, 2: local_fit_impl)
+// bit 5: 1 - |x|^2 <= SER2_MAX on the patch (two-term 1/|x| series, see fit_pair)
 enum : int { SWEEP_TABLE = 0, SWEEP_FIT0 = 1, SWEEP_FIT1 = 2, SWEEP_FIT2 = 3, SWEEP_SERIES = 4,
-             SWEEP_DROP_SHIFT = 3 };
+             SWEEP_DROP_SHIFT = 3, SWEEP_SER2 = 32 };
+// 5 d^3 / 16 <= 3e-17: the bound the three-term series is admitted with (35 d^4 / 128 at
+// d = 1e-4)
+constexpr double SER2_MAX = 4.6e-6;
 
 template <int KIND>
 SCVT_HD int sym7_prologue(const DensityParams& dp, const SubTri& s, LocalFit* f) {
@@ -1500,6 +1508,7 @@ SCVT_HD int sym7_prologue(const DensityParams& dp, const SubTri& s, LocalFit* f)
     const V3 nv = cross(s.e1, s.e2);
     const double nn = dot(nv, nv), h = dot(nv, s.v0);
     if (nn > 0.0 && nn - h * h <= 1e-4 * nn) mode |= SWEEP_SERIES;
+    if (nn > 0.0 && nn - h * h <= SER2_MAX * nn) mode |= SWEEP_SER2;
     return mode;
 }
 
@@ -1516,12 +1525,26 @@ SCVT_HD void sym7_sweep(int mode, const SubTri& s, V3 z, const double* l1, const
             // the lowest degree every patch of the warp on this path allows (same bits as the
             // degree-6 sweep: the dropped coefficients are exact zeros)
             int drop = (mode >> SWEEP_DROP_SHIFT) & 3;
+            const bool mine2 = (mode & SWEEP_SER2) != 0;
+            bool ser2 = mine2;
 #ifdef __CUDA_ARCH__
-            drop = __reduce_min_sync(__activemask(), drop);
+            const unsigned am = __activemask();
+            drop = __reduce_min_sync(am, drop);
+            ser2 = __all_sync(am, mine2);
 #endif
-            if (drop == 2) sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, 4>(s, z, l1, l2, w, fd, fd, acc);
-            else if (drop == 1) sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, 5>(s, z, l1, l2, w, fd, fd, acc);
-            else sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, 6>(s, z, l1, l2, w, fd, fd, acc);
+            // in a mixed warp a two-term patch takes the three-term sweep with c3 = 0: same bits
+            const double c3 = mine2 ? 0.0 : 0.3125;
+#define SCVT_SWEEP_DEG(DEG)                                                                      \
+    do {                                                                                         \
+        if (ser2) sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, DEG, true>(s, z, l1, l2, w, fd, \
+                                                                            fd, acc);            \
+        else sym7_fit_leaves_merged<DEN_TANH4_TAB, L, true, DEG, false>(s, z, l1, l2, w, fd, fd, \
+                                                                        acc, c3);                \
+    } while (0)
+            if (drop == 2) SCVT_SWEEP_DEG(4);
+            else if (drop == 1) SCVT_SWEEP_DEG(5);
+            else SCVT_SWEEP_DEG(6);
+#undef SCVT_SWEEP_DEG
             return;
         }
 #endif

@@ -226,7 +226,8 @@ extern "C" int harness_quad_sym7(const double* z, int n, const int* nbr, const i
 
 // distribution of the Chebyshev tail of the accepted single-centre fits, in the order given by
 // `order` (generator ids; the kernel's incidence order is by cube-map bucket): per
-// sub-triangle the tail sums |a6|, |a5|+|a6|, ... relative to min rho (tail[4 * idx ...]) and
+// sub-triangle the tail sums |a6|, |a5|+|a6|, |a4|+|a5|+|a6| relative to min rho and the patch's
+// bound of 1 - |x|^2 (tail[4 * idx ...]), and
 // the accepted flag; returns the number of sub-triangles
 extern "C" long long harness_fit_tails(const double* z, int n, const int* order, const int* nbr,
                                        const int* deg, const double* table, int tab_k,
@@ -251,7 +252,12 @@ extern "C" long long harness_fit_tails(const double* z, int n, const int* order,
                 double ts[4] = {1, 1, 1, 1};
                 bool a = local_fit_impl(dp, f.s[s], v3(dp.c0x, dp.c0y, dp.c0z), lf, &low, ts);
                 accepted[idx] = a ? 1 + low : 0;
-                for (int q = 0; q < 4; ++q) tail[4 * idx + q] = ts[q];
+                for (int q = 0; q < 3; ++q) tail[4 * idx + q] = ts[q];
+                {   // 1 - |x|^2 bound of the patch (the 1/|x| series criterion of sym7_prologue)
+                    const V3 nv = cross(f.s[s].e1, f.s[s].e2);
+                    const double nn = dot(nv, nv), hh = dot(nv, f.s[s].v0);
+                    tail[4 * idx + 3] = nn > 0.0 ? (nn - hh * hh) / nn : 1.0;
+                }
                 ++idx;
             }
         }
