@@ -320,17 +320,22 @@ def run_b200(a):
                 "share_of_step": ms[1] / total_ms if world == 1 else None,
                 "cells_ms_per_eval": ms[0] / max(cnt[0], 1),
                 "eval_ms": ms[2] / max(cnt[2], 1),
-                "traffic": _traffic_from_profiles(),
+                "traffic": _traffic_from_profiles(a.config),
                 # the whole iteration against the same peak (all kernels, host
                 # round trips and idle time included)
                 "step_frac": (flops_eval * world * evals / a.steps) / (total_ms / a.steps * 1e-3)
                              / 1e12 / peak.value}
-    if dname == "c5":
-        roofline["note"] = ("algorithmic FLOPs charge both centres' density at every node, as the "
-                            "reference formulation (d = min over the centres) does; where one "
-                            "centre's fit dominates a whole patch k_quad evaluates that fit only "
-                            "(DESIGN.md §3 item 5), so the fraction can exceed 1; the FP64 pipe "
-                            "utilisation is in profiles/")
+    pipe = _profile_value("k_quad_fp64_pipe_active_pct", a.config)
+    if pipe is not None:
+        roofline["fp64_pipe_active_pct_ncu"] = pipe
+    if dname != "const":
+        roofline["note"] = (
+            "frac is ALGORITHMIC FLOPs (SURVEY 8(d): the reference's closed-form density at "
+            "every node, both centres for the two-centre kind) over the measured DFMA peak; "
+            "k_quad evaluates a per-patch polynomial fit of rho (degree 4-6, one centre where it "
+            "dominates the patch) with fewer FP64 instructions than that count charges, so frac "
+            "can exceed 1 -- the hardware utilisation is fp64_pipe_active_pct_ncu (ncu "
+            "sm__pipe_fp64_cycles_active of the same kernel, profiles/)")
     line = {"metric": METRIC, "value": value, "unit": "generator-updates/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
             "higher_is_better": True, "scaling": "strong",
@@ -437,13 +442,20 @@ def _e2e(P, density, z0, m, steps, dev, world):
                     f"2-iteration warm-up call on a separate evaluator (allocator warm-up)"}
 
 
-def _traffic_from_profiles():
+def _profile_value(key, config=None):
+    """A number from the committed ncu summary (profiles/roofline_traffic.json): ncu cannot
+    run inside the timed bench, so its figures are read from the capture of the same build."""
     p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("k_quad_dram_bytes_per_launch")
+            v = json.load(f).get(key)
     except (OSError, ValueError):
         return None
+    return v.get(config) if isinstance(v, dict) else v
+
+
+def _traffic_from_profiles(config="c4"):
+    return _profile_value("k_quad_dram_bytes_per_launch", config)
 
 
 def _free_port() -> int:
