@@ -1512,7 +1512,24 @@ SCVT_HD int sym7_prologue(const DensityParams& dp, const SubTri& s, LocalFit* f)
     return mode;
 }
 
+// per-node table (or closed-form) density on the leaf grid: the sweep of a sub-triangle with
+// no accepted fit
 template <int KIND, int L>
+SCVT_HD void sym7_table_sweep(const SubTri& s, V3 z, const double* l1, const double* l2,
+                              const double* w, const DensityParams& dp, double* acc, int* pole) {
+    V3 o[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) o[q] = add(mul(s.e1, l1[q]), mul(s.e2, l2[q]));
+    double mo[5];
+    LocalFit none;     // not read (FIT = false)
+    sym7_leaves<KIND, L, false>(s, z, o, w[0], w[1], w[4], dp, none, none, mo, pole);
+    acc[0] += s.area * mo[0];
+    acc[1] += s.area * mo[1]; acc[2] += s.area * mo[2]; acc[3] += s.area * mo[3];
+    acc[4] += s.area * mo[4];
+}
+
+// NO_TABLE: the caller never passes a SWEEP_TABLE mode (k_quad<..., DEFER> queues those)
+template <int KIND, int L, bool NO_TABLE = false>
 SCVT_HD void sym7_sweep(int mode, const SubTri& s, V3 z, const double* l1, const double* l2,
                         const double* w, const DensityParams& dp, const LocalFit* f,
                         double* acc, int* pole) {
@@ -1557,14 +1574,8 @@ SCVT_HD void sym7_sweep(int mode, const SubTri& s, V3 z, const double* l1, const
         else SCVT_FIT_SWEEP<KIND, L, false>(s, z, l1, l2, w, f[0], f[1], acc);
         return;
     }
-    V3 o[7];
-#pragma unroll
-    for (int q = 0; q < 7; ++q) o[q] = add(mul(s.e1, l1[q]), mul(s.e2, l2[q]));
-    double mo[5];
-    sym7_leaves<KIND, L, false>(s, z, o, w[0], w[1], w[4], dp, f[0], f[0], mo, pole);
-    acc[0] += s.area * mo[0];
-    acc[1] += s.area * mo[1]; acc[2] += s.area * mo[2]; acc[3] += s.area * mo[3];
-    acc[4] += s.area * mo[4];
+    if (NO_TABLE) return;
+    sym7_table_sweep<KIND, L>(s, z, l1, l2, w, dp, acc, pole);
 }
 
 }  // namespace scvt

@@ -731,12 +731,20 @@ struct QuadArgs {
     double* part;         // [n_inc][PART_ROW]: per incidence, sub-triangle 0 then 1 (split mode)
     uint8_t* obtuse;      // [n_inc]
     int* status;
+    int* defer_list;      // [2 n_inc] fan sub-triangles left to k_quad_table (thread ids of k_quad)
+    int* defer_cnt;       // their count (zeroed before k_quad)
 };
 
 // SPLIT: one thread per fan sub-triangle instead of per incidence (twice the work units, a
 // finer last wave, shorter per-thread chains); the two halves land in part[0..5) and
 // part[5..10) and the gathers add them in a fixed order.
-template <int KIND, bool SPHERE, bool SYM7, bool SPLIT = false, bool DEVCOUNT = false>
+// DEFER (table kinds on the split fast path): a sub-triangle whose density fit was rejected is
+// not swept here -- one such lane would hold its whole warp through the per-node table sweep
+// (2.6x a fitted sweep) after the fitted one -- but queued for k_quad_table, which sweeps the
+// rejected patches of the whole launch in full warps.  The result of a sub-triangle is the
+// same bits whichever kernel computes it.
+template <int KIND, bool SPHERE, bool SYM7, bool SPLIT = false, bool DEVCOUNT = false,
+          bool DEFER = false>
 __global__ void __launch_bounds__(QUAD_THREADS, SYM7 ? (KIND == DEN_TANH4X2_TAB ? QUAD_MINB2 : QUAD_MINB) : 1)
 k_quad(QuadArgs a) {
     extern __shared__ double s_nodes[];
@@ -793,12 +801,24 @@ k_quad(QuadArgs a) {
         if (half == 0) a.obtuse[u] = (obt && i < j && i < k) ? 1 : 0;
         const DensityParams& dp = *a.dpg;
         const int mode = sym7_prologue<KIND>(dp, st0, s_fit[threadIdx.x]);
+        if (DEFER && (mode & 3) == SWEEP_TABLE) {
+            // one atomicAdd per warp; the queue's order does not matter (every entry writes
+            // its own partial row)
+            const unsigned m = __activemask();
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(m) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(a.defer_cnt, __popc(m));
+            base = __shfl_sync(m, base, leader);
+            a.defer_list[base + __popc(m & ((1u << lane) - 1u))] = t_id;
+            return;
+        }
         s_sub[threadIdx.x] = st0;
         s_z[threadIdx.x][0] = vi.x; s_z[threadIdx.x][1] = vi.y; s_z[threadIdx.x][2] = vi.z;
         asm volatile("" ::: "memory");    // the sweep reads its inputs back from the slot
         const SubTri st = s_sub[threadIdx.x];
         const V3 zc = v3(s_z[threadIdx.x][0], s_z[threadIdx.x][1], s_z[threadIdx.x][2]);
-        sym7_sweep<KIND, 8>(mode, st, zc, l1, l2, w, dp, s_fit[threadIdx.x], acc, &pole);
+        sym7_sweep<KIND, 8, DEFER>(mode, st, zc, l1, l2, w, dp, s_fit[threadIdx.x], acc, &pole);
         if (pole) atomicOr(a.status, ST_POLE);
         double* out = a.part + (int64_t)u * PART_ROW + (half ? 5 : 0);
 #pragma unroll
@@ -823,6 +843,42 @@ k_quad(QuadArgs a) {
 #pragma unroll
     for (int c = 0; c < 5; ++c) out[c] = acc[c];
     if (!SPLIT || half == 0) a.obtuse[u] = (f.obtuse && i < j && i < k) ? 1 : 0;
+}
+
+// The sub-triangles k_quad<..., DEFER> queued (rejected fits): per-node table evaluation of
+// the density on the same leaf grid, every lane of a warp on the same sweep.  Grid-stride over
+// the queue (its length is known on the device only).
+constexpr int QTAB_THREADS = 64;
+template <int KIND>
+__global__ void __launch_bounds__(QTAB_THREADS) k_quad_table(QuadArgs a) {
+    __shared__ double s_nodes[21];
+    for (int q = threadIdx.x; q < 21; q += blockDim.x)
+        s_nodes[q] = a.nodes[(q / 7) * a.nq + q % 7];
+    __syncthreads();
+    const double* l1 = s_nodes;
+    const double* l2 = s_nodes + 7;
+    const double* w = s_nodes + 14;
+    const int total = *a.defer_cnt;
+    const DensityParams& dp = *a.dpg;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += gridDim.x * blockDim.x) {
+        const int t_id = a.defer_list[idx];
+        const int u = t_id >> 1, half = t_id & 1;
+        const int i = a.inc_gen[u];
+        const int t = u - a.inc_base[i];
+        const int d = a.deg[i];
+        const int* row = a.nbr + (int64_t)i * MAXDEG;
+        const int j = row[t], k = row[t + 1 == d ? 0 : t + 1];
+        const V3 vi = load3(a.z, i), vj = load3(a.z, j), vk = load3(a.z, k);
+        int obt, degen, pole = 0;
+        const SubTri st = fan_sub(vi, vj, vk, i, j, k, half, &obt, &degen);
+        double acc[5] = {0, 0, 0, 0, 0};
+        sym7_table_sweep<KIND, 8>(st, vi, l1, l2, w, dp, acc, &pole);
+        if (pole) atomicOr(a.status, ST_POLE);
+        double* out = a.part + (int64_t)u * PART_ROW + (half ? 5 : 0);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) out[c] = acc[c];
+    }
 }
 
 // gradient epilogue (pipeline.py:265-279): g = 2(c.z)z - 2c, diag = 2 c.z
@@ -1912,6 +1968,7 @@ struct scvt_ctx {
     int* d_pairs = nullptr; int* d_cursor = nullptr;
     // quadrature
     double* d_part = nullptr; uint8_t* d_obt = nullptr;
+    int* d_defer = nullptr;            // [12 n + 1]: k_quad's queue for k_quad_table, count last
     double* d_egen = nullptr; double* d_g2gen = nullptr; double* d_obgen = nullptr;
     // reductions and status
     double* d_partials = nullptr;      // [MAX_SLOTS][RED_BLOCKS] and [MAX_RED_VALS][CHUNKS]
@@ -2550,13 +2607,24 @@ template <int KIND>
 int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t smem) {
     if (ctx->measure)
         k_quad<KIND, true, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
-    else if (ctx->sym7 && a.n_inc_dev)   // shards: incidence count on the device
-        k_quad<KIND, false, true, true, true><<<blocks_for(2 * (int64_t)a.n_inc, QUAD_THREADS),
-                                                 QUAD_THREADS, 21 * sizeof(double), ctx->stream>>>(a);
-    else if (ctx->sym7)         // the fast path always runs a thread per fan sub-triangle
-        k_quad<KIND, false, true, true><<<blocks_for(2 * (int64_t)a.n_inc, QUAD_THREADS),
-                                           QUAD_THREADS, 21 * sizeof(double), ctx->stream>>>(a);
-    else
+    else if (ctx->sym7) {       // the fast path always runs a thread per fan sub-triangle
+        // table kinds: rejected fits go to k_quad_table (see k_quad)
+        constexpr bool DEFER = KIND == DEN_TANH4_TAB || KIND == DEN_TANH4X2_TAB;
+        const unsigned g2 = blocks_for(2 * (int64_t)a.n_inc, QUAD_THREADS);
+        if (DEFER) CK(cudaMemsetAsync(a.defer_cnt, 0, sizeof(int), ctx->stream));
+        if (a.n_inc_dev)        // shards: incidence count on the device
+            k_quad<KIND, false, true, true, true, DEFER><<<g2, QUAD_THREADS, 21 * sizeof(double),
+                                                           ctx->stream>>>(a);
+        else
+            k_quad<KIND, false, true, true, false, DEFER><<<g2, QUAD_THREADS, 21 * sizeof(double),
+                                                            ctx->stream>>>(a);
+        if constexpr (DEFER) {
+            LAUNCHED();
+            const unsigned gt = std::min<unsigned>(blocks_for(2 * (int64_t)a.n_inc, QTAB_THREADS),
+                                                   148u * 16u);   // 16 resident CTAs of 64 threads per SM
+            k_quad_table<KIND><<<gt, QTAB_THREADS, 0, ctx->stream>>>(a);
+        }
+    } else
         k_quad<KIND, false, false><<<grid, QUAD_THREADS, smem, ctx->stream>>>(a);
     LAUNCHED();
     return SCVT_OK;
@@ -2595,6 +2663,8 @@ int quad_range(scvt_ctx* ctx, const double* z, int64_t n, int64_t lo, int64_t hi
     a.dp.tab = ctx->d_table;
     a.dpg = ctx->d_dp;
     a.status = ctx->d_status;
+    a.defer_list = ctx->d_defer;
+    a.defer_cnt = ctx->d_defer + 2 * 6 * ctx->n_max;
     if (n_inc <= 0) return SCVT_OK;
     // split mode (thread per fan sub-triangle) on the 7-point fast path: twice the work units,
     // a finer last wave and shorter per-thread chains (c4 k_quad 9.44 -> 8.84 ms, c3 -11 %)
@@ -3065,7 +3135,7 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     AL(d_nbr, n * MAXDEG); AL(d_deg, n + 1); AL(d_amb, n * MAXDEG);
     AL(d_inc_start, n + 1); AL(d_inc_gen, n_inc); AL(d_inc_base, n);
     AL(d_pairs, n * MAXDEG * 2); AL(d_cursor, n + 1);
-    AL(d_part, PART_ROW * n_inc); AL(d_obt, n_inc);   // [n_inc][2][5]: split mode uses both halves
+    AL(d_part, PART_ROW * n_inc); AL(d_obt, n_inc); AL(d_defer, 2 * n_inc + 1);   // [n_inc][2][5]: split mode uses both halves
     AL(d_egen, n); AL(d_g2gen, n); AL(d_obgen, n);
     AL(d_partials, std::max<int64_t>((int64_t)MAX_SLOTS * RED_BLOCKS, (int64_t)MAX_RED_VALS * CHUNKS));
     AL(d_scal, MAX_RED_VALS);
@@ -3137,11 +3207,12 @@ int scvt_create(scvt_ctx** out, int device, int64_t n_max, const scvt_config* cf
     {
         // the split fast path adds its static per-thread fit slots (up to ~40 KB) to the
         // node table: opt in so that static + dynamic may exceed 48 KB
-#define OPT7(K) \
-    cudaFuncSetAttribute(k_quad<K, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    cudaFuncSetAttribute(k_quad<K, false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-        OPT7(DEN_CONST); OPT7(DEN_X3); OPT7(DEN_X16); OPT7(DEN_TANH); OPT7(DEN_TANH4);
-        OPT7(DEN_TANH4X2); OPT7(DEN_TANH4_TAB); OPT7(DEN_TANH4X2_TAB);
+#define OPT7(K, D) \
+    cudaFuncSetAttribute(k_quad<K, false, true, true, false, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(k_quad<K, false, true, true, true, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+        OPT7(DEN_CONST, false); OPT7(DEN_X3, false); OPT7(DEN_X16, false); OPT7(DEN_TANH, false);
+        OPT7(DEN_TANH4, false); OPT7(DEN_TANH4X2, false); OPT7(DEN_TANH4_TAB, true);
+        OPT7(DEN_TANH4X2_TAB, true);
 #undef OPT7
     }
     DensityParams dpd = dp;          // device copy read by the out-of-line quadrature paths
