@@ -305,3 +305,40 @@ def test_orientation_against_the_origin_great_circle_tie(h):
     pts = [np.zeros(3), np.array([1.0, 0, 0]), np.array([0, 1.0, 0]), np.array([-1.0, 0, 0])]
     s, tier = _orient(h, pts, [-1, 5, 6, 7])
     assert s == 1 and tier == 2
+
+
+def test_fit_degree_classes_drop_only_noise_level_coefficients(h):
+    """k_quad's per-patch fit degree (scvt_device.cuh local_fit_impl): a fit of class 2 (3)
+    has had a6 (a5 and a6) set to exact zeros, which is allowed only when those Chebyshev
+    coefficients are at the rounding floor of the table values (4e-15 relative); the classes
+    must actually occur at a BASELINE-like patch size (the c4 density at N = 40,962: at full
+    size 86 % of the sub-triangles are class 3), and the two-term 1/|x| series bound is the
+    patch's 1 - |x|^2."""
+    import paper_1709_06924_b200 as P
+    from paper_1709_06924_b200 import density as D
+
+    f = D.density_preset("c4")
+    n = 40962
+    z = np.ascontiguousarray(P.sample_by_density(f, n, 0))
+    _, nbr, deg, _ = cells(h, z)
+    p = D.device_params(f)
+    prm = np.zeros(15)
+    prm[0:3] = [p["gamma"], p["beta"], p["alpha"]]
+    prm[3:9] = p["center"]
+    co, wd = p["table"]
+    co = np.ascontiguousarray(co)
+    order = np.arange(n, dtype=np.int32)
+    nsub = 2 * int(deg.sum())
+    tail = np.zeros((nsub, 4))
+    acc = np.zeros(nsub, np.int32)
+    h.harness_fit_tails.restype = ctypes.c_longlong
+    m = h.harness_fit_tails(dp(z), n, ip(order), ip(nbr), ip(deg), dp(co), co.shape[1],
+                            ctypes.c_double(wd), dp(prm), 6, dp(tail), ip(acc))
+    assert m == nsub
+    assert set(np.unique(acc)) <= {0, 1, 2, 3}
+    assert (acc > 0).mean() > 0.9                      # most patches are fitted
+    assert (acc >= 2).mean() > 0.05                    # and the lower degrees do occur
+    assert np.all(tail[acc >= 2, 0] <= 4e-15)          # |a6| at the noise floor
+    assert np.all(tail[acc == 3, 1] <= 4e-15)          # |a5| + |a6| at the noise floor
+    assert np.all(tail[acc == 1, 0] > 4e-15)           # full degree only where a6 matters
+    assert np.all((tail[:, 3] > -1e-12) & (tail[:, 3] < 0.1))     # 1 - |x|^2 bound of the patch
