@@ -849,8 +849,11 @@ k_quad(QuadArgs a) {
 // the density on the same leaf grid, every lane of a warp on the same sweep.  Grid-stride over
 // the queue (its length is known on the device only).
 constexpr int QTAB_THREADS = 64;
+#ifndef QTAB_MINB
+#define QTAB_MINB 8      // resident CTAs per SM the register budget must allow (one wave for the queue)
+#endif
 template <int KIND>
-__global__ void __launch_bounds__(QTAB_THREADS) k_quad_table(QuadArgs a) {
+__global__ void __launch_bounds__(QTAB_THREADS, QTAB_MINB) k_quad_table(QuadArgs a) {
     __shared__ double s_nodes[21];
     for (int q = threadIdx.x; q < 21; q += blockDim.x)
         s_nodes[q] = a.nodes[(q / 7) * a.nq + q % 7];
