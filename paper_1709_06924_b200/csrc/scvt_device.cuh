@@ -1114,18 +1114,23 @@ SCVT_HD double density_x(const DensityParams& dp, V3 x, double inv, TabCache& t0
 // Leaf sweep of one sub-triangle; FIT selects the per-patch fit (loop-invariant, so the two
 // density paths are separate loops: the table path's per-lane caches are not live in the
 // fitted loop).
+// part / nparts: the share of the leaves this call sweeps -- pass = part & 1 and the leaf rows
+// a = part >> 1 (mod nparts / 2) when nparts > 1 (k_quad_table splits a sub-triangle over four
+// lanes); everything with the defaults.
 template <int KIND, int L, bool FIT>
 SCVT_COLD void sym7_leaves(const SubTri& s, V3 z, const V3* o, double w0, double w1, double w2,
                          const DensityParams& dp, const LocalFit& f0, const LocalFit& f1,
-                         double* mo, int* pole) {
+                         double* mo, int* pole, int part = 0, int nparts = 1) {
     TabCache t0, t1;
     if (!FIT) { t0.key = -1; t1.key = -1; }
     double m = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, e = 0.0;
     const double invL = 1.0 / (double)L;
-    for (int pass = 0; pass < 2; ++pass) {          // 0: up-leaves, 1: down-leaves
+    const int pass_lo = nparts > 1 ? (part & 1) : 0, pass_hi = nparts > 1 ? pass_lo + 1 : 2;
+    const int a_lo = nparts > 1 ? (part >> 1) : 0, a_step = nparts > 1 ? nparts / 2 : 1;
+    for (int pass = pass_lo; pass < pass_hi; ++pass) {          // 0: up-leaves, 1: down-leaves
     const double sg = pass ? -1.0 : 1.0;
     const int M = L - pass;
-    for (int a = 0; a < M; ++a)
+    for (int a = a_lo; a < M; a += a_step)
     for (int b = 0; b < M - a; ++b) {
         const double fa = (a + pass) * invL, fb = (b + pass) * invL;
         const V3 P = v3(s.v0.x + fa * s.e1.x + fb * s.e2.x, s.v0.y + fa * s.e1.y + fb * s.e2.y,
@@ -1516,13 +1521,15 @@ SCVT_HD int sym7_prologue(const DensityParams& dp, const SubTri& s, LocalFit* f)
 // no accepted fit
 template <int KIND, int L>
 SCVT_HD void sym7_table_sweep(const SubTri& s, V3 z, const double* l1, const double* l2,
-                              const double* w, const DensityParams& dp, double* acc, int* pole) {
+                              const double* w, const DensityParams& dp, double* acc, int* pole,
+                              int part = 0, int nparts = 1) {
     V3 o[7];
 #pragma unroll
     for (int q = 0; q < 7; ++q) o[q] = add(mul(s.e1, l1[q]), mul(s.e2, l2[q]));
     double mo[5];
     LocalFit none;     // not read (FIT = false)
-    sym7_leaves<KIND, L, false>(s, z, o, w[0], w[1], w[4], dp, none, none, mo, pole);
+    sym7_leaves<KIND, L, false>(s, z, o, w[0], w[1], w[4], dp, none, none, mo, pole, part,
+                                nparts);
     acc[0] += s.area * mo[0];
     acc[1] += s.area * mo[1]; acc[2] += s.area * mo[2]; acc[3] += s.area * mo[3];
     acc[4] += s.area * mo[4];

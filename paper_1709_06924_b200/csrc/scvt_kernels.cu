@@ -863,24 +863,42 @@ __global__ void __launch_bounds__(QTAB_THREADS, QTAB_MINB) k_quad_table(QuadArgs
     const double* w = s_nodes + 14;
     const int total = *a.defer_cnt;
     const DensityParams& dp = *a.dpg;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += gridDim.x * blockDim.x) {
-        const int t_id = a.defer_list[idx];
-        const int u = t_id >> 1, half = t_id & 1;
-        const int i = a.inc_gen[u];
-        const int t = u - a.inc_base[i];
-        const int d = a.deg[i];
-        const int* row = a.nbr + (int64_t)i * MAXDEG;
-        const int j = row[t], k = row[t + 1 == d ? 0 : t + 1];
-        const V3 vi = load3(a.z, i), vj = load3(a.z, j), vk = load3(a.z, k);
-        int obt, degen, pole = 0;
-        const SubTri st = fan_sub(vi, vj, vk, i, j, k, half, &obt, &degen);
+    // four lanes per queued sub-triangle (up / down leaves x even / odd leaf rows: 20, 16, 16
+    // and 12 of the 64 leaves), summed in a fixed order by two shuffles: the sweep of one
+    // sub-triangle is ~30k dependent-ish FP64 instructions, and a short queue (a shard's, or
+    // c3's) is latency-, not throughput-bound
+    const int lane = threadIdx.x & 31, part = lane & 3;
+    const int per_pass = gridDim.x * (blockDim.x >> 2);
+    for (int e0 = blockIdx.x * (blockDim.x >> 2) + ((threadIdx.x >> 5) << 3); e0 < total;
+         e0 += per_pass) {           // e0: the warp's first entry (8 entries per warp)
+        const int idx = e0 + (lane >> 2);
+        const bool live = idx < total;
         double acc[5] = {0, 0, 0, 0, 0};
-        sym7_table_sweep<KIND, 8>(st, vi, l1, l2, w, dp, acc, &pole);
-        if (pole) atomicOr(a.status, ST_POLE);
-        double* out = a.part + (int64_t)u * PART_ROW + (half ? 5 : 0);
+        int u = 0, half = 0, pole = 0;
+        if (live) {
+            const int t_id = a.defer_list[idx];
+            u = t_id >> 1; half = t_id & 1;
+            const int i = a.inc_gen[u];
+            const int t = u - a.inc_base[i];
+            const int d = a.deg[i];
+            const int* row = a.nbr + (int64_t)i * MAXDEG;
+            const int j = row[t], k = row[t + 1 == d ? 0 : t + 1];
+            const V3 vi = load3(a.z, i), vj = load3(a.z, j), vk = load3(a.z, k);
+            int obt, degen;
+            const SubTri st = fan_sub(vi, vj, vk, i, j, k, half, &obt, &degen);
+            sym7_table_sweep<KIND, 8>(st, vi, l1, l2, w, dp, acc, &pole, part, 4);
+            if (pole) atomicOr(a.status, ST_POLE);
+        }
 #pragma unroll
-        for (int c = 0; c < 5; ++c) out[c] = acc[c];
+        for (int c = 0; c < 5; ++c) {
+            acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
+            acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
+        }
+        if (live && part == 0) {
+            double* out = a.part + (int64_t)u * PART_ROW + (half ? 5 : 0);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) out[c] = acc[c];
+        }
     }
 }
 
@@ -2623,8 +2641,10 @@ int launch_quad_kind(scvt_ctx* ctx, const QuadArgs& a, unsigned grid, size_t sme
                                                             ctx->stream>>>(a);
         if constexpr (DEFER) {
             LAUNCHED();
-            const unsigned gt = std::min<unsigned>(blocks_for(2 * (int64_t)a.n_inc, QTAB_THREADS),
-                                                   148u * 16u);   // 16 resident CTAs of 64 threads per SM
+            // 16 queued sub-triangles per block and pass; the grid covers ~95k of them at once
+            // (a c4 launch queues ~65k), longer queues take further grid-stride passes
+            const unsigned gt = std::min<unsigned>(blocks_for(8 * (int64_t)a.n_inc, QTAB_THREADS),
+                                                   148u * 40u);
             k_quad_table<KIND><<<gt, QTAB_THREADS, 0, ctx->stream>>>(a);
         }
     } else
