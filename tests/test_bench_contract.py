@@ -52,3 +52,26 @@ def test_world_size_must_match_gpus():
                           "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
                          cwd=ROOT, env=env, timeout=600)
     assert out.returncode != 0 and "WORLD_SIZE=2" in out.stderr
+
+
+def test_committed_ncu_figures_are_readable_per_config():
+    """bench.py reads the ncu figures it cannot measure inside the timed run (DRAM traffic and
+    FP64 pipe utilisation of k_quad) from profiles/roofline_traffic.json, per config; the
+    files the JSON cites must be committed."""
+    import re
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    for cfg in ("c3", "c4", "c5"):
+        t = bench._traffic_from_profiles(cfg)
+        p = bench._profile_value("k_quad_fp64_pipe_active_pct", cfg)
+        assert t is not None and 1e7 < t < 1e10
+        assert p is not None and 50.0 < p <= 100.0
+    assert bench._profile_value("k_quad_fp64_pipe_active_pct", "c1") is None   # const: no capture
+    with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+        src = json.load(f)["source"]
+    cited = re.findall(r"profiles/[\w.]+\.txt", src)
+    assert cited
+    for path in cited:
+        assert os.path.exists(os.path.join(ROOT, path)), path
